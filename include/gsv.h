@@ -1,0 +1,238 @@
+/*
+ * gsv.h -- C ABI of the B200 brick rasterizer (libgsv_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `gsvol`
+ * (arxiv/paper_2603_09621).  The reference has no native FFI: its kernels are
+ * numba @njit functions that take flat positional SoA arrays, scalars and
+ * caller-allocated outputs (SURVEY.md §8b "Kernel-level ABI").  Every entry
+ * point below replaces one of those call sites; the cited file:line is the
+ * reference code whose semantics it reproduces (paths relative to
+ * /root/reference/pkg/src/gsvol/).
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA storage),
+ *    except where a parameter says "host".  The library never allocates device
+ *    memory: outputs and workspaces belong to the caller (raster.py:305-307,
+ *    494-497, 517-520 -- the reference wrapper allocates every output too).
+ *  - `stream` is a cudaStream_t passed as void*; every call only enqueues work
+ *    on it (no device synchronisation) unless documented otherwise.
+ *  - Field arrays are float64, C-contiguous, in GaussianField's SoA layout
+ *    (field.py:33-70): positions (N,3), log_scales (N,3), rotations (N,4) with
+ *    the quaternion scalar-first (w,x,y,z), raw_amplitude (N), raw_relax (N).
+ *  - Volumes are linear, x-fastest: lin = ix + nx*(iy + ny*iz)
+ *    (volume.py:100-102, raster.py:271).
+ *  - Brick b covers voxels [bx*bdx, ...) with b = bx + bgx*(by + bgy*bz)
+ *    (raster.py:209, 247-256).
+ *  - Return value: GSV_OK (0) or a gsv_status code; gsv_last_error() returns
+ *    a thread-local message for the last failure.
+ */
+#ifndef GSV_B200_H
+#define GSV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSV_ABI_VERSION 1
+
+typedef enum {
+  GSV_OK = 0,
+  GSV_ERR_ARG = 1,      /* invalid argument (shape, null pointer, range) */
+  GSV_ERR_CUDA = 2,     /* a CUDA runtime call failed */
+  GSV_ERR_CAPACITY = 3, /* a count exceeds what the caller allocated / int32 */
+} gsv_status;
+
+/* Cell-centred sampling lattice; origin is the centre of voxel (0,0,0)
+ * (volume.py:16-41 GridSpec). */
+typedef struct {
+  int32_t nx, ny, nz;
+  int32_t _pad;
+  double ox, oy, oz;
+  double sx, sy, sz;
+} gsv_grid;
+
+/* Brick decomposition (raster.py:152-156) plus the z-slab [bz0, bz1) of brick
+ * layers this call owns.  A whole-grid call uses bz0 = 0, bz1 = bgz.  The
+ * slab's bricks are the contiguous brick-id range [bgx*bgy*bz0, bgx*bgy*bz1)
+ * (SURVEY.md §8e), so a slab index is an exact slice of the global index. */
+typedef struct {
+  int32_t bdx, bdy, bdz;
+  int32_t bgx, bgy, bgz;
+  int32_t bz0, bz1;
+} gsv_bricks;
+
+/* Per-Gaussian fp32 record consumed by the pair kernels (64 bytes). */
+typedef struct {
+  float l[9];      /* whitening factor L = diag(exp(-ls)) R^T, row-major     */
+  float amp;       /* A = sigmoid(raw_amplitude)                            */
+  float relax;     /* r = sigmoid(raw_relax), or 1 when relax is disabled    */
+  float half[3];   /* cutoff*sqrt(Sigma_kk): world-axis half extents        */
+  float _pad[2];
+} gsv_record32;
+
+/* Per-Gaussian fp64 record for the f64 engine (precision="f64"). */
+typedef struct {
+  double l[9];
+  double amp;
+  double relax;
+  double _pad;
+} gsv_record64;
+
+int gsv_abi_version(void);
+const char* gsv_last_error(void);
+/* Number of SMs of the current device (host query, for grid sizing). */
+int gsv_device_sm_count(void);
+
+/* ------------------------------------------------------------------------
+ * Preprocess + bin count: one fused per-Gaussian kernel.
+ * Replaces field.rotation_matrices (field.py:141-154), _whitening_factors
+ * (raster.py:233-237), activated_amplitude / activated_relax
+ * (field.py:86-94) and the per-Gaussian AABB part of build_brick_index
+ * (raster.py:175-198), computed in f64 with the reference's unfused operation
+ * order (numpy einsum "nkm,nm->nk" sums (p0+p2)+p1).
+ *   rec32  (N)   : gsv_record32, always written
+ *   rec64  (N)   : gsv_record64, written when non-NULL
+ *   counts (N)   : pairs Gaussian i emits inside the slab (0 if outside)
+ *   box    (N,4) : int32 {blo_x | blo_y<<16, blo_z | nb_x<<16, nb_y | nb_z<<16, 0}
+ *                  brick box of Gaussian i clipped to the slab.
+ * cutoff_sigma may be +inf (dense lists, raster.py:166-171).
+ * ------------------------------------------------------------------------ */
+int gsv_preprocess(const double* positions, const double* log_scales,
+                   const double* rotations, const double* raw_amplitude,
+                   const double* raw_relax, int64_t n, int relax_enabled,
+                   double cutoff_sigma, const gsv_grid* grid,
+                   const gsv_bricks* bricks, gsv_record32* rec32,
+                   gsv_record64* rec64, int32_t* counts, int32_t* box,
+                   void* stream);
+
+/* Workspace bytes needed by gsv_bin_scan / gsv_bin_fill (CUB temp storage).*/
+int gsv_bin_workspace(int64_t n, int64_t max_pairs, int32_t nbricks,
+                      size_t* bytes);
+
+/* Exclusive scan of counts -> gstart (N+1, int64).  gstart[N] = P.  The
+ * caller reads gstart[N] (one 8-byte D2H) to size the pair buffers. */
+int gsv_bin_scan(const int32_t* counts, int64_t n, int64_t* gstart,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Emit (brick, gid) pairs in gid-major order (raster.py:200-209), stable
+ * radix sort by brick id (raster.py:211-216; LSD radix sort is stable so
+ * each brick's list is ascending in gid), CSR starts for the slab's bricks.
+ *   keys_tmp, vals_tmp, keys_out : int32 (P) scratch
+ *   gids_out : int32 (P), starts_out : int64 (nbricks_slab + 1). */
+int gsv_bin_fill(const int32_t* counts, const int32_t* box,
+                 const int64_t* gstart, int64_t n, int64_t pairs,
+                 const gsv_bricks* bricks, int32_t* keys_tmp,
+                 int32_t* vals_tmp, int32_t* keys_out, int32_t* gids_out,
+                 int64_t* starts_out, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* Canonical-order check and repair for caller-supplied lists
+ * (BrickIndex.lists_sorted / canonicalized, raster.py:91-112).
+ * gsv_lists_unsorted writes 1 to *flag (device int32) if any brick list is
+ * not strictly ascending.  gsv_canonicalize sorts every list ascending. */
+int gsv_lists_unsorted(const int64_t* starts, const int32_t* gids,
+                       int32_t nbricks, int64_t pairs, int32_t* flag,
+                       void* stream);
+int gsv_canonicalize_workspace(int64_t pairs, int32_t nbricks, size_t* bytes);
+int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
+                     int32_t* gids_out, int32_t nbricks, int64_t pairs,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Forward render, CTA per brick.  Replaces _forward_kernel
+ * (raster.py:240-293).  precision 0 = f32 (S/W/I float32; truncation decided
+ * exactly in f64 inside a guard band), 1 = f64 (S/W/I float64, rec64 needed).
+ * The slab's voxels only are written.  If target != NULL the L1/L2 loss of
+ * optimize.loss_and_grad (optimize.py:91-103) is fused into the epilogue:
+ *   ab (V,2) float : {alpha, beta} = {dL/dI / W, dL/dI * I / W} (0 where
+ *                    W < eps_w), the backward's per-voxel inputs;
+ *   loss_part (nbricks_slab) double : per-brick sum |I-T| (l1) or (I-T)^2.
+ * loss_kind: 0 = l1, 1 = l2.  inv_v = 1 / (global voxel count).
+ * ------------------------------------------------------------------------ */
+int gsv_forward(const double* positions, const gsv_record32* rec32,
+                const gsv_record64* rec64, const double* log_scales,
+                const double* rotations, const int64_t* starts,
+                const int32_t* gids, const gsv_grid* grid,
+                const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
+                int precision, void* S, void* W, void* I,
+                const float* target, int loss_kind, double inv_v, float* ab,
+                double* loss_part, void* stream);
+
+/* Per-voxel backward inputs from (W, I, dL/dI) for the unfused API path
+ * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) in the
+ * precision's type and *bad (device int64) = first non-finite voxel index or
+ * -1.  Slab voxels only. */
+int gsv_backward_prep(const void* W, const void* I, const double* dldi,
+                      const gsv_grid* grid, const gsv_bricks* bricks,
+                      double eps_w, int precision, void* ab, int64_t* bad,
+                      void* stream);
+
+/* Backward pair pass, per-pair partial gradients.  Replaces _backward_kernel
+ * (raster.py:322-409).  Writes for every pair of the slab its 11 partials
+ * {d_amp, d_relax, d_mu[3], G6[6]} (G6 = g00,g11,g22,g01,g02,g12) into
+ * partials[(e)*12 ...] where e is the pair's gid-major emission index
+ * gstart[gid] + rank of the brick in the Gaussian's box -- i.e. the order
+ * the reference merges in (raster.py:512-516: stable argsort by gid keeps
+ * ascending brick order).  partials: float (f32) or double (f64), (P,12). */
+int gsv_backward(const double* positions, const gsv_record32* rec32,
+                 const gsv_record64* rec64, const double* log_scales,
+                 const double* rotations, const int64_t* starts,
+                 const int32_t* gids, const int64_t* gstart,
+                 const int32_t* box, const gsv_grid* grid,
+                 const gsv_bricks* bricks, double cutoff_sigma,
+                 int precision, const void* ab, void* partials, void* stream);
+
+/* Deterministic per-Gaussian merge of pair partials in ascending brick order
+ * (_merge_pairs_kernel, raster.py:412-451).  gsum (N,12) double. */
+int gsv_merge(const void* partials, const int64_t* gstart, int64_t n,
+              int precision, double* gsum, void* stream);
+
+/* Chain rule to raw-parameter gradients (raster.py:524-549,
+ * _rotation_jacobians 454-467).  Outputs f64 arrays in GradientBuffer layout
+ * (raster.py:128-145). */
+int gsv_chain_rule(const double* gsum, const double* log_scales,
+                   const double* rotations, const double* raw_amplitude,
+                   const double* raw_relax, int64_t n, int relax_enabled,
+                   double* g_raw_amplitude, double* g_raw_relax,
+                   double* g_positions, double* g_log_scales,
+                   double* g_rotations, void* stream);
+
+/* loss_and_grad (optimize.py:91-103).  pred/target float32 or float64 (V)
+ * per pred_f64/target_f64; grad float64 (V); loss_part (nblocks) double where
+ * nblocks = gsv_loss_blocks(V).  The caller sums loss_part (gsv_sum) and
+ * divides by V. */
+int gsv_loss_blocks(int64_t v);
+int gsv_loss(const void* pred, int pred_f64, const void* target,
+             int target_f64, int64_t v, int loss_kind, double* grad,
+             double* loss_part, void* stream);
+
+/* Deterministic sum of a double array into *out (single-CTA tree). */
+int gsv_sum(const double* x, int64_t n, double* out, void* stream);
+
+/* One Adam step on one parameter group (step_optimizer, optimize.py:127-148):
+ * m = b1*m + (1-b1)*g; v = b2*v + ((1-b2)*g)*g;
+ * p -= lr*(m/bc1) / (sqrt(v/bc2) + eps), unfused f64 like numpy. */
+int gsv_adam(double* p, double* m, double* v, const double* g, int64_t count,
+             double lr, double beta1, double beta2, double eps, double bc1,
+             double bc2, void* stream);
+
+/* q /= |q| per Gaussian (GaussianField.normalize_rotations, field.py:100). */
+int gsv_normalize_rotations(double* rotations, int64_t n, void* stream);
+
+/* Brute-force O(N*V) render (render_naive / _naive_kernel, render.py:84-127)
+ * on the device, Sigma^-1 quadratic form, f64 math.  precision selects the
+ * accumulator / output type. */
+int gsv_render_naive(const double* positions, const double* log_scales,
+                     const double* rotations, const double* raw_amplitude,
+                     const double* raw_relax, int64_t n, int relax_enabled,
+                     const gsv_grid* grid, double cutoff_sigma, double eps_w,
+                     int precision, void* I, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GSV_B200_H */

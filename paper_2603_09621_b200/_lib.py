@@ -1,0 +1,152 @@
+"""ctypes binding of libgsv_b200.so (the C ABI declared in include/gsv.h).
+
+This is the only way the package reaches the GPU kernels.  There is no
+fallback: if the library is missing or CUDA is unavailable, every entry point
+raises.  Device pointers come from torch tensors (torch is plumbing here:
+device memory, streams, torch.distributed).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsv_b200.so")
+
+c_int = ctypes.c_int
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+c_szp = ctypes.POINTER(ctypes.c_size_t)
+
+
+class GsvGrid(ctypes.Structure):
+    _fields_ = [("nx", c_i32), ("ny", c_i32), ("nz", c_i32), ("_pad", c_i32),
+                ("ox", c_dbl), ("oy", c_dbl), ("oz", c_dbl),
+                ("sx", c_dbl), ("sy", c_dbl), ("sz", c_dbl)]
+
+
+class GsvBricks(ctypes.Structure):
+    _fields_ = [("bdx", c_i32), ("bdy", c_i32), ("bdz", c_i32),
+                ("bgx", c_i32), ("bgy", c_i32), ("bgz", c_i32),
+                ("bz0", c_i32), ("bz1", c_i32)]
+
+
+GP = ctypes.POINTER(GsvGrid)
+BP = ctypes.POINTER(GsvBricks)
+
+# name -> argtypes (all return int status unless listed in _RESTYPES)
+_SIGS = {
+    "gsv_abi_version": [],
+    "gsv_last_error": [],
+    "gsv_device_sm_count": [],
+    "gsv_preprocess": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_dbl, GP, BP,
+                       c_vp, c_vp, c_vp, c_vp, c_vp],
+    "gsv_bin_workspace": [c_i64, c_i64, c_i32, c_szp],
+    "gsv_bin_scan": [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp],
+    "gsv_bin_fill": [c_vp, c_vp, c_vp, c_i64, c_i64, BP, c_vp, c_vp, c_vp, c_vp, c_vp,
+                     c_vp, ctypes.c_size_t, c_vp],
+    "gsv_lists_unsorted": [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp],
+    "gsv_canonicalize_workspace": [c_i64, c_i32, c_szp],
+    "gsv_canonicalize": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp],
+    "gsv_forward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl, c_dbl, c_int,
+                    c_vp, c_vp, c_vp, c_vp, c_int, c_dbl, c_vp, c_vp, c_vp],
+    "gsv_backward_prep": [c_vp, c_vp, c_vp, GP, BP, c_dbl, c_int, c_vp, c_vp, c_vp],
+    "gsv_backward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl,
+                     c_int, c_vp, c_vp, c_vp],
+    "gsv_merge": [c_vp, c_vp, c_i64, c_int, c_vp, c_vp],
+    "gsv_chain_rule": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp,
+                       c_vp, c_vp],
+    "gsv_loss_blocks": [c_i64],
+    "gsv_loss": [c_vp, c_int, c_vp, c_int, c_i64, c_int, c_vp, c_vp, c_vp],
+    "gsv_sum": [c_vp, c_i64, c_vp, c_vp],
+    "gsv_adam": [c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl,
+                 c_vp],
+    "gsv_normalize_rotations": [c_vp, c_i64, c_vp],
+    "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
+                         c_vp, c_vp],
+}
+_RESTYPES = {"gsv_last_error": ctypes.c_char_p}
+
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+
+
+class GsvLibraryError(RuntimeError):
+    """The CUDA extension is missing, failed to load, or a call failed."""
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the C ABI.  Raises if the library is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise GsvLibraryError(
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, c_int)
+    _lib = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    l = load()
+    if not torch.cuda.is_available():
+        raise GsvLibraryError("CUDA device not available; the B200 rasterizer has no CPU path")
+    return l
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = load().gsv_last_error().decode(errors="replace")
+        raise GsvLibraryError(f"{what} failed (status {status}): {msg}")
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def make_grid(grid) -> GsvGrid:
+    nx, ny, nz = grid.dims
+    ox, oy, oz = grid.origin
+    sx, sy, sz = grid.spacing
+    return GsvGrid(nx, ny, nz, 0, ox, oy, oz, sx, sy, sz)
+
+
+def make_bricks(grid, brick_dims, slab=None) -> GsvBricks:
+    bdx, bdy, bdz = brick_dims
+    nx, ny, nz = grid.dims
+    bgx, bgy, bgz = -(-nx // bdx), -(-ny // bdy), -(-nz // bdz)
+    bz0, bz1 = (0, bgz) if slab is None else slab
+    return GsvBricks(bdx, bdy, bdz, bgx, bgy, bgz, bz0, bz1)
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device, key: str = "default") -> torch.Tensor:
+    """Grow-only scratch buffer per (device, key) for CUB temp storage."""
+    k = (str(device), key)
+    buf = _ws_cache.get(k)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes * 1.25), 1 << 16), dtype=torch.uint8, device=device)
+        _ws_cache[k] = buf
+    return buf

@@ -1,0 +1,342 @@
+// gsv_bin.cu -- fused per-Gaussian preprocessing and brick binning.
+//
+// Replaces build_brick_index (raster.py:148-217), _whitening_factors
+// (raster.py:233-237) and the sigmoid activations (field.py:86-94).
+//
+//   preprocess_kernel   one thread per Gaussian, f64 AABB in the reference's
+//                       exact operation order -> per-Gaussian pair count and
+//                       brick box; fp32 (and optionally fp64) record for the
+//                       pair kernels.
+//   cub ExclusiveSum    counts -> gstart (gid-major emission offsets)
+//   emit_kernel         (slab-local brick id, gid) in gid-major order, each
+//                       Gaussian's bricks x-fastest (raster.py:200-209)
+//   cub SortPairs       stable LSD radix sort on the brick id, only
+//                       ceil(log2 B) key bits -> lists ascending in gid
+//   starts_kernel       CSR starts from the sorted keys (raster.py:213-215)
+//
+// This translation unit is compiled with -fmad=false in addition to using
+// the explicit _rn intrinsics, so no f64 expression that feeds a binning
+// decision can be contracted.
+#include <cub/cub.cuh>
+
+#include "gsv_common.cuh"
+
+namespace gsv {
+namespace {
+
+// numpy float64 -> int64 cast on x86-64 (cvttsd2si / vcvttpd2qq): truncation,
+// with NaN and out-of-range values mapping to INT64_MIN.
+__device__ __forceinline__ int64_t np_to_int64(double x) {
+  if (!(x > -9.2233720368547758e18 && x < 9.2233720368547758e18)) return INT64_MIN;
+  return (int64_t)x;
+}
+
+__device__ __forceinline__ int64_t clip64(int64_t v, int64_t lo, int64_t hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+__global__ void __launch_bounds__(256)
+preprocess_kernel(const double* __restrict__ pos, const double* __restrict__ ls,
+                  const double* __restrict__ rot, const double* __restrict__ ra,
+                  const double* __restrict__ rr, int64_t n, int relax_enabled,
+                  double cutoff, int dense, gsv_grid g, gsv_bricks k,
+                  gsv_record32* __restrict__ rec32, gsv_record64* __restrict__ rec64,
+                  int32_t* __restrict__ counts, int32_t* __restrict__ box) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+
+  double q[4], l[3], p[3];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) q[a] = rot[4 * i + a];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    l[a] = ls[3 * i + a];
+    p[a] = pos[3 * i + a];
+  }
+  double R[9];
+  rotation_f64(q, R);
+  const double inv_s[3] = {exp(-l[0]), exp(-l[1]), exp(-l[2])};
+  double L[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) L[3 * a + b] = mul(inv_s[a], R[3 * b + a]);
+  const double A = expit_f64(ra[i]);
+  const double r = relax_enabled ? expit_f64(rr[i]) : 1.0;
+
+  // Marginal variance Sigma_kk = einsum("nkm,nm->nk", R*R, exp(2 ls)); numpy
+  // 2.3 reduces the length-3 axis as (p0 + p2) + p1 (SURVEY.md §0 finding 2).
+  const double var[3] = {exp(mul(2.0, l[0])), exp(mul(2.0, l[1])), exp(mul(2.0, l[2]))};
+  double half[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double p0 = mul(mul(R[3 * a + 0], R[3 * a + 0]), var[0]);
+    const double p1 = mul(mul(R[3 * a + 1], R[3 * a + 1]), var[1]);
+    const double p2 = mul(mul(R[3 * a + 2], R[3 * a + 2]), var[2]);
+    const double skk = add(add(p0, p2), p1);
+    half[a] = dense ? __longlong_as_double(0x7ff0000000000000ULL) : mul(cutoff, sqrt(skk));
+  }
+
+  gsv_record32 o;
+#pragma unroll
+  for (int a = 0; a < 9; ++a) o.l[a] = (float)L[a];
+  o.amp = (float)A;
+  o.relax = (float)r;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) o.half[a] = (float)half[a];
+  o._pad[0] = 0.f;
+  o._pad[1] = 0.f;
+  {
+    float4* dst = reinterpret_cast<float4*>(rec32 + i);
+    const float4* src = reinterpret_cast<const float4*>(&o);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) dst[a] = src[a];
+  }
+  if (rec64) {
+    gsv_record64 d;
+#pragma unroll
+    for (int a = 0; a < 9; ++a) d.l[a] = L[a];
+    d.amp = A;
+    d.relax = r;
+    d._pad = 0.0;
+    rec64[i] = d;
+  }
+
+  // ---- brick box (raster.py:160-198), clipped to the slab [bz0, bz1).
+  const int dims[3] = {g.nx, g.ny, g.nz};
+  const int bd[3] = {k.bdx, k.bdy, k.bdz};
+  const int bg[3] = {k.bgx, k.bgy, k.bgz};
+  int64_t blo[3], bhi[3];
+  bool inside = true;
+  if (dense) {
+    // cutoff = inf: every Gaussian in every brick (raster.py:166-171).
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      blo[a] = 0;
+      bhi[a] = bg[a] - 1;
+    }
+  } else {
+    const double org[3] = {g.ox, g.oy, g.oz};
+    const double spc[3] = {g.sx, g.sy, g.sz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double glo = __ddiv_rn(sub(sub(p[a], half[a]), org[a]), spc[a]);
+      const double ghi = __ddiv_rn(sub(add(p[a], half[a]), org[a]), spc[a]);
+      int64_t vlo = np_to_int64(ceil(sub(glo, 0.5)));
+      int64_t vhi = np_to_int64(floor(add(ghi, 0.5)));
+      vlo = clip64(vlo, 0, dims[a] - 1);
+      vhi = clip64(vhi, 0, dims[a] - 1);
+      inside = inside && (ghi >= -0.5) && (glo <= (double)dims[a] - 0.5);
+      blo[a] = vlo / bd[a];
+      bhi[a] = vhi / bd[a];
+    }
+  }
+  // z-slab clip: the slab owns brick layers [bz0, bz1).
+  if (blo[2] < k.bz0) blo[2] = k.bz0;
+  if (bhi[2] > k.bz1 - 1) bhi[2] = k.bz1 - 1;
+  int64_t cnt = 0;
+  int nb[3] = {0, 0, 0};
+  if (inside && bhi[2] >= blo[2]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) nb[a] = (int)(bhi[a] - blo[a] + 1);
+    cnt = (int64_t)nb[0] * nb[1] * nb[2];
+  }
+  counts[i] = (int32_t)cnt;
+  int4 bx;
+  bx.x = (int)(blo[0] & 0xFFFF) | ((int)(blo[1] & 0xFFFF) << 16);
+  bx.y = (int)(blo[2] & 0xFFFF) | ((nb[0] & 0xFFFF) << 16);
+  bx.z = (nb[1] & 0xFFFF) | ((nb[2] & 0xFFFF) << 16);
+  bx.w = 0;
+  reinterpret_cast<int4*>(box)[i] = bx;
+}
+
+struct ToI64 {
+  __host__ __device__ __forceinline__ int64_t operator()(int32_t v) const { return (int64_t)v; }
+};
+
+__global__ void scan_tail_kernel(const int32_t* counts, int64_t n, int64_t* gstart) {
+  gstart[n] = n > 0 ? gstart[n - 1] + (int64_t)counts[n - 1] : 0;
+}
+
+// One thread per Gaussian writes its pairs at gstart[i]: bricks of its box
+// x-fastest, exactly the reference's emission order (raster.py:200-209).
+__global__ void __launch_bounds__(256)
+emit_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
+            const int64_t* __restrict__ gstart, int64_t n, gsv_bricks k,
+            int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || counts[i] == 0) return;
+  const GBox b = unpack_box(box, i);
+  int64_t off = gstart[i];
+  const int64_t first = (int64_t)k.bgx * k.bgy * k.bz0;
+  for (int z = 0; z < b.nb_z; ++z)
+    for (int y = 0; y < b.nb_y; ++y) {
+      const int64_t row = (int64_t)(b.blo_x) +
+                          (int64_t)k.bgx * ((b.blo_y + y) + (int64_t)k.bgy * (b.blo_z + z)) - first;
+      for (int x = 0; x < b.nb_x; ++x) {
+        keys[off] = (int32_t)(row + x);
+        vals[off] = (int32_t)i;
+        ++off;
+      }
+    }
+}
+
+// starts[b] = first sorted position with key >= b, for b in [0, B].
+__global__ void starts_kernel(const int32_t* __restrict__ keys, int64_t p, int32_t nb,
+                              int64_t* __restrict__ starts) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j > p) return;
+  const int32_t cur = j < p ? keys[j] : nb;
+  const int32_t prev = j > 0 ? keys[j - 1] : -1;
+  for (int32_t b = prev + 1; b <= cur; ++b) starts[b] = j;
+}
+
+__global__ void unsorted_kernel(const int64_t* __restrict__ starts,
+                                const int32_t* __restrict__ gids, int32_t nb,
+                                int32_t* flag) {
+  const int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  for (int64_t j = starts[b] + 1; j < starts[b + 1]; ++j)
+    if (gids[j] <= gids[j - 1]) {
+      *flag = 1;
+      return;
+    }
+}
+
+int key_bits(int64_t nb) {
+  int bits = 1;
+  while (((int64_t)1 << bits) < nb + 1) ++bits;
+  return bits;
+}
+
+}  // namespace
+}  // namespace gsv
+
+using namespace gsv;
+
+extern "C" {
+
+int gsv_preprocess(const double* positions, const double* log_scales,
+                   const double* rotations, const double* raw_amplitude,
+                   const double* raw_relax, int64_t n, int relax_enabled,
+                   double cutoff_sigma, const gsv_grid* grid,
+                   const gsv_bricks* bricks, gsv_record32* rec32,
+                   gsv_record64* rec64, int32_t* counts, int32_t* box,
+                   void* stream) {
+  if (int s = validate_grid_bricks(grid, bricks)) return s;
+  GSV_REQUIRE(n >= 0, "n must be >= 0");
+  GSV_REQUIRE(cutoff_sigma > 0, "cutoff_sigma must be positive");
+  GSV_REQUIRE(n == 0 || (positions && log_scales && rotations && raw_amplitude &&
+                         raw_relax && rec32 && counts && box),
+              "null pointer argument");
+  if (n == 0) return GSV_OK;
+  const int dense = isinf(cutoff_sigma) ? 1 : 0;
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  preprocess_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
+      positions, log_scales, rotations, raw_amplitude, raw_relax, n, relax_enabled,
+      cutoff_sigma, dense, *grid, *bricks, rec32, rec64, counts, box);
+  GSV_CHECK_LAUNCH("preprocess_kernel");
+  return GSV_OK;
+}
+
+int gsv_bin_workspace(int64_t n, int64_t max_pairs, int32_t nbricks, size_t* bytes) {
+  GSV_REQUIRE(bytes != nullptr, "bytes must not be NULL");
+  GSV_REQUIRE(max_pairs < (int64_t)INT32_MAX, "pair count %lld exceeds int32",
+              (long long)max_pairs);
+  size_t scan_bytes = 0, sort_bytes = 0;
+  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(nullptr, ToI64());
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, it, (int64_t*)nullptr,
+                                                (int)(n > 0 ? n : 1));
+  if (e != cudaSuccess) return cuda_status(e, "DeviceScan sizing");
+  e = cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int32_t*)nullptr,
+                                      (int32_t*)nullptr, (const int32_t*)nullptr,
+                                      (int32_t*)nullptr, (int)(max_pairs > 0 ? max_pairs : 1),
+                                      0, key_bits(nbricks));
+  if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort sizing");
+  *bytes = (scan_bytes > sort_bytes ? scan_bytes : sort_bytes) + 256;
+  return GSV_OK;
+}
+
+int gsv_bin_scan(const int32_t* counts, int64_t n, int64_t* gstart, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  GSV_REQUIRE(n >= 0 && n < (int64_t)INT32_MAX, "n out of range");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(gstart, 0, sizeof(int64_t), s);
+    if (e != cudaSuccess) return cuda_status(e, "memset gstart");
+    return GSV_OK;
+  }
+  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(counts, ToI64());
+  size_t bytes = workspace_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(workspace, bytes, it, gstart, (int)n, s);
+  if (e != cudaSuccess) return cuda_status(e, "DeviceScan::ExclusiveSum");
+  scan_tail_kernel<<<1, 1, 0, s>>>(counts, n, gstart);
+  GSV_CHECK_LAUNCH("scan_tail_kernel");
+  return GSV_OK;
+}
+
+int gsv_bin_fill(const int32_t* counts, const int32_t* box, const int64_t* gstart,
+                 int64_t n, int64_t pairs, const gsv_bricks* bricks, int32_t* keys_tmp,
+                 int32_t* vals_tmp, int32_t* keys_out, int32_t* gids_out,
+                 int64_t* starts_out, void* workspace, size_t workspace_bytes,
+                 void* stream) {
+  GSV_REQUIRE(bricks != nullptr, "bricks must not be NULL");
+  GSV_REQUIRE(pairs >= 0 && pairs < (int64_t)INT32_MAX, "pair count %lld exceeds int32",
+              (long long)pairs);
+  cudaStream_t s = as_stream(stream);
+  const int64_t nb = slab_bricks(*bricks);
+  if (pairs > 0) {
+    emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(counts, box, gstart, n, *bricks,
+                                                           keys_tmp, vals_tmp);
+    GSV_CHECK_LAUNCH("emit_kernel");
+    size_t bytes = workspace_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, bytes, keys_tmp, keys_out,
+                                                    vals_tmp, gids_out, (int)pairs, 0,
+                                                    key_bits(nb), s);
+    if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort::SortPairs");
+  }
+  const int64_t threads = 256, items = pairs + 1;
+  starts_kernel<<<(unsigned)((items + threads - 1) / threads), (unsigned)threads, 0, s>>>(
+      keys_out, pairs, (int32_t)nb, starts_out);
+  GSV_CHECK_LAUNCH("starts_kernel");
+  return GSV_OK;
+}
+
+int gsv_lists_unsorted(const int64_t* starts, const int32_t* gids, int32_t nbricks,
+                       int64_t pairs, int32_t* flag, void* stream) {
+  (void)pairs;
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int32_t), s);
+  if (e != cudaSuccess) return cuda_status(e, "memset flag");
+  if (nbricks <= 0) return GSV_OK;
+  unsorted_kernel<<<(nbricks + 255) / 256, 256, 0, s>>>(starts, gids, nbricks, flag);
+  GSV_CHECK_LAUNCH("unsorted_kernel");
+  return GSV_OK;
+}
+
+int gsv_canonicalize_workspace(int64_t pairs, int32_t nbricks, size_t* bytes) {
+  GSV_REQUIRE(bytes != nullptr, "bytes must not be NULL");
+  size_t b = 0;
+  cudaError_t e = cub::DeviceSegmentedSort::SortKeys(
+      nullptr, b, (const int32_t*)nullptr, (int32_t*)nullptr, (int)(pairs > 0 ? pairs : 1),
+      nbricks > 0 ? nbricks : 1, (const int64_t*)nullptr, (const int64_t*)nullptr);
+  if (e != cudaSuccess) return cuda_status(e, "DeviceSegmentedSort sizing");
+  *bytes = b + 256;
+  return GSV_OK;
+}
+
+int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in, int32_t* gids_out,
+                     int32_t nbricks, int64_t pairs, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  GSV_REQUIRE(pairs >= 0 && pairs < (int64_t)INT32_MAX, "pair count exceeds int32");
+  if (pairs == 0 || nbricks == 0) return GSV_OK;
+  size_t bytes = workspace_bytes;
+  cudaError_t e = cub::DeviceSegmentedSort::SortKeys(workspace, bytes, gids_in, gids_out,
+                                                     (int)pairs, nbricks, starts, starts + 1,
+                                                     as_stream(stream));
+  if (e != cudaSuccess) return cuda_status(e, "DeviceSegmentedSort::SortKeys");
+  return GSV_OK;
+}
+
+}  // extern "C"

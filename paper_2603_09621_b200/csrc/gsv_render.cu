@@ -1,0 +1,696 @@
+// gsv_render.cu -- forward render and backward pair pass, one CTA per brick.
+//
+// forward  (raster.py:240-293): each CTA owns one brick's voxels, walks the
+//          brick's Gaussian list in chunks staged in shared memory, and
+//          accumulates S = sum A w, W = sum w in registers in list order (no
+//          depth sort, no atomics: bit-reproducible).  The epilogue
+//          normalises I = S/W and optionally fuses the L1/L2 loss
+//          (optimize.py:91-103), emitting the backward's per-voxel inputs.
+// backward (raster.py:322-409): one thread per (brick, Gaussian) pair walks
+//          the pair's exact 3-sigma sub-box of the brick and keeps the 11
+//          partial sums in registers; one 48-byte store per pair at the
+//          pair's gid-major emission slot, so the merge is a contiguous
+//          segmented reduction in ascending brick order (raster.py:512-522).
+//
+// f32 engine: per-pair math in fp32 with the voxel offset taken relative to
+// the brick origin (computed in f64), so |delta| stays small; the truncation
+// test d2 <= cutoff^2 is re-decided in f64 with the reference's exact
+// operation order inside a guard band around the cutoff (SURVEY.md §7 hard
+// part 2), so both engines agree on which pairs are live.
+// f64 engine: the reference arithmetic in double (precision="f64").
+#include <cfloat>
+
+#include "gsv_common.cuh"
+
+namespace gsv {
+namespace {
+
+constexpr int kFwdThreads = 256;
+constexpr int kBwdThreads = 128;
+constexpr float kGuardRel = 1e-4f;   // guard band relative to cutoff^2
+constexpr float kGuardMag = 4e-5f;   // guard band relative to term magnitude
+
+// Shared-memory record of one staged pair (f32 forward), 80 bytes.
+struct __align__(16) Pair32 {
+  float u[3];    // v at the brick's first voxel: L (p_b0 - mu)
+  float ex[3];   // v step per voxel along x: sx * L[:,0]
+  float ey[3];
+  float ez[3];
+  float amp, relax, guard;
+  int gid;
+  int box0;      // xlo | xhi<<8 | ylo<<16 | yhi<<24 (brick-local voxels)
+  int box1;      // zlo | zhi<<8
+  int _pad[2];
+};
+
+struct BrickGeom {
+  int x0, y0, z0;     // first voxel (global)
+  int ex, ey, ez;     // voxels of this brick inside the grid
+  double px, py, pz;  // world centre of the first voxel
+};
+
+__device__ __forceinline__ BrickGeom brick_geom(int b, const gsv_grid& g,
+                                                const gsv_bricks& k) {
+  const BrickXYZ c = brick_xyz(b, k);
+  BrickGeom r;
+  r.x0 = c.bx * k.bdx;
+  r.y0 = c.by * k.bdy;
+  r.z0 = c.bz * k.bdz;
+  r.ex = min(k.bdx, g.nx - r.x0);
+  r.ey = min(k.bdy, g.ny - r.y0);
+  r.ez = min(k.bdz, g.nz - r.z0);
+  r.px = g.ox + (double)r.x0 * g.sx;
+  r.py = g.oy + (double)r.y0 * g.sy;
+  r.pz = g.oz + (double)r.z0 * g.sz;
+  return r;
+}
+
+// Brick-local voxel range [lo, hi] that can hold live voxels of a Gaussian
+// with world centre offset c = mu - p_b0 and half extent h (3-sigma AABB,
+// widened by 1e-3 voxel so rounding can never drop a live voxel).
+__device__ __forceinline__ void sub_range(double c, double h, double s, int n,
+                                          int& lo, int& hi) {
+  const double ctr = c / s, hv = h / s;
+  double a = ceil(ctr - hv - 1e-3), b = floor(ctr + hv + 1e-3);
+  a = fmax(a, 0.0);
+  b = fmin(b, (double)(n - 1));
+  if (!(a <= b)) {
+    lo = 1;
+    hi = 0;
+    return;
+  }
+  lo = (int)a;
+  hi = (int)b;
+}
+
+// f64 whitening factor recomputed from the field (guard-band path).
+__device__ __noinline__ bool exact_live(int gid, int gx, int gy, int gz,
+                                        const double* __restrict__ pos,
+                                        const double* __restrict__ ls,
+                                        const double* __restrict__ rot,
+                                        const gsv_grid& g, double cutoff2) {
+  double L[9];
+  whitening_f64(ls + 3 * (int64_t)gid, rot + 4 * (int64_t)gid, L);
+  const double* m = pos + 3 * (int64_t)gid;
+  return ref_d2(L, m[0], m[1], m[2], gx, gy, gz, g) <= cutoff2;
+}
+
+// Deterministic block reduction of one double (fixed tree).
+template <int THREADS>
+__device__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < THREADS / 32; ++w) t += sh[w];
+  return t;  // valid in thread 0
+}
+
+// --------------------------------------------------------------- forward f32
+__global__ void __launch_bounds__(kFwdThreads)
+forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
+                 const double* __restrict__ ls, const double* __restrict__ rot,
+                 const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
+                 gsv_grid g, gsv_bricks k, float cut2, double cut2d, double eps_w,
+                 float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
+                 const float* __restrict__ target, int loss_kind, double inv_v,
+                 float2* __restrict__ ab, double* __restrict__ loss_part) {
+  __shared__ Pair32 sp[kFwdThreads];
+  __shared__ double red[kFwdThreads / 32];
+  const int lb = blockIdx.x;                               // slab-local brick
+  const int b = (int)slab_first(k) + lb;                   // global brick id
+  const BrickGeom bg = brick_geom(b, g, k);
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  const int nvb = k.bdx * k.bdy * k.bdz;
+  const int tid = threadIdx.x;
+  const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
+  double lsum = 0.0;
+
+  for (int vbase = 0; vbase < nvb; vbase += kFwdThreads) {
+    const int vl = vbase + tid;
+    const int lx = vl % k.bdx, ly = (vl / k.bdx) % k.bdy, lz = vl / (k.bdx * k.bdy);
+    const bool own = vl < nvb && lx < bg.ex && ly < bg.ey && lz < bg.ez;
+    const float fx = (float)lx, fy = (float)ly, fz = (float)lz;
+    float accS = 0.f, accW = 0.f;
+
+    for (int64_t cb = lbeg; cb < lend; cb += kFwdThreads) {
+      const int cnt = (int)min((int64_t)kFwdThreads, lend - cb);
+      __syncthreads();
+      if (tid < cnt) {
+        const int gid = gids[cb + tid];
+        const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+        const float4 q0 = r4[0], q1 = r4[1], q2 = r4[2], q3 = r4[3];
+        const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+        const double* m = pos + 3 * (int64_t)gid;
+        const double cx = m[0] - bg.px, cy = m[1] - bg.py, cz = m[2] - bg.pz;  // mu - p_b0
+        const float c0 = (float)(-cx), c1 = (float)(-cy), c2 = (float)(-cz);   // p_b0 - mu
+        Pair32 p;
+        float umax = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          p.u[a] = fmaf(L[3 * a + 0], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
+          p.ex[a] = L[3 * a + 0] * fsx;
+          p.ey[a] = L[3 * a + 1] * fsy;
+          p.ez[a] = L[3 * a + 2] * fsz;
+          umax = fmaxf(umax, fabsf(p.u[a]) + fabsf(p.ex[a]) * k.bdx +
+                                 fabsf(p.ey[a]) * k.bdy + fabsf(p.ez[a]) * k.bdz);
+        }
+        p.amp = q2.y;
+        p.relax = q2.z;
+        p.guard = fmaxf(kGuardRel * cut2, kGuardMag * umax * (umax + 3.f));
+        p.gid = gid;
+        int xl, xh, yl, yh, zl, zh;
+        sub_range(cx, (double)q2.w, g.sx, bg.ex, xl, xh);
+        sub_range(cy, (double)q3.x, g.sy, bg.ey, yl, yh);
+        sub_range(cz, (double)q3.y, g.sz, bg.ez, zl, zh);
+        if (xl > xh || yl > yh || zl > zh) {
+          xl = 255; xh = 0;
+        }
+        p.box0 = (xl & 255) | ((xh & 255) << 8) | ((yl & 255) << 16) | ((yh & 255) << 24);
+        p.box1 = (zl & 255) | ((zh & 255) << 8);
+        p._pad[0] = p._pad[1] = 0;
+        sp[tid] = p;
+      }
+      __syncthreads();
+      if (own) {
+        for (int j = 0; j < cnt; ++j) {
+          const int b0 = sp[j].box0, b1 = sp[j].box1;
+          if (lx < (b0 & 255) || lx > ((b0 >> 8) & 255) || ly < ((b0 >> 16) & 255) ||
+              ly > ((b0 >> 24) & 255) || lz < (b1 & 255) || lz > ((b1 >> 8) & 255))
+            continue;
+          const Pair32& p = sp[j];
+          const float v0 = fmaf(fz, p.ez[0], fmaf(fy, p.ey[0], fmaf(fx, p.ex[0], p.u[0])));
+          const float v1 = fmaf(fz, p.ez[1], fmaf(fy, p.ey[1], fmaf(fx, p.ex[1], p.u[1])));
+          const float v2 = fmaf(fz, p.ez[2], fmaf(fy, p.ey[2], fmaf(fx, p.ex[2], p.u[2])));
+          const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+          if (d2 > cut2 + p.guard) continue;
+          if (d2 >= cut2 - p.guard &&
+              !exact_live(p.gid, bg.x0 + lx, bg.y0 + ly, bg.z0 + lz, pos, ls, rot, g, cut2d))
+            continue;
+          const float w = __expf(-0.5f * d2) * p.relax;
+          accS = fmaf(p.amp, w, accS);
+          accW += w;
+        }
+      }
+    }
+    if (own) {
+      const int64_t lin = (int64_t)(bg.x0 + lx) +
+                          (int64_t)g.nx * ((bg.y0 + ly) + (int64_t)g.ny * (bg.z0 + lz));
+      const bool cov = (double)accW >= eps_w;
+      const float iv = cov ? __fdiv_rn(accS, accW) : 0.f;
+      S[lin] = accS;
+      W[lin] = accW;
+      I[lin] = iv;
+      if (target) {
+        const double d = (double)iv - (double)target[lin];
+        double dl;
+        if (loss_kind == 0) {
+          lsum += fabs(d);
+          dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_v;
+        } else {
+          lsum += d * d;
+          dl = 2.0 * d * inv_v;
+        }
+        const float alpha = (cov && dl != 0.0) ? (float)(dl / (double)accW) : 0.f;
+        ab[lin] = make_float2(alpha, alpha * iv);
+      }
+    }
+  }
+  if (target) {
+    const double t = block_sum<kFwdThreads>(lsum, red);
+    if (tid == 0) loss_part[lb] = t;
+  }
+}
+
+// --------------------------------------------------------------- forward f64
+struct __align__(16) Pair64 {
+  double l[9];
+  double mx, my, mz;
+  double amp, relax;
+  int box0, box1;
+  double _pad;
+};
+
+__global__ void __launch_bounds__(128)
+forward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict__ rec,
+                 const double* __restrict__ half_src, const int64_t* __restrict__ starts,
+                 const int32_t* __restrict__ gids, gsv_grid g, gsv_bricks k, double cut2,
+                 double eps_w, double* __restrict__ S, double* __restrict__ W,
+                 double* __restrict__ I, const float* __restrict__ target, int loss_kind,
+                 double inv_v, double2* __restrict__ ab, double* __restrict__ loss_part,
+                 const gsv_record32* __restrict__ rec32) {
+  constexpr int T = 128;
+  __shared__ Pair64 sp[T];
+  __shared__ double red[T / 32];
+  (void)half_src;
+  const int lb = blockIdx.x;
+  const int b = (int)slab_first(k) + lb;
+  const BrickGeom bg = brick_geom(b, g, k);
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  const int nvb = k.bdx * k.bdy * k.bdz;
+  const int tid = threadIdx.x;
+  double lsum = 0.0;
+  for (int vbase = 0; vbase < nvb; vbase += T) {
+    const int vl = vbase + tid;
+    const int lx = vl % k.bdx, ly = (vl / k.bdx) % k.bdy, lz = vl / (k.bdx * k.bdy);
+    const bool own = vl < nvb && lx < bg.ex && ly < bg.ey && lz < bg.ez;
+    const int ix = bg.x0 + lx, iy = bg.y0 + ly, iz = bg.z0 + lz;
+    const double px = add(g.ox, mul((double)ix, g.sx));
+    const double py = add(g.oy, mul((double)iy, g.sy));
+    const double pz = add(g.oz, mul((double)iz, g.sz));
+    double accS = 0.0, accW = 0.0;
+    for (int64_t cb = lbeg; cb < lend; cb += T) {
+      const int cnt = (int)min((int64_t)T, lend - cb);
+      __syncthreads();
+      if (tid < cnt) {
+        const int gid = gids[cb + tid];
+        const gsv_record64 r = rec[gid];
+        const gsv_record32 r32 = rec32[gid];
+        Pair64 p;
+#pragma unroll
+        for (int a = 0; a < 9; ++a) p.l[a] = r.l[a];
+        const double* m = pos + 3 * (int64_t)gid;
+        p.mx = m[0]; p.my = m[1]; p.mz = m[2];
+        p.amp = r.amp;
+        p.relax = r.relax;
+        int xl, xh, yl, yh, zl, zh;
+        sub_range(p.mx - bg.px, (double)r32.half[0], g.sx, bg.ex, xl, xh);
+        sub_range(p.my - bg.py, (double)r32.half[1], g.sy, bg.ey, yl, yh);
+        sub_range(p.mz - bg.pz, (double)r32.half[2], g.sz, bg.ez, zl, zh);
+        if (xl > xh || yl > yh || zl > zh) {
+          xl = 255; xh = 0;
+        }
+        p.box0 = (xl & 255) | ((xh & 255) << 8) | ((yl & 255) << 16) | ((yh & 255) << 24);
+        p.box1 = (zl & 255) | ((zh & 255) << 8);
+        p._pad = 0.0;
+        sp[tid] = p;
+      }
+      __syncthreads();
+      if (own) {
+        for (int j = 0; j < cnt; ++j) {
+          const Pair64& p = sp[j];
+          const int b0 = p.box0, b1 = p.box1;
+          if (lx < (b0 & 255) || lx > ((b0 >> 8) & 255) || ly < ((b0 >> 16) & 255) ||
+              ly > ((b0 >> 24) & 255) || lz < (b1 & 255) || lz > ((b1 >> 8) & 255))
+            continue;
+          const double dx = sub(px, p.mx), dy = sub(py, p.my), dz = sub(pz, p.mz);
+          const double v0 = add(add(mul(p.l[0], dx), mul(p.l[1], dy)), mul(p.l[2], dz));
+          const double v1 = add(add(mul(p.l[3], dx), mul(p.l[4], dy)), mul(p.l[5], dz));
+          const double v2 = add(add(mul(p.l[6], dx), mul(p.l[7], dy)), mul(p.l[8], dz));
+          const double d2 = add(add(mul(v0, v0), mul(v1, v1)), mul(v2, v2));
+          if (d2 <= cut2) {
+            const double w = mul(exp(mul(-0.5, d2)), p.relax);
+            accS = add(accS, mul(p.amp, w));
+            accW = add(accW, w);
+          }
+        }
+      }
+    }
+    if (own) {
+      const int64_t lin = (int64_t)ix + (int64_t)g.nx * (iy + (int64_t)g.ny * iz);
+      const bool cov = accW >= eps_w;
+      const double iv = cov ? __ddiv_rn(accS, accW) : 0.0;
+      S[lin] = accS;
+      W[lin] = accW;
+      I[lin] = iv;
+      if (target) {
+        const double d = iv - (double)target[lin];
+        double dl;
+        if (loss_kind == 0) {
+          lsum += fabs(d);
+          dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_v;
+        } else {
+          lsum += d * d;
+          dl = 2.0 * d * inv_v;
+        }
+        const double alpha = (cov && dl != 0.0) ? dl / accW : 0.0;
+        ab[lin] = make_double2(alpha, alpha * iv);
+      }
+    }
+  }
+  if (target) {
+    const double t = block_sum<T>(lsum, red);
+    if (tid == 0) loss_part[lb] = t;
+  }
+}
+
+// ------------------------------------------------------------- backward prep
+template <typename T, typename T2>
+__global__ void backward_prep_kernel(const T* __restrict__ W, const T* __restrict__ I,
+                                     const double* __restrict__ dldi, gsv_grid g,
+                                     int64_t v0, int64_t v1, double eps_w, T2* __restrict__ ab,
+                                     unsigned long long* bad) {
+  const int64_t lin = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (lin >= v1) return;
+  const double dl = dldi[lin];
+  if (!isfinite(dl)) atomicMin(bad, (unsigned long long)lin);
+  const double w = (double)W[lin];
+  T alpha = 0, beta = 0;
+  if (w >= eps_w && dl != 0.0 && isfinite(dl)) {
+    alpha = (T)(dl / w);
+    beta = (T)(dl * (double)I[lin] / w);
+  }
+  T2 o;
+  o.x = alpha;
+  o.y = beta;
+  ab[lin] = o;
+}
+
+// ------------------------------------------------------------- backward f32
+__global__ void __launch_bounds__(kBwdThreads)
+backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
+                  const double* __restrict__ ls, const double* __restrict__ rot,
+                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
+                  const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
+                  gsv_grid g, gsv_bricks k, float cut2, double cut2d,
+                  const float2* __restrict__ ab, float4* __restrict__ partials) {
+  const int lb = blockIdx.x;
+  const int b = (int)slab_first(k) + lb;
+  const BrickGeom bg = brick_geom(b, g, k);
+  const BrickXYZ bc = brick_xyz(b, k);
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
+  for (int64_t j = lbeg + threadIdx.x; j < lend; j += kBwdThreads) {
+    const int gid = gids[j];
+    const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+    const float4 q0 = r4[0], q1 = r4[1], q2 = r4[2], q3 = r4[3];
+    const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+    const float A = q2.y, r = q2.z;
+    const double* m = pos + 3 * (int64_t)gid;
+    const double cx = m[0] - bg.px, cy = m[1] - bg.py, cz = m[2] - bg.pz;  // mu - p_b0
+    int xl, xh, yl, yh, zl, zh;
+    sub_range(cx, (double)q2.w, g.sx, bg.ex, xl, xh);
+    sub_range(cy, (double)q3.x, g.sy, bg.ey, yl, yh);
+    sub_range(cz, (double)q3.y, g.sz, bg.ez, zl, zh);
+    const float c0 = (float)(-cx), c1 = (float)(-cy), c2 = (float)(-cz);
+    float umax = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float ua = fmaf(L[3 * a], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
+      umax = fmaxf(umax, fabsf(ua) + fabsf(L[3 * a] * fsx) * k.bdx +
+                             fabsf(L[3 * a + 1] * fsy) * k.bdy + fabsf(L[3 * a + 2] * fsz) * k.bdz);
+    }
+    const float guard = fmaxf(kGuardRel * cut2, kGuardMag * umax * (umax + 3.f));
+    float acc_a = 0.f, acc_r = 0.f, mu0 = 0.f, mu1 = 0.f, mu2 = 0.f;
+    float g00 = 0.f, g11 = 0.f, g22 = 0.f, g01 = 0.f, g02 = 0.f, g12 = 0.f;
+    for (int z = zl; z <= zh; ++z) {
+      const float dz = fmaf((float)z, fsz, c2);
+      for (int y = yl; y <= yh; ++y) {
+        const float dy = fmaf((float)y, fsy, c1);
+        const int64_t row = (int64_t)bg.x0 + (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
+        for (int x = xl; x <= xh; ++x) {
+          const float2 v_ab = __ldg(ab + row + x);
+          if (v_ab.x == 0.f) continue;
+          const float dx = fmaf((float)x, fsx, c0);
+          const float v0 = fmaf(L[0], dx, fmaf(L[1], dy, L[2] * dz));
+          const float v1 = fmaf(L[3], dx, fmaf(L[4], dy, L[5] * dz));
+          const float v2 = fmaf(L[6], dx, fmaf(L[7], dy, L[8] * dz));
+          const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+          if (d2 > cut2 + guard) continue;
+          if (d2 >= cut2 - guard &&
+              !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, pos, ls, rot, g, cut2d))
+            continue;
+          const float kern = __expf(-0.5f * d2);
+          const float w = kern * r;
+          acc_a = fmaf(w, v_ab.x, acc_a);
+          const float common = fmaf(A, v_ab.x, -v_ab.y);
+          acc_r = fmaf(common, kern, acc_r);
+          const float cw = common * w;
+          mu0 = fmaf(cw, fmaf(L[0], v0, fmaf(L[3], v1, L[6] * v2)), mu0);
+          mu1 = fmaf(cw, fmaf(L[1], v0, fmaf(L[4], v1, L[7] * v2)), mu1);
+          mu2 = fmaf(cw, fmaf(L[2], v0, fmaf(L[5], v1, L[8] * v2)), mu2);
+          const float h = -0.5f * cw;
+          const float hx = h * dx, hy = h * dy;
+          g00 = fmaf(hx, dx, g00);
+          g11 = fmaf(hy, dy, g11);
+          g22 = fmaf(h * dz, dz, g22);
+          g01 = fmaf(hx, dy, g01);
+          g02 = fmaf(hx, dz, g02);
+          g12 = fmaf(hy, dz, g12);
+        }
+      }
+    }
+    const GBox gb = unpack_box(box, gid);
+    const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
+    // A caller-built list may hold a pair the binning would not emit: skip it.
+    if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
+    const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+    float4* dst = partials + 3 * e;
+    dst[0] = make_float4(acc_a, acc_r, mu0, mu1);
+    dst[1] = make_float4(mu2, g00, g11, g22);
+    dst[2] = make_float4(g01, g02, g12, 0.f);
+  }
+}
+
+// ------------------------------------------------------------- backward f64
+__global__ void __launch_bounds__(kBwdThreads)
+backward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict__ rec,
+                  const gsv_record32* __restrict__ rec32, const int64_t* __restrict__ starts,
+                  const int32_t* __restrict__ gids, const int64_t* __restrict__ gstart,
+                  const int32_t* __restrict__ box, gsv_grid g, gsv_bricks k, double cut2,
+                  const double2* __restrict__ ab, double* __restrict__ partials) {
+  const int lb = blockIdx.x;
+  const int b = (int)slab_first(k) + lb;
+  const BrickGeom bg = brick_geom(b, g, k);
+  const BrickXYZ bc = brick_xyz(b, k);
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  for (int64_t j = lbeg + threadIdx.x; j < lend; j += kBwdThreads) {
+    const int gid = gids[j];
+    const gsv_record64 rc = rec[gid];
+    const gsv_record32 r32 = rec32[gid];
+    const double* L = rc.l;
+    const double A = rc.amp, r = rc.relax;
+    const double* m = pos + 3 * (int64_t)gid;
+    const double mx = m[0], my = m[1], mz = m[2];
+    int xl, xh, yl, yh, zl, zh;
+    sub_range(mx - bg.px, (double)r32.half[0], g.sx, bg.ex, xl, xh);
+    sub_range(my - bg.py, (double)r32.half[1], g.sy, bg.ey, yl, yh);
+    sub_range(mz - bg.pz, (double)r32.half[2], g.sz, bg.ez, zl, zh);
+    double acc_a = 0, acc_r = 0, mu0 = 0, mu1 = 0, mu2 = 0;
+    double g00 = 0, g11 = 0, g22 = 0, g01 = 0, g02 = 0, g12 = 0;
+    for (int z = zl; z <= zh; ++z) {
+      const int iz = bg.z0 + z;
+      const double dz = sub(add(g.oz, mul((double)iz, g.sz)), mz);
+      for (int y = yl; y <= yh; ++y) {
+        const int iy = bg.y0 + y;
+        const double dy = sub(add(g.oy, mul((double)iy, g.sy)), my);
+        const int64_t row = (int64_t)g.nx * (iy + (int64_t)g.ny * iz);
+        for (int x = xl; x <= xh; ++x) {
+          const int ix = bg.x0 + x;
+          const double2 v_ab = ab[row + ix];
+          if (v_ab.x == 0.0) continue;
+          const double dx = sub(add(g.ox, mul((double)ix, g.sx)), mx);
+          const double v0 = add(add(mul(L[0], dx), mul(L[1], dy)), mul(L[2], dz));
+          const double v1 = add(add(mul(L[3], dx), mul(L[4], dy)), mul(L[5], dz));
+          const double v2 = add(add(mul(L[6], dx), mul(L[7], dy)), mul(L[8], dz));
+          const double d2 = add(add(mul(v0, v0), mul(v1, v1)), mul(v2, v2));
+          if (d2 > cut2) continue;
+          const double kern = exp(-0.5 * d2);
+          const double w = kern * r;
+          acc_a += w * v_ab.x;
+          const double common = A * v_ab.x - v_ab.y;
+          acc_r += common * kern;
+          const double cw = common * w;
+          mu0 += cw * (L[0] * v0 + L[3] * v1 + L[6] * v2);
+          mu1 += cw * (L[1] * v0 + L[4] * v1 + L[7] * v2);
+          mu2 += cw * (L[2] * v0 + L[5] * v1 + L[8] * v2);
+          const double h = -0.5 * cw;
+          g00 += h * dx * dx;
+          g11 += h * dy * dy;
+          g22 += h * dz * dz;
+          g01 += h * dx * dy;
+          g02 += h * dx * dz;
+          g12 += h * dy * dz;
+        }
+      }
+    }
+    const GBox gb = unpack_box(box, gid);
+    const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
+    // A caller-built list may hold a pair the binning would not emit: skip it.
+    if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
+    const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+    double* dst = partials + 12 * e;
+    dst[0] = acc_a; dst[1] = acc_r; dst[2] = mu0; dst[3] = mu1; dst[4] = mu2;
+    dst[5] = g00; dst[6] = g11; dst[7] = g22; dst[8] = g01; dst[9] = g02; dst[10] = g12;
+    dst[11] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------ naive render
+// render_naive / _naive_kernel (render.py:84-110): every Gaussian at every
+// voxel, explicit Sigma^-1 = R diag(exp(-2 ls)) R^T quadratic form in f64.
+template <typename T>
+__global__ void __launch_bounds__(128)
+naive_kernel(const double* __restrict__ pos, const double* __restrict__ ls,
+             const double* __restrict__ rot, const double* __restrict__ ra,
+             const double* __restrict__ rr, int64_t n, int relax_enabled, gsv_grid g,
+             double cut2, double eps_w, T* __restrict__ I) {
+  constexpr int TB = 128;
+  __shared__ double sm[TB][16];
+  const int64_t nvox = (int64_t)g.nx * g.ny * g.nz;
+  const int64_t lin = blockIdx.x * (int64_t)TB + threadIdx.x;
+  const bool own = lin < nvox;
+  const int ix = (int)(lin % g.nx);
+  const int64_t rem = lin / g.nx;
+  const int iy = (int)(rem % g.ny), iz = (int)(rem / g.ny);
+  const double px = g.ox + ix * g.sx, py = g.oy + iy * g.sy, pz = g.oz + iz * g.sz;
+  T S = 0, Wt = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += TB) {
+    const int cnt = (int)min((int64_t)TB, n - t0);
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const int64_t i = t0 + threadIdx.x;
+      double R[9];
+      rotation_f64(rot + 4 * i, R);
+      const double iv[3] = {exp(-2.0 * ls[3 * i]), exp(-2.0 * ls[3 * i + 1]),
+                            exp(-2.0 * ls[3 * i + 2])};
+      double* o = sm[threadIdx.x];
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c)
+          o[3 * a + c] = R[3 * a] * iv[0] * R[3 * c] + R[3 * a + 1] * iv[1] * R[3 * c + 1] +
+                         R[3 * a + 2] * iv[2] * R[3 * c + 2];
+      o[9] = pos[3 * i];
+      o[10] = pos[3 * i + 1];
+      o[11] = pos[3 * i + 2];
+      o[12] = expit_f64(ra[i]);
+      o[13] = relax_enabled ? expit_f64(rr[i]) : 1.0;
+    }
+    __syncthreads();
+    if (own) {
+      for (int j = 0; j < cnt; ++j) {
+        const double* s = sm[j];
+        const double dx = sub(px, s[9]), dy = sub(py, s[10]), dz = sub(pz, s[11]);
+        const double d2 =
+            add(add(mul(dx, add(add(mul(s[0], dx), mul(s[1], dy)), mul(s[2], dz))),
+                    mul(dy, add(add(mul(s[3], dx), mul(s[4], dy)), mul(s[5], dz)))),
+                mul(dz, add(add(mul(s[6], dx), mul(s[7], dy)), mul(s[8], dz))));
+        if (d2 <= cut2) {
+          const double w = exp(-0.5 * d2) * s[13];
+          S = (T)((double)S + s[12] * w);
+          Wt = (T)((double)Wt + w);
+        }
+      }
+    }
+  }
+  if (own) I[lin] = ((double)Wt >= eps_w) ? (T)((double)S / (double)Wt) : (T)0;
+}
+
+}  // namespace
+}  // namespace gsv
+
+using namespace gsv;
+
+extern "C" {
+
+int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_record64* rec64,
+                const double* log_scales, const double* rotations, const int64_t* starts,
+                const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
+                double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
+                const float* target, int loss_kind, double inv_v, float* ab,
+                double* loss_part, void* stream) {
+  if (int s = validate_grid_bricks(grid, bricks)) return s;
+  GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
+  GSV_REQUIRE(precision == 0 || rec64 != nullptr, "f64 forward needs rec64");
+  GSV_REQUIRE(target == nullptr || (ab != nullptr && loss_part != nullptr),
+              "fused loss needs ab and loss_part");
+  GSV_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (l1) or 1 (l2)");
+  const int64_t nb = slab_bricks(*bricks);
+  if (nb == 0) return GSV_OK;
+  const double cut2d = cutoff_sigma * cutoff_sigma;
+  cudaStream_t s = as_stream(stream);
+  if (precision == 0) {
+    forward32_kernel<<<(unsigned)nb, kFwdThreads, 0, s>>>(
+        positions, rec32, log_scales, rotations, starts, gids, *grid, *bricks, (float)cut2d,
+        cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, inv_v,
+        (float2*)ab, loss_part);
+    GSV_CHECK_LAUNCH("forward32_kernel");
+  } else {
+    forward64_kernel<<<(unsigned)nb, 128, 0, s>>>(
+        positions, rec64, nullptr, starts, gids, *grid, *bricks, cut2d, eps_w, (double*)S,
+        (double*)W, (double*)I, target, loss_kind, inv_v, (double2*)ab, loss_part, rec32);
+    GSV_CHECK_LAUNCH("forward64_kernel");
+  }
+  return GSV_OK;
+}
+
+int gsv_backward_prep(const void* W, const void* I, const double* dldi, const gsv_grid* grid,
+                      const gsv_bricks* bricks, double eps_w, int precision, void* ab,
+                      int64_t* bad, void* stream) {
+  if (int s = validate_grid_bricks(grid, bricks)) return s;
+  GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(bad, 0x7F, sizeof(int64_t), s);
+  if (e != cudaSuccess) return cuda_status(e, "memset bad");
+  // The slab's voxels: whole z-layers [bz0*bdz, min(bz1*bdz, nz)).
+  const int64_t plane = (int64_t)grid->nx * grid->ny;
+  const int64_t v0 = plane * ((int64_t)bricks->bz0 * bricks->bdz);
+  const int64_t zend = (int64_t)bricks->bz1 * bricks->bdz;
+  const int64_t v1 = plane * (zend < grid->nz ? zend : (int64_t)grid->nz);
+  if (v1 <= v0) return GSV_OK;
+  const unsigned blocks = (unsigned)((v1 - v0 + 255) / 256);
+  if (precision == 0)
+    backward_prep_kernel<float, float2><<<blocks, 256, 0, s>>>(
+        (const float*)W, (const float*)I, dldi, *grid, v0, v1, eps_w, (float2*)ab,
+        (unsigned long long*)bad);
+  else
+    backward_prep_kernel<double, double2><<<blocks, 256, 0, s>>>(
+        (const double*)W, (const double*)I, dldi, *grid, v0, v1, eps_w, (double2*)ab,
+        (unsigned long long*)bad);
+  GSV_CHECK_LAUNCH("backward_prep_kernel");
+  return GSV_OK;
+}
+
+int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_record64* rec64,
+                 const double* log_scales, const double* rotations, const int64_t* starts,
+                 const int32_t* gids, const int64_t* gstart, const int32_t* box,
+                 const gsv_grid* grid, const gsv_bricks* bricks, double cutoff_sigma,
+                 int precision, const void* ab, void* partials, void* stream) {
+  if (int s = validate_grid_bricks(grid, bricks)) return s;
+  GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
+  GSV_REQUIRE(precision == 0 || rec64 != nullptr, "f64 backward needs rec64");
+  const int64_t nb = slab_bricks(*bricks);
+  if (nb == 0) return GSV_OK;
+  const double cut2d = cutoff_sigma * cutoff_sigma;
+  cudaStream_t s = as_stream(stream);
+  if (precision == 0) {
+    backward32_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(
+        positions, rec32, log_scales, rotations, starts, gids, gstart, box, *grid, *bricks,
+        (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
+    GSV_CHECK_LAUNCH("backward32_kernel");
+  } else {
+    backward64_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(
+        positions, rec64, rec32, starts, gids, gstart, box, *grid, *bricks, cut2d,
+        (const double2*)ab, (double*)partials);
+    GSV_CHECK_LAUNCH("backward64_kernel");
+  }
+  return GSV_OK;
+}
+
+int gsv_render_naive(const double* positions, const double* log_scales,
+                     const double* rotations, const double* raw_amplitude,
+                     const double* raw_relax, int64_t n, int relax_enabled,
+                     const gsv_grid* grid, double cutoff_sigma, double eps_w, int precision,
+                     void* I, void* stream) {
+  GSV_REQUIRE(grid && grid->nx >= 1 && grid->ny >= 1 && grid->nz >= 1, "bad grid");
+  GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
+  const int64_t nvox = (int64_t)grid->nx * grid->ny * grid->nz;
+  const double cut2 = cutoff_sigma * cutoff_sigma;
+  const unsigned blocks = (unsigned)((nvox + 127) / 128);
+  cudaStream_t s = as_stream(stream);
+  if (precision == 0)
+    naive_kernel<float><<<blocks, 128, 0, s>>>(positions, log_scales, rotations,
+                                                raw_amplitude, raw_relax, n, relax_enabled,
+                                                *grid, cut2, eps_w, (float*)I);
+  else
+    naive_kernel<double><<<blocks, 128, 0, s>>>(positions, log_scales, rotations,
+                                                 raw_amplitude, raw_relax, n, relax_enabled,
+                                                 *grid, cut2, eps_w, (double*)I);
+  GSV_CHECK_LAUNCH("naive_kernel");
+  return GSV_OK;
+}
+
+}  // extern "C"

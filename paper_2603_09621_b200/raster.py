@@ -1,0 +1,406 @@
+"""Brick rasterizer: the drop-in API of gsvol/raster.py on B200 kernels.
+
+Same public names, signatures, dataclass fields and exceptions as
+raster.py:55-570; every computation runs in libgsv_b200.so (include/gsv.h):
+
+  build_brick_index  gsv_preprocess -> gsv_bin_scan -> gsv_bin_fill
+                     (fused f64 AABB + count, CUB scan, emit + CUB stable radix
+                     sort + CSR starts); bit-exact lists (raster.py:148-217)
+  forward            gsv_preprocess (records) -> gsv_forward (CTA per brick)
+  backward           gsv_backward_prep -> gsv_backward (pair partials) ->
+                     gsv_merge (ascending brick order) -> gsv_chain_rule
+
+Extensions (keyword-only, defaults keep the reference behaviour):
+``slab=(bz0, bz1)`` restricts binning/render/backward to a contiguous range
+of brick layers -- the z-slab sharding unit of the multi-GPU path.
+
+Arrays are torch tensors on the field's CUDA device.  ``BrickIndex.gids`` is
+int32 (the reference uses int64; values are identical), ``starts`` int64.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import NumericalError, StaleIndexError
+from .field import GaussianField
+from .render import RenderOptions
+from .volume import GridSpec, Volume
+
+DEFAULT_BRICK_DIMS = (8, 8, 4)
+
+_WORKERS = [8]
+
+
+def set_worker_count(n: int) -> None:
+    """Kept for API parity (raster.py:55-59); the GPU engine has no thread pool."""
+    if n < 1:
+        raise ValueError("worker count must be >= 1")
+    _WORKERS[0] = int(n)
+
+
+def worker_count() -> int:
+    return _WORKERS[0]
+
+
+def _as_device_tensor(a, dtype, device):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.dtype(str(dtype).split(".")[-1]))).to(device)
+
+
+@dataclass
+class _Aux:
+    """Per-Gaussian products of preprocessing kept with an index we built."""
+    rec32: torch.Tensor
+    rec64: torch.Tensor | None
+    counts: torch.Tensor
+    box: torch.Tensor
+    gstart: torch.Tensor
+    field_version: int
+    canonical: bool = True
+
+
+@dataclass(frozen=True)
+class BrickIndex:
+    """CSR layout of per-brick Gaussian lists (raster.py:66-112).
+
+    gids[starts[b]:starts[b+1]] are the Gaussians binned to brick b,
+    ascending; bricks x-fastest.  With ``slab=(bz0, bz1)`` the index covers
+    only brick layers [bz0, bz1) and ``starts`` has one entry per slab brick.
+    """
+    grid: GridSpec
+    brick_dims: tuple
+    brick_grid: tuple
+    starts: object
+    gids: object
+    field_version: int
+    field_count: int
+    cutoff_sigma: float
+    slab: tuple | None = None
+    _aux: object = dc_field(default=None, compare=False, repr=False)
+
+    def __post_init__(self):
+        dev = self.starts.device if isinstance(self.starts, torch.Tensor) else None
+        if dev is None and isinstance(self.gids, torch.Tensor):
+            dev = self.gids.device
+        if dev is None:
+            dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
+                else torch.device("cpu")
+        object.__setattr__(self, "starts", _as_device_tensor(self.starts, torch.int64, dev))
+        object.__setattr__(self, "gids", _as_device_tensor(self.gids, torch.int32, dev))
+        object.__setattr__(self, "brick_dims", tuple(int(b) for b in self.brick_dims))
+        object.__setattr__(self, "brick_grid", tuple(int(b) for b in self.brick_grid))
+
+    @property
+    def brick_count(self) -> int:
+        return int(self.starts.shape[0]) - 1
+
+    @property
+    def pair_count(self) -> int:
+        return int(self.gids.shape[0])
+
+    @property
+    def slab_range(self) -> tuple:
+        return self.slab if self.slab is not None else (0, self.brick_grid[2])
+
+    def lists_sorted(self) -> bool:
+        """True when every brick's list is ascending (canonical order)."""
+        if self._aux is not None and self._aux.canonical:
+            return True
+        if self.pair_count == 0:
+            return True
+        lib = _lib.lib()
+        flag = torch.zeros(1, dtype=torch.int32, device=self.gids.device)
+        _lib.check(lib.gsv_lists_unsorted(self.starts.data_ptr(), self.gids.data_ptr(),
+                                          self.brick_count, self.pair_count, flag.data_ptr(),
+                                          _lib.stream_ptr()), "lists_unsorted")
+        return int(flag.item()) == 0
+
+    def canonicalized(self) -> "BrickIndex":
+        """An index with every brick list sorted ascending (segmented GPU sort)."""
+        if self.lists_sorted():
+            return self
+        lib = _lib.lib()
+        import ctypes
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(lib.gsv_canonicalize_workspace(self.pair_count, self.brick_count,
+                                                  ctypes.byref(nbytes)), "canonicalize_workspace")
+        ws = _lib.workspace(nbytes.value, self.gids.device, "canon")
+        out = torch.empty_like(self.gids)
+        _lib.check(lib.gsv_canonicalize(self.starts.data_ptr(), self.gids.data_ptr(),
+                                        out.data_ptr(), self.brick_count, self.pair_count,
+                                        ws.data_ptr(), ws.numel(), _lib.stream_ptr()),
+                   "canonicalize")
+        return BrickIndex(self.grid, self.brick_dims, self.brick_grid, self.starts, out,
+                          self.field_version, self.field_count, self.cutoff_sigma, self.slab,
+                          None)
+
+
+@dataclass(frozen=True)
+class RenderCache:
+    """Forward products: per-voxel numerator, denominator, render (raster.py:115-125)."""
+    grid: GridSpec
+    S: torch.Tensor
+    W: torch.Tensor
+    I: torch.Tensor
+    field_version: int
+
+    def volume(self) -> Volume:
+        return Volume.from_linear(self.grid, self.I)
+
+
+@dataclass
+class GradientBuffer:
+    """Per-Gaussian gradients w.r.t. the raw parameters (raster.py:128-145)."""
+    raw_amplitude: torch.Tensor
+    raw_relax: torch.Tensor
+    positions: torch.Tensor
+    log_scales: torch.Tensor
+    rotations: torch.Tensor
+
+    @classmethod
+    def zeros(cls, n: int, device=None) -> "GradientBuffer":
+        dev = device if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else torch.device("cpu"))
+        z = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev)  # noqa: E731
+        return cls(z(n), z(n), z(n, 3), z(n, 3), z(n, 4))
+
+    @classmethod
+    def empty(cls, n: int, device) -> "GradientBuffer":
+        e = lambda *s: torch.empty(*s, dtype=torch.float64, device=device)  # noqa: E731
+        return cls(e(n), e(n), e(n, 3), e(n, 3), e(n, 4))
+
+    def tensors(self):
+        return (self.raw_amplitude, self.raw_relax, self.positions, self.log_scales,
+                self.rotations)
+
+    def all_finite(self) -> bool:
+        return all(bool(torch.isfinite(a).all()) for a in self.tensors())
+
+
+# ----------------------------------------------------------------- binning
+def _preprocess(f: GaussianField, grid: GridSpec, cutoff_sigma: float, brick_dims, slab,
+                want64: bool):
+    lib = _lib.lib()
+    n, dev = f.count, f.device
+    rec32 = torch.empty((n, 16), dtype=torch.float32, device=dev)
+    rec64 = torch.empty((n, 12), dtype=torch.float64, device=dev) if want64 else None
+    counts = torch.empty(n, dtype=torch.int32, device=dev)
+    box = torch.empty((n, 4), dtype=torch.int32, device=dev)
+    _lib.check(lib.gsv_preprocess(
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), n, int(f.relax_enabled),
+        float(cutoff_sigma), _lib.make_grid(grid), _lib.make_bricks(grid, brick_dims, slab),
+        rec32.data_ptr(), _lib.ptr(rec64), counts.data_ptr(), box.data_ptr(),
+        _lib.stream_ptr()), "preprocess")
+    return rec32, rec64, counts, box
+
+
+def _scan(counts: torch.Tensor, nbricks: int) -> torch.Tensor:
+    import ctypes
+    lib = _lib.lib()
+    n = counts.shape[0]
+    gstart = torch.empty(n + 1, dtype=torch.int64, device=counts.device)
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.gsv_bin_workspace(n, 1, nbricks, ctypes.byref(nbytes)), "bin_workspace")
+    ws = _lib.workspace(nbytes.value, counts.device, "bin")
+    _lib.check(lib.gsv_bin_scan(counts.data_ptr(), n, gstart.data_ptr(), ws.data_ptr(),
+                                ws.numel(), _lib.stream_ptr()), "bin_scan")
+    return gstart
+
+
+def _fill(counts, box, gstart, pairs: int, bricks, nbricks: int):
+    import ctypes
+    lib = _lib.lib()
+    dev = counts.device
+    n = counts.shape[0]
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.gsv_bin_workspace(n, max(pairs, 1), nbricks, ctypes.byref(nbytes)),
+               "bin_workspace")
+    ws = _lib.workspace(nbytes.value, dev, "bin")
+    keys_tmp = torch.empty(max(pairs, 1), dtype=torch.int32, device=dev)
+    vals_tmp = torch.empty(max(pairs, 1), dtype=torch.int32, device=dev)
+    keys_out = torch.empty(max(pairs, 1), dtype=torch.int32, device=dev)
+    gids = torch.empty(pairs, dtype=torch.int32, device=dev)
+    starts = torch.empty(nbricks + 1, dtype=torch.int64, device=dev)
+    _lib.check(lib.gsv_bin_fill(counts.data_ptr(), box.data_ptr(), gstart.data_ptr(), n, pairs,
+                                bricks, keys_tmp.data_ptr(), vals_tmp.data_ptr(),
+                                keys_out.data_ptr(), gids.data_ptr() if pairs else keys_out.data_ptr(),
+                                starts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr()),
+               "bin_fill")
+    return starts, gids
+
+
+def build_brick_index(f: GaussianField, grid: GridSpec, opts: RenderOptions = RenderOptions(),
+                      brick_dims=DEFAULT_BRICK_DIMS, *, slab=None) -> BrickIndex:
+    """Conservative Gaussian-to-brick binning via AABB overlap (raster.py:148-217).
+
+    Lists are bit-identical to the reference's (same f64 bounds, same
+    gid-major emission, stable sort by brick id).
+    """
+    if any(d < 1 for d in brick_dims):
+        raise ValueError(f"brick_dims must be positive, got {brick_dims}")
+    brick_dims = tuple(int(d) for d in brick_dims)
+    bricks = _lib.make_bricks(grid, brick_dims, slab)
+    nbricks = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
+    rec32, rec64, counts, box = _preprocess(f, grid, opts.cutoff_sigma, brick_dims, slab,
+                                            opts.precision == "f64")
+    gstart = _scan(counts, nbricks)
+    pairs = int(gstart[-1].item())  # the one host read binning needs (buffer sizing)
+    starts, gids = _fill(counts, box, gstart, pairs, bricks, nbricks)
+    aux = _Aux(rec32, rec64, counts, box, gstart, f.version, True)
+    return BrickIndex(grid, brick_dims, (bricks.bgx, bricks.bgy, bricks.bgz), starts, gids,
+                      f.version, f.count, opts.cutoff_sigma, slab, aux)
+
+
+def _check_index(f: GaussianField, grid: GridSpec, idx: BrickIndex, opts: RenderOptions) -> None:
+    """Staleness guards, same messages as raster.py:220-230."""
+    if idx.field_version != f.version or idx.field_count != f.count:
+        raise StaleIndexError(
+            f"rebuild brick index: built for field version {idx.field_version}, "
+            f"field is at version {f.version}")
+    if idx.grid != grid:
+        raise StaleIndexError("rebuild brick index: grid changed")
+    if idx.cutoff_sigma != opts.cutoff_sigma:
+        raise StaleIndexError("rebuild brick index: cutoff_sigma changed")
+
+
+def _records(f, grid, idx: BrickIndex, opts: RenderOptions):
+    """rec32 (and rec64 for f64) for the current field state."""
+    aux = idx._aux
+    want64 = opts.precision == "f64"
+    if aux is not None and aux.field_version == f.version and (aux.rec64 is not None or not want64):
+        return aux.rec32, aux.rec64
+    rec32, rec64, _, _ = _preprocess(f, grid, opts.cutoff_sigma, idx.brick_dims, idx.slab, want64)
+    return rec32, rec64
+
+
+# ----------------------------------------------------------------- forward
+def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_kind=0,
+                  ab=None, loss_part=None):
+    lib = _lib.lib()
+    _lib.check(lib.gsv_forward(
+        f.positions.data_ptr(), rec32.data_ptr(), _lib.ptr(rec64), f.log_scales.data_ptr(),
+        f.rotations.data_ptr(), idx.starts.data_ptr(), idx.gids.data_ptr(),
+        _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
+        float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
+        S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
+        1.0 / grid.num_voxels, _lib.ptr(ab), _lib.ptr(loss_part), _lib.stream_ptr()), "forward")
+
+
+def forward(f: GaussianField, grid: GridSpec, idx: BrickIndex,
+            opts: RenderOptions = RenderOptions()) -> RenderCache:
+    """Brick-parallel render (raster.py:296-319); equals render_naive up to
+    accumulation noise.  Output arrays are linear x-fastest, opts' dtype."""
+    _check_index(f, grid, idx, opts)
+    if opts.deterministic:
+        idx = idx.canonicalized()
+    rec32, rec64 = _records(f, grid, idx, opts)
+    nvox = grid.num_voxels
+    dt = opts.torch_dtype
+    alloc = torch.zeros if idx.slab is not None else torch.empty
+    S = alloc(nvox, dtype=dt, device=f.device)
+    W = alloc(nvox, dtype=dt, device=f.device)
+    I = alloc(nvox, dtype=dt, device=f.device)
+    _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I)
+    return RenderCache(grid, S, W, I, f.version)
+
+
+# ----------------------------------------------------------------- backward
+def _emission_layout(f, grid, idx: BrickIndex, opts: RenderOptions):
+    """(gstart, box, trusted): the pair slots the backward writes into."""
+    aux = idx._aux
+    if aux is not None and aux.field_version == f.version:
+        return aux.gstart, aux.box, True
+    _, _, counts, box = _preprocess(f, grid, opts.cutoff_sigma, idx.brick_dims, idx.slab, False)
+    b = _lib.make_bricks(grid, idx.brick_dims, idx.slab)
+    gstart = _scan(counts, b.bgx * b.bgy * (b.bz1 - b.bz0))
+    return gstart, box, False
+
+
+def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: bool):
+    lib = _lib.lib()
+    n = f.count
+    pdt = opts.torch_dtype
+    npairs = int(gstart[-1].item()) if not trusted else idx.pair_count
+    alloc = torch.empty if trusted else torch.zeros
+    partials = alloc((max(npairs, 1), 12), dtype=pdt, device=f.device)
+    _lib.check(lib.gsv_backward(
+        f.positions.data_ptr(), rec32.data_ptr(), _lib.ptr(rec64), f.log_scales.data_ptr(),
+        f.rotations.data_ptr(), idx.starts.data_ptr(), idx.gids.data_ptr(), gstart.data_ptr(),
+        box.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
+        float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), partials.data_ptr(),
+        _lib.stream_ptr()), "backward")
+    gsum = torch.empty((n, 12), dtype=torch.float64, device=f.device)
+    _lib.check(lib.gsv_merge(partials.data_ptr(), gstart.data_ptr(), n, opts.precision_code,
+                             gsum.data_ptr(), _lib.stream_ptr()), "merge")
+    return gsum
+
+
+def _chain_rule(f: GaussianField, gsum: torch.Tensor) -> GradientBuffer:
+    lib = _lib.lib()
+    out = GradientBuffer.empty(f.count, f.device)
+    _lib.check(lib.gsv_chain_rule(
+        gsum.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), f.count, int(f.relax_enabled),
+        out.raw_amplitude.data_ptr(), out.raw_relax.data_ptr(), out.positions.data_ptr(),
+        out.log_scales.data_ptr(), out.rotations.data_ptr(), _lib.stream_ptr()), "chain_rule")
+    return out
+
+
+def backward(f: GaussianField, grid: GridSpec, idx: BrickIndex, cache: RenderCache, dL_dI,
+             opts: RenderOptions = RenderOptions()) -> GradientBuffer:
+    """Analytic gradients through the normalized render (raster.py:470-549).
+
+    dL_dI: per-voxel upstream gradient, linear x-fastest (numpy or torch).
+    Gradients are w.r.t. the raw stored parameters; quaternion gradients are
+    ambient (4-d).
+    """
+    _check_index(f, grid, idx, opts)
+    if cache.field_version != f.version:
+        raise StaleIndexError("rebuild brick index: cache is stale")
+    if opts.deterministic:
+        idx = idx.canonicalized()
+    dl = _as_device_tensor(dL_dI, torch.float64, f.device).reshape(-1)
+    nvox = grid.num_voxels
+    if dl.shape[0] != nvox:
+        raise ValueError(f"dL_dI has {dl.shape[0]} entries, grid has {nvox} voxels")
+    lib = _lib.lib()
+    pdt = opts.torch_dtype
+    ab = torch.zeros((nvox, 2), dtype=pdt, device=f.device)
+    bad = torch.empty(1, dtype=torch.int64, device=f.device)
+    _lib.check(lib.gsv_backward_prep(
+        cache.W.to(pdt).data_ptr() if cache.W.dtype != pdt else cache.W.data_ptr(),
+        cache.I.to(pdt).data_ptr() if cache.I.dtype != pdt else cache.I.data_ptr(),
+        dl.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
+        float(opts.epsilon_w), opts.precision_code, ab.data_ptr(), bad.data_ptr(),
+        _lib.stream_ptr()), "backward_prep")
+    k = int(bad.item())
+    if k < nvox:
+        raise NumericalError(f"non-finite dL_dI at voxel index {k}")
+    rec32, rec64 = _records(f, grid, idx, opts)
+    gstart, box, trusted = _emission_layout(f, grid, idx, opts)
+    gsum = _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted)
+    return _chain_rule(f, gsum)
+
+
+def merge_gradients(partials) -> GradientBuffer:
+    """Sum per-brick GradientBuffers in ascending brick-index order (raster.py:552-570)."""
+    items = sorted(partials, key=lambda kv: kv[0])
+    if not items:
+        raise ValueError("no partials to merge")
+    first = items[0][1]
+    n = first.raw_amplitude.shape[0]
+    dev = first.raw_amplitude.device if isinstance(first.raw_amplitude, torch.Tensor) else None
+    out = GradientBuffer.zeros(n, device=dev)
+    for _, buf in items:
+        for dst, src in zip(out.tensors(), buf.tensors()):
+            dst += src if isinstance(src, torch.Tensor) else torch.as_tensor(src, device=dst.device)
+    return out

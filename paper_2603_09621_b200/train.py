@@ -1,0 +1,116 @@
+"""The fused training step: one iteration of fit() (optimize.py:171-184).
+
+  forward(f):  build_brick_index -> gsv_forward with the L1/L2 loss fused into
+               the epilogue (per-voxel backward inputs {dL/dI / W, dL/dI I / W}
+               written in the same pass) -> per-brick loss partials ->
+               gsv_sum.  No separate loss kernel, no dL/dI round trip.
+  backward(f): gsv_backward (pair partials at their gid-major emission slots)
+               -> gsv_merge (ascending brick order) -> [allreduce of the
+               N x 12 partial sums, the only collective, when sharded] ->
+               gsv_chain_rule.
+
+Sharding: with ``slab=(bz0, bz1)`` a rank bins, renders and
+back-propagates only its contiguous range of brick layers; the per-Gaussian
+merged partials (and the loss, carried in the spare 12th column) are summed
+across ranks by one NCCL all_reduce, after which every rank applies the same
+chain rule and Adam step, so parameters stay replicated.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .field import GaussianField
+from .raster import (BrickIndex, GradientBuffer, RenderCache, _chain_rule, _forward_into,
+                     _pair_partials, build_brick_index)
+from .render import RenderOptions
+from .volume import Volume
+
+LOSS_KINDS = {"l1": 0, "l2": 1}
+
+
+@dataclass
+class StepOutput:
+    idx: BrickIndex
+    cache: RenderCache
+    ab: torch.Tensor
+    loss_sum: torch.Tensor     # (1,) float64 on device: sum of |I-T| (l1) or (I-T)^2
+    nvox: int
+    reduced: bool = False
+
+    def loss(self) -> float:
+        """Mean loss as a Python float (one 8-byte device->host read).  When
+        sharded, valid after TrainStep.backward (the loss rides its all_reduce)."""
+        if not self.reduced:
+            raise RuntimeError("sharded loss is only global after backward()")
+        return float(self.loss_sum.item()) / self.nvox
+
+
+class TrainStep:
+    """Reusable fused train step bound to one target volume and options."""
+
+    def __init__(self, target: Volume, opts: RenderOptions = RenderOptions(),
+                 brick_dims=(8, 8, 4), loss: str = "l1", slab=None, process_group=None,
+                 world_size: int = 1):
+        if loss not in LOSS_KINDS:
+            raise ValueError(f"unknown loss kind {loss!r}")
+        self.grid = target.grid
+        lin = target.linear()
+        if lin.device.type != "cuda":
+            lin = lin.to(torch.device("cuda", torch.cuda.current_device()))
+        self.target = lin.to(torch.float32).contiguous()
+        self.opts = opts
+        self.brick_dims = tuple(brick_dims)
+        self.loss_kind = LOSS_KINDS[loss]
+        self.slab = slab
+        self.group = process_group
+        self.world_size = world_size
+
+    def set_target(self, target_linear: torch.Tensor) -> None:
+        """Swap the target buffer (e.g. after a host->device copy)."""
+        self.target = target_linear
+
+    def forward(self, f: GaussianField) -> StepOutput:
+        lib = _lib.lib()
+        grid, opts = self.grid, self.opts
+        idx = build_brick_index(f, grid, opts, self.brick_dims, slab=self.slab)
+        aux = idx._aux
+        nvox = grid.num_voxels
+        dt = opts.torch_dtype
+        S = torch.empty(nvox, dtype=dt, device=f.device)
+        W = torch.empty(nvox, dtype=dt, device=f.device)
+        I = torch.empty(nvox, dtype=dt, device=f.device)
+        ab = torch.empty((nvox, 2), dtype=dt if opts.precision == "f64" else torch.float32,
+                         device=f.device)
+        nb = max(idx.brick_count, 1)
+        loss_part = torch.zeros(nb, dtype=torch.float64, device=f.device)
+        _forward_into(f, grid, idx, opts, aux.rec32, aux.rec64, S, W, I, target=self.target,
+                      loss_kind=self.loss_kind, ab=ab, loss_part=loss_part)
+        loss_sum = torch.empty(1, dtype=torch.float64, device=f.device)
+        _lib.check(lib.gsv_sum(loss_part.data_ptr(), idx.brick_count, loss_sum.data_ptr(),
+                               _lib.stream_ptr()), "sum")
+        return StepOutput(idx, RenderCache(grid, S, W, I, f.version), ab, loss_sum, nvox,
+                          reduced=not self.sharded)
+
+    @property
+    def sharded(self) -> bool:
+        return self.group is not None and self.world_size > 1
+
+    def backward(self, f: GaussianField, out: StepOutput) -> GradientBuffer:
+        idx = out.idx
+        aux = idx._aux
+        gsum = _pair_partials(f, self.grid, idx, self.opts, aux.rec32, aux.rec64, out.ab,
+                              aux.gstart, aux.box, True)
+        if self.sharded:
+            # One collective per step: the merged per-Gaussian partials, with
+            # this rank's loss partial riding in the spare 12th column.
+            import torch.distributed as dist
+            gsum[0, 11] = out.loss_sum[0]
+            dist.all_reduce(gsum, group=self.group)
+            out.loss_sum.copy_(gsum[0, 11:12])
+            gsum[0, 11] = 0.0
+            out.reduced = True
+        return _chain_rule(f, gsum)

@@ -1,0 +1,202 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (the reference is importable only here):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/nb_golden \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz / *.json.  Every array the CUDA path must match
+bit-exactly is stored as a sha256 (tiny); tolerance-compared arrays are stored
+as float32 where small.  The synthetic inputs are rebuilt with this repo's
+host restatement (paper_2603_09621_b200.synth) and checked against the
+reference's own generator, so the GPU box (which has no reference) rebuilds
+identical inputs.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import platform
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+
+import gsvol  # noqa: E402  (the reference)
+from gsvol import (GridSpec, InitConfig, RenderOptions, backward, build_brick_index,  # noqa: E402
+                   forward, init_from_volume, loss_and_grad, random_field)
+from gsvol.phantom import generate_phantom, random_phantom  # noqa: E402
+from gsvol.volume import grid_covering_extent, resample_trilinear  # noqa: E402
+
+from paper_2603_09621_b200 import synth  # noqa: E402
+from paper_2603_09621_b200.field import random_field_arrays  # noqa: E402
+
+sha = synth.sha256
+F = ("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax")
+G = ("raw_amplitude", "raw_relax", "positions", "log_scales", "rotations")
+
+SWEEP_GRIDS = [((8, 8, 8), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0)),
+               ((16, 16, 16), (0.7, 1.0, 1.3), (-2.0, 0.0, 1.0)),
+               ((32, 24, 16), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0)),
+               ((32, 32, 32), (0.5, 0.5, 0.5), (1.0, 1.0, 1.0)),
+               ((24, 24, 24), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))]
+
+
+def versions():
+    import numba
+    import scipy
+    return {"python": platform.python_version(), "numpy": np.__version__,
+            "scipy": scipy.__version__, "numba": numba.__version__,
+            "reference": "gsvol " + gsvol.__version__, "machine": platform.machine()}
+
+
+def field_sha(f):
+    return sha(*(getattr(f, k) for k in F))
+
+
+def sweep():
+    """test_acceptance.py:40-66 cases x precisions x brick dims: reference hashes."""
+    out = []
+    for n in (1, 10, 100, 1000):
+        for i, (dims, sp, org) in enumerate(SWEEP_GRIDS):
+            grid = GridSpec(dims, sp, org)
+            seed = 100 * n + i
+            f = random_field(n, grid, seed=seed, scale_lo=0.4, scale_hi=2.0)
+            mine = random_field_arrays(n, grid, seed, 0.4, 2.0)
+            assert sha(*mine) == field_sha(f), "random_field restatement differs"
+            dl = np.random.default_rng(5).normal(size=grid.num_voxels)
+            for bd in ((8, 8, 4), (8, 8, 8), (4, 4, 4)):
+                for prec in ("f32", "f64"):
+                    opts = RenderOptions(precision=prec)
+                    idx = build_brick_index(f, grid, opts, bd)
+                    c = forward(f, grid, idx, opts)
+                    gr = backward(f, grid, idx, c, dl, opts)
+                    out.append({"n": n, "grid": i, "seed": seed, "brick_dims": bd,
+                                "precision": prec, "pairs": idx.pair_count,
+                                "starts": sha(idx.starts), "gids": sha(idx.gids),
+                                "S": sha(c.S), "W": sha(c.W), "I": sha(c.I),
+                                "grads": sha(*(getattr(gr, k) for k in G)),
+                                "I_sum": float(np.sum(c.I, dtype=np.float64))})
+    return out
+
+
+def problem(cfg_id):
+    cfg = synth.CONFIGS[cfg_id]
+    hr_grid = GridSpec(cfg.hr_dims, (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    hr = generate_phantom(random_phantom("ellipsoids", hr_grid, seed=11), hr_grid,
+                          smooth_sigma=0.7)
+    lr = resample_trilinear(hr, grid_covering_extent(hr_grid, cfg.lr_dims))
+    f = init_from_volume(lr, InitConfig(background_threshold=0.0))
+    mine = synth.make_problem(cfg)
+    assert sha(mine["hr"]) == sha(hr.data), "phantom restatement differs"
+    assert sha(mine["lr"]) == sha(lr.data), "degrade restatement differs"
+    assert (mine["lr_grid"].dims, mine["lr_grid"].spacing, mine["lr_grid"].origin) == (lr.grid.dims, lr.grid.spacing, lr.grid.origin)
+    if cfg.jitter:
+        arrs = mine["field"]
+        f = gsvol.GaussianField(*arrs)
+    assert sha(*mine["field"]) == field_sha(f), "init restatement differs"
+    return cfg, hr, lr, f, mine
+
+
+def config1():
+    cfg, hr, lr, f, mine = problem(1)
+    opts = RenderOptions()
+    out = {}
+    idx = build_brick_index(f, lr.grid, opts)
+    c = forward(f, lr.grid, idx, opts)
+    loss, dl = loss_and_grad(c.volume(), lr, "l1")
+    gr = backward(f, lr.grid, idx, c, dl, opts)
+    idx_hr = build_brick_index(f, hr.grid, opts)
+    c_hr = forward(f, hr.grid, idx_hr, opts)
+    arrays = {
+        "lr_starts": idx.starts, "lr_gids": idx.gids.astype(np.int32),
+        "lr_I": c.I, "lr_W": c.W, "hr_I": c_hr.I,
+        "dl": dl.astype(np.float32) * lr.grid.num_voxels,  # sign(d) in {-1,0,1}
+    }
+    for k in G:
+        arrays["grad_" + k] = getattr(gr, k)
+    out.update({"loss": loss, "lr_pairs": idx.pair_count, "hr_pairs": idx_hr.pair_count,
+                "lr_starts": sha(idx.starts), "lr_gids": sha(idx.gids),
+                "hr_starts": sha(idx_hr.starts), "hr_gids": sha(idx_hr.gids),
+                "lr_volume": sha(lr.data), "field": field_sha(f),
+                "lr_I": sha(c.I), "hr_I": sha(c_hr.I)})
+    # f64 engine on the same inputs
+    o64 = RenderOptions(precision="f64")
+    i64 = build_brick_index(f, lr.grid, o64)
+    c64 = forward(f, lr.grid, i64, o64)
+    arrays["lr_I64"] = c64.I
+    return out, arrays
+
+
+def fit_quality(iterations=200):
+    """Reference fit on the config-1 phantom, threshold 0."""
+    from gsvol.metrics import psnr, ssim3d
+    from gsvol.optimize import FitConfig, fit
+    cfg, hr, lr, f0, mine = problem(1)
+    t0 = time.perf_counter()
+    f, report = fit(lr, InitConfig(background_threshold=0.0), FitConfig(iterations=iterations))
+    t = time.perf_counter() - t0
+    idx = build_brick_index(f, hr.grid, RenderOptions())
+    sr = forward(f, hr.grid, idx, RenderOptions()).volume()
+    return {"iterations": iterations, "psnr": psnr(sr, hr), "ssim": ssim3d(sr, hr),
+            "losses_head": report.losses[:20], "final_loss": report.final["loss"],
+            "seconds": t, "trilinear_psnr": psnr(resample_trilinear(lr, hr.grid), hr),
+            "trilinear_ssim": ssim3d(resample_trilinear(lr, hr.grid), hr)}
+
+
+def full_configs():
+    """Bit-exact binning hashes at BASELINE sizes + sampled forward values."""
+    res = {}
+    opts = RenderOptions()
+    for cid in (2, 3, 4, 5):
+        t0 = time.perf_counter()
+        cfg, hr, lr, f, mine = problem(cid)
+        entry = {"lr_volume": sha(lr.data), "field": field_sha(f), "N": f.count}
+        grids = {"render": mine["render_grid"]} if cid == 5 else {"lr": lr.grid, "hr": hr.grid}
+        for name, grid in grids.items():
+            idx = build_brick_index(f, grid, opts)
+            entry[name] = {"dims": list(grid.dims), "pairs": idx.pair_count,
+                           "starts": sha(idx.starts), "gids": sha(idx.gids)}
+            if name == "lr":
+                c = forward(f, grid, idx, opts)
+                loss, _ = loss_and_grad(c.volume(), lr, "l1")
+                rng = np.random.default_rng(cid)
+                sel = rng.choice(grid.num_voxels, size=4096, replace=False)
+                entry[name].update({"loss": loss, "sample_idx": sel.tolist(),
+                                    "sample_I": c.I[sel].astype(float).tolist(),
+                                    "I_sum": float(np.sum(c.I, dtype=np.float64))})
+            del idx
+        res[str(cid)] = entry
+        print(f"config {cid}: {time.perf_counter() - t0:.1f}s", flush=True)
+    return res
+
+
+def main():
+    meta = {"versions": versions(), "generated_by": "tests/golden/make_golden.py"}
+    which = set(sys.argv[1:]) or {"sweep", "config1", "full", "fit"}
+    if "sweep" in which:
+        with open(os.path.join(HERE, "sweep.json"), "w") as fh:
+            json.dump({"meta": meta, "cases": sweep()}, fh)
+        print("sweep done", flush=True)
+    if "config1" in which:
+        out, arrays = config1()
+        np.savez_compressed(os.path.join(HERE, "config1.npz"), **arrays)
+        with open(os.path.join(HERE, "config1.json"), "w") as fh:
+            json.dump({"meta": meta, **out}, fh, indent=1)
+        print("config1 done", flush=True)
+    if "full" in which:
+        with open(os.path.join(HERE, "full_configs.json"), "w") as fh:
+            json.dump({"meta": meta, "configs": full_configs()}, fh)
+    if "fit" in which:
+        with open(os.path.join(HERE, "fit_quality.json"), "w") as fh:
+            json.dump({"meta": meta, **fit_quality()}, fh, indent=1)
+        print("fit done", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,432 @@
+"""CUDA path vs the oracle and the reference's golden vectors (needs a B200).
+
+Bars (north_star): brick lists bit-exact; voxel intensities within 1e-5
+(f32; the reference's own brick-vs-naive bar, test_acceptance.py:40-66) and
+1e-10 (f64); gradients within 1e-5 relative, norm-wise per parameter group,
+with the reference's W / I / dL/dI injected (SURVEY.md §0 finding 5).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2603_09621_b200 as gs
+from paper_2603_09621_b200.field import random_field_arrays
+from paper_2603_09621_b200.raster import RenderCache
+from paper_2603_09621_b200.synth import sha256
+
+from conftest import GRAD_KEYS, SWEEP_GRIDS, field_dict, load_json
+
+pytestmark = pytest.mark.gpu
+
+TOL_I = {"f32": 1e-5, "f64": 1e-10}
+TOL_G = {"f32": 1e-5, "f64": 1e-10}
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def rel_norm(got, ref):
+    den = np.linalg.norm(ref)
+    if den == 0.0:
+        return float(np.linalg.norm(got))
+    return float(np.linalg.norm(got - ref) / den)
+
+
+def _sweep_field(n, gi):
+    dims, sp, org = SWEEP_GRIDS[gi]
+    grid = gs.GridSpec(dims, sp, org)
+    arrs = random_field_arrays(n, grid, 100 * n + gi, 0.4, 2.0)
+    return grid, arrs
+
+
+SWEEP = [(n, gi) for n in (1, 10, 100, 1000) for gi in range(5)]
+
+
+# ------------------------------------------------------------ binning
+def test_sweep_binning_bit_exact_vs_reference_hashes():
+    cases = load_json("sweep.json")["cases"]
+    seen = set()
+    for c in cases:
+        key = (c["n"], c["grid"], tuple(c["brick_dims"]))
+        if key in seen:
+            continue
+        seen.add(key)
+        grid, arrs = _sweep_field(c["n"], c["grid"])
+        f = gs.GaussianField(*arrs)
+        idx = gs.build_brick_index(f, grid, gs.RenderOptions(), tuple(c["brick_dims"]))
+        assert idx.pair_count == c["pairs"], key
+        assert sha256(np_(idx.starts)) == c["starts"], key
+        assert sha256(np_(idx.gids).astype(np.int64)) == c["gids"], key
+    assert len(seen) == 60
+
+
+def test_config1_binning_bit_exact():
+    meta = load_json("config1.json")
+    from paper_2603_09621_b200.synth import CONFIGS, make_problem
+    p = make_problem(CONFIGS[1])
+    assert sha256(*p["field"]) == meta["field"]
+    f = gs.GaussianField(*p["field"])
+    for name, grid in (("lr", p["lr_grid"]), ("hr", p["hr_grid"])):
+        idx = gs.build_brick_index(f, grid)
+        assert idx.pair_count == meta[f"{name}_pairs"]
+        assert sha256(np_(idx.starts)) == meta[f"{name}_starts"]
+        assert sha256(np_(idx.gids).astype(np.int64)) == meta[f"{name}_gids"]
+
+
+@pytest.mark.parametrize("bd", [(8, 8, 4), (8, 8, 8), (4, 4, 4), (16, 8, 8), (3, 5, 7)])
+def test_binning_matches_oracle_any_brick_dims(bd):
+    grid = gs.GridSpec((21, 18, 13), (0.9, 1.1, 1.7), (-3.0, 2.0, 0.5))
+    arrs = random_field_arrays(700, grid, 77, 0.3, 2.5)
+    f = gs.GaussianField(*arrs)
+    idx = gs.build_brick_index(f, grid, gs.RenderOptions(), bd)
+    st, gi = oracle.build_index(field_dict(arrs), grid.dims, grid.spacing, grid.origin, bd, 3.0)
+    np.testing.assert_array_equal(np_(idx.starts), st)
+    np.testing.assert_array_equal(np_(idx.gids), gi)
+
+
+# ------------------------------------------------------------ forward
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_sweep_forward_vs_oracle(precision):
+    opts = gs.RenderOptions(precision=precision)
+    for n, gi in SWEEP:
+        grid, arrs = _sweep_field(n, gi)
+        f = gs.GaussianField(*arrs)
+        idx = gs.build_brick_index(f, grid, opts)
+        c = gs.forward(f, grid, idx, opts)
+        fd = field_dict(arrs)
+        S, W, I = oracle.forward(fd, grid.dims, grid.spacing, grid.origin, np_(idx.starts),
+                                 np_(idx.gids), precision=precision)
+        err = np.abs(np_(c.I).astype(np.float64) - I.astype(np.float64)).max()
+        assert err <= TOL_I[precision], (n, gi, precision, err)
+        # coverage decisions identical: I == 0 exactly where the oracle's is
+        np.testing.assert_array_equal(np_(c.I) == 0, I == 0)
+
+
+def test_config1_forward_vs_reference_golden():
+    g = np.load(__import__("os").path.join(__import__("conftest").GOLDEN, "config1.npz"))
+    from paper_2603_09621_b200.synth import CONFIGS, make_problem
+    p = make_problem(CONFIGS[1])
+    f = gs.GaussianField(*p["field"])
+    for grid, key in ((p["lr_grid"], "lr_I"), (p["hr_grid"], "hr_I")):
+        idx = gs.build_brick_index(f, grid)
+        c = gs.forward(f, grid, idx)
+        err = np.abs(np_(c.I).astype(np.float64) - g[key].astype(np.float64)).max()
+        assert err <= 1e-5, (key, err)
+    o64 = gs.RenderOptions(precision="f64")
+    idx = gs.build_brick_index(f, p["lr_grid"], o64)
+    c = gs.forward(f, p["lr_grid"], idx, o64)
+    assert np.abs(np_(c.I) - g["lr_I64"]).max() <= 1e-10
+
+
+def test_forward_equals_naive_gpu():
+    grid = gs.GridSpec((16, 16, 16), (0.7, 1.0, 1.3), (-2.0, 0.0, 1.0))
+    f = gs.GaussianField(*random_field_arrays(200, grid, 9, 0.4, 2.0))
+    for prec, tol in (("f32", 1e-5), ("f64", 1e-10)):
+        opts = gs.RenderOptions(precision=prec)
+        brick = gs.forward(f, grid, gs.build_brick_index(f, grid, opts), opts).volume()
+        naive = gs.render_naive(f, grid, opts)
+        assert np.abs(brick.numpy().astype(np.float64) - naive.numpy()).max() <= tol
+
+
+# ------------------------------------------------------------ backward
+def _backward_case(n, gi, precision, relax_enabled=True):
+    grid, arrs = _sweep_field(n, gi)
+    f = gs.GaussianField(*arrs)
+    f.relax_enabled = relax_enabled
+    fd = field_dict(arrs, relax_enabled=relax_enabled)
+    opts = gs.RenderOptions(precision=precision)
+    idx = gs.build_brick_index(f, grid, opts)
+    st, gi_ = np_(idx.starts), np_(idx.gids)
+    S, W, I = oracle.forward(fd, grid.dims, grid.spacing, grid.origin, st, gi_,
+                             precision=precision)
+    dl = np.random.default_rng(5).normal(size=grid.num_voxels)
+    dev = f.device
+    cache = RenderCache(grid, torch.from_numpy(S).to(dev), torch.from_numpy(W).to(dev),
+                        torch.from_numpy(I).to(dev), f.version)
+    got = gs.backward(f, grid, idx, cache, dl, opts)
+    ref = oracle.backward(fd, grid.dims, grid.spacing, grid.origin, st, gi_, W, I, dl,
+                          precision=precision)
+    return got, ref
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_sweep_backward_vs_oracle(precision):
+    for n, gi in SWEEP:
+        got, ref = _backward_case(n, gi, precision)
+        for k in GRAD_KEYS:
+            if n == 1 and k in ("positions", "log_scales", "rotations", "raw_relax"):
+                # a lone Gaussian: geometry gradients are pure rounding noise
+                assert np.abs(np_(getattr(got, k))).max() < (1e-6 if precision == "f32" else 1e-12)
+                continue
+            e = rel_norm(np_(getattr(got, k)), ref[k])
+            assert e <= TOL_G[precision], (n, gi, precision, k, e)
+
+
+def test_config1_backward_vs_reference_golden():
+    g = np.load(__import__("os").path.join(__import__("conftest").GOLDEN, "config1.npz"))
+    from paper_2603_09621_b200.synth import CONFIGS, make_problem
+    p = make_problem(CONFIGS[1])
+    grid = p["lr_grid"]
+    f = gs.GaussianField(*p["field"])
+    idx = gs.build_brick_index(f, grid)
+    dev = f.device
+    W = torch.from_numpy(g["lr_W"]).to(dev)
+    I = torch.from_numpy(g["lr_I"]).to(dev)
+    cache = RenderCache(grid, torch.zeros_like(W), W, I, f.version)
+    dl = g["dl"].astype(np.float64) / grid.num_voxels
+    got = gs.backward(f, grid, idx, cache, dl)
+    for k in GRAD_KEYS:
+        e = rel_norm(np_(getattr(got, k)), g["grad_" + k])
+        assert e <= 1e-5, (k, e)
+
+
+def test_backward_relax_disabled_vs_oracle():
+    got, ref = _backward_case(100, 1, "f32", relax_enabled=False)
+    assert np.all(np_(got.raw_relax) == 0.0)
+    for k in ("raw_amplitude", "positions", "log_scales", "rotations"):
+        assert rel_norm(np_(getattr(got, k)), ref[k]) <= 1e-5
+
+
+# ------------------------------------------------------------ KATs (test_raster / test_render)
+def _point_field(position, scale):
+    return gs.GaussianField(np.asarray([position], dtype=np.float64),
+                            np.log(np.full((1, 3), scale)), np.asarray([[1.0, 0, 0, 0]]),
+                            np.zeros(1), np.zeros(1))
+
+
+def test_kat_binning_cases(unit_grid):
+    idx = gs.build_brick_index(_point_field([4.0, 4.0, 1.0], 0.1), unit_grid)
+    assert idx.brick_grid == (1, 1, 2) and idx.pair_count == 1
+    assert int(idx.starts[1] - idx.starts[0]) == 1
+    assert gs.build_brick_index(_point_field([4.0, 4.0, 4.0], 50.0), unit_grid).pair_count == 2
+    assert gs.build_brick_index(_point_field([4.0, 4.0, 3.5], 0.2), unit_grid).pair_count == 2
+    far = _point_field([500.0, 0.0, 0.0], 1.0)
+    idx = gs.build_brick_index(far, unit_grid)
+    assert idx.pair_count == 0
+    v = gs.forward(far, unit_grid, idx, gs.RenderOptions(precision="f64")).volume()
+    assert np.all(v.numpy() == 0.0)
+    f = gs.random_field(7, unit_grid, seed=31)
+    assert gs.build_brick_index(f, unit_grid, gs.RenderOptions(cutoff_sigma=np.inf)).pair_count == 14
+
+
+def test_kat_infinite_cutoff_render_matches_oracle(unit_grid):
+    arrs = random_field_arrays(8, unit_grid, 9)
+    f = gs.GaussianField(*arrs)
+    opts = gs.RenderOptions(cutoff_sigma=np.inf, precision="f64")
+    c = gs.forward(f, unit_grid, gs.build_brick_index(f, unit_grid, opts), opts)
+    st, gi = oracle.build_index(field_dict(arrs), unit_grid.dims, unit_grid.spacing,
+                                unit_grid.origin, (8, 8, 4), np.inf)
+    _, _, I = oracle.forward(field_dict(arrs), unit_grid.dims, unit_grid.spacing,
+                             unit_grid.origin, st, gi, cutoff=np.inf, precision="f64")
+    assert np.abs(np_(c.I) - I).max() <= 1e-10
+
+
+def test_kat_single_gaussian_renders_amplitude():
+    g = gs.GridSpec((4, 4, 4))
+    amp = 0.7
+    f = gs.GaussianField(np.asarray([[1.5, 1.5, 1.5]]), np.full((1, 3), 0.3),
+                         np.asarray([[1.0, 0, 0, 0]]), np.asarray([np.log(amp / (1 - amp))]),
+                         np.asarray([20.0]))
+    for prec, tol in (("f64", 1e-9), ("f32", 1e-6)):
+        o = gs.RenderOptions(precision=prec)
+        v = gs.forward(f, g, gs.build_brick_index(f, g, o), o).numpy()
+        cov = v > 0
+        assert cov.any()
+        np.testing.assert_allclose(v[cov], amp, atol=tol)
+
+
+def test_kat_two_equal_kernels_average():
+    g = gs.GridSpec((1, 1, 1))
+    f = gs.GaussianField(np.asarray([[-0.4, 0, 0], [0.4, 0, 0]]), np.zeros((2, 3)),
+                         np.tile([1.0, 0, 0, 0], (2, 1)),
+                         np.asarray([np.log(0.25), np.log(4.0)]), np.full(2, 20.0))
+    for prec in ("f32", "f64"):
+        o = gs.RenderOptions(precision=prec)
+        v = gs.forward(f, g, gs.build_brick_index(f, g, o), o).numpy()
+        assert abs(float(v[0, 0, 0]) - 0.5) <= 1e-6
+
+
+def test_kat_normalization_properties():
+    # test_acceptance.py:86-117 (criterion 3) on the production engine
+    grid = gs.GridSpec((16, 16, 16))
+    opts = gs.RenderOptions()
+    arrs = list(random_field_arrays(200, grid, 30))
+    arrs[3] = np.full(200, 0.31)
+    f = gs.GaussianField(*arrs)
+    out = gs.forward(f, grid, gs.build_brick_index(f, grid, opts), opts).numpy()
+    amp = 1.0 / (1.0 + np.exp(-0.31))
+    cov = out != 0.0
+    assert cov.any() and np.abs(out[cov] - amp).max() <= 1e-6
+    arrs = random_field_arrays(200, grid, 31)
+    f = gs.GaussianField(*arrs)
+    out = gs.forward(f, grid, gs.build_brick_index(f, grid, opts), opts).numpy()
+    amps = 1.0 / (1.0 + np.exp(-arrs[3]))
+    cov = out != 0.0
+    assert out[cov].min() >= amps.min() - 1e-6 and out[cov].max() <= amps.max() + 1e-6
+    from scipy.special import logit
+    r = 1.0 / (1.0 + np.exp(-arrs[4]))
+    arrs2 = list(arrs)
+    arrs2[4] = logit(0.37 * r)
+    g2 = gs.GaussianField(*arrs2)
+    scaled = gs.forward(g2, grid, gs.build_brick_index(g2, grid, opts), opts).numpy()
+    assert np.abs(scaled - out).max() <= 1e-6
+
+
+def test_zero_upstream_is_exactly_zero(unit_grid):
+    f = gs.random_field(10, unit_grid, seed=38)
+    for prec in ("f32", "f64"):
+        o = gs.RenderOptions(precision=prec)
+        idx = gs.build_brick_index(f, unit_grid, o)
+        c = gs.forward(f, unit_grid, idx, o)
+        g = gs.backward(f, unit_grid, idx, c, np.zeros(unit_grid.num_voxels), o)
+        for k in GRAD_KEYS:
+            assert np.all(np_(getattr(g, k)) == 0.0), (prec, k)
+
+
+def test_single_gaussian_geometry_gradients_vanish(unit_grid):
+    f = gs.random_field(1, unit_grid, seed=15)
+    o = gs.RenderOptions(precision="f64")
+    idx = gs.build_brick_index(f, unit_grid, o)
+    c = gs.forward(f, unit_grid, idx, o)
+    g = gs.backward(f, unit_grid, idx, c, np.random.default_rng(16).normal(size=512), o)
+    for k in ("positions", "log_scales", "rotations", "raw_relax"):
+        assert np.abs(np_(getattr(g, k))).max() < 1e-12
+    assert np.abs(np_(g.raw_amplitude)).max() > 1e-6
+
+
+# ------------------------------------------------------------ errors
+def test_staleness_and_upstream_errors(unit_grid):
+    f = gs.random_field(5, unit_grid, seed=34)
+    idx = gs.build_brick_index(f, unit_grid)
+    f.bump_version()
+    with pytest.raises(gs.StaleIndexError, match="version"):
+        gs.forward(f, unit_grid, idx)
+    f = gs.random_field(5, unit_grid, seed=35)
+    idx = gs.build_brick_index(f, unit_grid)
+    with pytest.raises(gs.StaleIndexError, match="grid"):
+        gs.forward(f, gs.GridSpec((4, 4, 4)), idx)
+    with pytest.raises(gs.StaleIndexError, match="cutoff"):
+        gs.forward(f, unit_grid, idx, gs.RenderOptions(cutoff_sigma=2.0))
+    cache = gs.forward(f, unit_grid, idx)
+    f.bump_version()
+    idx2 = gs.build_brick_index(f, unit_grid)
+    with pytest.raises(gs.StaleIndexError, match="stale"):
+        gs.backward(f, unit_grid, idx2, cache, np.ones(unit_grid.num_voxels))
+    f = gs.random_field(4, unit_grid, seed=39)
+    idx = gs.build_brick_index(f, unit_grid)
+    cache = gs.forward(f, unit_grid, idx)
+    with pytest.raises(ValueError, match="entries"):
+        gs.backward(f, unit_grid, idx, cache, np.ones(3))
+    dl = np.ones(unit_grid.num_voxels)
+    dl[7] = np.nan
+    with pytest.raises(gs.NumericalError, match="voxel index 7"):
+        gs.backward(f, unit_grid, idx, cache, dl)
+
+
+# ------------------------------------------------------------ determinism
+def _shuffle(idx, seed):
+    rng = np.random.default_rng(seed)
+    gids = np_(idx.gids).copy()
+    st = np_(idx.starts)
+    for b in range(idx.brick_count):
+        gids[st[b]:st[b + 1]] = rng.permutation(gids[st[b]:st[b + 1]])
+    return gs.BrickIndex(idx.grid, idx.brick_dims, idx.brick_grid, st, gids,
+                         idx.field_version, idx.field_count, idx.cutoff_sigma)
+
+
+def test_bit_identity_across_list_order_and_runs():
+    grid = gs.GridSpec((16, 16, 16))
+    f = gs.random_field(500, grid, seed=40)
+    dl = np.random.default_rng(41).normal(size=grid.num_voxels)
+    for opts in (gs.RenderOptions(), gs.RenderOptions(precision="f64")):
+        idx = gs.build_brick_index(f, grid, opts)
+        ref_i = ref_g = None
+        for seed in (None, 1, 2, None):
+            variant = idx if seed is None else _shuffle(idx, seed)
+            if seed is not None:
+                assert not variant.lists_sorted()
+                np.testing.assert_array_equal(np_(variant.canonicalized().gids), np_(idx.gids))
+            c = gs.forward(f, grid, variant, opts)
+            g = gs.backward(f, grid, variant, c, dl, opts)
+            packed = np.concatenate([np_(getattr(g, k)).ravel() for k in GRAD_KEYS])
+            if ref_i is None:
+                ref_i, ref_g = np_(c.I), packed
+            else:
+                np.testing.assert_array_equal(np_(c.I), ref_i)
+                np.testing.assert_array_equal(packed, ref_g)
+
+
+# ------------------------------------------------------------ loss / Adam
+def test_loss_kats():
+    g2 = gs.GridSpec((2, 2, 2))
+    data = np.zeros((2, 2, 2))
+    data[1, 0, 0] = 0.1
+    loss, grad = gs.loss_and_grad(gs.Volume(g2, data), gs.Volume(g2, np.zeros((2, 2, 2))), "l1")
+    assert loss == pytest.approx(0.1 / 8)
+    gr = np_(grad)
+    assert gr[1] == pytest.approx(1.0 / 8) and np.count_nonzero(gr) == 1
+    loss, grad = gs.loss_and_grad(gs.Volume(g2, np.full((2, 2, 2), 0.25)),
+                                  gs.Volume(g2, np.zeros((2, 2, 2))), "l2")
+    assert loss == pytest.approx(0.0625)
+    np.testing.assert_allclose(np_(grad), 2 * 0.25 / 8)
+    with pytest.raises(gs.GridMismatchError, match="grid"):
+        gs.loss_and_grad(gs.Volume(g2, data), gs.Volume(gs.GridSpec((8, 8, 8)), np.zeros((8, 8, 8))))
+    with pytest.raises(ValueError, match="loss kind"):
+        gs.loss_and_grad(gs.Volume(g2, data), gs.Volume(g2, data), "huber")
+
+
+def test_adam_first_step_sign_like(unit_grid):
+    f = gs.random_field(3, unit_grid, seed=51)
+    before = np_(f.raw_amplitude).copy()
+    g = gs.GradientBuffer.zeros(3)
+    g.raw_amplitude[:] = torch.tensor([0.5, -2.0, 1e-3], dtype=torch.float64)
+    state = gs.AdamState.create(f)
+    lrs = {k: 0.0 for k in gs.FitConfig().resolved_lrs(unit_grid.spacing)}
+    lrs["raw_amplitude"] = 0.01
+    gs.step_optimizer(f, g, state, lrs)
+    ga = np.asarray([0.5, -2.0, 1e-3])
+    np.testing.assert_allclose(np_(f.raw_amplitude), before - 0.01 * ga / (np.abs(ga) + 1e-8),
+                               rtol=1e-12)
+    assert state.t == 1
+
+
+def test_adam_matches_oracle_bit_exact(unit_grid):
+    arrs = random_field_arrays(50, unit_grid, 52)
+    f = gs.GaussianField(*arrs)
+    fd = field_dict(arrs)
+    rng = np.random.default_rng(53)
+    grads = {k: rng.normal(size=fd[k].shape) for k in GRAD_KEYS}
+    gb = gs.GradientBuffer(*(torch.from_numpy(grads[k]).to(f.device) for k in GRAD_KEYS))
+    st_gpu, st_cpu = gs.AdamState.create(f), oracle.adam_state(fd)
+    lrs = gs.FitConfig().resolved_lrs(unit_grid.spacing)
+    for _ in range(3):
+        gs.step_optimizer(f, gb, st_gpu, lrs)
+        f.normalize_rotations()
+        oracle.adam_step(fd, grads, st_cpu, lrs)
+    for k in ("positions", "log_scales", "raw_amplitude", "raw_relax"):
+        np.testing.assert_array_equal(np_(getattr(f, k)), fd[k])
+    np.testing.assert_allclose(np_(f.rotations), fd["rotations"], rtol=0, atol=1e-15)
+
+
+# ------------------------------------------------------------ fused train step
+def test_train_step_matches_unfused_api():
+    from paper_2603_09621_b200.synth import CONFIGS, make_problem
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    out = step.forward(f)
+    grads = step.backward(f, out)
+    idx = gs.build_brick_index(f, lr.grid)
+    c = gs.forward(f, lr.grid, idx)
+    loss, dl = gs.loss_and_grad(c.volume(), lr, "l1")
+    g2 = gs.backward(f, lr.grid, idx, c, dl)
+    assert abs(out.loss() - loss) <= 1e-12
+    np.testing.assert_array_equal(np_(out.cache.I), np_(c.I))
+    for k in GRAD_KEYS:
+        assert rel_norm(np_(getattr(grads, k)), np_(getattr(g2, k))) <= 1e-6
+    meta = load_json("config1.json")
+    assert abs(out.loss() - meta["loss"]) <= 1e-6
