@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""bench.py -- B200 brick rasterizer benchmark (BASELINE.json metric).
+
+Workload (config 3 of BASELINE.json): 128^3 LR synthetic phantom, x2 -> 256^3
+HR, N = 2,097,152 Gaussians (one per LR voxel).  A step is one fit()
+iteration (optimize.py:171-184): bin -> forward + fused L1 -> backward ->
+merge -> chain rule -> Adam -> quaternion renorm, on the 128^3 LR grid the
+reference trains on.  `value` = train iterations/s (whole job), timed with
+CUDA events, inputs resident in HBM.  The same line carries the 256^3 render
+(bin + forward at the HR grid) in Gvoxel/s and the 512^3 render of config 5.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1: launched by torch.distributed.run, one rank per GPU; each rank owns a
+contiguous z-slab of brick layers; one NCCL all_reduce per train step.
+--impl reference: the reference's CPU algorithm (oracle/ port, OpenMP, all
+host cores) on the same config, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train iters/s + render Gvoxel/s at 256^3 HR, 1/2/4/8 B200, % FP32/HBM roofline"
+FWD_FLOP, BWD_FLOP = 28, 74          # per live pair-voxel
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--no-render512", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_setup(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist, ws, rank, local
+    if torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return None, 1, 0, 0
+
+
+def slab_ranges(layers: int, ws: int):
+    """Contiguous, balanced split of brick layers [0, layers) over ws ranks."""
+    base, rem = divmod(layers, ws)
+    out, z = [], 0
+    for r in range(ws):
+        n = base + (1 if r < rem else 0)
+        out.append((z, z + n))
+        z += n
+    return out
+
+
+def problem_for(cfg_id):
+    from paper_2603_09621_b200 import synth
+    return synth.make_problem(synth.CONFIGS[cfg_id])
+
+
+# ----------------------------------------------------------------- CPU arm
+def cpu_train_step_seconds(p, steps: int, warmup: int):
+    """Oracle (port of the reference CPU path) train iterations on this host."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    from paper_2603_09621_b200.optimize import FitConfig
+    oracle.build()
+    g = p["lr_grid"]
+    fd = dict(zip(("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax"),
+                  [np.array(a, copy=True) for a in p["field"]]))
+    st = oracle.adam_state(fd)
+    lrs = FitConfig().resolved_lrs(g.spacing)
+    tgt = np.ascontiguousarray(p["lr"].ravel(order="F"))
+    for _ in range(warmup):
+        oracle.train_step_fast(fd, g.dims, g.spacing, g.origin, tgt, st, lrs)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.train_step_fast(fd, g.dims, g.spacing, g.origin, tgt, st, lrs)
+    return (time.perf_counter() - t0) / steps
+
+
+def run_reference(args, dist, rank):
+    if rank != 0:
+        return
+    p = problem_for(args.config)
+    sec = cpu_train_step_seconds(p, args.steps, args.warmup)
+    cores = os.cpu_count()
+    v = 1.0 / sec
+    cfg = _config_dict(args, p, None, 1)
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "it/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "it/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} full config-{args.config} train "
+                                       "iterations (oracle/: numpy binning + OpenMP C loops)"},
+            "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(args, p, pairs, ws):
+    return {"workload": f"config {args.config}: fit step on {p['lr_grid'].dims} LR "
+                        f"(x2 -> {p['hr_grid'].dims} HR), N={p['field'][0].shape[0]} Gaussians",
+            "lr_dims": list(p["lr_grid"].dims), "hr_dims": list(p["hr_grid"].dims),
+            "N": int(p["field"][0].shape[0]), "pairs_lr": pairs, "brick_dims": [8, 8, 4],
+            "loss": "l1", "optimizer": "Adam (f64 master)", "parallelism": f"z-slab x{ws}",
+            "l2": "inputs larger than L2 (f64 field + Adam moments = 0.7 GB, pairs 0.1 GB)"}
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_ours(args, dist, ws, rank, local):
+    import torch
+    import paper_2603_09621_b200 as gs
+    from paper_2603_09621_b200 import _lib
+    from paper_2603_09621_b200.train import PhaseTimer
+
+    dev = torch.device("cuda", local)
+    lib = _lib.lib()
+    p = problem_for(args.config)
+    lr_grid, hr_grid = p["lr_grid"], p["hr_grid"]
+    lr = gs.Volume(lr_grid, p["lr"])
+    opts = gs.RenderOptions()
+    bd = (8, 8, 4)
+    lr_layers = -(-lr_grid.dims[2] // bd[2])
+    hr_layers = -(-hr_grid.dims[2] // bd[2])
+    my_slab = slab_ranges(lr_layers, ws)[rank] if ws > 1 else None
+    my_hr_slab = slab_ranges(hr_layers, ws)[rank] if ws > 1 else None
+    group = dist.group.WORLD if dist else None
+
+    f = gs.GaussianField(*p["field"], device=dev)
+    state = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr_grid.spacing)
+    timer = PhaseTimer()
+    step = gs.TrainStep(lr, opts, bd, "l1", slab=my_slab, process_group=group, world_size=ws,
+                        timer=timer)
+
+    def train_iter():
+        out = step.forward(f)
+        grads = step.backward(f, out)
+        timer("adam")
+        gs.step_optimizer(f, grads, state, lrs)
+        f.normalize_rotations()
+        timer(None)
+        return out
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    # ---------------- train: warmup, then exactly K timed steps
+    for _ in range(args.warmup):
+        out = train_iter()
+    barrier()
+    timer.reset()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    outs = []
+    for _ in range(args.steps):
+        outs.append(train_iter().loss_sum)
+    e1.record(s)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    phases = timer.summary()
+    losses = [float(x.item()) / lr_grid.num_voxels for x in outs]
+    assert all(math.isfinite(x) for x in losses), "non-finite loss in timed steps"
+    pairs = out.idx.pair_count
+
+    # ---------------- render at the 256^3 HR grid (bin + forward)
+    def render_iter(grid, slab):
+        idx = gs.build_brick_index(f, grid, opts, bd, slab=slab)
+        return gs.forward(f, grid, idx, opts), idx
+
+    kr = max(1, min(args.steps, 10))
+    for _ in range(min(args.warmup, 3)):
+        render_iter(hr_grid, my_hr_slab)
+    barrier()
+    e0.record(s)
+    for _ in range(kr):
+        _, hidx = render_iter(hr_grid, my_hr_slab)
+    e1.record(s)
+    barrier()
+    ms_r = max_over_ranks(e0.elapsed_time(e1) / kr)
+    render = {"grid": list(hr_grid.dims), "value": hr_grid.num_voxels / (ms_r * 1e-3) / 1e9,
+              "unit": "Gvoxel/s", "ms_per_render": ms_r, "renders": kr,
+              "pairs": hidx.pair_count if ws == 1 else None}
+
+    render512 = None
+    if not args.no_render512:
+        from paper_2603_09621_b200 import synth
+        arr5 = synth.jitter_field([np.asarray(a) for a in p["field"]], lr_grid)
+        f5 = gs.GaussianField(*arr5, device=dev)
+        g5 = gs.grid_covering_extent(lr_grid, (512, 512, 512))
+        slab5 = slab_ranges(-(-512 // bd[2]), ws)[rank] if ws > 1 else None
+
+        def r5():
+            idx = gs.build_brick_index(f5, g5, opts, bd, slab=slab5)
+            return gs.forward(f5, g5, idx, opts), idx
+        r5()
+        barrier()
+        k5 = max(1, min(args.steps, 5))
+        e0.record(s)
+        for _ in range(k5):
+            _, i5 = r5()
+        e1.record(s)
+        barrier()
+        ms5 = max_over_ranks(e0.elapsed_time(e1) / k5)
+        render512 = {"grid": [512, 512, 512], "value": g5.num_voxels / (ms5 * 1e-3) / 1e9,
+                     "unit": "Gvoxel/s", "ms_per_render": ms5, "renders": k5,
+                     "pairs": i5.pair_count if ws == 1 else None, "field": "config-5 jittered"}
+        del f5, i5
+    clocks = sampler.stop()
+
+    # ---------------- roofline of the dominant pair kernel (live pair-voxels)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    out_idx = out.idx
+    _lib.check(lib.gsv_diag_count_live(
+        f.positions.data_ptr(), out_idx._aux.rec32.data_ptr(), f.log_scales.data_ptr(),
+        f.rotations.data_ptr(), out_idx.starts.data_ptr(), out_idx.gids.data_ptr(),
+        _lib.make_grid(lr_grid), _lib.make_bricks(lr_grid, bd, my_slab), 3.0, cnt.data_ptr(),
+        _lib.stream_ptr()), "count_live")
+    e_live, e_brick = (int(x) for x in cnt.tolist())
+    peak = fp32_peak(lib, dev)
+    t_fwd = phases.get("forward", (0, float("nan")))[1]
+    t_bwd = phases.get("backward", (0, float("nan")))[1]
+    dom, t_dom, fl = ("backward", t_bwd, BWD_FLOP) if t_bwd >= t_fwd else ("forward", t_fwd, FWD_FLOP)
+    achieved = e_live * fl / (t_dom * 1e-3) / 1e12
+    n_g = f.count
+    bytes_alg = {"forward": 48 * n_g + 4 * pairs + 12 * lr_grid.num_voxels,
+                 "backward": 96 * n_g + 4 * pairs + 12 * lr_grid.num_voxels}[dom]
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as fh:
+            traffic = json.load(fh).get(dom)
+    hbm_peak = 6552.0  # MEASURED_PEAKS.json (driver-written) when present
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        with open(mp) as fh:
+            hbm_peak = float(json.load(fh).get("hbm_gbs", hbm_peak))
+    roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak["tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peak["tflops"], "traffic": traffic,
+                "peak_source": peak["source"], "work": {"E_live": e_live, "E_brick": e_brick,
+                "flop_per_live_pair_voxel": fl, "ms_per_launch": t_dom},
+                "hbm": {"algorithmic_bytes": bytes_alg,
+                        "achieved_gbs": bytes_alg / (t_dom * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                        "frac": bytes_alg / (t_dom * 1e-3) / 1e9 / hbm_peak}}
+
+    # ---------------- kernel launches per step (CUPTI, outside the timed region)
+    launches = count_launches(train_iter)
+
+    # ---------------- e2e: fit()'s loop with host buffers (pinned H2D target, loss D2H)
+    e2e = None
+    if not args.no_e2e:
+        host_t = torch.from_numpy(np.ascontiguousarray(p["lr"].ravel(order="F"))).pin_memory()
+        dev_t = torch.empty_like(host_t, device=dev)
+        for _ in range(min(args.warmup, 3)):
+            dev_t.copy_(host_t, non_blocking=True)
+            step.set_target(dev_t)
+            o = step.forward(f)
+            g = step.backward(f, o)
+            _ = o.loss()
+            gs.step_optimizer(f, g, state, lrs)
+            f.normalize_rotations()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            dev_t.copy_(host_t, non_blocking=True)
+            step.set_target(dev_t)
+            o = step.forward(f)
+            g = step.backward(f, o)
+            loss = o.loss()                    # device -> host, like fit()
+            gs.step_optimizer(f, g, state, lrs)
+            f.normalize_rotations()
+        barrier()
+        sec = max_over_ranks((time.perf_counter() - t0) / args.steps)
+        e2e = {"value": 1.0 / sec, "unit": "it/s", "h2d_bytes_per_step": host_t.numel() * 4,
+               "d2h_bytes_per_step": 8, "api": "TrainStep.forward/backward + step_optimizer "
+               "+ normalize_rotations (fit() loop body)", "last_loss": loss}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        sec = cpu_train_step_seconds(p, 1, 0)
+        cpu = {"value": 1.0 / sec, "unit": "it/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"1 full config-{args.config} train iteration on the host "
+                         "(oracle/: numpy binning + OpenMP C loops, all cores)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": 1000.0 / ms, "unit": "it/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic", "config": _config_dict(args, p, pairs, ws),
+                "render": render, "render512": render512,
+                "phases_ms": {k: v[1] for k, v in phases.items()},
+                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+                "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
+                "loss_last": losses[-1]}
+        print(json.dumps(line), flush=True)
+
+
+def fp32_peak(lib, dev) -> dict:
+    """Measured FP32 FMA throughput of this GPU (our probe kernel)."""
+    import torch
+    from paper_2603_09621_b200 import _lib
+    sms = lib.gsv_device_sm_count()
+    blocks, iters = sms * 8, 4096
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        _lib.check(lib.gsv_diag_fma_probe(blocks, iters, sink.data_ptr(), _lib.stream_ptr()),
+                   "fma_probe")
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(5):
+        lib.gsv_diag_fma_probe(blocks, iters, sink.data_ptr(), _lib.stream_ptr())
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 5
+    tflops = blocks * 256 * iters * 16 * 2 / (ms * 1e-3) / 1e12
+    return {"tflops": tflops, "source": f"measured FFMA probe ({blocks} CTAs x 256 thr)"}
+
+
+def count_launches(fn) -> int:
+    """Kernel launches of one step, counted by the CUDA profiler (CUPTI)."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        n = 0
+        for e in prof.events():
+            if e.device_type.name == "CUDA" and ("gsv" in e.name or "cub" in e.name.lower()):
+                n += 1
+        return n
+    except Exception:
+        return -1
+
+
+def main():
+    args = parse()
+    dist, ws, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist, rank)
+        else:
+            run_ours(args, dist, ws, rank, local)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -147,10 +147,11 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  * exactly in f64 inside a guard band), 1 = f64 (S/W/I float64, rec64 needed).
  * The slab's voxels only are written.  If target != NULL the L1/L2 loss of
  * optimize.loss_and_grad (optimize.py:91-103) is fused into the epilogue:
- *   ab (V,2) float : {alpha, beta} = {dL/dI / W, dL/dI * I / W} (0 where
- *                    W < eps_w), the backward's per-voxel inputs;
+ *   ab (V,2) float : {alpha, I} with alpha = dL/dI / W (0 where W < eps_w or
+ *                    dL/dI == 0), the backward's per-voxel inputs;
  *   loss_part (nbricks_slab) double : per-brick sum |I-T| (l1) or (I-T)^2.
- * loss_kind: 0 = l1, 1 = l2.  inv_v = 1 / (global voxel count).
+ * loss_kind: 0 = l1, 1 = l2.  vox_count = global voxel count V, so
+ * dL/dI = sign(I-T)/V (l1) or 2(I-T)/V (l2) exactly as optimize.py:99-102.
  * ------------------------------------------------------------------------ */
 int gsv_forward(const double* positions, const gsv_record32* rec32,
                 const gsv_record64* rec64, const double* log_scales,
@@ -158,12 +159,12 @@ int gsv_forward(const double* positions, const gsv_record32* rec32,
                 const int32_t* gids, const gsv_grid* grid,
                 const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
                 int precision, void* S, void* W, void* I,
-                const float* target, int loss_kind, double inv_v, float* ab,
+                const float* target, int loss_kind, double vox_count, float* ab,
                 double* loss_part, void* stream);
 
 /* Per-voxel backward inputs from (W, I, dL/dI) for the unfused API path
- * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) in the
- * precision's type and *bad (device int64) = first non-finite voxel index or
+ * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) = {dL/dI / W, I}
+ * in the precision's type and *bad (device int64) = first non-finite voxel index or
  * -1.  Slab voxels only. */
 int gsv_backward_prep(const void* W, const void* I, const double* dldi,
                       const gsv_grid* grid, const gsv_bricks* bricks,

@@ -197,3 +197,89 @@ void oracle_merge(int64_t n, const int64_t* gstarts, const int64_t* porder, cons
 }
 
 int oracle_abi_version(void) { return 1; }
+
+/* Chain rule of backward (raster.py:524-549, _rotation_jacobians 454-467) in
+ * C for the CPU-baseline leg: same formulas as the numpy einsums (summation
+ * order differs at the 1e-16 level).  sums (N,11) -> grads. */
+void oracle_chain_rule(int64_t n, const double* sums, const double* ls, const double* q,
+                       const double* ra, const double* rr, int relax_enabled,
+                       double* g_amp, double* g_rel, double* g_pos, double* g_ls,
+                       double* g_rot) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double* s = sums + 11 * i;
+    double G[9] = {s[5], s[8], s[9], s[8], s[6], s[10], s[9], s[10], s[7]};
+    const double w = q[4 * i], x = q[4 * i + 1], y = q[4 * i + 2], z = q[4 * i + 3];
+    const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                         2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                         2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    const double iv[3] = {exp(-2.0 * ls[3 * i]), exp(-2.0 * ls[3 * i + 1]),
+                          exp(-2.0 * ls[3 * i + 2])};
+    for (int k = 0; k < 3; ++k) {
+      double t = 0.0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) t += R[3 * a + k] * G[3 * a + b] * R[3 * b + k];
+      g_ls[3 * i + k] = -2.0 * iv[k] * t;
+    }
+    const double J[4][9] = {
+        {0, -2 * z, 2 * y, 2 * z, 0, -2 * x, -2 * y, 2 * x, 0},
+        {0, 2 * y, 2 * z, 2 * y, -4 * x, -2 * w, 2 * z, 2 * w, -4 * x},
+        {-4 * y, 2 * x, 2 * w, 2 * x, 0, 2 * z, -2 * w, 2 * z, -4 * y},
+        {-4 * z, -2 * w, 2 * x, 2 * w, -4 * z, 2 * y, 2 * x, 2 * y, 0}};
+    for (int j = 0; j < 4; ++j) {
+      double t = 0.0;
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) {
+          double pm = 0.0;
+          for (int m = 0; m < 3; ++m) pm += J[j][3 * c + m] * iv[m] * R[3 * a + m];
+          t += G[3 * a + c] * pm;
+        }
+      g_rot[4 * i + j] = 2.0 * t;
+    }
+    g_pos[3 * i] = s[2];
+    g_pos[3 * i + 1] = s[3];
+    g_pos[3 * i + 2] = s[4];
+    const double A = 1.0 / (1.0 + exp(-ra[i]));
+    g_amp[i] = s[0] * A * (1.0 - A);
+    if (relax_enabled) {
+      const double r = 1.0 / (1.0 + exp(-rr[i]));
+      g_rel[i] = s[1] * r * (1.0 - r);
+    } else {
+      g_rel[i] = 0.0;
+    }
+  }
+}
+
+/* One Adam step on one group (optimize.py:139-147), numpy operand order. */
+void oracle_adam(int64_t count, double* p, double* m, double* v, const double* g, double lr,
+                 double b1, double b2, double eps, double bc1, double bc2) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < count; ++i) {
+    m[i] = m[i] * b1 + (1.0 - b1) * g[i];
+    v[i] = v[i] * b2 + ((1.0 - b2) * g[i]) * g[i];
+    p[i] -= lr * (m[i] / bc1) / (sqrt(v[i] / bc2) + eps);
+  }
+}
+
+/* q /= |q| (field.py:100-102). */
+void oracle_normalize(int64_t n, double* q) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double* r = q + 4 * i;
+    const double nrm = sqrt(((r[0] * r[0] + r[1] * r[1]) + r[2] * r[2]) + r[3] * r[3]);
+    for (int a = 0; a < 4; ++a) r[a] /= nrm;
+  }
+}
+
+/* Per-Gaussian gstarts + porder of the merge (raster.py:514-516) by a
+ * counting sort on gid (stable => ascending brick order within a gid). */
+void oracle_merge_order(int64_t n, int64_t p, const int64_t* gids, int64_t* gstarts,
+                        int64_t* porder) {
+  memset(gstarts, 0, sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t j = 0; j < p; ++j) gstarts[gids[j] + 1]++;
+  for (int64_t i = 0; i < n; ++i) gstarts[i + 1] += gstarts[i];
+  int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) cur[i] = gstarts[i];
+  for (int64_t j = 0; j < p; ++j) porder[cur[gids[j]]++] = j;
+  free(cur);
+}

@@ -69,6 +69,9 @@ _SIGS = {
     "gsv_normalize_rotations": [c_vp, c_i64, c_vp],
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
+    # include/gsv_diag.h (measurement only)
+    "gsv_diag_count_live": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl, c_vp, c_vp],
+    "gsv_diag_fma_probe": [c_int, c_int, c_vp, c_vp],
 }
 _RESTYPES = {"gsv_last_error": ctypes.c_char_p}
 

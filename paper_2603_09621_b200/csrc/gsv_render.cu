@@ -117,7 +117,7 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                  gsv_grid g, gsv_bricks k, float cut2, double cut2d, double eps_w,
                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
-                 const float* __restrict__ target, int loss_kind, double inv_v,
+                 const float* __restrict__ target, int loss_kind, double vox_count,
                  float2* __restrict__ ab, double* __restrict__ loss_part) {
   __shared__ Pair32 sp[kFwdThreads];
   __shared__ double red[kFwdThreads / 32];
@@ -210,13 +210,13 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
         double dl;
         if (loss_kind == 0) {
           lsum += fabs(d);
-          dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_v;
+          dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / vox_count;
         } else {
           lsum += d * d;
-          dl = 2.0 * d * inv_v;
+          dl = 2.0 * d / vox_count;
         }
         const float alpha = (cov && dl != 0.0) ? (float)(dl / (double)accW) : 0.f;
-        ab[lin] = make_float2(alpha, alpha * iv);
+        ab[lin] = make_float2(alpha, iv);
       }
     }
   }
@@ -241,7 +241,7 @@ forward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict_
                  const int32_t* __restrict__ gids, gsv_grid g, gsv_bricks k, double cut2,
                  double eps_w, double* __restrict__ S, double* __restrict__ W,
                  double* __restrict__ I, const float* __restrict__ target, int loss_kind,
-                 double inv_v, double2* __restrict__ ab, double* __restrict__ loss_part,
+                 double vox_count, double2* __restrict__ ab, double* __restrict__ loss_part,
                  const gsv_record32* __restrict__ rec32) {
   constexpr int T = 128;
   __shared__ Pair64 sp[T];
@@ -322,13 +322,13 @@ forward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict_
         double dl;
         if (loss_kind == 0) {
           lsum += fabs(d);
-          dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_v;
+          dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / vox_count;
         } else {
           lsum += d * d;
-          dl = 2.0 * d * inv_v;
+          dl = 2.0 * d / vox_count;
         }
         const double alpha = (cov && dl != 0.0) ? dl / accW : 0.0;
-        ab[lin] = make_double2(alpha, alpha * iv);
+        ab[lin] = make_double2(alpha, iv);
       }
     }
   }
@@ -349,14 +349,11 @@ __global__ void backward_prep_kernel(const T* __restrict__ W, const T* __restric
   const double dl = dldi[lin];
   if (!isfinite(dl)) atomicMin(bad, (unsigned long long)lin);
   const double w = (double)W[lin];
-  T alpha = 0, beta = 0;
-  if (w >= eps_w && dl != 0.0 && isfinite(dl)) {
-    alpha = (T)(dl / w);
-    beta = (T)(dl * (double)I[lin] / w);
-  }
+  T alpha = 0;
+  if (w >= eps_w && dl != 0.0 && isfinite(dl)) alpha = (T)(dl / w);
   T2 o;
   o.x = alpha;
-  o.y = beta;
+  o.y = I[lin];
   ab[lin] = o;
 }
 
@@ -417,7 +414,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
           const float kern = __expf(-0.5f * d2);
           const float w = kern * r;
           acc_a = fmaf(w, v_ab.x, acc_a);
-          const float common = fmaf(A, v_ab.x, -v_ab.y);
+          const float common = v_ab.x * (A - v_ab.y);   // dL/dI (A - I) / W
           acc_r = fmaf(common, kern, acc_r);
           const float cw = common * w;
           mu0 = fmaf(cw, fmaf(L[0], v0, fmaf(L[3], v1, L[6] * v2)), mu0);
@@ -492,7 +489,7 @@ backward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict
           const double kern = exp(-0.5 * d2);
           const double w = kern * r;
           acc_a += w * v_ab.x;
-          const double common = A * v_ab.x - v_ab.y;
+          const double common = v_ab.x * (A - v_ab.y);
           acc_r += common * kern;
           const double cw = common * w;
           mu0 += cw * (L[0] * v0 + L[3] * v1 + L[6] * v2);
@@ -590,7 +587,7 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
                 const double* log_scales, const double* rotations, const int64_t* starts,
                 const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
                 double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
-                const float* target, int loss_kind, double inv_v, float* ab,
+                const float* target, int loss_kind, double vox_count, float* ab,
                 double* loss_part, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
@@ -605,13 +602,13 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
   if (precision == 0) {
     forward32_kernel<<<(unsigned)nb, kFwdThreads, 0, s>>>(
         positions, rec32, log_scales, rotations, starts, gids, *grid, *bricks, (float)cut2d,
-        cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, inv_v,
+        cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
         (float2*)ab, loss_part);
     GSV_CHECK_LAUNCH("forward32_kernel");
   } else {
     forward64_kernel<<<(unsigned)nb, 128, 0, s>>>(
         positions, rec64, nullptr, starts, gids, *grid, *bricks, cut2d, eps_w, (double*)S,
-        (double*)W, (double*)I, target, loss_kind, inv_v, (double2*)ab, loss_part, rec32);
+        (double*)W, (double*)I, target, loss_kind, vox_count, (double2*)ab, loss_part, rec32);
     GSV_CHECK_LAUNCH("forward64_kernel");
   }
   return GSV_OK;

@@ -292,7 +292,7 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
-        1.0 / grid.num_voxels, _lib.ptr(ab), _lib.ptr(loss_part), _lib.stream_ptr()), "forward")
+        float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.stream_ptr()), "forward")
 
 
 def forward(f: GaussianField, grid: GridSpec, idx: BrickIndex,
@@ -325,13 +325,16 @@ def _emission_layout(f, grid, idx: BrickIndex, opts: RenderOptions):
     return gstart, box, False
 
 
-def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: bool):
+def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: bool,
+                   timer=None):
     lib = _lib.lib()
     n = f.count
     pdt = opts.torch_dtype
     npairs = int(gstart[-1].item()) if not trusted else idx.pair_count
     alloc = torch.empty if trusted else torch.zeros
     partials = alloc((max(npairs, 1), 12), dtype=pdt, device=f.device)
+    if timer is not None:
+        timer("backward")
     _lib.check(lib.gsv_backward(
         f.positions.data_ptr(), rec32.data_ptr(), _lib.ptr(rec64), f.log_scales.data_ptr(),
         f.rotations.data_ptr(), idx.starts.data_ptr(), idx.gids.data_ptr(), gstart.data_ptr(),
@@ -339,8 +342,12 @@ def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: b
         float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), partials.data_ptr(),
         _lib.stream_ptr()), "backward")
     gsum = torch.empty((n, 12), dtype=torch.float64, device=f.device)
+    if timer is not None:
+        timer("merge")
     _lib.check(lib.gsv_merge(partials.data_ptr(), gstart.data_ptr(), n, opts.precision_code,
                              gsum.data_ptr(), _lib.stream_ptr()), "merge")
+    if timer is not None:
+        timer(None)
     return gsum
 
 

@@ -1,11 +1,11 @@
 """The fused training step: one iteration of fit() (optimize.py:171-184).
 
   forward(f):  build_brick_index -> gsv_forward with the L1/L2 loss fused into
-               the epilogue (per-voxel backward inputs {dL/dI / W, dL/dI I / W}
-               written in the same pass) -> per-brick loss partials ->
-               gsv_sum.  No separate loss kernel, no dL/dI round trip.
+               the epilogue (per-voxel backward inputs {dL/dI / W, I} written
+               in the same pass) -> per-brick loss partials -> gsv_sum.  No
+               separate loss kernel, no dL/dI round trip through HBM.
   backward(f): gsv_backward (pair partials at their gid-major emission slots)
-               -> gsv_merge (ascending brick order) -> [allreduce of the
+               -> gsv_merge (ascending brick order) -> [all_reduce of the
                N x 12 partial sums, the only collective, when sharded] ->
                gsv_chain_rule.
 
@@ -32,6 +32,38 @@ from .volume import Volume
 LOSS_KINDS = {"l1": 0, "l2": 1}
 
 
+class PhaseTimer:
+    """CUDA events on the launching stream around each kernel phase.
+
+    ``mark(name)`` closes the open phase and opens ``name`` (None closes only).
+    ``summary()`` synchronizes and returns {phase: (launches, mean_ms)}.
+    """
+
+    def __init__(self):
+        self.events: list = []          # (name, start_event, end_event)
+        self._open = None
+
+    def __call__(self, name):
+        s = torch.cuda.current_stream()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(s)
+        if self._open is not None:
+            self.events.append((self._open[0], self._open[1], ev))
+        self._open = (name, ev) if name is not None else None
+
+    def reset(self):
+        self.events.clear()
+        self._open = None
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out: dict = {}
+        for name, a, b in self.events:
+            n, t = out.get(name, (0, 0.0))
+            out[name] = (n + 1, t + a.elapsed_time(b))
+        return {k: (n, t / n) for k, (n, t) in out.items()}
+
+
 @dataclass
 class StepOutput:
     idx: BrickIndex
@@ -54,7 +86,7 @@ class TrainStep:
 
     def __init__(self, target: Volume, opts: RenderOptions = RenderOptions(),
                  brick_dims=(8, 8, 4), loss: str = "l1", slab=None, process_group=None,
-                 world_size: int = 1):
+                 world_size: int = 1, timer: PhaseTimer | None = None):
         if loss not in LOSS_KINDS:
             raise ValueError(f"unknown loss kind {loss!r}")
         self.grid = target.grid
@@ -68,14 +100,24 @@ class TrainStep:
         self.slab = slab
         self.group = process_group
         self.world_size = world_size
+        self.timer = timer
+
+    @property
+    def sharded(self) -> bool:
+        return self.group is not None and self.world_size > 1
 
     def set_target(self, target_linear: torch.Tensor) -> None:
         """Swap the target buffer (e.g. after a host->device copy)."""
         self.target = target_linear
 
+    def _mark(self, name):
+        if self.timer is not None:
+            self.timer(name)
+
     def forward(self, f: GaussianField) -> StepOutput:
         lib = _lib.lib()
         grid, opts = self.grid, self.opts
+        self._mark("bin")
         idx = build_brick_index(f, grid, opts, self.brick_dims, slab=self.slab)
         aux = idx._aux
         nvox = grid.num_voxels
@@ -83,34 +125,37 @@ class TrainStep:
         S = torch.empty(nvox, dtype=dt, device=f.device)
         W = torch.empty(nvox, dtype=dt, device=f.device)
         I = torch.empty(nvox, dtype=dt, device=f.device)
-        ab = torch.empty((nvox, 2), dtype=dt if opts.precision == "f64" else torch.float32,
-                         device=f.device)
+        ab = torch.empty((nvox, 2), dtype=dt, device=f.device)
         nb = max(idx.brick_count, 1)
-        loss_part = torch.zeros(nb, dtype=torch.float64, device=f.device)
+        loss_part = torch.empty(nb, dtype=torch.float64, device=f.device)
+        self._mark("forward")
         _forward_into(f, grid, idx, opts, aux.rec32, aux.rec64, S, W, I, target=self.target,
                       loss_kind=self.loss_kind, ab=ab, loss_part=loss_part)
-        loss_sum = torch.empty(1, dtype=torch.float64, device=f.device)
-        _lib.check(lib.gsv_sum(loss_part.data_ptr(), idx.brick_count, loss_sum.data_ptr(),
-                               _lib.stream_ptr()), "sum")
+        self._mark("loss_sum")
+        loss_sum = torch.zeros(1, dtype=torch.float64, device=f.device)
+        if idx.brick_count > 0:
+            _lib.check(lib.gsv_sum(loss_part.data_ptr(), idx.brick_count, loss_sum.data_ptr(),
+                                   _lib.stream_ptr()), "sum")
+        self._mark(None)
         return StepOutput(idx, RenderCache(grid, S, W, I, f.version), ab, loss_sum, nvox,
                           reduced=not self.sharded)
-
-    @property
-    def sharded(self) -> bool:
-        return self.group is not None and self.world_size > 1
 
     def backward(self, f: GaussianField, out: StepOutput) -> GradientBuffer:
         idx = out.idx
         aux = idx._aux
         gsum = _pair_partials(f, self.grid, idx, self.opts, aux.rec32, aux.rec64, out.ab,
-                              aux.gstart, aux.box, True)
+                              aux.gstart, aux.box, True, timer=self.timer)
         if self.sharded:
             # One collective per step: the merged per-Gaussian partials, with
             # this rank's loss partial riding in the spare 12th column.
             import torch.distributed as dist
+            self._mark("allreduce")
             gsum[0, 11] = out.loss_sum[0]
             dist.all_reduce(gsum, group=self.group)
             out.loss_sum.copy_(gsum[0, 11:12])
             gsum[0, 11] = 0.0
             out.reduced = True
-        return _chain_rule(f, gsum)
+        self._mark("chain")
+        g = _chain_rule(f, gsum)
+        self._mark(None)
+        return g

@@ -158,8 +158,14 @@ def test_sweep_backward_vs_oracle(precision):
         got, ref = _backward_case(n, gi, precision)
         for k in GRAD_KEYS:
             if n == 1 and k in ("positions", "log_scales", "rotations", "raw_relax"):
-                # a lone Gaussian: geometry gradients are pure rounding noise
-                assert np.abs(np_(getattr(got, k))).max() < (1e-6 if precision == "f32" else 1e-12)
+                # a lone Gaussian: geometry gradients are pure rounding noise,
+                # bounded relative to the one real gradient (the amplitude's)
+                scale = np.linalg.norm(ref["raw_amplitude"])
+                noise = np.abs(np_(getattr(got, k))).max()
+                ref_noise = np.abs(ref[k]).max()   # the reference engine's own noise
+                print("n=1 noise", precision, k, noise, ref_noise, scale)
+                bound = max(4.0 * ref_noise, (1e-6 if precision == "f32" else 1e-12) * max(scale, 1.0))
+                assert noise <= bound, (k, noise, ref_noise)
                 continue
             e = rel_norm(np_(getattr(got, k)), ref[k])
             assert e <= TOL_G[precision], (n, gi, precision, k, e)
@@ -232,7 +238,7 @@ def test_kat_single_gaussian_renders_amplitude():
                          np.asarray([20.0]))
     for prec, tol in (("f64", 1e-9), ("f32", 1e-6)):
         o = gs.RenderOptions(precision=prec)
-        v = gs.forward(f, g, gs.build_brick_index(f, g, o), o).numpy()
+        v = gs.forward(f, g, gs.build_brick_index(f, g, o), o).volume().numpy()
         cov = v > 0
         assert cov.any()
         np.testing.assert_allclose(v[cov], amp, atol=tol)
@@ -245,7 +251,7 @@ def test_kat_two_equal_kernels_average():
                          np.asarray([np.log(0.25), np.log(4.0)]), np.full(2, 20.0))
     for prec in ("f32", "f64"):
         o = gs.RenderOptions(precision=prec)
-        v = gs.forward(f, g, gs.build_brick_index(f, g, o), o).numpy()
+        v = gs.forward(f, g, gs.build_brick_index(f, g, o), o).volume().numpy()
         assert abs(float(v[0, 0, 0]) - 0.5) <= 1e-6
 
 
@@ -256,13 +262,13 @@ def test_kat_normalization_properties():
     arrs = list(random_field_arrays(200, grid, 30))
     arrs[3] = np.full(200, 0.31)
     f = gs.GaussianField(*arrs)
-    out = gs.forward(f, grid, gs.build_brick_index(f, grid, opts), opts).numpy()
+    out = gs.forward(f, grid, gs.build_brick_index(f, grid, opts), opts).volume().numpy()
     amp = 1.0 / (1.0 + np.exp(-0.31))
     cov = out != 0.0
     assert cov.any() and np.abs(out[cov] - amp).max() <= 1e-6
     arrs = random_field_arrays(200, grid, 31)
     f = gs.GaussianField(*arrs)
-    out = gs.forward(f, grid, gs.build_brick_index(f, grid, opts), opts).numpy()
+    out = gs.forward(f, grid, gs.build_brick_index(f, grid, opts), opts).volume().numpy()
     amps = 1.0 / (1.0 + np.exp(-arrs[3]))
     cov = out != 0.0
     assert out[cov].min() >= amps.min() - 1e-6 and out[cov].max() <= amps.max() + 1e-6
@@ -271,7 +277,7 @@ def test_kat_normalization_properties():
     arrs2 = list(arrs)
     arrs2[4] = logit(0.37 * r)
     g2 = gs.GaussianField(*arrs2)
-    scaled = gs.forward(g2, grid, gs.build_brick_index(g2, grid, opts), opts).numpy()
+    scaled = gs.forward(g2, grid, gs.build_brick_index(g2, grid, opts), opts).volume().numpy()
     assert np.abs(scaled - out).max() <= 1e-6
 
 
@@ -426,7 +432,7 @@ def test_train_step_matches_unfused_api():
     g2 = gs.backward(f, lr.grid, idx, c, dl)
     assert abs(out.loss() - loss) <= 1e-12
     np.testing.assert_array_equal(np_(out.cache.I), np_(c.I))
-    for k in GRAD_KEYS:
-        assert rel_norm(np_(getattr(grads, k)), np_(getattr(g2, k))) <= 1e-6
+    for k in GRAD_KEYS:  # same kernels, same inputs: bit-identical
+        np.testing.assert_array_equal(np_(getattr(grads, k)), np_(getattr(g2, k)))
     meta = load_json("config1.json")
     assert abs(out.loss() - meta["loss"]) <= 1e-6
