@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-render512", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-count", action="store_true", help="skip the CUPTI launch count "
+                    "(needed under ncu)")
     return ap.parse_args()
 
 
@@ -336,7 +338,7 @@ def run_ours(args, dist, ws, rank, local):
                         "frac": bytes_alg / (t_dom * 1e-3) / 1e9 / hbm_peak}}
 
     # ---------------- kernel launches per step (CUPTI, outside the timed region)
-    launches = count_launches(train_iter)
+    launches = -1 if args.no_count else count_launches(train_iter)
 
     # ---------------- e2e: fit()'s loop with host buffers (pinned H2D target, loss D2H)
     e2e = None
