@@ -94,7 +94,8 @@ int gsv_device_sm_count(void);
  * (raster.py:175-198), computed in f64 with the reference's unfused operation
  * order (numpy einsum "nkm,nm->nk" sums (p0+p2)+p1).
  *   rec32  (N)   : gsv_record32, always written
- *   rec64  (N)   : gsv_record64, written when non-NULL
+ *   rec64  (N)   : gsv_record64, written when non-NULL (the f32 engine needs it
+ *                  too: its guard-band re-decisions use the f64 factor)
  *   counts (N)   : pairs Gaussian i emits inside the slab (0 if outside)
  *   box    (N,4) : int32 {blo_x | blo_y<<16, blo_z | nb_x<<16, nb_y | nb_z<<16, 0}
  *                  brick box of Gaussian i clipped to the slab.
@@ -154,8 +155,7 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  * dL/dI = sign(I-T)/V (l1) or 2(I-T)/V (l2) exactly as optimize.py:99-102.
  * ------------------------------------------------------------------------ */
 int gsv_forward(const double* positions, const gsv_record32* rec32,
-                const gsv_record64* rec64, const double* log_scales,
-                const double* rotations, const int64_t* starts,
+                const gsv_record64* rec64, const int64_t* starts,
                 const int32_t* gids, const gsv_grid* grid,
                 const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
                 int precision, void* S, void* W, void* I,
@@ -179,8 +179,7 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi,
  * the reference merges in (raster.py:512-516: stable argsort by gid keeps
  * ascending brick order).  partials: float (f32) or double (f64), (P,12). */
 int gsv_backward(const double* positions, const gsv_record32* rec32,
-                 const gsv_record64* rec64, const double* log_scales,
-                 const double* rotations, const int64_t* starts,
+                 const gsv_record64* rec64, const int64_t* starts,
                  const int32_t* gids, const int64_t* gstart,
                  const int32_t* box, const gsv_grid* grid,
                  const gsv_bricks* bricks, double cutoff_sigma,

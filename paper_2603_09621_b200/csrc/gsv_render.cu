@@ -25,22 +25,25 @@
 namespace gsv {
 namespace {
 
-constexpr int kFwdThreads = 256;
-constexpr int kBwdThreads = 128;
-constexpr float kGuardRel = 1e-4f;   // guard band relative to cutoff^2
-constexpr float kGuardMag = 4e-5f;   // guard band relative to term magnitude
+constexpr int kFwdThreads = 128;     // 4 warps; each warp owns one voxel tile
+constexpr int kBwdThreads = 256;
+constexpr int kBwdSmemVoxels = 2048; // brick voxels staged in smem by the backward
+// f32 truncation guard band.  Each v component is u + x e_x + y e_y + z e_z
+// with |terms| <= umax, so |dv| <= ~8 ulp(umax) ~ 4.8e-7 umax (f32 rounding of
+// p_b0 - mu, of L, of u and of three FMAs); near the cutoff
+// |d(d2)| <= 2 sqrt(3) cutoff |dv| + 3 ulp(d2) ~ 1.7e-6 cutoff umax + 2e-7 d2.
+// The band is ~6x that; inside it the f64 reference decision is recomputed.
+constexpr float kGuardRel = 2e-6f;   // x cutoff^2
+constexpr float kGuardMag = 1e-5f;   // x umax x cutoff
+constexpr unsigned kFull = 0xffffffffu;
 
-// Shared-memory record of one staged pair (f32 forward), 80 bytes.
+// Shared-memory record of one staged pair (f32 forward), 64 bytes: four
+// broadcast LDS.128 per (pair, warp-tile) evaluation.
 struct __align__(16) Pair32 {
-  float u[3];    // v at the brick's first voxel: L (p_b0 - mu)
-  float ex[3];   // v step per voxel along x: sx * L[:,0]
-  float ey[3];
-  float ez[3];
-  float amp, relax, guard;
-  int gid;
-  int box0;      // xlo | xhi<<8 | ylo<<16 | yhi<<24 (brick-local voxels)
-  int box1;      // zlo | zhi<<8
-  int _pad[2];
+  float4 a;  // u0 u1 u2 amp      u = L (p_b0 - mu): v at the brick's first voxel
+  float4 b;  // ex0 ex1 ex2 relax e_x = sx L[:,0]: v step per voxel along x
+  float4 c;  // ey0 ey1 ey2 guard
+  float4 d;  // ez0 ez1 ez2 gid
 };
 
 struct BrickGeom {
@@ -83,14 +86,29 @@ __device__ __forceinline__ void sub_range(double c, double h, double s, int n,
   hi = (int)b;
 }
 
-// f64 whitening factor recomputed from the field (guard-band path).
+// sub_range with precomputed 1/s (no f64 division on the staging path).
+__device__ __forceinline__ void sub_range_inv(double c, double h, double inv_s, int n, int& lo,
+                                              int& hi) {
+  const double ctr = c * inv_s, hv = h * inv_s;
+  double a = ceil(ctr - hv - 1e-3), b = floor(ctr + hv + 1e-3);
+  a = fmax(a, 0.0);
+  b = fmin(b, (double)(n - 1));
+  if (!(a <= b)) {
+    lo = 1 << 20;
+    hi = -1;
+    return;
+  }
+  lo = (int)a;
+  hi = (int)b;
+}
+
+// Exact f64 truncation decision of one (Gaussian, voxel) -- the rare
+// guard-band path -- from the f64 whitening factor written by preprocess.
 __device__ __noinline__ bool exact_live(int gid, int gx, int gy, int gz,
                                         const double* __restrict__ pos,
-                                        const double* __restrict__ ls,
-                                        const double* __restrict__ rot,
+                                        const gsv_record64* __restrict__ rec64,
                                         const gsv_grid& g, double cutoff2) {
-  double L[9];
-  whitening_f64(ls + 3 * (int64_t)gid, rot + 4 * (int64_t)gid, L);
+  const double* L = rec64[gid].l;
   const double* m = pos + 3 * (int64_t)gid;
   return ref_d2(L, m[0], m[1], m[2], gx, gy, gz, g) <= cutoff2;
 }
@@ -111,95 +129,165 @@ __device__ double block_sum(double v, double* sh) {
 }
 
 // --------------------------------------------------------------- forward f32
+// Thread -> voxel ownership.  A "unit" is a column pair of voxels (x, y, z0)
+// and (x, y, z0+1).  When the brick dims are multiples of 4 the 32 units of a
+// warp form one compact 4x4x4 voxel tile, so a Gaussian's 3-sigma box touches
+// as few warp tiles as possible; otherwise units are enumerated x-fastest.
+__device__ __forceinline__ void unit_voxel(int u, const gsv_bricks& k, bool tiled, int& x,
+                                           int& y, int& z0) {
+  if (tiled) {
+    const int t = u >> 5, l = u & 31;
+    const int tgx = k.bdx >> 2, tgy = k.bdy >> 2;
+    x = ((t % tgx) << 2) + (l & 3);
+    y = (((t / tgx) % tgy) << 2) + ((l >> 2) & 3);
+    z0 = ((t / (tgx * tgy)) << 2) + ((l >> 4) << 1);
+  } else {
+    x = u % k.bdx;
+    y = (u / k.bdx) % k.bdy;
+    z0 = (u / (k.bdx * k.bdy)) << 1;
+  }
+}
+
+__device__ __forceinline__ void live_accumulate(float d2, float amp, float relax, float guard,
+                                                float cut2, double cut2d, int gid, int gx,
+                                                int gy, int gz, const double* pos,
+                                                const gsv_record64* rec64,
+                                                const gsv_grid& g, float& S, float& W) {
+  if (d2 > cut2 + guard) return;
+  if (d2 >= cut2 - guard && !exact_live(gid, gx, gy, gz, pos, rec64, g, cut2d)) return;
+  const float w = __expf(-0.5f * d2) * relax;
+  S = fmaf(amp, w, S);
+  W += w;
+}
+
+// One CTA per brick, 4 warps.  Per chunk of 128 list entries: one thread per
+// pair stages the pair's brick-relative coefficients and a 4-bit mask of the
+// warp tiles its 3-sigma box overlaps; then every warp ballots the mask over
+// 32 pairs at a time and evaluates only the pairs that reach its tile, in
+// list order (deterministic accumulation, no atomics).
 __global__ void __launch_bounds__(kFwdThreads)
 forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
-                 const double* __restrict__ ls, const double* __restrict__ rot,
+                 const gsv_record64* __restrict__ rec64,
                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                  gsv_grid g, gsv_bricks k, float cut2, double cut2d, double eps_w,
                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
                  const float* __restrict__ target, int loss_kind, double vox_count,
                  float2* __restrict__ ab, double* __restrict__ loss_part) {
   __shared__ Pair32 sp[kFwdThreads];
+  __shared__ unsigned smask[kFwdThreads];
+  __shared__ int tbox[kFwdThreads / 32][6];
   __shared__ double red[kFwdThreads / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
   const BrickGeom bg = brick_geom(b, g, k);
   const int64_t lbeg = starts[lb], lend = starts[lb + 1];
-  const int nvb = k.bdx * k.bdy * k.bdz;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool tiled = ((k.bdx | k.bdy | k.bdz) & 3) == 0;
+  const int units = k.bdx * k.bdy * ((k.bdz + 1) >> 1);
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
+  const double isx = 1.0 / g.sx, isy = 1.0 / g.sy, isz = 1.0 / g.sz;
   double lsum = 0.0;
 
-  for (int vbase = 0; vbase < nvb; vbase += kFwdThreads) {
-    const int vl = vbase + tid;
-    const int lx = vl % k.bdx, ly = (vl / k.bdx) % k.bdy, lz = vl / (k.bdx * k.bdy);
-    const bool own = vl < nvb && lx < bg.ex && ly < bg.ey && lz < bg.ez;
+  for (int ubase = 0; ubase < units; ubase += kFwdThreads) {
+    const int u = ubase + tid;
+    int lx = 0, ly = 0, lz = 0;
+    if (u < units) unit_voxel(u, k, tiled, lx, ly, lz);
+    const bool ownA = u < units && lx < bg.ex && ly < bg.ey && lz < bg.ez;
+    const bool ownB = ownA && lz + 1 < bg.ez && lz + 1 < k.bdz;
+    // This warp's tile box (brick-local voxel coords) from its owned voxels.
+    {
+      int xl = ownA ? lx : 1 << 20, xh = ownA ? lx : -1;
+      int yl = ownA ? ly : 1 << 20, yh = ownA ? ly : -1;
+      int zl = ownA ? lz : 1 << 20, zh = ownB ? lz + 1 : (ownA ? lz : -1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        xl = min(xl, __shfl_xor_sync(kFull, xl, o));
+        xh = max(xh, __shfl_xor_sync(kFull, xh, o));
+        yl = min(yl, __shfl_xor_sync(kFull, yl, o));
+        yh = max(yh, __shfl_xor_sync(kFull, yh, o));
+        zl = min(zl, __shfl_xor_sync(kFull, zl, o));
+        zh = max(zh, __shfl_xor_sync(kFull, zh, o));
+      }
+      if (lane == 0) {
+        tbox[warp][0] = xl; tbox[warp][1] = xh; tbox[warp][2] = yl;
+        tbox[warp][3] = yh; tbox[warp][4] = zl; tbox[warp][5] = zh;
+      }
+    }
     const float fx = (float)lx, fy = (float)ly, fz = (float)lz;
-    float accS = 0.f, accW = 0.f;
+    const int gx = bg.x0 + lx, gy = bg.y0 + ly, gz = bg.z0 + lz;
+    float accSA = 0.f, accWA = 0.f, accSB = 0.f, accWB = 0.f;
 
     for (int64_t cb = lbeg; cb < lend; cb += kFwdThreads) {
       const int cnt = (int)min((int64_t)kFwdThreads, lend - cb);
-      __syncthreads();
+      __syncthreads();  // previous chunk consumed; tile boxes visible
       if (tid < cnt) {
         const int gid = gids[cb + tid];
         const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
-        const float4 q0 = r4[0], q1 = r4[1], q2 = r4[2], q3 = r4[3];
+        const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
         const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
         const double* m = pos + 3 * (int64_t)gid;
-        const double cx = m[0] - bg.px, cy = m[1] - bg.py, cz = m[2] - bg.pz;  // mu - p_b0
-        const float c0 = (float)(-cx), c1 = (float)(-cy), c2 = (float)(-cz);   // p_b0 - mu
-        Pair32 p;
-        float umax = 0.f;
+        const double cx = __ldg(m) - bg.px, cy = __ldg(m + 1) - bg.py, cz = __ldg(m + 2) - bg.pz;
+        const float c0 = (float)(-cx), c1 = (float)(-cy), c2 = (float)(-cz);  // p_b0 - mu
+        float u3[3], e[3][3], umax = 0.f;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          p.u[a] = fmaf(L[3 * a + 0], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
-          p.ex[a] = L[3 * a + 0] * fsx;
-          p.ey[a] = L[3 * a + 1] * fsy;
-          p.ez[a] = L[3 * a + 2] * fsz;
-          umax = fmaxf(umax, fabsf(p.u[a]) + fabsf(p.ex[a]) * k.bdx +
-                                 fabsf(p.ey[a]) * k.bdy + fabsf(p.ez[a]) * k.bdz);
+          u3[a] = fmaf(L[3 * a + 0], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
+          e[0][a] = L[3 * a + 0] * fsx;
+          e[1][a] = L[3 * a + 1] * fsy;
+          e[2][a] = L[3 * a + 2] * fsz;
+          umax = fmaxf(umax, fabsf(u3[a]) + fabsf(e[0][a]) * k.bdx + fabsf(e[1][a]) * k.bdy +
+                                 fabsf(e[2][a]) * k.bdz);
         }
-        p.amp = q2.y;
-        p.relax = q2.z;
-        p.guard = fmaxf(kGuardRel * cut2, kGuardMag * umax * (umax + 3.f));
-        p.gid = gid;
-        int xl, xh, yl, yh, zl, zh;
-        sub_range(cx, (double)q2.w, g.sx, bg.ex, xl, xh);
-        sub_range(cy, (double)q3.x, g.sy, bg.ey, yl, yh);
-        sub_range(cz, (double)q3.y, g.sz, bg.ez, zl, zh);
-        if (xl > xh || yl > yh || zl > zh) {
-          xl = 255; xh = 0;
-        }
-        p.box0 = (xl & 255) | ((xh & 255) << 8) | ((yl & 255) << 16) | ((yh & 255) << 24);
-        p.box1 = (zl & 255) | ((zh & 255) << 8);
-        p._pad[0] = p._pad[1] = 0;
+        const float guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
+        Pair32 p;
+        p.a = make_float4(u3[0], u3[1], u3[2], q2.y);
+        p.b = make_float4(e[0][0], e[0][1], e[0][2], q2.z);
+        p.c = make_float4(e[1][0], e[1][1], e[1][2], guard);
+        p.d = make_float4(e[2][0], e[2][1], e[2][2], __int_as_float(gid));
         sp[tid] = p;
+        // Conservative voxel box of the 3-sigma ellipsoid, brick-local.
+        int xl, xh, yl, yh, zl, zh;
+        sub_range_inv(cx, (double)q2.w, isx, bg.ex, xl, xh);
+        sub_range_inv(cy, (double)q3.x, isy, bg.ey, yl, yh);
+        sub_range_inv(cz, (double)q3.y, isz, bg.ez, zl, zh);
+        unsigned msk = 0;
+#pragma unroll
+        for (int w = 0; w < kFwdThreads / 32; ++w) {
+          const bool hit = xl <= tbox[w][1] && xh >= tbox[w][0] && yl <= tbox[w][3] &&
+                           yh >= tbox[w][2] && zl <= tbox[w][5] && zh >= tbox[w][4];
+          msk |= hit ? (1u << w) : 0u;
+        }
+        smask[tid] = msk;
       }
       __syncthreads();
-      if (own) {
-        for (int j = 0; j < cnt; ++j) {
-          const int b0 = sp[j].box0, b1 = sp[j].box1;
-          if (lx < (b0 & 255) || lx > ((b0 >> 8) & 255) || ly < ((b0 >> 16) & 255) ||
-              ly > ((b0 >> 24) & 255) || lz < (b1 & 255) || lz > ((b1 >> 8) & 255))
-            continue;
-          const Pair32& p = sp[j];
-          const float v0 = fmaf(fz, p.ez[0], fmaf(fy, p.ey[0], fmaf(fx, p.ex[0], p.u[0])));
-          const float v1 = fmaf(fz, p.ez[1], fmaf(fy, p.ey[1], fmaf(fx, p.ex[1], p.u[1])));
-          const float v2 = fmaf(fz, p.ez[2], fmaf(fy, p.ey[2], fmaf(fx, p.ex[2], p.u[2])));
-          const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
-          if (d2 > cut2 + p.guard) continue;
-          if (d2 >= cut2 - p.guard &&
-              !exact_live(p.gid, bg.x0 + lx, bg.y0 + ly, bg.z0 + lz, pos, ls, rot, g, cut2d))
-            continue;
-          const float w = __expf(-0.5f * d2) * p.relax;
-          accS = fmaf(p.amp, w, accS);
-          accW += w;
+      for (int base = 0; base < cnt; base += 32) {
+        const unsigned mm = (base + lane < cnt) ? smask[base + lane] : 0u;
+        unsigned ball = __ballot_sync(kFull, (mm >> warp) & 1u);
+        while (ball) {
+          const int j = base + __ffs(ball) - 1;
+          ball &= ball - 1;
+          const float4 pa = sp[j].a, pb = sp[j].b, pc = sp[j].c, pd = sp[j].d;
+          const float v0 = fmaf(fz, pd.x, fmaf(fy, pc.x, fmaf(fx, pb.x, pa.x)));
+          const float v1 = fmaf(fz, pd.y, fmaf(fy, pc.y, fmaf(fx, pb.y, pa.y)));
+          const float v2 = fmaf(fz, pd.z, fmaf(fy, pc.z, fmaf(fx, pb.z, pa.z)));
+          const float d2a = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+          const float w0 = v0 + pd.x, w1 = v1 + pd.y, w2 = v2 + pd.z;  // voxel z0+1
+          const float d2b = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
+          const int gid = __float_as_int(pd.w);
+          live_accumulate(d2a, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz, pos, rec64, g,
+                          accSA, accWA);
+          live_accumulate(d2b, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz + 1, pos, rec64,
+                          g, accSB, accWB);
         }
       }
     }
-    if (own) {
-      const int64_t lin = (int64_t)(bg.x0 + lx) +
-                          (int64_t)g.nx * ((bg.y0 + ly) + (int64_t)g.ny * (bg.z0 + lz));
+    // Epilogue: normalise, store, fused loss (optimize.py:91-103).
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool own = h == 0 ? ownA : ownB;
+      if (!own) continue;
+      const float accS = h == 0 ? accSA : accSB, accW = h == 0 ? accWA : accWB;
+      const int64_t lin = (int64_t)gx + (int64_t)g.nx * (gy + (int64_t)g.ny * (gz + h));
       const bool cov = (double)accW >= eps_w;
       const float iv = cov ? __fdiv_rn(accS, accW) : 0.f;
       S[lin] = accS;
@@ -358,88 +446,197 @@ __global__ void backward_prep_kernel(const T* __restrict__ W, const T* __restric
 }
 
 // ------------------------------------------------------------- backward f32
-__global__ void __launch_bounds__(kBwdThreads)
+// One thread per (brick, Gaussian) pair, but NOT in list order: the work of a
+// pair is its live voxel count, which varies 0..~50 inside a brick, and a warp
+// runs as long as its heaviest lane.  Each CTA therefore first bins its pairs
+// by sub-box volume (a smem counting sort, heaviest first) and hands warps
+// pairs of similar cost.  Processing order cannot change any result: each
+// pair's partial is computed by one thread in a fixed voxel order and written
+// to its own slot.  Per pair the live voxels are found row by row: along x,
+// d2(x) = |v_row + x e_x|^2 is a quadratic, so the x-span where it can be
+// <= cutoff^2 (+ guard) is solved directly; every voxel in it is still decided
+// exactly as the forward decides.  The brick's {dL/dI / W, I} are staged in
+// shared memory.  Accumulates sum cw v (whitened) and sum cw delta delta^T;
+// d_mu = L^T sum cw v is formed once per pair.
+constexpr int kBwdChunk = 2048;
+constexpr int kBwdBuckets = 128;
+
+template <bool kSmem>
+__global__ void __launch_bounds__(kBwdThreads, 2)
 backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
-                  const double* __restrict__ ls, const double* __restrict__ rot,
+                  const gsv_record64* __restrict__ rec64,
                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                   const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
                   gsv_grid g, gsv_bricks k, float cut2, double cut2d,
                   const float2* __restrict__ ab, float4* __restrict__ partials) {
+  __shared__ float2 sab[kSmem ? kBwdSmemVoxels : 1];
+  __shared__ int2 sbox[kBwdChunk];
+  __shared__ unsigned short sorder[kBwdChunk];
+  __shared__ int shist[kBwdBuckets];
   const int lb = blockIdx.x;
   const int b = (int)slab_first(k) + lb;
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  if (lbeg == lend) return;
   const BrickGeom bg = brick_geom(b, g, k);
   const BrickXYZ bc = brick_xyz(b, k);
-  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  const int tid = threadIdx.x;
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
-  for (int64_t j = lbeg + threadIdx.x; j < lend; j += kBwdThreads) {
-    const int gid = gids[j];
-    const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
-    const float4 q0 = r4[0], q1 = r4[1], q2 = r4[2], q3 = r4[3];
-    const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
-    const float A = q2.y, r = q2.z;
-    const double* m = pos + 3 * (int64_t)gid;
-    const double cx = m[0] - bg.px, cy = m[1] - bg.py, cz = m[2] - bg.pz;  // mu - p_b0
-    int xl, xh, yl, yh, zl, zh;
-    sub_range(cx, (double)q2.w, g.sx, bg.ex, xl, xh);
-    sub_range(cy, (double)q3.x, g.sy, bg.ey, yl, yh);
-    sub_range(cz, (double)q3.y, g.sz, bg.ez, zl, zh);
-    const float c0 = (float)(-cx), c1 = (float)(-cy), c2 = (float)(-cz);
-    float umax = 0.f;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const float ua = fmaf(L[3 * a], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
-      umax = fmaxf(umax, fabsf(ua) + fabsf(L[3 * a] * fsx) * k.bdx +
-                             fabsf(L[3 * a + 1] * fsy) * k.bdy + fabsf(L[3 * a + 2] * fsz) * k.bdz);
+  const double isx = 1.0 / g.sx, isy = 1.0 / g.sy, isz = 1.0 / g.sz;
+  if (kSmem) {
+    const int nv = bg.ex * bg.ey * bg.ez;
+    for (int v = tid; v < nv; v += kBwdThreads) {
+      const int x = v % bg.ex, y = (v / bg.ex) % bg.ey, z = v / (bg.ex * bg.ey);
+      const int64_t lin =
+          (int64_t)(bg.x0 + x) + (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
+      sab[x + k.bdx * (y + k.bdy * z)] = __ldg(ab + lin);
     }
-    const float guard = fmaxf(kGuardRel * cut2, kGuardMag * umax * (umax + 3.f));
-    float acc_a = 0.f, acc_r = 0.f, mu0 = 0.f, mu1 = 0.f, mu2 = 0.f;
-    float g00 = 0.f, g11 = 0.f, g22 = 0.f, g01 = 0.f, g02 = 0.f, g12 = 0.f;
-    for (int z = zl; z <= zh; ++z) {
-      const float dz = fmaf((float)z, fsz, c2);
-      for (int y = yl; y <= yh; ++y) {
-        const float dy = fmaf((float)y, fsy, c1);
-        const int64_t row = (int64_t)bg.x0 + (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
-        for (int x = xl; x <= xh; ++x) {
-          const float2 v_ab = __ldg(ab + row + x);
-          if (v_ab.x == 0.f) continue;
-          const float dx = fmaf((float)x, fsx, c0);
-          const float v0 = fmaf(L[0], dx, fmaf(L[1], dy, L[2] * dz));
-          const float v1 = fmaf(L[3], dx, fmaf(L[4], dy, L[5] * dz));
-          const float v2 = fmaf(L[6], dx, fmaf(L[7], dy, L[8] * dz));
-          const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
-          if (d2 > cut2 + guard) continue;
-          if (d2 >= cut2 - guard &&
-              !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, pos, ls, rot, g, cut2d))
-            continue;
-          const float kern = __expf(-0.5f * d2);
-          const float w = kern * r;
-          acc_a = fmaf(w, v_ab.x, acc_a);
-          const float common = v_ab.x * (A - v_ab.y);   // dL/dI (A - I) / W
-          acc_r = fmaf(common, kern, acc_r);
-          const float cw = common * w;
-          mu0 = fmaf(cw, fmaf(L[0], v0, fmaf(L[3], v1, L[6] * v2)), mu0);
-          mu1 = fmaf(cw, fmaf(L[1], v0, fmaf(L[4], v1, L[7] * v2)), mu1);
-          mu2 = fmaf(cw, fmaf(L[2], v0, fmaf(L[5], v1, L[8] * v2)), mu2);
-          const float h = -0.5f * cw;
-          const float hx = h * dx, hy = h * dy;
-          g00 = fmaf(hx, dx, g00);
-          g11 = fmaf(hy, dy, g11);
-          g22 = fmaf(h * dz, dz, g22);
-          g01 = fmaf(hx, dy, g01);
-          g02 = fmaf(hx, dz, g02);
-          g12 = fmaf(hy, dz, g12);
+  }
+  for (int64_t cbase = lbeg; cbase < lend; cbase += kBwdChunk) {
+    const int cnt = (int)min((int64_t)kBwdChunk, lend - cbase);
+    if (tid < kBwdBuckets) shist[tid] = 0;
+    __syncthreads();
+    // (1) sub-box of every pair; histogram of its volume (heaviest bucket 0).
+    for (int t = tid; t < cnt; t += kBwdThreads) {
+      const int gid = gids[cbase + t];
+      const float4 q2 = __ldg(reinterpret_cast<const float4*>(rec + gid) + 2);
+      const float4 q3 = __ldg(reinterpret_cast<const float4*>(rec + gid) + 3);
+      const double* m = pos + 3 * (int64_t)gid;
+      int xl, xh, yl, yh, zl, zh;
+      sub_range_inv(__ldg(m) - bg.px, (double)q2.w, isx, bg.ex, xl, xh);
+      sub_range_inv(__ldg(m + 1) - bg.py, (double)q3.x, isy, bg.ey, yl, yh);
+      sub_range_inv(__ldg(m + 2) - bg.pz, (double)q3.y, isz, bg.ez, zl, zh);
+      int vol = 0;
+      if (xl <= xh && yl <= yh && zl <= zh) {
+        vol = (xh - xl + 1) * (yh - yl + 1) * (zh - zl + 1);
+      } else {
+        xl = 1; xh = 0; yl = 0; yh = 0; zl = 0; zh = 0;
+      }
+      sbox[t] = make_int2(xl | (xh << 8) | (yl << 16) | (yh << 24), zl | (zh << 8));
+      atomicAdd(&shist[kBwdBuckets - 1 - min(vol, kBwdBuckets - 1)], 1);
+    }
+    __syncthreads();
+    // (2) exclusive scan of the histogram (warp 0, 4 buckets per lane).
+    if (tid < 32) {
+      int v[4], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { v[i] = shist[4 * tid + i]; sum += v[i]; }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(kFull, incl, o);
+        if (tid >= o) incl += n;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { shist[4 * tid + i] = run; run += v[i]; }
+    }
+    __syncthreads();
+    // (3) scatter pair slots into cost order (order within a bucket is free).
+    for (int t = tid; t < cnt; t += kBwdThreads) {
+      const int2 bx = sbox[t];
+      const int xl = bx.x & 255, xh = (bx.x >> 8) & 255, yl = (bx.x >> 16) & 255,
+                yh = (bx.x >> 24) & 255, zl = bx.y & 255, zh = (bx.y >> 8) & 255;
+      const int vol = xl <= xh ? (xh - xl + 1) * (yh - yl + 1) * (zh - zl + 1) : 0;
+      const int slot = atomicAdd(&shist[kBwdBuckets - 1 - min(vol, kBwdBuckets - 1)], 1);
+      sorder[slot] = (unsigned short)t;
+    }
+    __syncthreads();
+    // (4) per-pair gradient partials.
+    for (int s = tid; s < cnt; s += kBwdThreads) {
+      const int t = sorder[s];
+      const int gid = gids[cbase + t];
+      const int2 bx = sbox[t];
+      const int xl = bx.x & 255, xh = (bx.x >> 8) & 255, yl = (bx.x >> 16) & 255,
+                yh = (bx.x >> 24) & 255, zl = bx.y & 255, zh = (bx.y >> 8) & 255;
+      const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+      const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2);
+      const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+      const float A = q2.y, r = q2.z;
+      const double* m = pos + 3 * (int64_t)gid;
+      const float c0 = (float)(bg.px - __ldg(m)), c1 = (float)(bg.py - __ldg(m + 1)),
+                  c2 = (float)(bg.pz - __ldg(m + 2));   // p_b0 - mu
+      float u[3], ex[3], ey[3], ez[3], umax = 0.f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        u[a] = fmaf(L[3 * a], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
+        ex[a] = L[3 * a] * fsx;
+        ey[a] = L[3 * a + 1] * fsy;
+        ez[a] = L[3 * a + 2] * fsz;
+        umax = fmaxf(umax, fabsf(u[a]) + fabsf(ex[a]) * k.bdx + fabsf(ey[a]) * k.bdy +
+                               fabsf(ez[a]) * k.bdz);
+      }
+      const float guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
+      const float qa = fmaf(ex[0], ex[0], fmaf(ex[1], ex[1], ex[2] * ex[2]));
+      const float inv_qa = 1.0f / qa;
+      const float lim = cut2 + guard, lo_band = cut2 - guard;
+      float acc_a = 0.f, acc_r = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
+      float g00 = 0.f, g11 = 0.f, g22 = 0.f, g01 = 0.f, g02 = 0.f, g12 = 0.f;
+      for (int z = zl; z <= zh; ++z) {
+        const float dz = fmaf((float)z, fsz, c2);
+        for (int y = yl; y <= yh; ++y) {
+          const float dy = fmaf((float)y, fsy, c1);
+          const float vr0 = fmaf((float)z, ez[0], fmaf((float)y, ey[0], u[0]));
+          const float vr1 = fmaf((float)z, ez[1], fmaf((float)y, ey[1], u[1]));
+          const float vr2 = fmaf((float)z, ez[2], fmaf((float)y, ey[2], u[2]));
+          const float qb = fmaf(vr0, ex[0], fmaf(vr1, ex[1], vr2 * ex[2]));
+          const float qc = fmaf(vr0, vr0, fmaf(vr1, vr1, vr2 * vr2));
+          // (qa x + qb)^2 <= qb^2 - qa (qc - lim)
+          const float disc = fmaf(qb, qb, -qa * (qc - lim));
+          if (!(disc >= 0.f)) continue;
+          const float sq = sqrtf(disc);
+          const int xa = max(xl, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
+          const int xb = min(xh, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
+          const int srow = k.bdx * (y + k.bdy * z);
+          const int64_t grow =
+              (int64_t)bg.x0 + (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
+          for (int x = xa; x <= xb; ++x) {
+            const float2 v_ab = kSmem ? sab[srow + x] : __ldg(ab + grow + x);
+            if (v_ab.x == 0.f) continue;
+            const float fx = (float)x;
+            const float v0 = fmaf(fx, ex[0], vr0);
+            const float v1 = fmaf(fx, ex[1], vr1);
+            const float v2 = fmaf(fx, ex[2], vr2);
+            const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+            if (d2 > lim) continue;
+            if (d2 >= lo_band &&
+                !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
+              continue;
+            const float kern = __expf(-0.5f * d2);
+            const float w = kern * r;
+            acc_a = fmaf(w, v_ab.x, acc_a);
+            const float common = v_ab.x * (A - v_ab.y);   // dL/dI (A - I) / W
+            acc_r = fmaf(common, kern, acc_r);
+            const float cw = common * w;
+            s0 = fmaf(cw, v0, s0);
+            s1 = fmaf(cw, v1, s1);
+            s2 = fmaf(cw, v2, s2);
+            const float dx = fmaf(fx, fsx, c0);
+            const float h = -0.5f * cw;
+            const float hx = h * dx, hy = h * dy;
+            g00 = fmaf(hx, dx, g00);
+            g11 = fmaf(hy, dy, g11);
+            g22 = fmaf(h * dz, dz, g22);
+            g01 = fmaf(hx, dy, g01);
+            g02 = fmaf(hx, dz, g02);
+            g12 = fmaf(hy, dz, g12);
+          }
         }
       }
+      // d_mu = sum cw Sigma^-1 delta = L^T (sum cw v)
+      const float mu0 = fmaf(L[0], s0, fmaf(L[3], s1, L[6] * s2));
+      const float mu1 = fmaf(L[1], s0, fmaf(L[4], s1, L[7] * s2));
+      const float mu2 = fmaf(L[2], s0, fmaf(L[5], s1, L[8] * s2));
+      const GBox gb = unpack_box(box, gid);
+      const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
+      // A caller-built list may hold a pair the binning would not emit: skip it.
+      if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
+      const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+      float4* dst = partials + 3 * e;
+      dst[0] = make_float4(acc_a, acc_r, mu0, mu1);
+      dst[1] = make_float4(mu2, g00, g11, g22);
+      dst[2] = make_float4(g01, g02, g12, 0.f);
     }
-    const GBox gb = unpack_box(box, gid);
-    const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
-    // A caller-built list may hold a pair the binning would not emit: skip it.
-    if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
-    const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
-    float4* dst = partials + 3 * e;
-    dst[0] = make_float4(acc_a, acc_r, mu0, mu1);
-    dst[1] = make_float4(mu2, g00, g11, g22);
-    dst[2] = make_float4(g01, g02, g12, 0.f);
+    __syncthreads();
   }
 }
 
@@ -584,14 +781,14 @@ using namespace gsv;
 extern "C" {
 
 int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_record64* rec64,
-                const double* log_scales, const double* rotations, const int64_t* starts,
+                const int64_t* starts,
                 const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
                 double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
                 double* loss_part, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
-  GSV_REQUIRE(precision == 0 || rec64 != nullptr, "f64 forward needs rec64");
+  GSV_REQUIRE(rec64 != nullptr, "forward needs rec64 (f64 whitening factors)");
   GSV_REQUIRE(target == nullptr || (ab != nullptr && loss_part != nullptr),
               "fused loss needs ab and loss_part");
   GSV_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (l1) or 1 (l2)");
@@ -601,7 +798,7 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
   cudaStream_t s = as_stream(stream);
   if (precision == 0) {
     forward32_kernel<<<(unsigned)nb, kFwdThreads, 0, s>>>(
-        positions, rec32, log_scales, rotations, starts, gids, *grid, *bricks, (float)cut2d,
+        positions, rec32, rec64, starts, gids, *grid, *bricks, (float)cut2d,
         cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
         (float2*)ab, loss_part);
     GSV_CHECK_LAUNCH("forward32_kernel");
@@ -642,21 +839,27 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi, const gs
 }
 
 int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_record64* rec64,
-                 const double* log_scales, const double* rotations, const int64_t* starts,
+                 const int64_t* starts,
                  const int32_t* gids, const int64_t* gstart, const int32_t* box,
                  const gsv_grid* grid, const gsv_bricks* bricks, double cutoff_sigma,
                  int precision, const void* ab, void* partials, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
-  GSV_REQUIRE(precision == 0 || rec64 != nullptr, "f64 backward needs rec64");
+  GSV_REQUIRE(rec64 != nullptr, "backward needs rec64 (f64 whitening factors)");
   const int64_t nb = slab_bricks(*bricks);
   if (nb == 0) return GSV_OK;
   const double cut2d = cutoff_sigma * cutoff_sigma;
   cudaStream_t s = as_stream(stream);
   if (precision == 0) {
-    backward32_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(
-        positions, rec32, log_scales, rotations, starts, gids, gstart, box, *grid, *bricks,
-        (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
+    const bool smem = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz <= kBwdSmemVoxels;
+    if (smem)
+      backward32_kernel<true><<<(unsigned)nb, kBwdThreads, 0, s>>>(
+          positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
+          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
+    else
+      backward32_kernel<false><<<(unsigned)nb, kBwdThreads, 0, s>>>(
+          positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
+          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
     GSV_CHECK_LAUNCH("backward32_kernel");
   } else {
     backward64_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(

@@ -191,7 +191,9 @@ def _preprocess(f: GaussianField, grid: GridSpec, cutoff_sigma: float, brick_dim
     lib = _lib.lib()
     n, dev = f.count, f.device
     rec32 = torch.empty((n, 16), dtype=torch.float32, device=dev)
-    rec64 = torch.empty((n, 12), dtype=torch.float64, device=dev) if want64 else None
+    # rec64 is always built: the f64 engine uses it, and the f32 engine's
+    # guard-band re-decisions read the f64 whitening factor from it.
+    rec64 = torch.empty((n, 12), dtype=torch.float64, device=dev)
     counts = torch.empty(n, dtype=torch.int32, device=dev)
     box = torch.empty((n, 4), dtype=torch.int32, device=dev)
     _lib.check(lib.gsv_preprocess(
@@ -275,10 +277,9 @@ def _check_index(f: GaussianField, grid: GridSpec, idx: BrickIndex, opts: Render
 def _records(f, grid, idx: BrickIndex, opts: RenderOptions):
     """rec32 (and rec64 for f64) for the current field state."""
     aux = idx._aux
-    want64 = opts.precision == "f64"
-    if aux is not None and aux.field_version == f.version and (aux.rec64 is not None or not want64):
+    if aux is not None and aux.field_version == f.version:
         return aux.rec32, aux.rec64
-    rec32, rec64, _, _ = _preprocess(f, grid, opts.cutoff_sigma, idx.brick_dims, idx.slab, want64)
+    rec32, rec64, _, _ = _preprocess(f, grid, opts.cutoff_sigma, idx.brick_dims, idx.slab, True)
     return rec32, rec64
 
 
@@ -287,9 +288,9 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
                   ab=None, loss_part=None):
     lib = _lib.lib()
     _lib.check(lib.gsv_forward(
-        f.positions.data_ptr(), rec32.data_ptr(), _lib.ptr(rec64), f.log_scales.data_ptr(),
-        f.rotations.data_ptr(), idx.starts.data_ptr(), idx.gids.data_ptr(),
-        _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
+        f.positions.data_ptr(), rec32.data_ptr(), rec64.data_ptr(), idx.starts.data_ptr(),
+        idx.gids.data_ptr(), _lib.make_grid(grid),
+        _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.stream_ptr()), "forward")
@@ -336,8 +337,8 @@ def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: b
     if timer is not None:
         timer("backward")
     _lib.check(lib.gsv_backward(
-        f.positions.data_ptr(), rec32.data_ptr(), _lib.ptr(rec64), f.log_scales.data_ptr(),
-        f.rotations.data_ptr(), idx.starts.data_ptr(), idx.gids.data_ptr(), gstart.data_ptr(),
+        f.positions.data_ptr(), rec32.data_ptr(), rec64.data_ptr(), idx.starts.data_ptr(),
+        idx.gids.data_ptr(), gstart.data_ptr(),
         box.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), partials.data_ptr(),
         _lib.stream_ptr()), "backward")
