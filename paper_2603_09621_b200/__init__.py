@@ -20,7 +20,7 @@ from .raster import (DEFAULT_BRICK_DIMS, BrickIndex, GradientBuffer, RenderCache
                      build_brick_index, forward, merge_gradients, set_worker_count,
                      worker_count)
 from .optimize import (AdamState, FitConfig, FitReport, fit, loss_and_grad, step_optimizer)
-from .train import StepOutput, TrainStep
+from .train import Renderer, StepOutput, TrainStep
 
 __all__ = [
     "__version__",
@@ -33,5 +33,5 @@ __all__ = [
     "DEFAULT_BRICK_DIMS", "BrickIndex", "RenderCache", "GradientBuffer", "build_brick_index",
     "forward", "backward", "merge_gradients", "set_worker_count", "worker_count",
     "FitConfig", "FitReport", "AdamState", "fit", "loss_and_grad", "step_optimizer",
-    "TrainStep", "StepOutput",
+    "TrainStep", "StepOutput", "Renderer",
 ]

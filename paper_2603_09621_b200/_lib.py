@@ -153,3 +153,29 @@ def workspace(nbytes: int, device, key: str = "default") -> torch.Tensor:
         buf = torch.empty(max(int(nbytes * 1.25), 1 << 16), dtype=torch.uint8, device=device)
         _ws_cache[k] = buf
     return buf
+
+
+class BufferPool:
+    """Grow-only device buffers reused across iterations (train step / render).
+
+    ``get(name, shape, dtype)`` returns a view of a persistent flat buffer, so
+    the per-iteration allocations of the hot loop never reach cudaMalloc.
+    Views stay valid until the next ``get`` of the same name.
+    """
+
+    def __init__(self, device):
+        self.device = device
+        self._bufs: dict = {}
+
+    def get(self, name: str, shape, dtype) -> torch.Tensor:
+        shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+        numel = 1
+        for s in shape:
+            numel *= s
+        numel = max(numel, 1)
+        key = (name, dtype)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < numel:
+            buf = torch.empty(int(numel * 1.1) + 64, dtype=dtype, device=self.device)
+            self._bufs[key] = buf
+        return buf[:numel].view(shape) if shape else buf[:1].view(())

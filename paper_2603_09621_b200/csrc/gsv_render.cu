@@ -160,11 +160,14 @@ __device__ __forceinline__ void live_accumulate(float d2, float amp, float relax
   W += w;
 }
 
-// One CTA per brick, 4 warps.  Per chunk of 128 list entries: one thread per
-// pair stages the pair's brick-relative coefficients and a 4-bit mask of the
-// warp tiles its 3-sigma box overlaps; then every warp ballots the mask over
-// 32 pairs at a time and evaluates only the pairs that reach its tile, in
-// list order (deterministic accumulation, no atomics).
+// One CTA per brick, 4 warps, each owning one voxel tile (2 voxels per lane).
+// Warps walk the brick's list independently -- no CTA barrier in the pair
+// loop: per round of 32 list entries every lane stages one pair into the
+// warp's private smem slots and tests its 3-sigma box against the warp's
+// tile; a ballot leaves only the pairs that reach the tile, evaluated in list
+// order (deterministic accumulation, no atomics).  Staging is repeated per
+// warp (4x, L1-resident loads) -- cheaper than the barrier stalls of shared
+// staging, where every warp waits for the slowest tile each chunk.
 __global__ void __launch_bounds__(kFwdThreads)
 forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
                  const gsv_record64* __restrict__ rec64,
@@ -173,19 +176,18 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
                  const float* __restrict__ target, int loss_kind, double vox_count,
                  float2* __restrict__ ab, double* __restrict__ loss_part) {
-  __shared__ Pair32 sp[kFwdThreads];
-  __shared__ unsigned smask[kFwdThreads];
-  __shared__ int tbox[kFwdThreads / 32][6];
+  __shared__ Pair32 sp[kFwdThreads];   // 32 slots per warp
   __shared__ double red[kFwdThreads / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
   const BrickGeom bg = brick_geom(b, g, k);
   const int64_t lbeg = starts[lb], lend = starts[lb + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Pair32* wsp = sp + (warp << 5);
   const bool tiled = ((k.bdx | k.bdy | k.bdz) & 3) == 0;
   const int units = k.bdx * k.bdy * ((k.bdz + 1) >> 1);
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
-  const double isx = 1.0 / g.sx, isy = 1.0 / g.sy, isz = 1.0 / g.sz;
+  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
   double lsum = 0.0;
 
   for (int ubase = 0; ubase < units; ubase += kFwdThreads) {
@@ -195,91 +197,82 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
     const bool ownA = u < units && lx < bg.ex && ly < bg.ey && lz < bg.ez;
     const bool ownB = ownA && lz + 1 < bg.ez && lz + 1 < k.bdz;
     // This warp's tile box (brick-local voxel coords) from its owned voxels.
-    {
-      int xl = ownA ? lx : 1 << 20, xh = ownA ? lx : -1;
-      int yl = ownA ? ly : 1 << 20, yh = ownA ? ly : -1;
-      int zl = ownA ? lz : 1 << 20, zh = ownB ? lz + 1 : (ownA ? lz : -1);
+    int txl = ownA ? lx : 1 << 20, txh = ownA ? lx : -(1 << 20);
+    int tyl = ownA ? ly : 1 << 20, tyh = ownA ? ly : -(1 << 20);
+    int tzl = ownA ? lz : 1 << 20, tzh = ownB ? lz + 1 : (ownA ? lz : -(1 << 20));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        xl = min(xl, __shfl_xor_sync(kFull, xl, o));
-        xh = max(xh, __shfl_xor_sync(kFull, xh, o));
-        yl = min(yl, __shfl_xor_sync(kFull, yl, o));
-        yh = max(yh, __shfl_xor_sync(kFull, yh, o));
-        zl = min(zl, __shfl_xor_sync(kFull, zl, o));
-        zh = max(zh, __shfl_xor_sync(kFull, zh, o));
-      }
-      if (lane == 0) {
-        tbox[warp][0] = xl; tbox[warp][1] = xh; tbox[warp][2] = yl;
-        tbox[warp][3] = yh; tbox[warp][4] = zl; tbox[warp][5] = zh;
-      }
+    for (int o = 16; o > 0; o >>= 1) {
+      txl = min(txl, __shfl_xor_sync(kFull, txl, o));
+      txh = max(txh, __shfl_xor_sync(kFull, txh, o));
+      tyl = min(tyl, __shfl_xor_sync(kFull, tyl, o));
+      tyh = max(tyh, __shfl_xor_sync(kFull, tyh, o));
+      tzl = min(tzl, __shfl_xor_sync(kFull, tzl, o));
+      tzh = max(tzh, __shfl_xor_sync(kFull, tzh, o));
     }
+    const float ftxl = (float)txl, ftxh = (float)txh, ftyl = (float)tyl, ftyh = (float)tyh,
+                ftzl = (float)tzl, ftzh = (float)tzh;
     const float fx = (float)lx, fy = (float)ly, fz = (float)lz;
     const int gx = bg.x0 + lx, gy = bg.y0 + ly, gz = bg.z0 + lz;
     float accSA = 0.f, accWA = 0.f, accSB = 0.f, accWB = 0.f;
 
-    for (int64_t cb = lbeg; cb < lend; cb += kFwdThreads) {
-      const int cnt = (int)min((int64_t)kFwdThreads, lend - cb);
-      __syncthreads();  // previous chunk consumed; tile boxes visible
-      if (tid < cnt) {
-        const int gid = gids[cb + tid];
+    for (int64_t base = lbeg; base < lend; base += 32) {
+      const int64_t j = base + lane;
+      bool hit = false;
+      if (j < lend) {
+        const int gid = gids[j];
         const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
         const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
-        const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
         const double* m = pos + 3 * (int64_t)gid;
-        const double cx = __ldg(m) - bg.px, cy = __ldg(m + 1) - bg.py, cz = __ldg(m + 2) - bg.pz;
-        const float c0 = (float)(-cx), c1 = (float)(-cy), c2 = (float)(-cz);  // p_b0 - mu
-        float u3[3], e[3][3], umax = 0.f;
+        // mu - p_b0 in f64, then f32 (small: |mu - p_b0| ~ brick size + 3 sigma)
+        const float mx = (float)(__ldg(m) - bg.px), my = (float)(__ldg(m + 1) - bg.py),
+                    mz = (float)(__ldg(m + 2) - bg.pz);
+        // 3-sigma box (voxel units, brick-local) vs this warp's tile, widened
+        // by 1e-3 voxel so rounding can never drop a live voxel.
+        const float cxv = mx * isx, cyv = my * isy, czv = mz * isz;
+        const float hxv = fmaf(q2.w, isx, 1e-3f), hyv = fmaf(q3.x, isy, 1e-3f),
+                    hzv = fmaf(q3.y, isz, 1e-3f);
+        hit = cxv + hxv >= ftxl && cxv - hxv <= ftxh && cyv + hyv >= ftyl &&
+              cyv - hyv <= ftyh && czv + hzv >= ftzl && czv - hzv <= ftzh;
+        if (hit) {
+          const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+          float u3[3], e[3][3], umax = 0.f;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          u3[a] = fmaf(L[3 * a + 0], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
-          e[0][a] = L[3 * a + 0] * fsx;
-          e[1][a] = L[3 * a + 1] * fsy;
-          e[2][a] = L[3 * a + 2] * fsz;
-          umax = fmaxf(umax, fabsf(u3[a]) + fabsf(e[0][a]) * k.bdx + fabsf(e[1][a]) * k.bdy +
-                                 fabsf(e[2][a]) * k.bdz);
-        }
-        const float guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
-        Pair32 p;
-        p.a = make_float4(u3[0], u3[1], u3[2], q2.y);
-        p.b = make_float4(e[0][0], e[0][1], e[0][2], q2.z);
-        p.c = make_float4(e[1][0], e[1][1], e[1][2], guard);
-        p.d = make_float4(e[2][0], e[2][1], e[2][2], __int_as_float(gid));
-        sp[tid] = p;
-        // Conservative voxel box of the 3-sigma ellipsoid, brick-local.
-        int xl, xh, yl, yh, zl, zh;
-        sub_range_inv(cx, (double)q2.w, isx, bg.ex, xl, xh);
-        sub_range_inv(cy, (double)q3.x, isy, bg.ey, yl, yh);
-        sub_range_inv(cz, (double)q3.y, isz, bg.ez, zl, zh);
-        unsigned msk = 0;
-#pragma unroll
-        for (int w = 0; w < kFwdThreads / 32; ++w) {
-          const bool hit = xl <= tbox[w][1] && xh >= tbox[w][0] && yl <= tbox[w][3] &&
-                           yh >= tbox[w][2] && zl <= tbox[w][5] && zh >= tbox[w][4];
-          msk |= hit ? (1u << w) : 0u;
-        }
-        smask[tid] = msk;
-      }
-      __syncthreads();
-      for (int base = 0; base < cnt; base += 32) {
-        const unsigned mm = (base + lane < cnt) ? smask[base + lane] : 0u;
-        unsigned ball = __ballot_sync(kFull, (mm >> warp) & 1u);
-        while (ball) {
-          const int j = base + __ffs(ball) - 1;
-          ball &= ball - 1;
-          const float4 pa = sp[j].a, pb = sp[j].b, pc = sp[j].c, pd = sp[j].d;
-          const float v0 = fmaf(fz, pd.x, fmaf(fy, pc.x, fmaf(fx, pb.x, pa.x)));
-          const float v1 = fmaf(fz, pd.y, fmaf(fy, pc.y, fmaf(fx, pb.y, pa.y)));
-          const float v2 = fmaf(fz, pd.z, fmaf(fy, pc.z, fmaf(fx, pb.z, pa.z)));
-          const float d2a = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
-          const float w0 = v0 + pd.x, w1 = v1 + pd.y, w2 = v2 + pd.z;  // voxel z0+1
-          const float d2b = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
-          const int gid = __float_as_int(pd.w);
-          live_accumulate(d2a, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz, pos, rec64, g,
-                          accSA, accWA);
-          live_accumulate(d2b, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz + 1, pos, rec64,
-                          g, accSB, accWB);
+          for (int a = 0; a < 3; ++a) {
+            u3[a] = -fmaf(L[3 * a + 0], mx, fmaf(L[3 * a + 1], my, L[3 * a + 2] * mz));
+            e[0][a] = L[3 * a + 0] * fsx;
+            e[1][a] = L[3 * a + 1] * fsy;
+            e[2][a] = L[3 * a + 2] * fsz;
+            umax = fmaxf(umax, fabsf(u3[a]) + fabsf(e[0][a]) * k.bdx +
+                                   fabsf(e[1][a]) * k.bdy + fabsf(e[2][a]) * k.bdz);
+          }
+          const float guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
+          Pair32 p;
+          p.a = make_float4(u3[0], u3[1], u3[2], q2.y);
+          p.b = make_float4(e[0][0], e[0][1], e[0][2], q2.z);
+          p.c = make_float4(e[1][0], e[1][1], e[1][2], guard);
+          p.d = make_float4(e[2][0], e[2][1], e[2][2], __int_as_float(gid));
+          wsp[lane] = p;
         }
       }
+      unsigned ball = __ballot_sync(kFull, hit);
+      __syncwarp();
+      while (ball) {
+        const int jj = __ffs(ball) - 1;
+        ball &= ball - 1;
+        const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c, pd = wsp[jj].d;
+        const float v0 = fmaf(fz, pd.x, fmaf(fy, pc.x, fmaf(fx, pb.x, pa.x)));
+        const float v1 = fmaf(fz, pd.y, fmaf(fy, pc.y, fmaf(fx, pb.y, pa.y)));
+        const float v2 = fmaf(fz, pd.z, fmaf(fy, pc.z, fmaf(fx, pb.z, pa.z)));
+        const float d2a = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+        const float w0 = v0 + pd.x, w1 = v1 + pd.y, w2 = v2 + pd.z;  // voxel z0+1
+        const float d2b = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
+        const int gid = __float_as_int(pd.w);
+        live_accumulate(d2a, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz, pos, rec64, g,
+                        accSA, accWA);
+        live_accumulate(d2b, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz + 1, pos, rec64,
+                        g, accSB, accWB);
+      }
+      __syncwarp();
     }
     // Epilogue: normalise, store, fused loss (optimize.py:91-103).
 #pragma unroll
@@ -446,42 +439,95 @@ __global__ void backward_prep_kernel(const T* __restrict__ W, const T* __restric
 }
 
 // ------------------------------------------------------------- backward f32
-// One thread per (brick, Gaussian) pair, but NOT in list order: the work of a
-// pair is its live voxel count, which varies 0..~50 inside a brick, and a warp
-// runs as long as its heaviest lane.  Each CTA therefore first bins its pairs
-// by sub-box volume (a smem counting sort, heaviest first) and hands warps
-// pairs of similar cost.  Processing order cannot change any result: each
-// pair's partial is computed by one thread in a fixed voxel order and written
-// to its own slot.  Per pair the live voxels are found row by row: along x,
-// d2(x) = |v_row + x e_x|^2 is a quadratic, so the x-span where it can be
-// <= cutoff^2 (+ guard) is solved directly; every voxel in it is still decided
-// exactly as the forward decides.  The brick's {dL/dI / W, I} are staged in
-// shared memory.  Accumulates sum cw v (whitened) and sum cw delta delta^T;
-// d_mu = L^T sum cw v is formed once per pair.
-constexpr int kBwdChunk = 2048;
+// One thread per (brick, Gaussian) pair.  Three phases per chunk of up to 256
+// list entries:
+//  (1) per pair: brick-relative coefficients and, row by row, the exact x-span
+//      where d2(x) = |v_row + x e_x|^2 (a quadratic) can be <= cutoff^2 +
+//      guard; the spans go to shared memory, the candidate-voxel count is the
+//      pair's cost.
+//  (2) a smem counting sort of the pairs by cost, heaviest first.
+//  (3) warps pull groups of 32 pairs of similar cost (dynamic, heaviest
+//      first) and every lane runs ONE flattened loop over its pair's candidate
+//      voxels, so a warp costs max(candidates) iterations rather than the sum
+//      over rows of the per-row maxima.
+// Order of processing never changes a result: each pair's partial is computed
+// by one thread in a fixed voxel order and written to its own slot.  Every
+// candidate is still decided exactly as the forward decides.  The brick's
+// {dL/dI / W, I} are staged in shared memory.  Accumulates sum cw v
+// (whitened) and sum cw delta delta^T; d_mu = L^T sum cw v once per pair.
+constexpr int kBwdChunk = 256;      // pairs per chunk (one per thread)
+constexpr int kBwdRows = 24;        // span slots per pair (LR/HR bricks need <= 20)
 constexpr int kBwdBuckets = 128;
 
+struct BwdPair;
+size_t bwd_smem_bytes(int ab_voxels);
+
+struct __align__(16) BwdPair {
+  float u[3], ex[3], ey[3], ez[3];
+  float c[3];          // p_b0 - mu
+  float guard;
+  int gid;
+  int nspan;           // stored spans; -1 = overflow (rows > kBwdRows)
+  int cost;            // candidate voxels
+};
+
+__device__ __forceinline__ void bwd_accumulate(float d2, float kernw_r, float A, float2 v_ab,
+                                               float v0, float v1, float v2, float dx,
+                                               float dy, float dz, float& acc_a,
+                                               float& acc_r, float& s0, float& s1,
+                                               float& s2, float& g00, float& g11,
+                                               float& g22, float& g01, float& g02,
+                                               float& g12) {
+  const float kern = __expf(-0.5f * d2);
+  const float w = kern * kernw_r;
+  acc_a = fmaf(w, v_ab.x, acc_a);
+  const float common = v_ab.x * (A - v_ab.y);   // dL/dI (A - I) / W
+  acc_r = fmaf(common, kern, acc_r);
+  const float cw = common * w;
+  s0 = fmaf(cw, v0, s0);
+  s1 = fmaf(cw, v1, s1);
+  s2 = fmaf(cw, v2, s2);
+  const float h = -0.5f * cw;
+  const float hx = h * dx, hy = h * dy;
+  g00 = fmaf(hx, dx, g00);
+  g11 = fmaf(hy, dy, g11);
+  g22 = fmaf(h * dz, dz, g22);
+  g01 = fmaf(hx, dy, g01);
+  g02 = fmaf(hx, dz, g02);
+  g12 = fmaf(hy, dz, g12);
+}
+
+size_t bwd_smem_bytes(int ab_voxels) {
+  return sizeof(BwdPair) * kBwdChunk + sizeof(unsigned) * kBwdChunk * kBwdRows +
+         sizeof(unsigned short) * kBwdChunk + sizeof(int) * (kBwdBuckets + 4) +
+         sizeof(float2) * (size_t)ab_voxels;
+}
+
 template <bool kSmem>
-__global__ void __launch_bounds__(kBwdThreads, 2)
+__global__ void __launch_bounds__(kBwdThreads, 3)
 backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
                   const gsv_record64* __restrict__ rec64,
                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                   const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
                   gsv_grid g, gsv_bricks k, float cut2, double cut2d,
                   const float2* __restrict__ ab, float4* __restrict__ partials) {
-  __shared__ float2 sab[kSmem ? kBwdSmemVoxels : 1];
-  __shared__ int2 sbox[kBwdChunk];
-  __shared__ unsigned short sorder[kBwdChunk];
-  __shared__ int shist[kBwdBuckets];
+  extern __shared__ __align__(16) unsigned char bwd_smem[];
+  BwdPair* spair = reinterpret_cast<BwdPair*>(bwd_smem);
+  unsigned* sspan = reinterpret_cast<unsigned*>(spair + kBwdChunk);  // y|z<<8|xa<<16|xb<<24
+  unsigned short* sorder = reinterpret_cast<unsigned short*>(sspan + kBwdChunk * kBwdRows);
+  int* shist = reinterpret_cast<int*>(sorder + kBwdChunk);
+  int* snextp = shist + kBwdBuckets;
+  float2* sab = reinterpret_cast<float2*>(snextp + 4);
   const int lb = blockIdx.x;
   const int b = (int)slab_first(k) + lb;
   const int64_t lbeg = starts[lb], lend = starts[lb + 1];
   if (lbeg == lend) return;
   const BrickGeom bg = brick_geom(b, g, k);
   const BrickXYZ bc = brick_xyz(b, k);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
-  const double isx = 1.0 / g.sx, isy = 1.0 / g.sy, isz = 1.0 / g.sz;
+  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  const float lo_cut = cut2;
   if (kSmem) {
     const int nv = bg.ex * bg.ey * bg.ez;
     for (int v = tid; v < nv; v += kBwdThreads) {
@@ -494,28 +540,68 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
   for (int64_t cbase = lbeg; cbase < lend; cbase += kBwdChunk) {
     const int cnt = (int)min((int64_t)kBwdChunk, lend - cbase);
     if (tid < kBwdBuckets) shist[tid] = 0;
+    if (tid == 0) *snextp = 0;
     __syncthreads();
-    // (1) sub-box of every pair; histogram of its volume (heaviest bucket 0).
-    for (int t = tid; t < cnt; t += kBwdThreads) {
-      const int gid = gids[cbase + t];
-      const float4 q2 = __ldg(reinterpret_cast<const float4*>(rec + gid) + 2);
-      const float4 q3 = __ldg(reinterpret_cast<const float4*>(rec + gid) + 3);
+    // ---- (1) coefficients + exact row spans
+    if (tid < cnt) {
+      BwdPair P;
+      const int gid = gids[cbase + tid];
+      const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+      const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
+      const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
       const double* m = pos + 3 * (int64_t)gid;
-      int xl, xh, yl, yh, zl, zh;
-      sub_range_inv(__ldg(m) - bg.px, (double)q2.w, isx, bg.ex, xl, xh);
-      sub_range_inv(__ldg(m + 1) - bg.py, (double)q3.x, isy, bg.ey, yl, yh);
-      sub_range_inv(__ldg(m + 2) - bg.pz, (double)q3.y, isz, bg.ez, zl, zh);
-      int vol = 0;
-      if (xl <= xh && yl <= yh && zl <= zh) {
-        vol = (xh - xl + 1) * (yh - yl + 1) * (zh - zl + 1);
-      } else {
-        xl = 1; xh = 0; yl = 0; yh = 0; zl = 0; zh = 0;
+      const float mx = (float)(__ldg(m) - bg.px), my = (float)(__ldg(m + 1) - bg.py),
+                  mz = (float)(__ldg(m + 2) - bg.pz);   // mu - p_b0
+      P.c[0] = -mx; P.c[1] = -my; P.c[2] = -mz;
+      float umax = 0.f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        P.u[a] = -fmaf(L[3 * a], mx, fmaf(L[3 * a + 1], my, L[3 * a + 2] * mz));
+        P.ex[a] = L[3 * a] * fsx;
+        P.ey[a] = L[3 * a + 1] * fsy;
+        P.ez[a] = L[3 * a + 2] * fsz;
+        umax = fmaxf(umax, fabsf(P.u[a]) + fabsf(P.ex[a]) * k.bdx + fabsf(P.ey[a]) * k.bdy +
+                               fabsf(P.ez[a]) * k.bdz);
       }
-      sbox[t] = make_int2(xl | (xh << 8) | (yl << 16) | (yh << 24), zl | (zh << 8));
-      atomicAdd(&shist[kBwdBuckets - 1 - min(vol, kBwdBuckets - 1)], 1);
+      P.guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
+      P.gid = gid;
+      // 3-sigma voxel box (brick-local), widened by 1e-3 voxel.
+      const float cyv = my * isy, czv = mz * isz;
+      const float hyv = fmaf(q3.x, isy, 1e-3f), hzv = fmaf(q3.y, isz, 1e-3f);
+      const int yl = max(0, (int)ceilf(cyv - hyv)), yh = min(bg.ey - 1, (int)floorf(cyv + hyv));
+      const int zl = max(0, (int)ceilf(czv - hzv)), zh = min(bg.ez - 1, (int)floorf(czv + hzv));
+      const float qa = fmaf(P.ex[0], P.ex[0], fmaf(P.ex[1], P.ex[1], P.ex[2] * P.ex[2]));
+      const float inv_qa = 1.0f / qa;
+      const float lim = cut2 + P.guard;
+      int ns = 0, cost = 0;
+      unsigned* my_sp = sspan + tid * kBwdRows;
+      for (int z = zl; z <= zh; ++z) {
+        for (int y = yl; y <= yh; ++y) {
+          const float vr0 = fmaf((float)z, P.ez[0], fmaf((float)y, P.ey[0], P.u[0]));
+          const float vr1 = fmaf((float)z, P.ez[1], fmaf((float)y, P.ey[1], P.u[1]));
+          const float vr2 = fmaf((float)z, P.ez[2], fmaf((float)y, P.ey[2], P.u[2]));
+          const float qb = fmaf(vr0, P.ex[0], fmaf(vr1, P.ex[1], vr2 * P.ex[2]));
+          const float qc = fmaf(vr0, vr0, fmaf(vr1, vr1, vr2 * vr2));
+          // (qa x + qb)^2 <= qb^2 - qa (qc - lim)
+          const float disc = fmaf(qb, qb, -qa * (qc - lim));
+          if (!(disc >= 0.f)) continue;
+          const float sq = sqrtf(disc);
+          const int xa = max(0, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
+          const int xb = min(bg.ex - 1, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
+          if (xa > xb) continue;
+          if (ns < kBwdRows) my_sp[ns] = (unsigned)y | ((unsigned)z << 8) |
+                                         ((unsigned)xa << 16) | ((unsigned)xb << 24);
+          ++ns;
+          cost += xb - xa + 1;
+        }
+      }
+      P.nspan = ns <= kBwdRows ? ns : -1;
+      P.cost = cost;
+      spair[tid] = P;
+      atomicAdd(&shist[kBwdBuckets - 1 - min(cost, kBwdBuckets - 1)], 1);
     }
     __syncthreads();
-    // (2) exclusive scan of the histogram (warp 0, 4 buckets per lane).
+    // ---- (2) counting sort by cost, heaviest first
     if (tid < 32) {
       int v[4], sum = 0;
 #pragma unroll
@@ -531,101 +617,98 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       for (int i = 0; i < 4; ++i) { shist[4 * tid + i] = run; run += v[i]; }
     }
     __syncthreads();
-    // (3) scatter pair slots into cost order (order within a bucket is free).
-    for (int t = tid; t < cnt; t += kBwdThreads) {
-      const int2 bx = sbox[t];
-      const int xl = bx.x & 255, xh = (bx.x >> 8) & 255, yl = (bx.x >> 16) & 255,
-                yh = (bx.x >> 24) & 255, zl = bx.y & 255, zh = (bx.y >> 8) & 255;
-      const int vol = xl <= xh ? (xh - xl + 1) * (yh - yl + 1) * (zh - zl + 1) : 0;
-      const int slot = atomicAdd(&shist[kBwdBuckets - 1 - min(vol, kBwdBuckets - 1)], 1);
-      sorder[slot] = (unsigned short)t;
+    if (tid < cnt) {
+      const int slot = atomicAdd(&shist[kBwdBuckets - 1 - min(spair[tid].cost, kBwdBuckets - 1)], 1);
+      sorder[slot] = (unsigned short)tid;
     }
     __syncthreads();
-    // (4) per-pair gradient partials.
-    for (int s = tid; s < cnt; s += kBwdThreads) {
+    // ---- (3) warps pull 32-pair groups, heaviest first
+    const int ngroups = (cnt + 31) >> 5;
+    for (;;) {
+      int grp = 0;
+      if (lane == 0) grp = atomicAdd(snextp, 1);
+      grp = __shfl_sync(kFull, grp, 0);
+      if (grp >= ngroups) break;
+      const int s = (grp << 5) + lane;
+      if (s >= cnt) continue;
       const int t = sorder[s];
-      const int gid = gids[cbase + t];
-      const int2 bx = sbox[t];
-      const int xl = bx.x & 255, xh = (bx.x >> 8) & 255, yl = (bx.x >> 16) & 255,
-                yh = (bx.x >> 24) & 255, zl = bx.y & 255, zh = (bx.y >> 8) & 255;
+      const BwdPair& P = spair[t];
+      const int gid = P.gid;
       const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
       const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2);
-      const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
       const float A = q2.y, r = q2.z;
-      const double* m = pos + 3 * (int64_t)gid;
-      const float c0 = (float)(bg.px - __ldg(m)), c1 = (float)(bg.py - __ldg(m + 1)),
-                  c2 = (float)(bg.pz - __ldg(m + 2));   // p_b0 - mu
-      float u[3], ex[3], ey[3], ez[3], umax = 0.f;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        u[a] = fmaf(L[3 * a], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
-        ex[a] = L[3 * a] * fsx;
-        ey[a] = L[3 * a + 1] * fsy;
-        ez[a] = L[3 * a + 2] * fsz;
-        umax = fmaxf(umax, fabsf(u[a]) + fabsf(ex[a]) * k.bdx + fabsf(ey[a]) * k.bdy +
-                               fabsf(ez[a]) * k.bdz);
-      }
-      const float guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
-      const float qa = fmaf(ex[0], ex[0], fmaf(ex[1], ex[1], ex[2] * ex[2]));
-      const float inv_qa = 1.0f / qa;
-      const float lim = cut2 + guard, lo_band = cut2 - guard;
+      const float ex0 = P.ex[0], ex1 = P.ex[1], ex2 = P.ex[2];
+      const float c0 = P.c[0], c1 = P.c[1], c2 = P.c[2];
+      const float lim = cut2 + P.guard, lo_band = lo_cut - P.guard;
       float acc_a = 0.f, acc_r = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
       float g00 = 0.f, g11 = 0.f, g22 = 0.f, g01 = 0.f, g02 = 0.f, g12 = 0.f;
-      for (int z = zl; z <= zh; ++z) {
-        const float dz = fmaf((float)z, fsz, c2);
-        for (int y = yl; y <= yh; ++y) {
-          const float dy = fmaf((float)y, fsy, c1);
-          const float vr0 = fmaf((float)z, ez[0], fmaf((float)y, ey[0], u[0]));
-          const float vr1 = fmaf((float)z, ez[1], fmaf((float)y, ey[1], u[1]));
-          const float vr2 = fmaf((float)z, ez[2], fmaf((float)y, ey[2], u[2]));
-          const float qb = fmaf(vr0, ex[0], fmaf(vr1, ex[1], vr2 * ex[2]));
-          const float qc = fmaf(vr0, vr0, fmaf(vr1, vr1, vr2 * vr2));
-          // (qa x + qb)^2 <= qb^2 - qa (qc - lim)
-          const float disc = fmaf(qb, qb, -qa * (qc - lim));
-          if (!(disc >= 0.f)) continue;
-          const float sq = sqrtf(disc);
-          const int xa = max(xl, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
-          const int xb = min(xh, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
-          const int srow = k.bdx * (y + k.bdy * z);
-          const int64_t grow =
-              (int64_t)bg.x0 + (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
-          for (int x = xa; x <= xb; ++x) {
-            const float2 v_ab = kSmem ? sab[srow + x] : __ldg(ab + grow + x);
-            if (v_ab.x == 0.f) continue;
-            const float fx = (float)x;
-            const float v0 = fmaf(fx, ex[0], vr0);
-            const float v1 = fmaf(fx, ex[1], vr1);
-            const float v2 = fmaf(fx, ex[2], vr2);
-            const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
-            if (d2 > lim) continue;
-            if (d2 >= lo_band &&
-                !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
-              continue;
-            const float kern = __expf(-0.5f * d2);
-            const float w = kern * r;
-            acc_a = fmaf(w, v_ab.x, acc_a);
-            const float common = v_ab.x * (A - v_ab.y);   // dL/dI (A - I) / W
-            acc_r = fmaf(common, kern, acc_r);
-            const float cw = common * w;
-            s0 = fmaf(cw, v0, s0);
-            s1 = fmaf(cw, v1, s1);
-            s2 = fmaf(cw, v2, s2);
-            const float dx = fmaf(fx, fsx, c0);
-            const float h = -0.5f * cw;
-            const float hx = h * dx, hy = h * dy;
-            g00 = fmaf(hx, dx, g00);
-            g11 = fmaf(hy, dy, g11);
-            g22 = fmaf(h * dz, dz, g22);
-            g01 = fmaf(hx, dy, g01);
-            g02 = fmaf(hx, dz, g02);
-            g12 = fmaf(hy, dz, g12);
+      if (P.nspan >= 0) {
+        // Flattened loop over the candidate voxels of all spans.
+        const unsigned* my_sp = sspan + t * kBwdRows;
+        int si = 0, x = 0, xb = -1, y = 0, z = 0, srow = 0;
+        float vr0 = 0.f, vr1 = 0.f, vr2 = 0.f, dy = 0.f, dz = 0.f;
+        for (int it = 0; it < P.cost; ++it) {
+          if (x > xb) {   // next span
+            const unsigned sp = my_sp[si++];
+            y = sp & 255; z = (sp >> 8) & 255; x = (sp >> 16) & 255; xb = sp >> 24;
+            vr0 = fmaf((float)z, P.ez[0], fmaf((float)y, P.ey[0], P.u[0]));
+            vr1 = fmaf((float)z, P.ez[1], fmaf((float)y, P.ey[1], P.u[1]));
+            vr2 = fmaf((float)z, P.ez[2], fmaf((float)y, P.ey[2], P.u[2]));
+            dy = fmaf((float)y, fsy, c1);
+            dz = fmaf((float)z, fsz, c2);
+            srow = k.bdx * (y + k.bdy * z);
+          }
+          const float2 v_ab = kSmem ? sab[srow + x]
+                                    : __ldg(ab + (int64_t)(bg.x0 + x) +
+                                            (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z)));
+          const float fx = (float)x;
+          ++x;
+          if (v_ab.x == 0.f) continue;
+          const float v0 = fmaf(fx, ex0, vr0), v1 = fmaf(fx, ex1, vr1), v2 = fmaf(fx, ex2, vr2);
+          const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+          if (d2 > lim) continue;
+          if (d2 >= lo_band &&
+              !exact_live(gid, bg.x0 + (int)fx, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
+            continue;
+          bwd_accumulate(d2, r, A, v_ab, v0, v1, v2, fmaf(fx, fsx, c0), dy, dz, acc_a, acc_r, s0,
+                         s1, s2, g00, g11, g22, g01, g02, g12);
+        }
+      } else {
+        // More candidate rows than span slots (very large bricks): nested loops.
+        const float cyv = -c1 * isy, czv = -c2 * isz;
+        const float4 q3 = __ldg(r4 + 3);
+        const float hyv = fmaf(q3.x, isy, 1e-3f), hzv = fmaf(q3.y, isz, 1e-3f);
+        const int yl = max(0, (int)ceilf(cyv - hyv)), yh = min(bg.ey - 1, (int)floorf(cyv + hyv));
+        const int zl = max(0, (int)ceilf(czv - hzv)), zh = min(bg.ez - 1, (int)floorf(czv + hzv));
+        for (int z = zl; z <= zh; ++z) {
+          const float dz = fmaf((float)z, fsz, c2);
+          for (int y = yl; y <= yh; ++y) {
+            const float dy = fmaf((float)y, fsy, c1);
+            const float vr0 = fmaf((float)z, P.ez[0], fmaf((float)y, P.ey[0], P.u[0]));
+            const float vr1 = fmaf((float)z, P.ez[1], fmaf((float)y, P.ey[1], P.u[1]));
+            const float vr2 = fmaf((float)z, P.ez[2], fmaf((float)y, P.ey[2], P.u[2]));
+            for (int x = 0; x < bg.ex; ++x) {
+              const float2 v_ab = kSmem ? sab[k.bdx * (y + k.bdy * z) + x]
+                                        : __ldg(ab + (int64_t)(bg.x0 + x) +
+                                                (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z)));
+              if (v_ab.x == 0.f) continue;
+              const float fx = (float)x;
+              const float v0 = fmaf(fx, ex0, vr0), v1 = fmaf(fx, ex1, vr1), v2 = fmaf(fx, ex2, vr2);
+              const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+              if (d2 > lim) continue;
+              if (d2 >= lo_band &&
+                  !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
+                continue;
+              bwd_accumulate(d2, r, A, v_ab, v0, v1, v2, fmaf(fx, fsx, c0), dy, dz, acc_a, acc_r,
+                             s0, s1, s2, g00, g11, g22, g01, g02, g12);
+            }
           }
         }
       }
-      // d_mu = sum cw Sigma^-1 delta = L^T (sum cw v)
-      const float mu0 = fmaf(L[0], s0, fmaf(L[3], s1, L[6] * s2));
-      const float mu1 = fmaf(L[1], s0, fmaf(L[4], s1, L[7] * s2));
-      const float mu2 = fmaf(L[2], s0, fmaf(L[5], s1, L[8] * s2));
+      // d_mu = sum cw Sigma^-1 delta = L^T (sum cw v); L row-major in q0,q1,q2.x
+      const float mu0 = fmaf(q0.x, s0, fmaf(q0.w, s1, q1.z * s2));
+      const float mu1 = fmaf(q0.y, s0, fmaf(q1.x, s1, q1.w * s2));
+      const float mu2b = fmaf(q0.z, s0, fmaf(q1.y, s1, q2.x * s2));
       const GBox gb = unpack_box(box, gid);
       const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
       // A caller-built list may hold a pair the binning would not emit: skip it.
@@ -633,7 +716,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
       float4* dst = partials + 3 * e;
       dst[0] = make_float4(acc_a, acc_r, mu0, mu1);
-      dst[1] = make_float4(mu2, g00, g11, g22);
+      dst[1] = make_float4(mu2b, g00, g11, g22);
       dst[2] = make_float4(g01, g02, g12, 0.f);
     }
     __syncthreads();
@@ -851,13 +934,25 @@ int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_r
   const double cut2d = cutoff_sigma * cutoff_sigma;
   cudaStream_t s = as_stream(stream);
   if (precision == 0) {
-    const bool smem = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz <= kBwdSmemVoxels;
+    const int64_t bvox = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz;
+    const bool smem = bvox <= kBwdSmemVoxels;
+    const size_t shm = bwd_smem_bytes(smem ? (int)bvox : 0);
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[smem]) {
+      const int maxb = (int)bwd_smem_bytes(smem ? kBwdSmemVoxels : 0);
+      cudaError_t e = smem ? cudaFuncSetAttribute(backward32_kernel<true>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, maxb)
+                           : cudaFuncSetAttribute(backward32_kernel<false>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(backward32)");
+      attr_set[smem] = true;
+    }
     if (smem)
-      backward32_kernel<true><<<(unsigned)nb, kBwdThreads, 0, s>>>(
+      backward32_kernel<true><<<(unsigned)nb, kBwdThreads, shm, s>>>(
           positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
           (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
     else
-      backward32_kernel<false><<<(unsigned)nb, kBwdThreads, 0, s>>>(
+      backward32_kernel<false><<<(unsigned)nb, kBwdThreads, shm, s>>>(
           positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
           (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
     GSV_CHECK_LAUNCH("backward32_kernel");

@@ -186,30 +186,36 @@ class GradientBuffer:
 
 
 # ----------------------------------------------------------------- binning
+def _alloc(pool, name, shape, dtype, device):
+    if pool is not None:
+        return pool.get(name, shape, dtype)
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
 def _preprocess(f: GaussianField, grid: GridSpec, cutoff_sigma: float, brick_dims, slab,
-                want64: bool):
+                want64: bool = True, pool=None):
     lib = _lib.lib()
     n, dev = f.count, f.device
-    rec32 = torch.empty((n, 16), dtype=torch.float32, device=dev)
+    rec32 = _alloc(pool, "rec32", (n, 16), torch.float32, dev)
     # rec64 is always built: the f64 engine uses it, and the f32 engine's
     # guard-band re-decisions read the f64 whitening factor from it.
-    rec64 = torch.empty((n, 12), dtype=torch.float64, device=dev)
-    counts = torch.empty(n, dtype=torch.int32, device=dev)
-    box = torch.empty((n, 4), dtype=torch.int32, device=dev)
+    rec64 = _alloc(pool, "rec64", (n, 12), torch.float64, dev)
+    counts = _alloc(pool, "counts", (n,), torch.int32, dev)
+    box = _alloc(pool, "box", (n, 4), torch.int32, dev)
     _lib.check(lib.gsv_preprocess(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), n, int(f.relax_enabled),
         float(cutoff_sigma), _lib.make_grid(grid), _lib.make_bricks(grid, brick_dims, slab),
-        rec32.data_ptr(), _lib.ptr(rec64), counts.data_ptr(), box.data_ptr(),
+        rec32.data_ptr(), rec64.data_ptr(), counts.data_ptr(), box.data_ptr(),
         _lib.stream_ptr()), "preprocess")
     return rec32, rec64, counts, box
 
 
-def _scan(counts: torch.Tensor, nbricks: int) -> torch.Tensor:
+def _scan(counts: torch.Tensor, nbricks: int, pool=None) -> torch.Tensor:
     import ctypes
     lib = _lib.lib()
     n = counts.shape[0]
-    gstart = torch.empty(n + 1, dtype=torch.int64, device=counts.device)
+    gstart = _alloc(pool, "gstart", (n + 1,), torch.int64, counts.device)
     nbytes = ctypes.c_size_t(0)
     _lib.check(lib.gsv_bin_workspace(n, 1, nbricks, ctypes.byref(nbytes)), "bin_workspace")
     ws = _lib.workspace(nbytes.value, counts.device, "bin")
@@ -218,7 +224,7 @@ def _scan(counts: torch.Tensor, nbricks: int) -> torch.Tensor:
     return gstart
 
 
-def _fill(counts, box, gstart, pairs: int, bricks, nbricks: int):
+def _fill(counts, box, gstart, pairs: int, bricks, nbricks: int, pool=None):
     import ctypes
     lib = _lib.lib()
     dev = counts.device
@@ -227,11 +233,13 @@ def _fill(counts, box, gstart, pairs: int, bricks, nbricks: int):
     _lib.check(lib.gsv_bin_workspace(n, max(pairs, 1), nbricks, ctypes.byref(nbytes)),
                "bin_workspace")
     ws = _lib.workspace(nbytes.value, dev, "bin")
-    keys_tmp = torch.empty(max(pairs, 1), dtype=torch.int32, device=dev)
-    vals_tmp = torch.empty(max(pairs, 1), dtype=torch.int32, device=dev)
-    keys_out = torch.empty(max(pairs, 1), dtype=torch.int32, device=dev)
-    gids = torch.empty(pairs, dtype=torch.int32, device=dev)
-    starts = torch.empty(nbricks + 1, dtype=torch.int64, device=dev)
+    # sort scratch is never returned: always from the grow-only scratch pool
+    scratch = _lib.workspace(3 * 4 * max(pairs, 1) + 64, dev, "bin_keys")
+    keys_tmp = scratch[: 4 * max(pairs, 1)].view(torch.int32)
+    vals_tmp = scratch[4 * max(pairs, 1): 8 * max(pairs, 1)].view(torch.int32)
+    keys_out = scratch[8 * max(pairs, 1): 12 * max(pairs, 1)].view(torch.int32)
+    gids = _alloc(pool, "gids", (pairs,), torch.int32, dev)
+    starts = _alloc(pool, "starts", (nbricks + 1,), torch.int64, dev)
     _lib.check(lib.gsv_bin_fill(counts.data_ptr(), box.data_ptr(), gstart.data_ptr(), n, pairs,
                                 bricks, keys_tmp.data_ptr(), vals_tmp.data_ptr(),
                                 keys_out.data_ptr(), gids.data_ptr() if pairs else keys_out.data_ptr(),
@@ -241,11 +249,13 @@ def _fill(counts, box, gstart, pairs: int, bricks, nbricks: int):
 
 
 def build_brick_index(f: GaussianField, grid: GridSpec, opts: RenderOptions = RenderOptions(),
-                      brick_dims=DEFAULT_BRICK_DIMS, *, slab=None) -> BrickIndex:
+                      brick_dims=DEFAULT_BRICK_DIMS, *, slab=None, pool=None) -> BrickIndex:
     """Conservative Gaussian-to-brick binning via AABB overlap (raster.py:148-217).
 
     Lists are bit-identical to the reference's (same f64 bounds, same
-    gid-major emission, stable sort by brick id).
+    gid-major emission, stable sort by brick id).  ``pool`` (a
+    _lib.BufferPool) makes the index's arrays views of reusable buffers --
+    valid until the next build with the same pool (TrainStep / Renderer).
     """
     if any(d < 1 for d in brick_dims):
         raise ValueError(f"brick_dims must be positive, got {brick_dims}")
@@ -253,10 +263,10 @@ def build_brick_index(f: GaussianField, grid: GridSpec, opts: RenderOptions = Re
     bricks = _lib.make_bricks(grid, brick_dims, slab)
     nbricks = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
     rec32, rec64, counts, box = _preprocess(f, grid, opts.cutoff_sigma, brick_dims, slab,
-                                            opts.precision == "f64")
-    gstart = _scan(counts, nbricks)
+                                            True, pool)
+    gstart = _scan(counts, nbricks, pool)
     pairs = int(gstart[-1].item())  # the one host read binning needs (buffer sizing)
-    starts, gids = _fill(counts, box, gstart, pairs, bricks, nbricks)
+    starts, gids = _fill(counts, box, gstart, pairs, bricks, nbricks, pool)
     aux = _Aux(rec32, rec64, counts, box, gstart, f.version, True)
     return BrickIndex(grid, brick_dims, (bricks.bgx, bricks.bgy, bricks.bgz), starts, gids,
                       f.version, f.count, opts.cutoff_sigma, slab, aux)
@@ -327,13 +337,15 @@ def _emission_layout(f, grid, idx: BrickIndex, opts: RenderOptions):
 
 
 def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: bool,
-                   timer=None):
+                   timer=None, pool=None):
     lib = _lib.lib()
     n = f.count
     pdt = opts.torch_dtype
     npairs = int(gstart[-1].item()) if not trusted else idx.pair_count
-    alloc = torch.empty if trusted else torch.zeros
-    partials = alloc((max(npairs, 1), 12), dtype=pdt, device=f.device)
+    if trusted:
+        partials = _alloc(pool, "partials", (max(npairs, 1), 12), pdt, f.device)
+    else:
+        partials = torch.zeros((max(npairs, 1), 12), dtype=pdt, device=f.device)
     if timer is not None:
         timer("backward")
     _lib.check(lib.gsv_backward(
@@ -342,7 +354,7 @@ def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: b
         box.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), partials.data_ptr(),
         _lib.stream_ptr()), "backward")
-    gsum = torch.empty((n, 12), dtype=torch.float64, device=f.device)
+    gsum = _alloc(pool, "gsum", (n, 12), torch.float64, f.device)
     if timer is not None:
         timer("merge")
     _lib.check(lib.gsv_merge(partials.data_ptr(), gstart.data_ptr(), n, opts.precision_code,
@@ -352,9 +364,15 @@ def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: b
     return gsum
 
 
-def _chain_rule(f: GaussianField, gsum: torch.Tensor) -> GradientBuffer:
+def _chain_rule(f: GaussianField, gsum: torch.Tensor, pool=None) -> GradientBuffer:
     lib = _lib.lib()
-    out = GradientBuffer.empty(f.count, f.device)
+    n = f.count
+    if pool is None:
+        out = GradientBuffer.empty(n, f.device)
+    else:
+        gb = pool.get("grads", (12 * n,), torch.float64)
+        out = GradientBuffer(gb[:n], gb[n:2 * n], gb[2 * n:5 * n].view(n, 3),
+                             gb[5 * n:8 * n].view(n, 3), gb[8 * n:].view(n, 4))
     _lib.check(lib.gsv_chain_rule(
         gsum.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), f.count, int(f.relax_enabled),

@@ -101,6 +101,9 @@ class TrainStep:
         self.group = process_group
         self.world_size = world_size
         self.timer = timer
+        # Persistent buffers: index, voxel arrays, pair partials, gradients.
+        # Everything a step returns is a view valid until the next step.
+        self.pool = _lib.BufferPool(self.target.device)
 
     @property
     def sharded(self) -> bool:
@@ -118,21 +121,23 @@ class TrainStep:
         lib = _lib.lib()
         grid, opts = self.grid, self.opts
         self._mark("bin")
-        idx = build_brick_index(f, grid, opts, self.brick_dims, slab=self.slab)
+        idx = build_brick_index(f, grid, opts, self.brick_dims, slab=self.slab, pool=self.pool)
         aux = idx._aux
         nvox = grid.num_voxels
         dt = opts.torch_dtype
-        S = torch.empty(nvox, dtype=dt, device=f.device)
-        W = torch.empty(nvox, dtype=dt, device=f.device)
-        I = torch.empty(nvox, dtype=dt, device=f.device)
-        ab = torch.empty((nvox, 2), dtype=dt, device=f.device)
+        pool = self.pool
+        S = pool.get("S", (nvox,), dt)
+        W = pool.get("W", (nvox,), dt)
+        I = pool.get("I", (nvox,), dt)
+        ab = pool.get("ab", (nvox, 2), dt)
         nb = max(idx.brick_count, 1)
-        loss_part = torch.empty(nb, dtype=torch.float64, device=f.device)
+        loss_part = pool.get("loss_part", (nb,), torch.float64)
         self._mark("forward")
         _forward_into(f, grid, idx, opts, aux.rec32, aux.rec64, S, W, I, target=self.target,
                       loss_kind=self.loss_kind, ab=ab, loss_part=loss_part)
         self._mark("loss_sum")
-        loss_sum = torch.zeros(1, dtype=torch.float64, device=f.device)
+        loss_sum = pool.get("loss_sum", (1,), torch.float64)
+        loss_sum.zero_()
         if idx.brick_count > 0:
             _lib.check(lib.gsv_sum(loss_part.data_ptr(), idx.brick_count, loss_sum.data_ptr(),
                                    _lib.stream_ptr()), "sum")
@@ -144,7 +149,7 @@ class TrainStep:
         idx = out.idx
         aux = idx._aux
         gsum = _pair_partials(f, self.grid, idx, self.opts, aux.rec32, aux.rec64, out.ab,
-                              aux.gstart, aux.box, True, timer=self.timer)
+                              aux.gstart, aux.box, True, timer=self.timer, pool=self.pool)
         if self.sharded:
             # One collective per step: the merged per-Gaussian partials, with
             # this rank's loss partial riding in the spare 12th column.
@@ -156,6 +161,34 @@ class TrainStep:
             gsum[0, 11] = 0.0
             out.reduced = True
         self._mark("chain")
-        g = _chain_rule(f, gsum)
+        g = _chain_rule(f, gsum, pool=self.pool)
         self._mark(None)
         return g
+
+
+class Renderer:
+    """Repeated renders of fields at one grid with reusable buffers: the
+    render path of the reference (build_brick_index + forward, cli.py:231-233)
+    without per-call allocations.  Returned tensors are views valid until the
+    next call."""
+
+    def __init__(self, grid, opts: RenderOptions = RenderOptions(), brick_dims=(8, 8, 4),
+                 slab=None, device=None):
+        self.grid = grid
+        self.opts = opts
+        self.brick_dims = tuple(brick_dims)
+        self.slab = slab
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.pool = _lib.BufferPool(dev)
+
+    def __call__(self, f: GaussianField) -> RenderCache:
+        idx = build_brick_index(f, self.grid, self.opts, self.brick_dims, slab=self.slab,
+                                pool=self.pool)
+        n = self.grid.num_voxels
+        dt = self.opts.torch_dtype
+        S = self.pool.get("S", (n,), dt)
+        W = self.pool.get("W", (n,), dt)
+        I = self.pool.get("I", (n,), dt)
+        _forward_into(f, self.grid, idx, self.opts, idx._aux.rec32, idx._aux.rec64, S, W, I)
+        self.last_index = idx
+        return RenderCache(self.grid, S, W, I, f.version)
