@@ -217,11 +217,7 @@ def run_ours(args, dist, ws, rank, local):
 
     def train_iter():
         out = step.forward(f)
-        grads = step.backward(f, out)
-        timer("adam")
-        gs.step_optimizer(f, grads, state, lrs)
-        f.normalize_rotations()
-        timer(None)
+        step.update(f, out, state, lrs)   # backward + fused merge/chain/Adam/renorm
         return out
 
     def barrier():
@@ -319,6 +315,7 @@ def run_ours(args, dist, ws, rank, local):
     t_fwd = phases.get("forward", (0, float("nan")))[1]
     t_bwd = phases.get("backward", (0, float("nan")))[1]
     dom, t_dom, fl = ("backward", t_bwd, BWD_FLOP) if t_bwd >= t_fwd else ("forward", t_fwd, FWD_FLOP)
+    t_upd = phases.get("update", (0, float("nan")))[1]
     achieved = e_live * fl / (t_dom * 1e-3) / 1e12
     n_g = f.count
     bytes_alg = {"forward": 48 * n_g + 4 * pairs + 12 * lr_grid.num_voxels,
@@ -353,25 +350,21 @@ def run_ours(args, dist, ws, rank, local):
             dev_t.copy_(host_t, non_blocking=True)
             step.set_target(dev_t)
             o = step.forward(f)
-            g = step.backward(f, o)
+            step.update(f, o, state, lrs)
             _ = o.loss()
-            gs.step_optimizer(f, g, state, lrs)
-            f.normalize_rotations()
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             dev_t.copy_(host_t, non_blocking=True)
             step.set_target(dev_t)
             o = step.forward(f)
-            g = step.backward(f, o)
+            step.update(f, o, state, lrs)
             loss = o.loss()                    # device -> host, like fit()
-            gs.step_optimizer(f, g, state, lrs)
-            f.normalize_rotations()
         barrier()
         sec = max_over_ranks((time.perf_counter() - t0) / args.steps)
         e2e = {"value": 1.0 / sec, "unit": "it/s", "h2d_bytes_per_step": host_t.numel() * 4,
-               "d2h_bytes_per_step": 8, "api": "TrainStep.forward/backward + step_optimizer "
-               "+ normalize_rotations (fit() loop body)", "last_loss": loss}
+               "d2h_bytes_per_step": 8, "api": "TrainStep.forward + TrainStep.update (the "
+               "fit() loop body)", "last_loss": loss}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

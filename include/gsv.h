@@ -219,6 +219,29 @@ int gsv_adam(double* p, double* m, double* v, const double* g, int64_t count,
              double lr, double beta1, double beta2, double eps, double bc1,
              double bc2, void* stream);
 
+/* Adam hyper-parameters of one step: per-group learning rates in field order
+ * positions, log_scales, rotations, raw_amplitude, raw_relax
+ * (FitConfig.resolved_lrs, optimize.py:62-74) and the bias corrections
+ * bc1 = 1 - b1^t, bc2 = 1 - b2^t computed by the caller (optimize.py:131-132). */
+typedef struct {
+  double lr[5];
+  double b1, b2, eps, bc1, bc2;
+} gsv_adam_hparams;
+
+/* The optimizer tail of one fit() iteration fused into one pass over the
+ * per-Gaussian state: merge of the pair partials in ascending brick order
+ * (or, when gsum != NULL, the already all-reduced sums (N,12) double), chain
+ * rule (raster.py:524-549), Adam on every enabled group (optimize.py:127-148)
+ * and quaternion renormalisation (field.py:100-102).  Same arithmetic as
+ * gsv_merge + gsv_chain_rule + gsv_adam + gsv_normalize_rotations.
+ * moments: host array of 10 device pointers {m_pos, m_ls, m_rot, m_amp,
+ * m_rel, v_pos, v_ls, v_rot, v_amp, v_rel} (AdamState.m / .v). */
+int gsv_fused_update(const void* partials, const int64_t* gstart, const double* gsum,
+                     int64_t n, int precision, double* positions, double* log_scales,
+                     double* rotations, double* raw_amplitude, double* raw_relax,
+                     double* const* moments, int amplitude_enabled, int relax_enabled,
+                     const gsv_adam_hparams* hp, void* stream);
+
 /* q /= |q| per Gaussian (GaussianField.normalize_rotations, field.py:100). */
 int gsv_normalize_rotations(double* rotations, int64_t n, void* stream);
 

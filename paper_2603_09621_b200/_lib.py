@@ -36,6 +36,11 @@ class GsvBricks(ctypes.Structure):
                 ("bz0", c_i32), ("bz1", c_i32)]
 
 
+class GsvAdamHparams(ctypes.Structure):
+    _fields_ = [("lr", c_dbl * 5), ("b1", c_dbl), ("b2", c_dbl), ("eps", c_dbl),
+                ("bc1", c_dbl), ("bc2", c_dbl)]
+
+
 GP = ctypes.POINTER(GsvGrid)
 BP = ctypes.POINTER(GsvBricks)
 
@@ -67,6 +72,9 @@ _SIGS = {
     "gsv_adam": [c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, c_dbl,
                  c_vp],
     "gsv_normalize_rotations": [c_vp, c_i64, c_vp],
+    "gsv_fused_update": [c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
+                         ctypes.POINTER(c_vp), c_int, c_int, ctypes.POINTER(GsvAdamHparams),
+                         c_vp],
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
     # include/gsv_diag.h (measurement only)

@@ -148,16 +148,12 @@ __device__ __forceinline__ void unit_voxel(int u, const gsv_bricks& k, bool tile
   }
 }
 
-__device__ __forceinline__ void live_accumulate(float d2, float amp, float relax, float guard,
-                                                float cut2, double cut2d, int gid, int gx,
-                                                int gy, int gz, const double* pos,
-                                                const gsv_record64* rec64,
-                                                const gsv_grid& g, float& S, float& W) {
-  if (d2 > cut2 + guard) return;
-  if (d2 >= cut2 - guard && !exact_live(gid, gx, gy, gz, pos, rec64, g, cut2d)) return;
-  const float w = __expf(-0.5f * d2) * relax;
-  S = fmaf(amp, w, S);
-  W += w;
+// exp(-d2/2) as one FMUL + MUFU.EX2 (rel. error ~2e-7, well inside the 1e-5
+// parity bar).
+__device__ __forceinline__ float exp_neg_half(float d2) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d2 * -0.72134752044448170f));
+  return r;
 }
 
 // One CTA per brick, 4 warps, each owning one voxel tile (2 voxels per lane).
@@ -245,7 +241,7 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
             umax = fmaxf(umax, fabsf(u3[a]) + fabsf(e[0][a]) * k.bdx +
                                    fabsf(e[1][a]) * k.bdy + fabsf(e[2][a]) * k.bdz);
           }
-          const float guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
+          const float guard = isinf(cut2) ? 0.f : kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
           Pair32 p;
           p.a = make_float4(u3[0], u3[1], u3[2], q2.y);
           p.b = make_float4(e[0][0], e[0][1], e[0][2], q2.z);
@@ -266,11 +262,24 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
         const float d2a = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
         const float w0 = v0 + pd.x, w1 = v1 + pd.y, w2 = v2 + pd.z;  // voxel z0+1
         const float d2b = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
-        const int gid = __float_as_int(pd.w);
-        live_accumulate(d2a, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz, pos, rec64, g,
-                        accSA, accWA);
-        live_accumulate(d2b, pa.w, pb.w, pc.w, cut2, cut2d, gid, gx, gy, gz + 1, pos, rec64,
-                        g, accSB, accWB);
+        // Branch-free accumulation: every lane evaluates both voxels; a voxel
+        // is live when d2 <= cutoff^2, decided in f32 outside the guard band
+        // and re-decided exactly in f64 inside it (a rare, warp-voted path).
+        const float guard = pc.w;
+        bool liveA = d2a <= cut2 - guard, liveB = d2b <= cut2 - guard;
+        const bool bandA = !liveA && d2a <= cut2 + guard;
+        const bool bandB = !liveB && d2b <= cut2 + guard;
+        if (__any_sync(kFull, bandA || bandB)) {
+          const int gid = __float_as_int(pd.w);
+          if (bandA) liveA = exact_live(gid, gx, gy, gz, pos, rec64, g, cut2d);
+          if (bandB) liveB = exact_live(gid, gx, gy, gz + 1, pos, rec64, g, cut2d);
+        }
+        const float wa = liveA ? exp_neg_half(d2a) * pb.w : 0.f;
+        const float wb = liveB ? exp_neg_half(d2b) * pb.w : 0.f;
+        accSA = fmaf(pa.w, wa, accSA);
+        accWA += wa;
+        accSB = fmaf(pa.w, wb, accSB);
+        accWB += wb;
       }
       __syncwarp();
     }
@@ -439,67 +448,86 @@ __global__ void backward_prep_kernel(const T* __restrict__ W, const T* __restric
 }
 
 // ------------------------------------------------------------- backward f32
-// One thread per (brick, Gaussian) pair.  Three phases per chunk of up to 256
+// One thread per (brick, Gaussian) pair, three phases per chunk of up to 1024
 // list entries:
-//  (1) per pair: brick-relative coefficients and, row by row, the exact x-span
-//      where d2(x) = |v_row + x e_x|^2 (a quadratic) can be <= cutoff^2 +
-//      guard; the spans go to shared memory, the candidate-voxel count is the
-//      pair's cost.
-//  (2) a smem counting sort of the pairs by cost, heaviest first.
-//  (3) warps pull groups of 32 pairs of similar cost (dynamic, heaviest
-//      first) and every lane runs ONE flattened loop over its pair's candidate
-//      voxels, so a warp costs max(candidates) iterations rather than the sum
-//      over rows of the per-row maxima.
-// Order of processing never changes a result: each pair's partial is computed
-// by one thread in a fixed voxel order and written to its own slot.  Every
-// candidate is still decided exactly as the forward decides.  The brick's
+//  (1) per pair: the 3-sigma y/z row range and, row by row, the exact x-span
+//      where d2(x) = |v_row + x e_x|^2 (a quadratic in x) can be <= cutoff^2 +
+//      guard: one byte per row in shared memory (xa | xb << 4); the number of
+//      candidate voxels is the pair's cost.
+//  (2) a smem counting sort of the chunk's pairs by cost, heaviest first.
+//  (3) warps pull groups of 32 pairs of similar cost (heaviest first, so the
+//      CTA's warps finish together) and each lane runs ONE flattened loop over
+//      its pair's candidate voxels: a warp costs max(candidates) iterations,
+//      not the sum over rows of per-row maxima.
+// Processing order never changes a result: each pair's partial is computed by
+// one thread in a fixed voxel order and stored in its own slot.  Every
+// candidate is decided exactly as the forward decides.  The brick's
 // {dL/dI / W, I} are staged in shared memory.  Accumulates sum cw v
 // (whitened) and sum cw delta delta^T; d_mu = L^T sum cw v once per pair.
-constexpr int kBwdChunk = 256;      // pairs per chunk (one per thread)
-constexpr int kBwdRows = 24;        // span slots per pair (LR/HR bricks need <= 20)
+constexpr int kBwdChunkMax = 1024;
+constexpr int kBwdSpanBytes = 32768;
 constexpr int kBwdBuckets = 128;
 
-struct BwdPair;
-size_t bwd_smem_bytes(int ab_voxels);
-
-struct __align__(16) BwdPair {
-  float u[3], ex[3], ey[3], ez[3];
-  float c[3];          // p_b0 - mu
-  float guard;
-  int gid;
-  int nspan;           // stored spans; -1 = overflow (rows > kBwdRows)
-  int cost;            // candidate voxels
+struct BwdCoef {
+  float u[3], ex[3], ey[3], ez[3], c[3];
+  float A, r, guard;
 };
 
-__device__ __forceinline__ void bwd_accumulate(float d2, float kernw_r, float A, float2 v_ab,
+// Brick-relative coefficients of one pair (recomputed in phases 1 and 3 from
+// the L1-resident per-Gaussian record; cheaper than keeping them in smem).
+__device__ __forceinline__ void bwd_coef(const gsv_record32* __restrict__ rec,
+                                         const double* __restrict__ pos, int gid,
+                                         const BrickGeom& bg, const gsv_bricks& k, float fsx,
+                                         float fsy, float fsz, float cut2, BwdCoef& C,
+                                         float4& q0o, float4& q1o, float4& q2o, float4& q3o) {
+  const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+  const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
+  const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+  const double* m = pos + 3 * (int64_t)gid;
+  const float mx = (float)(__ldg(m) - bg.px), my = (float)(__ldg(m + 1) - bg.py),
+              mz = (float)(__ldg(m + 2) - bg.pz);   // mu - p_b0
+  C.c[0] = -mx; C.c[1] = -my; C.c[2] = -mz;
+  float umax = 0.f;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    C.u[a] = -fmaf(L[3 * a], mx, fmaf(L[3 * a + 1], my, L[3 * a + 2] * mz));
+    C.ex[a] = L[3 * a] * fsx;
+    C.ey[a] = L[3 * a + 1] * fsy;
+    C.ez[a] = L[3 * a + 2] * fsz;
+    umax = fmaxf(umax, fabsf(C.u[a]) + fabsf(C.ex[a]) * k.bdx + fabsf(C.ey[a]) * k.bdy +
+                           fabsf(C.ez[a]) * k.bdz);
+  }
+  C.guard = isinf(cut2) ? 0.f : kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
+  C.A = q2.y;
+  C.r = q2.z;
+  q0o = q0; q1o = q1; q2o = q2; q3o = q3;
+}
+
+__device__ __forceinline__ void bwd_accumulate(float d2, float relax, float A, float2 v_ab,
                                                float v0, float v1, float v2, float dx,
-                                               float dy, float dz, float& acc_a,
-                                               float& acc_r, float& s0, float& s1,
-                                               float& s2, float& g00, float& g11,
-                                               float& g22, float& g01, float& g02,
-                                               float& g12) {
+                                               float dy, float dz, float* acc) {
   const float kern = __expf(-0.5f * d2);
-  const float w = kern * kernw_r;
-  acc_a = fmaf(w, v_ab.x, acc_a);
+  const float w = kern * relax;
+  acc[0] = fmaf(w, v_ab.x, acc[0]);
   const float common = v_ab.x * (A - v_ab.y);   // dL/dI (A - I) / W
-  acc_r = fmaf(common, kern, acc_r);
+  acc[1] = fmaf(common, kern, acc[1]);
   const float cw = common * w;
-  s0 = fmaf(cw, v0, s0);
-  s1 = fmaf(cw, v1, s1);
-  s2 = fmaf(cw, v2, s2);
+  acc[2] = fmaf(cw, v0, acc[2]);
+  acc[3] = fmaf(cw, v1, acc[3]);
+  acc[4] = fmaf(cw, v2, acc[4]);
   const float h = -0.5f * cw;
   const float hx = h * dx, hy = h * dy;
-  g00 = fmaf(hx, dx, g00);
-  g11 = fmaf(hy, dy, g11);
-  g22 = fmaf(h * dz, dz, g22);
-  g01 = fmaf(hx, dy, g01);
-  g02 = fmaf(hx, dz, g02);
-  g12 = fmaf(hy, dz, g12);
+  acc[5] = fmaf(hx, dx, acc[5]);
+  acc[6] = fmaf(hy, dy, acc[6]);
+  acc[7] = fmaf(h * dz, dz, acc[7]);
+  acc[8] = fmaf(hx, dy, acc[8]);
+  acc[9] = fmaf(hx, dz, acc[9]);
+  acc[10] = fmaf(hy, dz, acc[10]);
 }
 
 size_t bwd_smem_bytes(int ab_voxels) {
-  return sizeof(BwdPair) * kBwdChunk + sizeof(unsigned) * kBwdChunk * kBwdRows +
-         sizeof(unsigned short) * kBwdChunk + sizeof(int) * (kBwdBuckets + 4) +
+  return (size_t)kBwdSpanBytes + sizeof(uint2) * kBwdChunkMax +
+         sizeof(unsigned short) * kBwdChunkMax + sizeof(int) * (kBwdBuckets + 4) +
          sizeof(float2) * (size_t)ab_voxels;
 }
 
@@ -512,10 +540,10 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
                   gsv_grid g, gsv_bricks k, float cut2, double cut2d,
                   const float2* __restrict__ ab, float4* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char bwd_smem[];
-  BwdPair* spair = reinterpret_cast<BwdPair*>(bwd_smem);
-  unsigned* sspan = reinterpret_cast<unsigned*>(spair + kBwdChunk);  // y|z<<8|xa<<16|xb<<24
-  unsigned short* sorder = reinterpret_cast<unsigned short*>(sspan + kBwdChunk * kBwdRows);
-  int* shist = reinterpret_cast<int*>(sorder + kBwdChunk);
+  unsigned char* sspan = bwd_smem;                                       // kBwdSpanBytes
+  uint2* smeta = reinterpret_cast<uint2*>(bwd_smem + kBwdSpanBytes);     // per pair
+  unsigned short* sorder = reinterpret_cast<unsigned short*>(smeta + kBwdChunkMax);
+  int* shist = reinterpret_cast<int*>(sorder + kBwdChunkMax);
   int* snextp = shist + kBwdBuckets;
   float2* sab = reinterpret_cast<float2*>(snextp + 4);
   const int lb = blockIdx.x;
@@ -526,8 +554,11 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
   const BrickXYZ bc = brick_xyz(b, k);
   const int tid = threadIdx.x, lane = tid & 31;
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
-  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
-  const float lo_cut = cut2;
+  const float isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  // rows per pair = y-range x z-range of the brick; spans need xb < 16.
+  const int rows_cap = k.bdy * k.bdz;
+  const bool spans_ok = k.bdx <= 16 && rows_cap <= 256;
+  const int chunk = spans_ok ? min(kBwdChunkMax, (kBwdSpanBytes / rows_cap) & ~31) : kBwdChunkMax;
   if (kSmem) {
     const int nv = bg.ex * bg.ey * bg.ez;
     for (int v = tid; v < nv; v += kBwdThreads) {
@@ -537,67 +568,53 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       sab[x + k.bdx * (y + k.bdy * z)] = __ldg(ab + lin);
     }
   }
-  for (int64_t cbase = lbeg; cbase < lend; cbase += kBwdChunk) {
-    const int cnt = (int)min((int64_t)kBwdChunk, lend - cbase);
+  for (int64_t cbase = lbeg; cbase < lend; cbase += chunk) {
+    const int cnt = (int)min((int64_t)chunk, lend - cbase);
     if (tid < kBwdBuckets) shist[tid] = 0;
     if (tid == 0) *snextp = 0;
     __syncthreads();
-    // ---- (1) coefficients + exact row spans
-    if (tid < cnt) {
-      BwdPair P;
-      const int gid = gids[cbase + tid];
-      const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
-      const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
-      const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
-      const double* m = pos + 3 * (int64_t)gid;
-      const float mx = (float)(__ldg(m) - bg.px), my = (float)(__ldg(m + 1) - bg.py),
-                  mz = (float)(__ldg(m + 2) - bg.pz);   // mu - p_b0
-      P.c[0] = -mx; P.c[1] = -my; P.c[2] = -mz;
-      float umax = 0.f;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        P.u[a] = -fmaf(L[3 * a], mx, fmaf(L[3 * a + 1], my, L[3 * a + 2] * mz));
-        P.ex[a] = L[3 * a] * fsx;
-        P.ey[a] = L[3 * a + 1] * fsy;
-        P.ez[a] = L[3 * a + 2] * fsz;
-        umax = fmaxf(umax, fabsf(P.u[a]) + fabsf(P.ex[a]) * k.bdx + fabsf(P.ey[a]) * k.bdy +
-                               fabsf(P.ez[a]) * k.bdz);
-      }
-      P.guard = kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
-      P.gid = gid;
-      // 3-sigma voxel box (brick-local), widened by 1e-3 voxel.
-      const float cyv = my * isy, czv = mz * isz;
+    // ---- (1) row spans + cost
+    for (int t = tid; t < cnt; t += kBwdThreads) {
+      BwdCoef C;
+      float4 q0, q1, q2, q3;
+      bwd_coef(rec, pos, gids[cbase + t], bg, k, fsx, fsy, fsz, cut2, C, q0, q1, q2, q3);
+      const float cyv = -C.c[1] * isy, czv = -C.c[2] * isz;
       const float hyv = fmaf(q3.x, isy, 1e-3f), hzv = fmaf(q3.y, isz, 1e-3f);
-      const int yl = max(0, (int)ceilf(cyv - hyv)), yh = min(bg.ey - 1, (int)floorf(cyv + hyv));
-      const int zl = max(0, (int)ceilf(czv - hzv)), zh = min(bg.ez - 1, (int)floorf(czv + hzv));
-      const float qa = fmaf(P.ex[0], P.ex[0], fmaf(P.ex[1], P.ex[1], P.ex[2] * P.ex[2]));
-      const float inv_qa = 1.0f / qa;
-      const float lim = cut2 + P.guard;
-      int ns = 0, cost = 0;
-      unsigned* my_sp = sspan + tid * kBwdRows;
-      for (int z = zl; z <= zh; ++z) {
-        for (int y = yl; y <= yh; ++y) {
-          const float vr0 = fmaf((float)z, P.ez[0], fmaf((float)y, P.ey[0], P.u[0]));
-          const float vr1 = fmaf((float)z, P.ez[1], fmaf((float)y, P.ey[1], P.u[1]));
-          const float vr2 = fmaf((float)z, P.ez[2], fmaf((float)y, P.ey[2], P.u[2]));
-          const float qb = fmaf(vr0, P.ex[0], fmaf(vr1, P.ex[1], vr2 * P.ex[2]));
-          const float qc = fmaf(vr0, vr0, fmaf(vr1, vr1, vr2 * vr2));
-          // (qa x + qb)^2 <= qb^2 - qa (qc - lim)
-          const float disc = fmaf(qb, qb, -qa * (qc - lim));
-          if (!(disc >= 0.f)) continue;
-          const float sq = sqrtf(disc);
-          const int xa = max(0, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
-          const int xb = min(bg.ex - 1, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
-          if (xa > xb) continue;
-          if (ns < kBwdRows) my_sp[ns] = (unsigned)y | ((unsigned)z << 8) |
-                                         ((unsigned)xa << 16) | ((unsigned)xb << 24);
-          ++ns;
-          cost += xb - xa + 1;
+      int yl = max(0, (int)ceilf(cyv - hyv)), yh = min(bg.ey - 1, (int)floorf(cyv + hyv));
+      int zl = max(0, (int)ceilf(czv - hzv)), zh = min(bg.ez - 1, (int)floorf(czv + hzv));
+      if (yl > yh || zl > zh) { yl = 0; yh = -1; zl = 0; zh = -1; }
+      int cost = 0;
+      if (spans_ok) {
+        const float qa = fmaf(C.ex[0], C.ex[0], fmaf(C.ex[1], C.ex[1], C.ex[2] * C.ex[2]));
+        const float inv_qa = 1.0f / qa;
+        const float lim = cut2 + C.guard;
+        unsigned char* my_sp = sspan + t * rows_cap;
+        int row = 0;
+        for (int z = zl; z <= zh; ++z) {
+          for (int y = yl; y <= yh; ++y, ++row) {
+            const float vr0 = fmaf((float)z, C.ez[0], fmaf((float)y, C.ey[0], C.u[0]));
+            const float vr1 = fmaf((float)z, C.ez[1], fmaf((float)y, C.ey[1], C.u[1]));
+            const float vr2 = fmaf((float)z, C.ez[2], fmaf((float)y, C.ey[2], C.u[2]));
+            const float qb = fmaf(vr0, C.ex[0], fmaf(vr1, C.ex[1], vr2 * C.ex[2]));
+            const float qc = fmaf(vr0, vr0, fmaf(vr1, vr1, vr2 * vr2));
+            // (qa x + qb)^2 <= qb^2 - qa (qc - lim)
+            const float disc = fmaf(qb, qb, -qa * (qc - lim));
+            int xa = 15, xb = 0;
+            if (disc >= 0.f) {
+              const float sq = sqrtf(disc);
+              xa = max(0, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
+              xb = min(bg.ex - 1, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
+              if (xa > xb) { xa = 15; xb = 0; } else { cost += xb - xa + 1; }
+            }
+            my_sp[row] = (unsigned char)(xa | (xb << 4));
+          }
         }
+      } else {
+        cost = (yh - yl + 1) * (zh - zl + 1) * bg.ex;
       }
-      P.nspan = ns <= kBwdRows ? ns : -1;
-      P.cost = cost;
-      spair[tid] = P;
+      smeta[t] = make_uint2((unsigned)yl | ((unsigned)(yh - yl + 1) << 8) | ((unsigned)zl << 16) |
+                                ((unsigned)(zh - zl + 1) << 24),
+                            (unsigned)cost);
       atomicAdd(&shist[kBwdBuckets - 1 - min(cost, kBwdBuckets - 1)], 1);
     }
     __syncthreads();
@@ -617,9 +634,10 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       for (int i = 0; i < 4; ++i) { shist[4 * tid + i] = run; run += v[i]; }
     }
     __syncthreads();
-    if (tid < cnt) {
-      const int slot = atomicAdd(&shist[kBwdBuckets - 1 - min(spair[tid].cost, kBwdBuckets - 1)], 1);
-      sorder[slot] = (unsigned short)tid;
+    for (int t = tid; t < cnt; t += kBwdThreads) {
+      const int c = (int)smeta[t].y;
+      const int slot = atomicAdd(&shist[kBwdBuckets - 1 - min(c, kBwdBuckets - 1)], 1);
+      sorder[slot] = (unsigned short)t;
     }
     __syncthreads();
     // ---- (3) warps pull 32-pair groups, heaviest first
@@ -632,92 +650,96 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       const int s = (grp << 5) + lane;
       if (s >= cnt) continue;
       const int t = sorder[s];
-      const BwdPair& P = spair[t];
-      const int gid = P.gid;
-      const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
-      const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2);
-      const float A = q2.y, r = q2.z;
-      const float ex0 = P.ex[0], ex1 = P.ex[1], ex2 = P.ex[2];
-      const float c0 = P.c[0], c1 = P.c[1], c2 = P.c[2];
-      const float lim = cut2 + P.guard, lo_band = lo_cut - P.guard;
-      float acc_a = 0.f, acc_r = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
-      float g00 = 0.f, g11 = 0.f, g22 = 0.f, g01 = 0.f, g02 = 0.f, g12 = 0.f;
-      if (P.nspan >= 0) {
-        // Flattened loop over the candidate voxels of all spans.
-        const unsigned* my_sp = sspan + t * kBwdRows;
-        int si = 0, x = 0, xb = -1, y = 0, z = 0, srow = 0;
+      const int gid = gids[cbase + t];
+      BwdCoef C;
+      float4 q0, q1, q2, q3;
+      bwd_coef(rec, pos, gid, bg, k, fsx, fsy, fsz, cut2, C, q0, q1, q2, q3);
+      const uint2 meta = smeta[t];
+      const int yl = meta.x & 255, ny = (meta.x >> 8) & 255, zl = (meta.x >> 16) & 255,
+                nz = meta.x >> 24;
+      const int cost = (int)meta.y;
+      const float lim = cut2 + C.guard, lo_band = cut2 - C.guard;
+      float acc[11];
+#pragma unroll
+      for (int a = 0; a < 11; ++a) acc[a] = 0.f;
+      if (spans_ok) {
+        const unsigned char* my_sp = sspan + t * rows_cap;
+        int row = -1, x = 1, xb = 0, y = 0, z = 0, srow = 0;
         float vr0 = 0.f, vr1 = 0.f, vr2 = 0.f, dy = 0.f, dz = 0.f;
-        for (int it = 0; it < P.cost; ++it) {
-          if (x > xb) {   // next span
-            const unsigned sp = my_sp[si++];
-            y = sp & 255; z = (sp >> 8) & 255; x = (sp >> 16) & 255; xb = sp >> 24;
-            vr0 = fmaf((float)z, P.ez[0], fmaf((float)y, P.ey[0], P.u[0]));
-            vr1 = fmaf((float)z, P.ez[1], fmaf((float)y, P.ey[1], P.u[1]));
-            vr2 = fmaf((float)z, P.ez[2], fmaf((float)y, P.ey[2], P.u[2]));
-            dy = fmaf((float)y, fsy, c1);
-            dz = fmaf((float)z, fsz, c2);
+        for (int it = 0; it < cost; ++it) {
+          if (x > xb) {   // advance to the next non-empty row
+            do {
+              ++row;
+              const int sp = my_sp[row];
+              x = sp & 15;
+              xb = sp >> 4;
+            } while (x > xb);
+            y = yl + row % ny;
+            z = zl + row / ny;
+            vr0 = fmaf((float)z, C.ez[0], fmaf((float)y, C.ey[0], C.u[0]));
+            vr1 = fmaf((float)z, C.ez[1], fmaf((float)y, C.ey[1], C.u[1]));
+            vr2 = fmaf((float)z, C.ez[2], fmaf((float)y, C.ey[2], C.u[2]));
+            dy = fmaf((float)y, fsy, C.c[1]);
+            dz = fmaf((float)z, fsz, C.c[2]);
             srow = k.bdx * (y + k.bdy * z);
           }
-          const float2 v_ab = kSmem ? sab[srow + x]
-                                    : __ldg(ab + (int64_t)(bg.x0 + x) +
+          const int xi = x++;
+          const float2 v_ab = kSmem ? sab[srow + xi]
+                                    : __ldg(ab + (int64_t)(bg.x0 + xi) +
                                             (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z)));
-          const float fx = (float)x;
-          ++x;
           if (v_ab.x == 0.f) continue;
-          const float v0 = fmaf(fx, ex0, vr0), v1 = fmaf(fx, ex1, vr1), v2 = fmaf(fx, ex2, vr2);
+          const float fx = (float)xi;
+          const float v0 = fmaf(fx, C.ex[0], vr0), v1 = fmaf(fx, C.ex[1], vr1),
+                      v2 = fmaf(fx, C.ex[2], vr2);
           const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
           if (d2 > lim) continue;
           if (d2 >= lo_band &&
-              !exact_live(gid, bg.x0 + (int)fx, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
+              !exact_live(gid, bg.x0 + xi, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
             continue;
-          bwd_accumulate(d2, r, A, v_ab, v0, v1, v2, fmaf(fx, fsx, c0), dy, dz, acc_a, acc_r, s0,
-                         s1, s2, g00, g11, g22, g01, g02, g12);
+          bwd_accumulate(d2, C.r, C.A, v_ab, v0, v1, v2, fmaf(fx, fsx, C.c[0]), dy, dz, acc);
         }
       } else {
-        // More candidate rows than span slots (very large bricks): nested loops.
-        const float cyv = -c1 * isy, czv = -c2 * isz;
-        const float4 q3 = __ldg(r4 + 3);
-        const float hyv = fmaf(q3.x, isy, 1e-3f), hzv = fmaf(q3.y, isz, 1e-3f);
-        const int yl = max(0, (int)ceilf(cyv - hyv)), yh = min(bg.ey - 1, (int)floorf(cyv + hyv));
-        const int zl = max(0, (int)ceilf(czv - hzv)), zh = min(bg.ez - 1, (int)floorf(czv + hzv));
-        for (int z = zl; z <= zh; ++z) {
-          const float dz = fmaf((float)z, fsz, c2);
-          for (int y = yl; y <= yh; ++y) {
-            const float dy = fmaf((float)y, fsy, c1);
-            const float vr0 = fmaf((float)z, P.ez[0], fmaf((float)y, P.ey[0], P.u[0]));
-            const float vr1 = fmaf((float)z, P.ez[1], fmaf((float)y, P.ey[1], P.u[1]));
-            const float vr2 = fmaf((float)z, P.ez[2], fmaf((float)y, P.ey[2], P.u[2]));
+        // Very large bricks: nested loops over the y/z rows of the 3-sigma box.
+        for (int zz = 0; zz < nz; ++zz) {
+          const int z = zl + zz;
+          const float dz = fmaf((float)z, fsz, C.c[2]);
+          for (int yy = 0; yy < ny; ++yy) {
+            const int y = yl + yy;
+            const float dy = fmaf((float)y, fsy, C.c[1]);
+            const float vr0 = fmaf((float)z, C.ez[0], fmaf((float)y, C.ey[0], C.u[0]));
+            const float vr1 = fmaf((float)z, C.ez[1], fmaf((float)y, C.ey[1], C.u[1]));
+            const float vr2 = fmaf((float)z, C.ez[2], fmaf((float)y, C.ey[2], C.u[2]));
             for (int x = 0; x < bg.ex; ++x) {
               const float2 v_ab = kSmem ? sab[k.bdx * (y + k.bdy * z) + x]
                                         : __ldg(ab + (int64_t)(bg.x0 + x) +
                                                 (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z)));
               if (v_ab.x == 0.f) continue;
               const float fx = (float)x;
-              const float v0 = fmaf(fx, ex0, vr0), v1 = fmaf(fx, ex1, vr1), v2 = fmaf(fx, ex2, vr2);
+              const float v0 = fmaf(fx, C.ex[0], vr0), v1 = fmaf(fx, C.ex[1], vr1),
+                          v2 = fmaf(fx, C.ex[2], vr2);
               const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
               if (d2 > lim) continue;
               if (d2 >= lo_band &&
                   !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
                 continue;
-              bwd_accumulate(d2, r, A, v_ab, v0, v1, v2, fmaf(fx, fsx, c0), dy, dz, acc_a, acc_r,
-                             s0, s1, s2, g00, g11, g22, g01, g02, g12);
+              bwd_accumulate(d2, C.r, C.A, v_ab, v0, v1, v2, fmaf(fx, fsx, C.c[0]), dy, dz, acc);
             }
           }
         }
       }
       // d_mu = sum cw Sigma^-1 delta = L^T (sum cw v); L row-major in q0,q1,q2.x
-      const float mu0 = fmaf(q0.x, s0, fmaf(q0.w, s1, q1.z * s2));
-      const float mu1 = fmaf(q0.y, s0, fmaf(q1.x, s1, q1.w * s2));
-      const float mu2b = fmaf(q0.z, s0, fmaf(q1.y, s1, q2.x * s2));
+      const float mu0 = fmaf(q0.x, acc[2], fmaf(q0.w, acc[3], q1.z * acc[4]));
+      const float mu1 = fmaf(q0.y, acc[2], fmaf(q1.x, acc[3], q1.w * acc[4]));
+      const float mu2 = fmaf(q0.z, acc[2], fmaf(q1.y, acc[3], q2.x * acc[4]));
       const GBox gb = unpack_box(box, gid);
       const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
       // A caller-built list may hold a pair the binning would not emit: skip it.
       if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
       const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
       float4* dst = partials + 3 * e;
-      dst[0] = make_float4(acc_a, acc_r, mu0, mu1);
-      dst[1] = make_float4(mu2b, g00, g11, g22);
-      dst[2] = make_float4(g01, g02, g12, 0.f);
+      dst[0] = make_float4(acc[0], acc[1], mu0, mu1);
+      dst[1] = make_float4(mu2, acc[5], acc[6], acc[7]);
+      dst[2] = make_float4(acc[8], acc[9], acc[10], 0.f);
     }
     __syncthreads();
   }

@@ -50,25 +50,21 @@ __device__ __forceinline__ void rotation_jacobians(const double* q, double J[4][
   }
 }
 
-__global__ void __launch_bounds__(128)
-chain_kernel(const double* __restrict__ gsum, const double* __restrict__ ls,
-             const double* __restrict__ rot, const double* __restrict__ ra,
-             const double* __restrict__ rr, int64_t n, int relax_enabled,
-             double* __restrict__ g_amp, double* __restrict__ g_rel, double* __restrict__ g_pos,
-             double* __restrict__ g_ls, double* __restrict__ g_rot) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double* s = gsum + 12 * i;
+// Chain rule of one Gaussian from its merged partials s[0..10]
+// (raster.py:524-549): G = sym(G6); d ls_k = -2 e^{-2 ls_k} (R^T G R)_kk;
+// d q_j = 2 tr(G dR_j D R^T); sigmoid chains.  out[12] in field order:
+// positions(3), log_scales(3), rotations(4), raw_amplitude, raw_relax.
+__device__ __forceinline__ void chain_one(const double* s, const double* ls, const double* q,
+                                          double ra, double rr, int relax_enabled,
+                                          double out[12]) {
   double G[9];
   G[0] = s[5]; G[4] = s[6]; G[8] = s[7];
   G[1] = G[3] = s[8];
   G[2] = G[6] = s[9];
   G[5] = G[7] = s[10];
-  const double* q = rot + 4 * i;
   double R[9];
   rotation_f64(q, R);
-  const double iv[3] = {exp(-2.0 * ls[3 * i]), exp(-2.0 * ls[3 * i + 1]), exp(-2.0 * ls[3 * i + 2])};
-  // d ls_k = -2 inv_var_k (R^T G R)_kk
+  const double iv[3] = {exp(-2.0 * ls[0]), exp(-2.0 * ls[1]), exp(-2.0 * ls[2])};
 #pragma unroll
   for (int kk = 0; kk < 3; ++kk) {
     double t = 0.0;
@@ -76,9 +72,8 @@ chain_kernel(const double* __restrict__ gsum, const double* __restrict__ ls,
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) t += R[3 * a + kk] * G[3 * a + b] * R[3 * b + kk];
-    g_ls[3 * i + kk] = -2.0 * iv[kk] * t;
+    out[3 + kk] = -2.0 * iv[kk] * t;
   }
-  // d q_j = 2 tr(G dR_j D R^T): pmat[a][c] = sum_m J[a][m] iv[m] R[c][m]
   double J[4][9];
   rotation_jacobians(q, J);
 #pragma unroll
@@ -93,19 +88,126 @@ chain_kernel(const double* __restrict__ gsum, const double* __restrict__ ls,
         for (int m = 0; m < 3; ++m) pm += J[j][3 * c + m] * iv[m] * R[3 * a + m];
         t += G[3 * a + c] * pm;
       }
-    g_rot[4 * i + j] = 2.0 * t;
+    out[6 + j] = 2.0 * t;
   }
-  g_pos[3 * i + 0] = s[2];
-  g_pos[3 * i + 1] = s[3];
-  g_pos[3 * i + 2] = s[4];
-  const double A = expit_f64(ra[i]);
-  g_amp[i] = s[0] * A * (1.0 - A);
+  out[0] = s[2];
+  out[1] = s[3];
+  out[2] = s[4];
+  const double A = expit_f64(ra);
+  out[10] = s[0] * A * (1.0 - A);
   if (relax_enabled) {
-    const double r = expit_f64(rr[i]);
-    g_rel[i] = s[1] * r * (1.0 - r);
+    const double r = expit_f64(rr);
+    out[11] = s[1] * r * (1.0 - r);
   } else {
-    g_rel[i] = 0.0;
+    out[11] = 0.0;
   }
+}
+
+__global__ void __launch_bounds__(128)
+chain_kernel(const double* __restrict__ gsum, const double* __restrict__ ls,
+             const double* __restrict__ rot, const double* __restrict__ ra,
+             const double* __restrict__ rr, int64_t n, int relax_enabled,
+             double* __restrict__ g_amp, double* __restrict__ g_rel, double* __restrict__ g_pos,
+             double* __restrict__ g_ls, double* __restrict__ g_rot) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double o[12];
+  chain_one(gsum + 12 * i, ls + 3 * i, rot + 4 * i, ra[i], rr[i], relax_enabled, o);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    g_pos[3 * i + a] = o[a];
+    g_ls[3 * i + a] = o[3 + a];
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) g_rot[4 * i + a] = o[6 + a];
+  g_amp[i] = o[10];
+  g_rel[i] = o[11];
+}
+
+// Adam on one element, numpy operand order of step_optimizer
+// (optimize.py:141-147): m*b1 + (1-b1) g; v*b2 + ((1-b2) g) g;
+// p -= (lr (m/bc1)) / (sqrt(v/bc2) + eps).
+__device__ __forceinline__ double adam_one(double p, double& m, double& v, double g, double lr,
+                                           double b1, double b2, double eps, double bc1,
+                                           double bc2) {
+  m = add(mul(m, b1), mul(sub(1.0, b1), g));
+  v = add(mul(v, b2), mul(mul(sub(1.0, b2), g), g));
+  return sub(p, __ddiv_rn(mul(lr, __ddiv_rn(m, bc1)), add(sqrt(__ddiv_rn(v, bc2)), eps)));
+}
+
+struct MomentPtrs {
+  double* p[10];
+  __device__ double* operator[](int k) const { return p[k]; }
+};
+
+// Fused optimizer tail of one fit() iteration, one thread per Gaussian:
+// merge of the pair partials in ascending brick order (raster.py:412-451)
+// [or the already all-reduced sums] -> chain rule -> Adam on every enabled
+// group (optimize.py:127-148) -> quaternion renormalisation (field.py:100).
+// Identical arithmetic to gsv_merge + gsv_chain_rule + gsv_adam x5 +
+// gsv_normalize_rotations, in one pass over the per-Gaussian state.
+template <typename T>
+__global__ void __launch_bounds__(128)
+fused_update_kernel(const T* __restrict__ partials, const int64_t* __restrict__ gstart,
+                    const double* __restrict__ gsum, int64_t n, double* __restrict__ pos,
+                    double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
+                    double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
+                    gsv_adam_hparams h) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s[11];
+  if (gsum != nullptr) {
+#pragma unroll
+    for (int a = 0; a < 11; ++a) s[a] = gsum[12 * i + a];
+  } else {
+#pragma unroll
+    for (int a = 0; a < 11; ++a) s[a] = 0.0;
+    for (int64_t e = gstart[i]; e < gstart[i + 1]; ++e) {
+      const T* p = partials + 12 * e;
+#pragma unroll
+      for (int a = 0; a < 11; ++a) s[a] += (double)p[a];
+    }
+  }
+  double q[4], l[3];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) q[a] = rot[4 * i + a];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) l[a] = ls[3 * i + a];
+  double g[12];
+  chain_one(s, l, q, ra[i], rr[i], relax_en, g);
+  // mv: m_pos, m_ls, m_rot, m_amp, m_rel, v_pos, v_ls, v_rot, v_amp, v_rel
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double m = mv[0][3 * i + a], v = mv[5][3 * i + a];
+    pos[3 * i + a] = adam_one(pos[3 * i + a], m, v, g[a], h.lr[0], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[0][3 * i + a] = m; mv[5][3 * i + a] = v;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double m = mv[1][3 * i + a], v = mv[6][3 * i + a];
+    ls[3 * i + a] = adam_one(l[a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[1][3 * i + a] = m; mv[6][3 * i + a] = v;
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double m = mv[2][4 * i + a], v = mv[7][4 * i + a];
+    q[a] = adam_one(q[a], m, v, g[6 + a], h.lr[2], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[2][4 * i + a] = m; mv[7][4 * i + a] = v;
+  }
+  if (amp_en) {
+    double m = mv[3][i], v = mv[8][i];
+    ra[i] = adam_one(ra[i], m, v, g[10], h.lr[3], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[3][i] = m; mv[8][i] = v;
+  }
+  if (relax_en) {
+    double m = mv[4][i], v = mv[9][i];
+    rr[i] = adam_one(rr[i], m, v, g[11], h.lr[4], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[4][i] = m; mv[9][i] = v;
+  }
+  const double nrm = sqrt(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
+                              mul(q[3], q[3])));
+#pragma unroll
+  for (int a = 0; a < 4; ++a) rot[4 * i + a] = __ddiv_rn(q[a], nrm);
 }
 
 constexpr int kLossThreads = 256;
@@ -258,6 +360,31 @@ int gsv_adam(double* p, double* m, double* v, const double* g, int64_t count, do
   adam_kernel<<<(unsigned)((count + 255) / 256), 256, 0, as_stream(stream)>>>(
       p, m, v, g, count, lr, beta1, beta2, eps, bc1, bc2);
   GSV_CHECK_LAUNCH("adam_kernel");
+  return GSV_OK;
+}
+
+int gsv_fused_update(const void* partials, const int64_t* gstart, const double* gsum,
+                     int64_t n, int precision, double* positions, double* log_scales,
+                     double* rotations, double* raw_amplitude, double* raw_relax,
+                     double* const* moments, int amplitude_enabled, int relax_enabled,
+                     const gsv_adam_hparams* hp, void* stream) {
+  GSV_REQUIRE(hp != nullptr && moments != nullptr, "null hparams/moments");
+  GSV_REQUIRE(gsum != nullptr || (partials != nullptr && gstart != nullptr),
+              "need gsum or partials+gstart");
+  if (n <= 0) return GSV_OK;
+  const unsigned blocks = (unsigned)((n + 127) / 128);
+  cudaStream_t s = as_stream(stream);
+  MomentPtrs mv;
+  for (int k = 0; k < 10; ++k) mv.p[k] = moments[k];
+  if (precision == 0)
+    fused_update_kernel<float><<<blocks, 128, 0, s>>>(
+        (const float*)partials, gstart, gsum, n, positions, log_scales, rotations, raw_amplitude,
+        raw_relax, mv, amplitude_enabled, relax_enabled, *hp);
+  else
+    fused_update_kernel<double><<<blocks, 128, 0, s>>>(
+        (const double*)partials, gstart, gsum, n, positions, log_scales, rotations,
+        raw_amplitude, raw_relax, mv, amplitude_enabled, relax_enabled, *hp);
+  GSV_CHECK_LAUNCH("fused_update_kernel");
   return GSV_OK;
 }
 

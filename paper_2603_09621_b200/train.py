@@ -24,8 +24,8 @@ import torch
 
 from . import _lib
 from .field import GaussianField
-from .raster import (BrickIndex, GradientBuffer, RenderCache, _chain_rule, _forward_into,
-                     _pair_partials, build_brick_index)
+from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule,
+                     _forward_into, _pair_partials, build_brick_index)
 from .render import RenderOptions
 from .volume import Volume
 
@@ -164,6 +164,75 @@ class TrainStep:
         g = _chain_rule(f, gsum, pool=self.pool)
         self._mark(None)
         return g
+
+
+def _adam_launch(f: GaussianField, state, lrs: dict, beta1: float, beta2: float, eps: float,
+                 partials, gstart, gsum, precision_code: int) -> None:
+    """gsv_fused_update: merge (or pre-reduced sums) -> chain rule -> Adam ->
+    renorm.  Bumps the field version twice, like step_optimizer +
+    normalize_rotations (optimize.py:148, field.py:102)."""
+    import ctypes
+    lib = _lib.lib()
+    state.t += 1
+    hp = _lib.GsvAdamHparams()
+    for k, name in enumerate(("positions", "log_scales", "rotations", "raw_amplitude",
+                              "raw_relax")):
+        hp.lr[k] = float(lrs[name])
+    hp.b1, hp.b2, hp.eps = beta1, beta2, eps
+    hp.bc1 = 1.0 - beta1 ** state.t
+    hp.bc2 = 1.0 - beta2 ** state.t
+    groups = ("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax")
+    mv = (ctypes.c_void_p * 10)(*([state.m[g].data_ptr() for g in groups] +
+                                  [state.v[g].data_ptr() for g in groups]))
+    _lib.check(lib.gsv_fused_update(
+        _lib.ptr(partials), _lib.ptr(gstart), _lib.ptr(gsum), f.count, precision_code,
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), mv, int(f.amplitude_enabled),
+        int(f.relax_enabled), ctypes.byref(hp), _lib.stream_ptr()), "fused_update")
+    f.bump_version()
+    f.bump_version()
+
+
+def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
+                   beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> None:
+    """Backward + fused optimizer tail of one fit() iteration: pair partials ->
+    [merge -> all_reduce when sharded] -> chain rule -> Adam -> renorm, without
+    materialising a GradientBuffer (the public backward/step_optimizer path
+    gives identical parameters)."""
+    import ctypes
+    lib = _lib.lib()
+    idx = out.idx
+    aux = idx._aux
+    opts = self.opts
+    if self.sharded:
+        gsum = _pair_partials(f, self.grid, idx, opts, aux.rec32, aux.rec64, out.ab, aux.gstart,
+                              aux.box, True, timer=self.timer, pool=self.pool)
+        import torch.distributed as dist
+        self._mark("allreduce")
+        gsum[0, 11] = out.loss_sum[0]
+        dist.all_reduce(gsum, group=self.group)
+        out.loss_sum.copy_(gsum[0, 11:12])
+        gsum[0, 11] = 0.0
+        out.reduced = True
+        self._mark("update")
+        _adam_launch(f, state, lrs, beta1, beta2, eps, None, None, gsum, opts.precision_code)
+    else:
+        pdt = opts.torch_dtype
+        partials = _alloc(self.pool, "partials", (max(idx.pair_count, 1), 12), pdt, f.device)
+        self._mark("backward")
+        _lib.check(lib.gsv_backward(
+            f.positions.data_ptr(), aux.rec32.data_ptr(), aux.rec64.data_ptr(),
+            idx.starts.data_ptr(), idx.gids.data_ptr(), aux.gstart.data_ptr(), aux.box.data_ptr(),
+            _lib.make_grid(self.grid), _lib.make_bricks(self.grid, idx.brick_dims, idx.slab),
+            float(opts.cutoff_sigma), opts.precision_code, out.ab.data_ptr(),
+            partials.data_ptr(), _lib.stream_ptr()), "backward")
+        self._mark("update")
+        _adam_launch(f, state, lrs, beta1, beta2, eps, partials, aux.gstart, None,
+                     opts.precision_code)
+    self._mark(None)
+
+
+TrainStep.update = _update_method
 
 
 class Renderer:

@@ -1,0 +1,148 @@
+"""Train-step API on the GPU: fused update, fit() contract, and quality parity
+with the reference's own 200-iteration fit (optimize.py:151-199)."""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2603_09621_b200 as gs
+import paper_2603_09621_b200.optimize as optimize_mod
+from paper_2603_09621_b200.synth import CONFIGS, make_problem
+
+from conftest import GRAD_KEYS, load_json
+
+pytestmark = pytest.mark.gpu
+
+FAST = dict(iterations=25, log_every=10)
+
+
+def _pack(f):
+    return np.concatenate([getattr(f, k).detach().cpu().numpy().ravel()
+                           for k in ("positions", "log_scales", "rotations", "raw_amplitude",
+                                     "raw_relax")])
+
+
+@pytest.fixture
+def noise_volume():
+    g = gs.GridSpec((8, 8, 8))
+    rng = np.random.default_rng(123)
+    return gs.Volume(g, rng.uniform(0.0, 1.0, size=g.dims))
+
+
+def test_fused_update_bit_identical_to_public_api():
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    for _ in range(3):
+        out = step.forward(fa)
+        step.update(fa, out, sa, lrs)
+        idx = gs.build_brick_index(fb, lr.grid)
+        c = gs.forward(fb, lr.grid, idx)
+        _, dl = gs.loss_and_grad(c.volume(), lr, "l1")
+        g = gs.backward(fb, lr.grid, idx, c, dl)
+        gs.step_optimizer(fb, g, sb, lrs)
+        fb.normalize_rotations()
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    assert fa.version == fb.version and sa.t == sb.t == 3
+    for k in sa.m:
+        np.testing.assert_array_equal(sa.m[k].cpu().numpy(), sb.m[k].cpu().numpy())
+
+
+def test_fit_is_deterministic(noise_volume):
+    a, ra = gs.fit(noise_volume, fit_cfg=gs.FitConfig(**FAST))
+    b, rb = gs.fit(noise_volume, fit_cfg=gs.FitConfig(**FAST))
+    np.testing.assert_array_equal(_pack(a), _pack(b))
+    assert ra.losses == rb.losses
+
+
+def test_fit_reduces_loss_and_reports(noise_volume):
+    _, report = gs.fit(noise_volume, fit_cfg=gs.FitConfig(iterations=150))
+    assert report.losses[-1] < report.losses[0]
+    assert len(report.losses) == 150
+    assert report.final["N"] > 0
+    assert report.final["loss"] == pytest.approx(report.losses[-1], rel=0.2)
+    _, report = gs.fit(noise_volume, fit_cfg=gs.FitConfig(iterations=25, log_every=10))
+    assert [e["iter"] for e in report.entries] == [0, 10, 20, 24]
+
+
+def test_fit_frozen_groups_keep_initialization(noise_volume):
+    init = gs.init_from_volume(noise_volume, gs.InitConfig())
+    f, _ = gs.fit(noise_volume, fit_cfg=gs.FitConfig(amplitude_enabled=False,
+                                                     relax_enabled=False, **FAST))
+    np.testing.assert_array_equal(f.raw_amplitude.cpu().numpy(), init.raw_amplitude.cpu().numpy())
+    np.testing.assert_array_equal(f.raw_relax.cpu().numpy(), init.raw_relax.cpu().numpy())
+    assert not np.array_equal(f.positions.cpu().numpy(), init.positions.cpu().numpy())
+
+
+def test_fit_checkpointing(tmp_path, noise_volume):
+    gs.fit(noise_volume, fit_cfg=gs.FitConfig(iterations=10, checkpoint_every=4),
+           checkpoint_dir=str(tmp_path))
+    files = sorted(p.name for p in tmp_path.iterdir())
+    assert files == ["checkpoint_00004.gsv", "checkpoint_00004.gsv.opt.json",
+                     "checkpoint_00008.gsv", "checkpoint_00008.gsv.opt.json"]
+    restored = gs.load_field(str(tmp_path / "checkpoint_00008.gsv"))
+    assert restored.count > 0
+    side = json.loads((tmp_path / "checkpoint_00008.gsv.opt.json").read_text())
+    assert side["iteration"] == 8 and side["t"] == 8
+
+
+def test_fit_aborts_on_nonfinite_loss(noise_volume, monkeypatch):
+    real = optimize_mod.loss_and_grad
+    calls = {"n": 0}
+
+    def poisoned(pred, target, kind="l1"):
+        calls["n"] += 1
+        loss, grad = real(pred, target, kind)
+        return (float("nan"), grad) if calls["n"] == 4 else (loss, grad)
+
+    monkeypatch.setattr(optimize_mod, "loss_and_grad", poisoned)
+    with pytest.raises(gs.NumericalError, match="iteration 3"):
+        gs.fit(noise_volume, fit_cfg=gs.FitConfig(iterations=10))
+
+
+def test_constant_volume_is_optimal_at_init():
+    g = gs.GridSpec((8, 8, 8))
+    lr = gs.Volume(g, np.full(g.dims, 0.6, dtype=np.float32))
+    f, report = gs.fit(lr, fit_cfg=gs.FitConfig(iterations=10, log_every=5, loss="l2"))
+    assert report.losses[0] < 1e-6 and report.final["loss"] < 1e-3
+
+
+def test_fit_loss_trace_tracks_reference():
+    """First 20 losses of the reference fit on the config-1 phantom
+    (threshold 0).  L1's sign(I - T) gradient and Adam's sign-like early
+    steps amplify last-ulp intensity differences between any two engines
+    (the reference's own f32 and f64 engines disagree on 384 of 32768 signs,
+    SURVEY.md §0 finding 5), so the trace is compared at 1e-2 relative; the
+    quality bar is the PSNR/SSIM test below."""
+    ref = load_json("fit_quality.json")
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    _, report = gs.fit(lr, gs.InitConfig(background_threshold=0.0),
+                       gs.FitConfig(iterations=20))
+    got = np.asarray(report.losses)
+    want = np.asarray(ref["losses_head"])
+    assert np.abs(got - want).max() / want.max() < 1e-2, (got, want)
+
+
+def test_fit_quality_matches_reference_psnr_ssim():
+    """PSNR/SSIM of the SR render after exactly 200 iterations vs the
+    reference's: within 0.05 dB / 0.001 (north_star)."""
+    ref = load_json("fit_quality.json")
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f, _ = gs.fit(lr, gs.InitConfig(background_threshold=0.0), gs.FitConfig(iterations=200))
+    idx = gs.build_brick_index(f, p["hr_grid"])
+    sr = gs.forward(f, p["hr_grid"], idx).volume().numpy()
+    got_psnr = oracle.psnr(sr, p["hr"])
+    got_ssim = oracle.ssim3d(sr, p["hr"])
+    assert abs(got_psnr - ref["psnr"]) <= 0.05, (got_psnr, ref["psnr"])
+    assert abs(got_ssim - ref["ssim"]) <= 0.001, (got_ssim, ref["ssim"])
+    assert got_psnr >= ref["trilinear_psnr"] + 2.0   # criterion 5: beats trilinear by 2 dB
