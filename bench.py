@@ -122,15 +122,7 @@ def dist_setup(args):
     return None, 1, 0, 0
 
 
-def slab_ranges(layers: int, ws: int):
-    """Contiguous, balanced split of brick layers [0, layers) over ws ranks."""
-    base, rem = divmod(layers, ws)
-    out, z = [], 0
-    for r in range(ws):
-        n = base + (1 if r < rem else 0)
-        out.append((z, z + n))
-        z += n
-    return out
+from paper_2603_09621_b200.distributed import slab_ranges  # noqa: E402
 
 
 def problem_for(cfg_id):
@@ -147,7 +139,7 @@ def cpu_train_step_seconds(p, steps: int, warmup: int):
     oracle.build()
     g = p["lr_grid"]
     fd = dict(zip(("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax"),
-                  [np.array(a, copy=True) for a in p["field"]]))
+                  [np.array(a, order="C", copy=True) for a in p["field"]]))
     st = oracle.adam_state(fd)
     lrs = FitConfig().resolved_lrs(g.spacing)
     tgt = np.ascontiguousarray(p["lr"].ravel(order="F"))

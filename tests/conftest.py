@@ -46,7 +46,7 @@ def load_json(name):
 
 
 def field_dict(arrays, relax_enabled=True, amplitude_enabled=True):
-    d = {k: np.array(a, dtype=np.float64, copy=True) for k, a in zip(FIELD_KEYS, arrays)}
+    d = {k: np.array(a, dtype=np.float64, order="C", copy=True) for k, a in zip(FIELD_KEYS, arrays)}
     d["relax_enabled"] = relax_enabled
     d["amplitude_enabled"] = amplitude_enabled
     return d
