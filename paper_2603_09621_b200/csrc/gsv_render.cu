@@ -38,12 +38,15 @@ constexpr float kGuardMag = 1e-5f;   // x umax x cutoff
 constexpr unsigned kFull = 0xffffffffu;
 
 // Shared-memory record of one staged pair (f32 forward), 64 bytes: four
-// broadcast LDS.128 per (pair, warp-tile) evaluation.
+// broadcast LDS.128 per (pair, warp-tile) evaluation.  The exponent
+// q = -(1/2) log2(e) d2 + log2(r) is a quadratic in the lane's voxel offset
+// (X, Y, Z) from the warp tile's centre, so w = A-free weight = 2^q needs 9
+// FMAs (+4 for the second voxel) and one EX2 per voxel.
 struct __align__(16) Pair32 {
-  float4 a;  // u0 u1 u2 amp      u = L (p_b0 - mu): v at the brick's first voxel
-  float4 b;  // ex0 ex1 ex2 relax e_x = sx L[:,0]: v step per voxel along x
-  float4 c;  // ey0 ey1 ey2 guard
-  float4 d;  // ez0 ez1 ez2 gid
+  float4 a;  // k0 kx ky kz
+  float4 b;  // kxx kyy kzz kxy
+  float4 c;  // kxz kyz amp t_live    q >= t_live: live for sure
+  float4 d;  // t_band gid - -        t_band <= q < t_live: re-decide in f64
 };
 
 struct BrickGeom {
@@ -148,6 +151,12 @@ __device__ __forceinline__ void unit_voxel(int u, const gsv_bricks& k, bool tile
   }
 }
 
+__device__ __forceinline__ float ex2_approx(float q) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+  return r;
+}
+
 // exp(-d2/2) as one FMUL + MUFU.EX2 (rel. error ~2e-7, well inside the 1e-5
 // parity bar).
 __device__ __forceinline__ float exp_neg_half(float d2) {
@@ -164,7 +173,7 @@ __device__ __forceinline__ float exp_neg_half(float d2) {
 // order (deterministic accumulation, no atomics).  Staging is repeated per
 // warp (4x, L1-resident loads) -- cheaper than the barrier stalls of shared
 // staging, where every warp waits for the slowest tile each chunk.
-__global__ void __launch_bounds__(kFwdThreads)
+__global__ void __launch_bounds__(kFwdThreads, 5)
 forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
                  const gsv_record64* __restrict__ rec64,
                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
@@ -207,15 +216,23 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
     }
     const float ftxl = (float)txl, ftxh = (float)txh, ftyl = (float)tyl, ftyh = (float)tyh,
                 ftzl = (float)tzl, ftzh = (float)tzh;
-    const float fx = (float)lx, fy = (float)ly, fz = (float)lz;
+    // Tile centre and this lane's voxel offsets from it (exact halves in f32).
+    const float ctx = 0.5f * (ftxl + ftxh), cty = 0.5f * (ftyl + ftyh), ctz = 0.5f * (ftzl + ftzh);
+    const float ext_x = fmaxf(0.5f * (ftxh - ftxl), 0.f), ext_y = fmaxf(0.5f * (ftyh - ftyl), 0.f),
+                ext_z = fmaxf(0.5f * (ftzh - ftzl), 0.f) + 1.f;
+    const float mX = (float)lx - ctx, mY = (float)ly - cty, mZ = (float)lz - ctz;
+    const float mXX = mX * mX, mYY = mY * mY, mZZ = mZ * mZ, mXY = mX * mY, mXZ = mX * mZ,
+                mYZ = mY * mZ, m2Z1 = fmaf(2.f, mZ, 1.f);
     const int gx = bg.x0 + lx, gy = bg.y0 + ly, gz = bg.z0 + lz;
     float accSA = 0.f, accWA = 0.f, accSB = 0.f, accWB = 0.f;
 
+    int gid_next = (lbeg + lane < lend) ? __ldg(gids + lbeg + lane) : -1;
     for (int64_t base = lbeg; base < lend; base += 32) {
-      const int64_t j = base + lane;
+      const int gid = gid_next;
+      gid_next = (base + 32 + lane < lend) ? __ldg(gids + base + 32 + lane) : -1;
       bool hit = false;
-      if (j < lend) {
-        const int gid = gids[j];
+      Pair32 p;
+      if (gid >= 0) {
         const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
         const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
         const double* m = pos + 3 * (int64_t)gid;
@@ -241,44 +258,76 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
             umax = fmaxf(umax, fabsf(u3[a]) + fabsf(e[0][a]) * k.bdx +
                                    fabsf(e[1][a]) * k.bdy + fabsf(e[2][a]) * k.bdz);
           }
-          const float guard = isinf(cut2) ? 0.f : kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2);
-          Pair32 p;
-          p.a = make_float4(u3[0], u3[1], u3[2], q2.y);
-          p.b = make_float4(e[0][0], e[0][1], e[0][2], q2.z);
-          p.c = make_float4(e[1][0], e[1][1], e[1][2], guard);
-          p.d = make_float4(e[2][0], e[2][1], e[2][2], __int_as_float(gid));
-          wsp[lane] = p;
+          // v at the tile centre, then the quadratic's coefficients (scaled by s)
+          float uc[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            uc[a] = fmaf(ctz, e[2][a], fmaf(cty, e[1][a], fmaf(ctx, e[0][a], u3[a])));
+          const float sc = -0.72134752044448170f;   // -(1/2) log2(e)
+          const float lr2 = __log2f(q2.z);
+          const float d00 = fmaf(uc[0], uc[0], fmaf(uc[1], uc[1], uc[2] * uc[2]));
+          p.a.x = fmaf(sc, d00, lr2);
+          p.a.y = 2.f * sc * fmaf(uc[0], e[0][0], fmaf(uc[1], e[0][1], uc[2] * e[0][2]));
+          p.a.z = 2.f * sc * fmaf(uc[0], e[1][0], fmaf(uc[1], e[1][1], uc[2] * e[1][2]));
+          p.a.w = 2.f * sc * fmaf(uc[0], e[2][0], fmaf(uc[1], e[2][1], uc[2] * e[2][2]));
+          p.b.x = sc * fmaf(e[0][0], e[0][0], fmaf(e[0][1], e[0][1], e[0][2] * e[0][2]));
+          p.b.y = sc * fmaf(e[1][0], e[1][0], fmaf(e[1][1], e[1][1], e[1][2] * e[1][2]));
+          p.b.z = sc * fmaf(e[2][0], e[2][0], fmaf(e[2][1], e[2][1], e[2][2] * e[2][2]));
+          p.b.w = 2.f * sc * fmaf(e[0][0], e[1][0], fmaf(e[0][1], e[1][1], e[0][2] * e[1][2]));
+          p.c.x = 2.f * sc * fmaf(e[0][0], e[2][0], fmaf(e[0][1], e[2][1], e[0][2] * e[2][2]));
+          p.c.y = 2.f * sc * fmaf(e[1][0], e[2][0], fmaf(e[1][1], e[2][1], e[1][2] * e[2][2]));
+          p.c.z = q2.y;
+          // Guard band in q units: the direct-v bound (kGuard*, scaled by |s|)
+          // plus the rounding of the expanded quadratic (~7e-7 of the sum of
+          // its term magnitudes over the tile), x8.
+          const float qmag = fabsf(p.a.x) + ext_x * fabsf(p.a.y) + ext_y * fabsf(p.a.z) +
+                             ext_z * fabsf(p.a.w) + ext_x * ext_x * fabsf(p.b.x) +
+                             ext_y * ext_y * fabsf(p.b.y) + ext_z * ext_z * fabsf(p.b.z) +
+                             ext_x * ext_y * fabsf(p.b.w) + ext_x * ext_z * fabsf(p.c.x) +
+                             ext_y * ext_z * fabsf(p.c.y);
+          const float guard = isinf(cut2) ? 0.f
+                              : 0.72134752f * (kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2)) +
+                                    2.5e-6f * qmag;
+          const float qcut = isinf(cut2) ? -INFINITY : fmaf(sc, cut2, lr2);
+          p.c.w = qcut + guard;          // live for sure above
+          p.d = make_float4(qcut - guard, __int_as_float(gid), 0.f, 0.f);
         }
       }
-      unsigned ball = __ballot_sync(kFull, hit);
+      // Compact this round's hits into consecutive slots (ballot rank), so the
+      // evaluation loop below is a plain counter over broadcast smem records.
+      const unsigned ball = __ballot_sync(kFull, hit);
+      if (hit) wsp[__popc(ball & ((1u << lane) - 1u))] = p;
       __syncwarp();
-      while (ball) {
-        const int jj = __ffs(ball) - 1;
-        ball &= ball - 1;
-        const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c, pd = wsp[jj].d;
-        const float v0 = fmaf(fz, pd.x, fmaf(fy, pc.x, fmaf(fx, pb.x, pa.x)));
-        const float v1 = fmaf(fz, pd.y, fmaf(fy, pc.y, fmaf(fx, pb.y, pa.y)));
-        const float v2 = fmaf(fz, pd.z, fmaf(fy, pc.z, fmaf(fx, pb.z, pa.z)));
-        const float d2a = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
-        const float w0 = v0 + pd.x, w1 = v1 + pd.y, w2 = v2 + pd.z;  // voxel z0+1
-        const float d2b = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
-        // Branch-free accumulation: every lane evaluates both voxels; a voxel
-        // is live when d2 <= cutoff^2, decided in f32 outside the guard band
-        // and re-decided exactly in f64 inside it (a rare, warp-voted path).
-        const float guard = pc.w;
-        bool liveA = d2a <= cut2 - guard, liveB = d2b <= cut2 - guard;
-        const bool bandA = !liveA && d2a <= cut2 + guard;
-        const bool bandB = !liveB && d2b <= cut2 + guard;
+      const int nh = __popc(ball);
+      for (int jj = 0; jj < nh; ++jj) {
+        const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c;
+        const float2 pd = *reinterpret_cast<const float2*>(&wsp[jj].d);
+        // q(X,Y,Z) for voxel A, then q at Z+1 by its finite difference
+        float qa = fmaf(pa.y, mX, pa.x);
+        qa = fmaf(pa.z, mY, qa);
+        qa = fmaf(pa.w, mZ, qa);
+        qa = fmaf(pb.x, mXX, qa);
+        qa = fmaf(pb.y, mYY, qa);
+        qa = fmaf(pb.z, mZZ, qa);
+        qa = fmaf(pb.w, mXY, qa);
+        qa = fmaf(pc.x, mXZ, qa);
+        qa = fmaf(pc.y, mYZ, qa);
+        const float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, m2Z1, pa.w)));
+        const float qb = qa + dq;
+        // Branch-free accumulation; the guard band re-decides in f64 (rare,
+        // warp-voted), exactly like the reference's truncation test.
+        float wa = qa >= pc.w ? ex2_approx(qa) : 0.f;
+        float wb = qb >= pc.w ? ex2_approx(qb) : 0.f;
+        const bool bandA = qa < pc.w && qa >= pd.x;
+        const bool bandB = qb < pc.w && qb >= pd.x;
         if (__any_sync(kFull, bandA || bandB)) {
-          const int gid = __float_as_int(pd.w);
-          if (bandA) liveA = exact_live(gid, gx, gy, gz, pos, rec64, g, cut2d);
-          if (bandB) liveB = exact_live(gid, gx, gy, gz + 1, pos, rec64, g, cut2d);
+          const int gidj = __float_as_int(pd.y);
+          if (bandA && exact_live(gidj, gx, gy, gz, pos, rec64, g, cut2d)) wa = ex2_approx(qa);
+          if (bandB && exact_live(gidj, gx, gy, gz + 1, pos, rec64, g, cut2d)) wb = ex2_approx(qb);
         }
-        const float wa = liveA ? exp_neg_half(d2a) * pb.w : 0.f;
-        const float wb = liveB ? exp_neg_half(d2b) * pb.w : 0.f;
-        accSA = fmaf(pa.w, wa, accSA);
+        accSA = fmaf(pc.z, wa, accSA);
         accWA += wa;
-        accSB = fmaf(pa.w, wb, accSB);
+        accSB = fmaf(pc.z, wb, accSB);
         accWB += wb;
       }
       __syncwarp();
@@ -526,7 +575,7 @@ __device__ __forceinline__ void bwd_accumulate(float d2, float relax, float A, f
 }
 
 size_t bwd_smem_bytes(int ab_voxels) {
-  return (size_t)kBwdSpanBytes + sizeof(uint2) * kBwdChunkMax +
+  return (size_t)kBwdSpanBytes + sizeof(uint4) * kBwdChunkMax +
          sizeof(unsigned short) * kBwdChunkMax + sizeof(int) * (kBwdBuckets + 4) +
          sizeof(float2) * (size_t)ab_voxels;
 }
@@ -541,7 +590,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
                   const float2* __restrict__ ab, float4* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char bwd_smem[];
   unsigned char* sspan = bwd_smem;                                       // kBwdSpanBytes
-  uint2* smeta = reinterpret_cast<uint2*>(bwd_smem + kBwdSpanBytes);     // per pair
+  uint4* smeta = reinterpret_cast<uint4*>(bwd_smem + kBwdSpanBytes);     // per pair
   unsigned short* sorder = reinterpret_cast<unsigned short*>(smeta + kBwdChunkMax);
   int* shist = reinterpret_cast<int*>(sorder + kBwdChunkMax);
   int* snextp = shist + kBwdBuckets;
@@ -557,7 +606,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
   const float isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
   // rows per pair = y-range x z-range of the brick; spans need xb < 16.
   const int rows_cap = k.bdy * k.bdz;
-  const bool spans_ok = k.bdx <= 16 && rows_cap <= 256;
+  const bool spans_ok = k.bdx <= 16 && rows_cap <= 64;
   const int chunk = spans_ok ? min(kBwdChunkMax, (kBwdSpanBytes / rows_cap) & ~31) : kBwdChunkMax;
   if (kSmem) {
     const int nv = bg.ex * bg.ey * bg.ez;
@@ -584,6 +633,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       int zl = max(0, (int)ceilf(czv - hzv)), zh = min(bg.ez - 1, (int)floorf(czv + hzv));
       if (yl > yh || zl > zh) { yl = 0; yh = -1; zl = 0; zh = -1; }
       int cost = 0;
+      unsigned long long rmask = 0ull;   // bit r: row r of the y/z box has a span
       if (spans_ok) {
         const float qa = fmaf(C.ex[0], C.ex[0], fmaf(C.ex[1], C.ex[1], C.ex[2] * C.ex[2]));
         const float inv_qa = 1.0f / qa;
@@ -604,7 +654,12 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
               const float sq = sqrtf(disc);
               xa = max(0, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
               xb = min(bg.ex - 1, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
-              if (xa > xb) { xa = 15; xb = 0; } else { cost += xb - xa + 1; }
+              if (xa > xb) {
+                xa = 15; xb = 0;
+              } else {
+                cost += xb - xa + 1;
+                rmask |= 1ull << row;
+              }
             }
             my_sp[row] = (unsigned char)(xa | (xb << 4));
           }
@@ -612,9 +667,9 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       } else {
         cost = (yh - yl + 1) * (zh - zl + 1) * bg.ex;
       }
-      smeta[t] = make_uint2((unsigned)yl | ((unsigned)(yh - yl + 1) << 8) | ((unsigned)zl << 16) |
+      smeta[t] = make_uint4((unsigned)yl | ((unsigned)(yh - yl + 1) << 8) | ((unsigned)zl << 16) |
                                 ((unsigned)(zh - zl + 1) << 24),
-                            (unsigned)cost);
+                            (unsigned)cost, (unsigned)rmask, (unsigned)(rmask >> 32));
       atomicAdd(&shist[kBwdBuckets - 1 - min(cost, kBwdBuckets - 1)], 1);
     }
     __syncthreads();
@@ -654,7 +709,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       BwdCoef C;
       float4 q0, q1, q2, q3;
       bwd_coef(rec, pos, gid, bg, k, fsx, fsy, fsz, cut2, C, q0, q1, q2, q3);
-      const uint2 meta = smeta[t];
+      const uint4 meta = smeta[t];
       const int yl = meta.x & 255, ny = (meta.x >> 8) & 255, zl = (meta.x >> 16) & 255,
                 nz = meta.x >> 24;
       const int cost = (int)meta.y;
@@ -664,18 +719,22 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
       for (int a = 0; a < 11; ++a) acc[a] = 0.f;
       if (spans_ok) {
         const unsigned char* my_sp = sspan + t * rows_cap;
-        int row = -1, x = 1, xb = 0, y = 0, z = 0, srow = 0;
+        unsigned long long rmask = ((unsigned long long)meta.w << 32) | meta.z;
+        // row r -> (y, z) = (yl + r % ny, zl + r / ny) by reciprocal multiply
+        // (exact for r < 64, ny <= 255): no integer division in the loop.
+        const unsigned recip_ny = ny > 1 ? (unsigned)((0xFFFFFFFFull + ny) / (unsigned)ny) : 0u;
+        int x = 1, xb = 0, y = 0, z = 0, srow = 0;
         float vr0 = 0.f, vr1 = 0.f, vr2 = 0.f, dy = 0.f, dz = 0.f;
         for (int it = 0; it < cost; ++it) {
-          if (x > xb) {   // advance to the next non-empty row
-            do {
-              ++row;
-              const int sp = my_sp[row];
-              x = sp & 15;
-              xb = sp >> 4;
-            } while (x > xb);
-            y = yl + row % ny;
-            z = zl + row / ny;
+          if (x > xb) {   // next non-empty row
+            const int row = __ffsll((long long)rmask) - 1;
+            rmask &= rmask - 1;
+            const int sp = my_sp[row];
+            x = sp & 15;
+            xb = sp >> 4;
+            const int zo = ny > 1 ? (int)__umulhi((unsigned)row, recip_ny) : row;
+            y = yl + row - zo * ny;
+            z = zl + zo;
             vr0 = fmaf((float)z, C.ez[0], fmaf((float)y, C.ey[0], C.u[0]));
             vr1 = fmaf((float)z, C.ez[1], fmaf((float)y, C.ey[1], C.u[1]));
             vr2 = fmaf((float)z, C.ez[2], fmaf((float)y, C.ey[2], C.u[2]));
