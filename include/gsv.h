@@ -153,6 +153,10 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  *   loss_part (nbricks_slab) double : per-brick sum |I-T| (l1) or (I-T)^2.
  * loss_kind: 0 = l1, 1 = l2.  vox_count = global voxel count V, so
  * dL/dI = sign(I-T)/V (l1) or 2(I-T)/V (l2) exactly as optimize.py:99-102.
+ * live_masks (optional, f32, bricks of <= 256 voxels): 4 planes of P uint2,
+ * plane w = warp tile w, entry j = list entry j: {live bits of the tile's
+ * voxel z0, voxel z0+1} -- the forward's exact truncation decisions, consumed
+ * by gsv_backward so the backward walks only live voxels.
  * ------------------------------------------------------------------------ */
 int gsv_forward(const double* positions, const gsv_record32* rec32,
                 const gsv_record64* rec64, const int64_t* starts,
@@ -160,7 +164,7 @@ int gsv_forward(const double* positions, const gsv_record32* rec32,
                 const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
                 int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, void* stream);
+                double* loss_part, uint32_t* live_masks, void* stream);
 
 /* Per-voxel backward inputs from (W, I, dL/dI) for the unfused API path
  * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) = {dL/dI / W, I}
@@ -177,13 +181,16 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi,
  * partials[(e)*12 ...] where e is the pair's gid-major emission index
  * gstart[gid] + rank of the brick in the Gaussian's box -- i.e. the order
  * the reference merges in (raster.py:512-516: stable argsort by gid keeps
- * ascending brick order).  partials: float (f32) or double (f64), (P,12). */
+ * ascending brick order).  partials: float (f32) or double (f64), (P,12).
+ * live_masks: the masks gsv_forward wrote for the same index (f32 only), or
+ * NULL to find live voxels from exact per-row spans. */
 int gsv_backward(const double* positions, const gsv_record32* rec32,
                  const gsv_record64* rec64, const int64_t* starts,
                  const int32_t* gids, const int64_t* gstart,
                  const int32_t* box, const gsv_grid* grid,
                  const gsv_bricks* bricks, double cutoff_sigma,
-                 int precision, const void* ab, void* partials, void* stream);
+                 int precision, const void* ab, const uint32_t* live_masks,
+                 void* partials, void* stream);
 
 /* Deterministic per-Gaussian merge of pair partials in ascending brick order
  * (_merge_pairs_kernel, raster.py:412-451).  gsum (N,12) double. */

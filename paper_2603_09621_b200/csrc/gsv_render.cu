@@ -19,6 +19,7 @@
 // part 2), so both engines agree on which pairs are live.
 // f64 engine: the reference arithmetic in double (precision="f64").
 #include <cfloat>
+#include <cstdlib>
 
 #include "gsv_common.cuh"
 
@@ -180,8 +181,10 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
                  gsv_grid g, gsv_bricks k, float cut2, double cut2d, double eps_w,
                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
                  const float* __restrict__ target, int loss_kind, double vox_count,
-                 float2* __restrict__ ab, double* __restrict__ loss_part) {
+                 float2* __restrict__ ab, double* __restrict__ loss_part,
+                 uint2* __restrict__ live_masks) {
   __shared__ Pair32 sp[kFwdThreads];   // 32 slots per warp
+  __shared__ uint2 smask[kFwdThreads]; // live bits of this round's pairs, per warp
   __shared__ double red[kFwdThreads / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
@@ -193,6 +196,9 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
   const int units = k.bdx * k.bdy * ((k.bdz + 1) >> 1);
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
   const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  // masks need one pass over the brick's voxel units (<= 128 units = 256 voxels)
+  const bool want_masks = live_masks != nullptr && units <= kFwdThreads;
+  const int64_t mstride = starts[gridDim.x];   // pairs of the slab: mask plane stride
   double lsum = 0.0;
 
   for (int ubase = 0; ubase < units; ubase += kFwdThreads) {
@@ -290,18 +296,19 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
                                     2.5e-6f * qmag;
           const float qcut = isinf(cut2) ? -INFINITY : fmaf(sc, cut2, lr2);
           p.c.w = qcut + guard;          // live for sure above
-          p.d = make_float4(qcut - guard, __int_as_float(gid), 0.f, 0.f);
+          p.d = make_float4(qcut - guard, __int_as_float(gid), __int_as_float(lane), 0.f);
         }
       }
       // Compact this round's hits into consecutive slots (ballot rank), so the
       // evaluation loop below is a plain counter over broadcast smem records.
       const unsigned ball = __ballot_sync(kFull, hit);
       if (hit) wsp[__popc(ball & ((1u << lane) - 1u))] = p;
+      if (want_masks) smask[(warp << 5) + lane] = make_uint2(0u, 0u);
       __syncwarp();
       const int nh = __popc(ball);
       for (int jj = 0; jj < nh; ++jj) {
         const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c;
-        const float2 pd = *reinterpret_cast<const float2*>(&wsp[jj].d);
+        const float4 pd = wsp[jj].d;
         // q(X,Y,Z) for voxel A, then q at Z+1 by its finite difference
         float qa = fmaf(pa.y, mX, pa.x);
         qa = fmaf(pa.z, mY, qa);
@@ -316,20 +323,30 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
         const float qb = qa + dq;
         // Branch-free accumulation; the guard band re-decides in f64 (rare,
         // warp-voted), exactly like the reference's truncation test.
-        float wa = qa >= pc.w ? ex2_approx(qa) : 0.f;
-        float wb = qb >= pc.w ? ex2_approx(qb) : 0.f;
-        const bool bandA = qa < pc.w && qa >= pd.x;
-        const bool bandB = qb < pc.w && qb >= pd.x;
+        bool la = qa >= pc.w, lb = qb >= pc.w;
+        const bool bandA = !la && qa >= pd.x;
+        const bool bandB = !lb && qb >= pd.x;
         if (__any_sync(kFull, bandA || bandB)) {
           const int gidj = __float_as_int(pd.y);
-          if (bandA && exact_live(gidj, gx, gy, gz, pos, rec64, g, cut2d)) wa = ex2_approx(qa);
-          if (bandB && exact_live(gidj, gx, gy, gz + 1, pos, rec64, g, cut2d)) wb = ex2_approx(qb);
+          if (bandA) la = exact_live(gidj, gx, gy, gz, pos, rec64, g, cut2d);
+          if (bandB) lb = exact_live(gidj, gx, gy, gz + 1, pos, rec64, g, cut2d);
+        }
+        const float wa = la ? ex2_approx(qa) : 0.f;
+        const float wb = lb ? ex2_approx(qb) : 0.f;
+        if (want_masks) {
+          const unsigned ma = __ballot_sync(kFull, la && ownA);
+          const unsigned mb = __ballot_sync(kFull, lb && ownB);
+          if (lane == 0) smask[(warp << 5) + __float_as_int(pd.z)] = make_uint2(ma, mb);
         }
         accSA = fmaf(pc.z, wa, accSA);
         accWA += wa;
         accSB = fmaf(pc.z, wb, accSB);
         accWB += wb;
       }
+      // live-voxel masks for the backward, plane [warp][pair]: one coalesced
+      // 256-byte store per warp and round (pairs missing the tile get zeros)
+      __syncwarp();
+      if (want_masks && gid >= 0) live_masks[warp * mstride + base + lane] = smask[(warp << 5) + lane];
       __syncwarp();
     }
     // Epilogue: normalise, store, fused loss (optimize.py:91-103).
@@ -587,7 +604,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                   const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
                   gsv_grid g, gsv_bricks k, float cut2, double cut2d,
-                  const float2* __restrict__ ab, float4* __restrict__ partials) {
+                  const float2* __restrict__ ab, float4* __restrict__ partials, int dbg) {
   extern __shared__ __align__(16) unsigned char bwd_smem[];
   unsigned char* sspan = bwd_smem;                                       // kBwdSpanBytes
   uint4* smeta = reinterpret_cast<uint4*>(bwd_smem + kBwdSpanBytes);     // per pair
@@ -639,28 +656,34 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
         const float inv_qa = 1.0f / qa;
         const float lim = cut2 + C.guard;
         unsigned char* my_sp = sspan + t * rows_cap;
-        int row = 0;
+        const int ny = yh - yl + 1;
+        // per-pair constants of the in-plane quadratics
+        const float b1 = fmaf(C.ey[0], C.ex[0], fmaf(C.ey[1], C.ex[1], C.ey[2] * C.ex[2]));
+        const float c2 = fmaf(C.ey[0], C.ey[0], fmaf(C.ey[1], C.ey[1], C.ey[2] * C.ey[2]));
         for (int z = zl; z <= zh; ++z) {
-          for (int y = yl; y <= yh; ++y, ++row) {
-            const float vr0 = fmaf((float)z, C.ez[0], fmaf((float)y, C.ey[0], C.u[0]));
-            const float vr1 = fmaf((float)z, C.ez[1], fmaf((float)y, C.ey[1], C.u[1]));
-            const float vr2 = fmaf((float)z, C.ez[2], fmaf((float)y, C.ey[2], C.u[2]));
-            const float qb = fmaf(vr0, C.ex[0], fmaf(vr1, C.ex[1], vr2 * C.ex[2]));
-            const float qc = fmaf(vr0, vr0, fmaf(vr1, vr1, vr2 * vr2));
+          // row y of plane z: v_row = w + y e_y with w = u + z e_z; along x
+          // d2(x) = qa x^2 + 2 qb x + qc, qb = b0 + y b1, qc = c0 + 2 y c1 + y^2 c2
+          const float w0 = fmaf((float)z, C.ez[0], C.u[0]);
+          const float w1 = fmaf((float)z, C.ez[1], C.u[1]);
+          const float w2 = fmaf((float)z, C.ez[2], C.u[2]);
+          const float b0 = fmaf(w0, C.ex[0], fmaf(w1, C.ex[1], w2 * C.ex[2]));
+          const float c0 = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
+          const float c1 = fmaf(w0, C.ey[0], fmaf(w1, C.ey[1], w2 * C.ey[2]));
+          const int rbase = (z - zl) * ny - yl;
+          for (int y = yl; y <= yh; ++y) {
+            const float fy = (float)y;
+            const float qb = fmaf(fy, b1, b0);
+            const float qc = fmaf(fy, fmaf(fy, c2, 2.f * c1), c0);
             // (qa x + qb)^2 <= qb^2 - qa (qc - lim)
             const float disc = fmaf(qb, qb, -qa * (qc - lim));
-            int xa = 15, xb = 0;
-            if (disc >= 0.f) {
-              const float sq = sqrtf(disc);
-              xa = max(0, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
-              xb = min(bg.ex - 1, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
-              if (xa > xb) {
-                xa = 15; xb = 0;
-              } else {
-                cost += xb - xa + 1;
-                rmask |= 1ull << row;
-              }
-            }
+            if (!(disc >= 0.f)) continue;
+            const float sq = sqrtf(disc);
+            const int xa = max(0, (int)ceilf((-qb - sq) * inv_qa - 1e-3f));
+            const int xb = min(bg.ex - 1, (int)floorf((-qb + sq) * inv_qa + 1e-3f));
+            if (xa > xb) continue;
+            const int row = rbase + y;
+            cost += xb - xa + 1;
+            rmask |= 1ull << row;
             my_sp[row] = (unsigned char)(xa | (xb << 4));
           }
         }
@@ -696,7 +719,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
     }
     __syncthreads();
     // ---- (3) warps pull 32-pair groups, heaviest first
-    const int ngroups = (cnt + 31) >> 5;
+    const int ngroups = dbg == 3 ? 0 : (cnt + 31) >> 5;
     for (;;) {
       int grp = 0;
       if (lane == 0) grp = atomicAdd(snextp, 1);
@@ -802,6 +825,163 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
     }
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------------- backward f32, masked
+// Train-step backward when the forward emitted live-voxel masks: per pair
+// four {voxel A, voxel B} 32-bit masks, one per warp tile (live_masks).  The
+// forward already decided every (pair, voxel) exactly (f32 + f64 guard
+// band), so here the pair's cost is its popcount, pairs are counting-sorted
+// by it (heaviest first), warps pull 32-pair groups, and each lane walks the
+// set bits of its pair -- exactly the live voxels, nothing else.
+constexpr int kBwdMChunk = 2048;
+
+__global__ void __launch_bounds__(kBwdThreads, 3)
+backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
+                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
+                   const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
+                   gsv_grid g, gsv_bricks k, float cut2, const uint2* __restrict__ masks,
+                   const float2* __restrict__ ab, float4* __restrict__ partials) {
+  __shared__ float2 sab[256];                 // brick voxels (units <= 128)
+  __shared__ unsigned sunit[128];             // unit -> lx | ly<<8 | lz0<<16
+  __shared__ unsigned short sorder[kBwdMChunk];
+  __shared__ unsigned char scost[kBwdMChunk];
+  __shared__ int shist[kBwdBuckets];
+  __shared__ int snext;
+  const int lb = blockIdx.x;
+  const int b = (int)slab_first(k) + lb;
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  if (lbeg == lend) return;
+  const BrickGeom bg = brick_geom(b, g, k);
+  const BrickXYZ bc = brick_xyz(b, k);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
+  const bool tiled = ((k.bdx | k.bdy | k.bdz) & 3) == 0;
+  const int units = k.bdx * k.bdy * ((k.bdz + 1) >> 1);
+  const int64_t mstride = starts[gridDim.x];   // mask plane stride = slab pairs
+  for (int u = tid; u < units; u += kBwdThreads) {
+    int x, y, z0;
+    unit_voxel(u, k, tiled, x, y, z0);
+    sunit[u] = (unsigned)x | ((unsigned)y << 8) | ((unsigned)z0 << 16);
+  }
+  {
+    const int nv = bg.ex * bg.ey * bg.ez;
+    for (int v = tid; v < nv; v += kBwdThreads) {
+      const int x = v % bg.ex, y = (v / bg.ex) % bg.ey, z = v / (bg.ex * bg.ey);
+      const int64_t lin =
+          (int64_t)(bg.x0 + x) + (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
+      sab[x + k.bdx * (y + k.bdy * z)] = __ldg(ab + lin);
+    }
+  }
+  for (int64_t cbase = lbeg; cbase < lend; cbase += kBwdMChunk) {
+    const int cnt = (int)min((int64_t)kBwdMChunk, lend - cbase);
+    if (tid < kBwdBuckets) shist[tid] = 0;
+    if (tid == 0) snext = 0;
+    __syncthreads();
+    // (1) cost = live voxels of the pair
+    for (int t = tid; t < cnt; t += kBwdThreads) {
+      const int64_t jt = cbase + t;
+      const uint2 a0 = __ldg(masks + jt), a1 = __ldg(masks + mstride + jt),
+                  a2 = __ldg(masks + 2 * mstride + jt), a3 = __ldg(masks + 3 * mstride + jt);
+      const int c = __popc(a0.x) + __popc(a0.y) + __popc(a1.x) + __popc(a1.y) + __popc(a2.x) +
+                    __popc(a2.y) + __popc(a3.x) + __popc(a3.y);
+      scost[t] = (unsigned char)min(c, 255);
+      atomicAdd(&shist[kBwdBuckets - 1 - min(c, kBwdBuckets - 1)], 1);
+    }
+    __syncthreads();
+    // (2) counting sort, heaviest first
+    if (tid < 32) {
+      int v[4], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { v[i] = shist[4 * tid + i]; sum += v[i]; }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(kFull, incl, o);
+        if (tid >= o) incl += n;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { shist[4 * tid + i] = run; run += v[i]; }
+    }
+    __syncthreads();
+    for (int t = tid; t < cnt; t += kBwdThreads) {
+      const int slot = atomicAdd(&shist[kBwdBuckets - 1 - min((int)scost[t], kBwdBuckets - 1)], 1);
+      sorder[slot] = (unsigned short)t;
+    }
+    __syncthreads();
+    // (3) warps pull groups; each lane walks its pair's live voxels
+    const int ngroups = (cnt + 31) >> 5;
+    for (;;) {
+      int grp = 0;
+      if (lane == 0) grp = atomicAdd(&snext, 1);
+      grp = __shfl_sync(kFull, grp, 0);
+      if (grp >= ngroups) break;
+      const int s = (grp << 5) + lane;
+      if (s >= cnt) continue;
+      const int t = sorder[s];
+      const int64_t j = cbase + t;
+      const int gid = gids[j];
+      const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+      const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2);
+      const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+      const float A = q2.y, r = q2.z;
+      const double* m = pos + 3 * (int64_t)gid;
+      const float c0 = (float)(bg.px - __ldg(m)), c1 = (float)(bg.py - __ldg(m + 1)),
+                  c2 = (float)(bg.pz - __ldg(m + 2));   // p_b0 - mu
+      float u[3], ex[3], ey[3], ez[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        u[a] = fmaf(L[3 * a], c0, fmaf(L[3 * a + 1], c1, L[3 * a + 2] * c2));
+        ex[a] = L[3 * a] * fsx;
+        ey[a] = L[3 * a + 1] * fsy;
+        ez[a] = L[3 * a + 2] * fsz;
+      }
+      const uint2 a0 = __ldg(masks + j), a1 = __ldg(masks + mstride + j),
+                  a2 = __ldg(masks + 2 * mstride + j), a3 = __ldg(masks + 3 * mstride + j);
+      const unsigned words[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+      float acc[11];
+#pragma unroll
+      for (int a = 0; a < 11; ++a) acc[a] = 0.f;
+      const int cost = scost[t];
+      int wi = 0;
+      unsigned cur = words[0];
+      for (int it = 0; it < cost; ++it) {
+        while (cur == 0u) {      // next non-empty word (static indexing)
+          ++wi;
+          cur = wi == 1 ? words[1] : wi == 2 ? words[2] : wi == 3 ? words[3] : wi == 4 ? words[4]
+              : wi == 5 ? words[5] : wi == 6 ? words[6] : words[7];
+        }
+        const int bit = __ffs(cur) - 1;
+        cur &= cur - 1u;
+        // word wi = 2*warp + half; lane bit -> unit warp*32 + bit; half -> z0 / z0+1
+        const unsigned uv = sunit[((wi >> 1) << 5) + bit];
+        const int x = uv & 255, y = (uv >> 8) & 255, z = ((uv >> 16) & 255) + (wi & 1);
+        const float2 v_ab = sab[x + k.bdx * (y + k.bdy * z)];
+        if (v_ab.x == 0.f) continue;
+        const float fx = (float)x, fy = (float)y, fz = (float)z;
+        const float v0 = fmaf(fz, ez[0], fmaf(fy, ey[0], fmaf(fx, ex[0], u[0])));
+        const float v1 = fmaf(fz, ez[1], fmaf(fy, ey[1], fmaf(fx, ex[1], u[1])));
+        const float v2 = fmaf(fz, ez[2], fmaf(fy, ey[2], fmaf(fx, ex[2], u[2])));
+        const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
+        bwd_accumulate(d2, r, A, v_ab, v0, v1, v2, fmaf(fx, fsx, c0), fmaf(fy, fsy, c1),
+                       fmaf(fz, fsz, c2), acc);
+      }
+      const float mu0 = fmaf(q0.x, acc[2], fmaf(q0.w, acc[3], q1.z * acc[4]));
+      const float mu1 = fmaf(q0.y, acc[2], fmaf(q1.x, acc[3], q1.w * acc[4]));
+      const float mu2 = fmaf(q0.z, acc[2], fmaf(q1.y, acc[3], q2.x * acc[4]));
+      const GBox gb = unpack_box(box, gid);
+      const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
+      if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
+      const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+      float4* dst = partials + 3 * e;
+      dst[0] = make_float4(acc[0], acc[1], mu0, mu1);
+      dst[1] = make_float4(mu2, acc[5], acc[6], acc[7]);
+      dst[2] = make_float4(acc[8], acc[9], acc[10], 0.f);
+    }
+    __syncthreads();
+  }
+  (void)cut2;
 }
 
 // ------------------------------------------------------------- backward f64
@@ -949,7 +1129,7 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
                 const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
                 double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, void* stream) {
+                double* loss_part, uint32_t* live_masks, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
   GSV_REQUIRE(rec64 != nullptr, "forward needs rec64 (f64 whitening factors)");
@@ -964,7 +1144,7 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
     forward32_kernel<<<(unsigned)nb, kFwdThreads, 0, s>>>(
         positions, rec32, rec64, starts, gids, *grid, *bricks, (float)cut2d,
         cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
-        (float2*)ab, loss_part);
+        (float2*)ab, loss_part, (uint2*)live_masks);
     GSV_CHECK_LAUNCH("forward32_kernel");
   } else {
     forward64_kernel<<<(unsigned)nb, 128, 0, s>>>(
@@ -1006,7 +1186,8 @@ int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_r
                  const int64_t* starts,
                  const int32_t* gids, const int64_t* gstart, const int32_t* box,
                  const gsv_grid* grid, const gsv_bricks* bricks, double cutoff_sigma,
-                 int precision, const void* ab, void* partials, void* stream) {
+                 int precision, const void* ab, const uint32_t* live_masks, void* partials,
+                 void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
   GSV_REQUIRE(rec64 != nullptr, "backward needs rec64 (f64 whitening factors)");
@@ -1014,10 +1195,18 @@ int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_r
   if (nb == 0) return GSV_OK;
   const double cut2d = cutoff_sigma * cutoff_sigma;
   cudaStream_t s = as_stream(stream);
-  if (precision == 0) {
+  const int64_t units = (int64_t)bricks->bdx * bricks->bdy * ((bricks->bdz + 1) / 2);
+  if (precision == 0 && live_masks != nullptr) {
+    GSV_REQUIRE(units <= kFwdThreads, "live masks need bricks of <= 256 voxels");
+    backward32m_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(
+        positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,
+        (const uint2*)live_masks, (const float2*)ab, (float4*)partials);
+    GSV_CHECK_LAUNCH("backward32m_kernel");
+  } else if (precision == 0) {
     const int64_t bvox = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz;
     const bool smem = bvox <= kBwdSmemVoxels;
     const size_t shm = bwd_smem_bytes(smem ? (int)bvox : 0);
+    static const int dbg = getenv("GSV_DEBUG_BWD") ? atoi(getenv("GSV_DEBUG_BWD")) : 0;
     static bool attr_set[2] = {false, false};
     if (!attr_set[smem]) {
       const int maxb = (int)bwd_smem_bytes(smem ? kBwdSmemVoxels : 0);
@@ -1031,11 +1220,11 @@ int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_r
     if (smem)
       backward32_kernel<true><<<(unsigned)nb, kBwdThreads, shm, s>>>(
           positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
-          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
+          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials, dbg);
     else
       backward32_kernel<false><<<(unsigned)nb, kBwdThreads, shm, s>>>(
           positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
-          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
+          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials, dbg);
     GSV_CHECK_LAUNCH("backward32_kernel");
   } else {
     backward64_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(

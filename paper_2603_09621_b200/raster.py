@@ -295,7 +295,7 @@ def _records(f, grid, idx: BrickIndex, opts: RenderOptions):
 
 # ----------------------------------------------------------------- forward
 def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_kind=0,
-                  ab=None, loss_part=None):
+                  ab=None, loss_part=None, live_masks=None):
     lib = _lib.lib()
     _lib.check(lib.gsv_forward(
         f.positions.data_ptr(), rec32.data_ptr(), rec64.data_ptr(), idx.starts.data_ptr(),
@@ -303,7 +303,8 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
-        float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.stream_ptr()), "forward")
+        float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
+        _lib.stream_ptr()), "forward")
 
 
 def forward(f: GaussianField, grid: GridSpec, idx: BrickIndex,
@@ -337,7 +338,7 @@ def _emission_layout(f, grid, idx: BrickIndex, opts: RenderOptions):
 
 
 def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: bool,
-                   timer=None, pool=None):
+                   timer=None, pool=None, live_masks=None):
     lib = _lib.lib()
     n = f.count
     pdt = opts.torch_dtype
@@ -352,8 +353,8 @@ def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: b
         f.positions.data_ptr(), rec32.data_ptr(), rec64.data_ptr(), idx.starts.data_ptr(),
         idx.gids.data_ptr(), gstart.data_ptr(),
         box.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
-        float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), partials.data_ptr(),
-        _lib.stream_ptr()), "backward")
+        float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), _lib.ptr(live_masks),
+        partials.data_ptr(), _lib.stream_ptr()), "backward")
     gsum = _alloc(pool, "gsum", (n, 12), torch.float64, f.device)
     if timer is not None:
         timer("merge")

@@ -18,6 +18,7 @@ chain rule and Adam step, so parameters stay replicated.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -104,6 +105,7 @@ class TrainStep:
         # Persistent buffers: index, voxel arrays, pair partials, gradients.
         # Everything a step returns is a view valid until the next step.
         self.pool = _lib.BufferPool(self.target.device)
+        self._masks = None
 
     @property
     def sharded(self) -> bool:
@@ -132,9 +134,17 @@ class TrainStep:
         ab = pool.get("ab", (nvox, 2), dt)
         nb = max(idx.brick_count, 1)
         loss_part = pool.get("loss_part", (nb,), torch.float64)
+        # live-voxel masks (f32, bricks <= 256 voxels): the backward then walks
+        # exactly the forward's live voxels
+        bd = self.brick_dims
+        masks = None
+        if (opts.precision == "f32" and bd[0] * bd[1] * ((bd[2] + 1) // 2) <= 128
+                and not os.environ.get("GSV_NO_LIVE_MASKS")):
+            masks = pool.get("live_masks", (4, max(idx.pair_count, 1), 2), torch.int32)
         self._mark("forward")
         _forward_into(f, grid, idx, opts, aux.rec32, aux.rec64, S, W, I, target=self.target,
-                      loss_kind=self.loss_kind, ab=ab, loss_part=loss_part)
+                      loss_kind=self.loss_kind, ab=ab, loss_part=loss_part, live_masks=masks)
+        self._masks = masks
         self._mark("loss_sum")
         loss_sum = pool.get("loss_sum", (1,), torch.float64)
         loss_sum.zero_()
@@ -149,7 +159,8 @@ class TrainStep:
         idx = out.idx
         aux = idx._aux
         gsum = _pair_partials(f, self.grid, idx, self.opts, aux.rec32, aux.rec64, out.ab,
-                              aux.gstart, aux.box, True, timer=self.timer, pool=self.pool)
+                              aux.gstart, aux.box, True, timer=self.timer, pool=self.pool,
+                              live_masks=self._masks)
         if self.sharded:
             # One collective per step: the merged per-Gaussian partials, with
             # this rank's loss partial riding in the spare 12th column.
@@ -206,7 +217,8 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
     opts = self.opts
     if self.sharded:
         gsum = _pair_partials(f, self.grid, idx, opts, aux.rec32, aux.rec64, out.ab, aux.gstart,
-                              aux.box, True, timer=self.timer, pool=self.pool)
+                              aux.box, True, timer=self.timer, pool=self.pool,
+                              live_masks=self._masks)
         import torch.distributed as dist
         self._mark("allreduce")
         gsum[0, 11] = out.loss_sum[0]
@@ -225,7 +237,7 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
             idx.starts.data_ptr(), idx.gids.data_ptr(), aux.gstart.data_ptr(), aux.box.data_ptr(),
             _lib.make_grid(self.grid), _lib.make_bricks(self.grid, idx.brick_dims, idx.slab),
             float(opts.cutoff_sigma), opts.precision_code, out.ab.data_ptr(),
-            partials.data_ptr(), _lib.stream_ptr()), "backward")
+            _lib.ptr(self._masks), partials.data_ptr(), _lib.stream_ptr()), "backward")
         self._mark("update")
         _adam_launch(f, state, lrs, beta1, beta2, eps, partials, aux.gstart, None,
                      opts.precision_code)

@@ -432,7 +432,8 @@ def test_train_step_matches_unfused_api():
     g2 = gs.backward(f, lr.grid, idx, c, dl)
     assert abs(out.loss() - loss) <= 1e-12
     np.testing.assert_array_equal(np_(out.cache.I), np_(c.I))
-    for k in GRAD_KEYS:  # same kernels, same inputs: bit-identical
-        np.testing.assert_array_equal(np_(getattr(grads, k)), np_(getattr(g2, k)))
+    for k in GRAD_KEYS:  # masked (train step) vs span (public API) backward
+        a, b = np_(getattr(grads, k)), np_(getattr(g2, k))
+        assert np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(b) + 1e-20, k
     meta = load_json("config1.json")
     assert abs(out.loss() - meta["loss"]) <= 1e-6
