@@ -157,6 +157,9 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  * plane w = warp tile w, entry j = list entry j: {live bits of the tile's
  * voxel z0, voxel z0+1} -- the forward's exact truncation decisions, consumed
  * by gsv_backward so the backward walks only live voxels.
+ * vpl_hint: voxels per lane of the f32 kernel's warp tiles; 4 (8x4x4 tiles)
+ * pays off when Gaussians span several bricks (e.g. pairs/Gaussian >= 8),
+ * else 2 (4x4x4 tiles).  Ignored (2) when live_masks != NULL.
  * ------------------------------------------------------------------------ */
 int gsv_forward(const double* positions, const gsv_record32* rec32,
                 const gsv_record64* rec64, const int64_t* starts,
@@ -164,7 +167,7 @@ int gsv_forward(const double* positions, const gsv_record32* rec32,
                 const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
                 int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, uint32_t* live_masks, void* stream);
+                double* loss_part, uint32_t* live_masks, int vpl_hint, void* stream);
 
 /* Per-voxel backward inputs from (W, I, dL/dI) for the unfused API path
  * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) = {dL/dI / W, I}

@@ -166,15 +166,38 @@ __device__ __forceinline__ float exp_neg_half(float d2) {
   return r;
 }
 
-// One CTA per brick, 4 warps, each owning one voxel tile (2 voxels per lane).
-// Warps walk the brick's list independently -- no CTA barrier in the pair
-// loop: per round of 32 list entries every lane stages one pair into the
-// warp's private smem slots and tests its 3-sigma box against the warp's
-// tile; a ballot leaves only the pairs that reach the tile, evaluated in list
-// order (deterministic accumulation, no atomics).  Staging is repeated per
-// warp (4x, L1-resident loads) -- cheaper than the barrier stalls of shared
-// staging, where every warp waits for the slowest tile each chunk.
-__global__ void __launch_bounds__(kFwdThreads, 5)
+// One CTA per brick.  Each lane owns a z-column of VPL voxels; a warp's 32
+// lanes form one voxel tile (VPL = 2: 4x4x4 tiles, 4 warps per 8x8x4 brick --
+// small Gaussians, the LR train grid; VPL = 4: 8x4x4 tiles, 2 warps per brick
+// -- Gaussians spanning several bricks, HR renders).  Warps walk the brick's
+// list independently -- no CTA barrier in the pair loop: per round of 32 list
+// entries every lane stages one pair, tests its 3-sigma box against the
+// warp's tile, and the hits are compacted (ballot rank) into warp-private smem
+// records, then evaluated in list order (deterministic, no atomics).  The
+// exponent q = -(1/2) log2(e) d2 + log2(r) is a quadratic in the lane's voxel
+// offset from the tile centre: 9 FMAs for the first voxel of the column, 2
+// FADDs (second differences) for each further one, one EX2 per voxel.
+// Staging is repeated per warp (L1-resident loads): cheaper than the barrier
+// stalls of shared staging, where every warp waits for the slowest tile.
+template <int VPL>
+__device__ __forceinline__ void unit_voxel_v(int u, const gsv_bricks& k, int& x, int& y,
+                                             int& z0) {
+  const bool tiled = VPL == 2 && ((k.bdx | k.bdy | k.bdz) & 3) == 0;
+  if (tiled) {
+    const int t = u >> 5, l = u & 31;
+    const int tgx = k.bdx >> 2, tgy = k.bdy >> 2;
+    x = ((t % tgx) << 2) + (l & 3);
+    y = (((t / tgx) % tgy) << 2) + ((l >> 2) & 3);
+    z0 = ((t / (tgx * tgy)) << 2) + ((l >> 4) << 1);
+  } else {
+    x = u % k.bdx;
+    y = (u / k.bdx) % k.bdy;
+    z0 = (u / (k.bdx * k.bdy)) * VPL;
+  }
+}
+
+template <int VPL, int THREADS>
+__global__ void __launch_bounds__(THREADS, 640 / THREADS)
 forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
                  const gsv_record64* __restrict__ rec64,
                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
@@ -183,34 +206,38 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
                  const float* __restrict__ target, int loss_kind, double vox_count,
                  float2* __restrict__ ab, double* __restrict__ loss_part,
                  uint2* __restrict__ live_masks) {
-  __shared__ Pair32 sp[kFwdThreads];   // 32 slots per warp
-  __shared__ uint2 smask[kFwdThreads]; // live bits of this round's pairs, per warp
-  __shared__ double red[kFwdThreads / 32];
+  __shared__ Pair32 sp[THREADS];       // 32 slots per warp
+  __shared__ uint2 smask[THREADS];     // live bits of this round's pairs, per warp
+  __shared__ double red[THREADS / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
   const BrickGeom bg = brick_geom(b, g, k);
   const int64_t lbeg = starts[lb], lend = starts[lb + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Pair32* wsp = sp + (warp << 5);
-  const bool tiled = ((k.bdx | k.bdy | k.bdz) & 3) == 0;
-  const int units = k.bdx * k.bdy * ((k.bdz + 1) >> 1);
+  const int units = k.bdx * k.bdy * ((k.bdz + VPL - 1) / VPL);
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
   const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
-  // masks need one pass over the brick's voxel units (<= 128 units = 256 voxels)
-  const bool want_masks = live_masks != nullptr && units <= kFwdThreads;
+  // masks: VPL 2, one pass over the brick's voxel units (4 warp tiles)
+  const bool want_masks = VPL == 2 && THREADS == 128 && live_masks != nullptr && units <= THREADS;
   const int64_t mstride = starts[gridDim.x];   // pairs of the slab: mask plane stride
   double lsum = 0.0;
 
-  for (int ubase = 0; ubase < units; ubase += kFwdThreads) {
+  for (int ubase = 0; ubase < units; ubase += THREADS) {
     const int u = ubase + tid;
     int lx = 0, ly = 0, lz = 0;
-    if (u < units) unit_voxel(u, k, tiled, lx, ly, lz);
-    const bool ownA = u < units && lx < bg.ex && ly < bg.ey && lz < bg.ez;
-    const bool ownB = ownA && lz + 1 < bg.ez && lz + 1 < k.bdz;
+    if (u < units) unit_voxel_v<VPL>(u, k, lx, ly, lz);
+    bool own[VPL];
+    int zmax = -(1 << 20);
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) {
+      own[h] = u < units && lx < bg.ex && ly < bg.ey && lz + h < bg.ez && lz + h < k.bdz;
+      if (own[h]) zmax = lz + h;
+    }
     // This warp's tile box (brick-local voxel coords) from its owned voxels.
-    int txl = ownA ? lx : 1 << 20, txh = ownA ? lx : -(1 << 20);
-    int tyl = ownA ? ly : 1 << 20, tyh = ownA ? ly : -(1 << 20);
-    int tzl = ownA ? lz : 1 << 20, tzh = ownB ? lz + 1 : (ownA ? lz : -(1 << 20));
+    int txl = own[0] ? lx : 1 << 20, txh = own[0] ? lx : -(1 << 20);
+    int tyl = own[0] ? ly : 1 << 20, tyh = own[0] ? ly : -(1 << 20);
+    int tzl = own[0] ? lz : 1 << 20, tzh = zmax;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       txl = min(txl, __shfl_xor_sync(kFull, txl, o));
@@ -225,12 +252,14 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
     // Tile centre and this lane's voxel offsets from it (exact halves in f32).
     const float ctx = 0.5f * (ftxl + ftxh), cty = 0.5f * (ftyl + ftyh), ctz = 0.5f * (ftzl + ftzh);
     const float ext_x = fmaxf(0.5f * (ftxh - ftxl), 0.f), ext_y = fmaxf(0.5f * (ftyh - ftyl), 0.f),
-                ext_z = fmaxf(0.5f * (ftzh - ftzl), 0.f) + 1.f;
+                ext_z = fmaxf(0.5f * (ftzh - ftzl), 0.f);
     const float mX = (float)lx - ctx, mY = (float)ly - cty, mZ = (float)lz - ctz;
     const float mXX = mX * mX, mYY = mY * mY, mZZ = mZ * mZ, mXY = mX * mY, mXZ = mX * mZ,
                 mYZ = mY * mZ, m2Z1 = fmaf(2.f, mZ, 1.f);
     const int gx = bg.x0 + lx, gy = bg.y0 + ly, gz = bg.z0 + lz;
-    float accSA = 0.f, accWA = 0.f, accSB = 0.f, accWB = 0.f;
+    float accS[VPL], accW[VPL];
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) accS[h] = accW[h] = 0.f;
 
     int gid_next = (lbeg + lane < lend) ? __ldg(gids + lbeg + lane) : -1;
     for (int64_t base = lbeg; base < lend; base += 32) {
@@ -284,8 +313,8 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
           p.c.y = 2.f * sc * fmaf(e[1][0], e[2][0], fmaf(e[1][1], e[2][1], e[1][2] * e[2][2]));
           p.c.z = q2.y;
           // Guard band in q units: the direct-v bound (kGuard*, scaled by |s|)
-          // plus the rounding of the expanded quadratic (~7e-7 of the sum of
-          // its term magnitudes over the tile), x8.
+          // plus the rounding of the expanded quadratic and its VPL-1 finite
+          // differences (~7e-7 of the sum of its term magnitudes), x3.5.
           const float qmag = fabsf(p.a.x) + ext_x * fabsf(p.a.y) + ext_y * fabsf(p.a.z) +
                              ext_z * fabsf(p.a.w) + ext_x * ext_x * fabsf(p.b.x) +
                              ext_y * ext_y * fabsf(p.b.y) + ext_z * ext_z * fabsf(p.b.z) +
@@ -309,7 +338,8 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
       for (int jj = 0; jj < nh; ++jj) {
         const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c;
         const float4 pd = wsp[jj].d;
-        // q(X,Y,Z) for voxel A, then q at Z+1 by its finite difference
+        // q(X,Y,Z) for the column's first voxel, then second differences
+        float q[VPL];
         float qa = fmaf(pa.y, mX, pa.x);
         qa = fmaf(pa.z, mY, qa);
         qa = fmaf(pa.w, mZ, qa);
@@ -319,47 +349,58 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
         qa = fmaf(pb.w, mXY, qa);
         qa = fmaf(pc.x, mXZ, qa);
         qa = fmaf(pc.y, mYZ, qa);
-        const float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, m2Z1, pa.w)));
-        const float qb = qa + dq;
+        q[0] = qa;
+        float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, m2Z1, pa.w)));
+        const float d2q = 2.f * pb.z;
+#pragma unroll
+        for (int h = 1; h < VPL; ++h) {
+          q[h] = q[h - 1] + dq;
+          dq += d2q;
+        }
         // Branch-free accumulation; the guard band re-decides in f64 (rare,
         // warp-voted), exactly like the reference's truncation test.
-        bool la = qa >= pc.w, lb = qb >= pc.w;
-        const bool bandA = !la && qa >= pd.x;
-        const bool bandB = !lb && qb >= pd.x;
-        if (__any_sync(kFull, bandA || bandB)) {
-          const int gidj = __float_as_int(pd.y);
-          if (bandA) la = exact_live(gidj, gx, gy, gz, pos, rec64, g, cut2d);
-          if (bandB) lb = exact_live(gidj, gx, gy, gz + 1, pos, rec64, g, cut2d);
+        bool live[VPL];
+        bool band = false;
+#pragma unroll
+        for (int h = 0; h < VPL; ++h) {
+          live[h] = q[h] >= pc.w;
+          band |= !live[h] && q[h] >= pd.x;
         }
-        const float wa = la ? ex2_approx(qa) : 0.f;
-        const float wb = lb ? ex2_approx(qb) : 0.f;
+        if (__any_sync(kFull, band)) {
+          const int gidj = __float_as_int(pd.y);
+#pragma unroll
+          for (int h = 0; h < VPL; ++h)
+            if (!live[h] && q[h] >= pd.x)
+              live[h] = exact_live(gidj, gx, gy, gz + h, pos, rec64, g, cut2d);
+        }
+#pragma unroll
+        for (int h = 0; h < VPL; ++h) {
+          const float w = live[h] ? ex2_approx(q[h]) : 0.f;
+          accS[h] = fmaf(pc.z, w, accS[h]);
+          accW[h] += w;
+        }
         if (want_masks) {
-          const unsigned ma = __ballot_sync(kFull, la && ownA);
-          const unsigned mb = __ballot_sync(kFull, lb && ownB);
+          const unsigned ma = __ballot_sync(kFull, live[0] && own[0]);
+          const unsigned mb = __ballot_sync(kFull, live[VPL - 1] && own[VPL - 1]);
           if (lane == 0) smask[(warp << 5) + __float_as_int(pd.z)] = make_uint2(ma, mb);
         }
-        accSA = fmaf(pc.z, wa, accSA);
-        accWA += wa;
-        accSB = fmaf(pc.z, wb, accSB);
-        accWB += wb;
       }
+      __syncwarp();
       // live-voxel masks for the backward, plane [warp][pair]: one coalesced
       // 256-byte store per warp and round (pairs missing the tile get zeros)
-      __syncwarp();
-      if (want_masks && gid >= 0) live_masks[warp * mstride + base + lane] = smask[(warp << 5) + lane];
+      if (want_masks && gid >= 0)
+        live_masks[warp * mstride + base + lane] = smask[(warp << 5) + lane];
       __syncwarp();
     }
     // Epilogue: normalise, store, fused loss (optimize.py:91-103).
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool own = h == 0 ? ownA : ownB;
-      if (!own) continue;
-      const float accS = h == 0 ? accSA : accSB, accW = h == 0 ? accWA : accWB;
+    for (int h = 0; h < VPL; ++h) {
+      if (!own[h]) continue;
       const int64_t lin = (int64_t)gx + (int64_t)g.nx * (gy + (int64_t)g.ny * (gz + h));
-      const bool cov = (double)accW >= eps_w;
-      const float iv = cov ? __fdiv_rn(accS, accW) : 0.f;
-      S[lin] = accS;
-      W[lin] = accW;
+      const bool cov = (double)accW[h] >= eps_w;
+      const float iv = cov ? __fdiv_rn(accS[h], accW[h]) : 0.f;
+      S[lin] = accS[h];
+      W[lin] = accW[h];
       I[lin] = iv;
       if (target) {
         const double d = (double)iv - (double)target[lin];
@@ -371,13 +412,13 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
           lsum += d * d;
           dl = 2.0 * d / vox_count;
         }
-        const float alpha = (cov && dl != 0.0) ? (float)(dl / (double)accW) : 0.f;
+        const float alpha = (cov && dl != 0.0) ? (float)(dl / (double)accW[h]) : 0.f;
         ab[lin] = make_float2(alpha, iv);
       }
     }
   }
   if (target) {
-    const double t = block_sum<kFwdThreads>(lsum, red);
+    const double t = block_sum<THREADS>(lsum, red);
     if (tid == 0) loss_part[lb] = t;
   }
 }
@@ -1129,7 +1170,7 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
                 const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
                 double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, uint32_t* live_masks, void* stream) {
+                double* loss_part, uint32_t* live_masks, int vpl_hint, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
   GSV_REQUIRE(rec64 != nullptr, "forward needs rec64 (f64 whitening factors)");
@@ -1141,10 +1182,19 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
   const double cut2d = cutoff_sigma * cutoff_sigma;
   cudaStream_t s = as_stream(stream);
   if (precision == 0) {
-    forward32_kernel<<<(unsigned)nb, kFwdThreads, 0, s>>>(
-        positions, rec32, rec64, starts, gids, *grid, *bricks, (float)cut2d,
-        cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
-        (float2*)ab, loss_part, (uint2*)live_masks);
+    // Column depth: 2 voxels for small Gaussians (LR train grid, and always
+    // when the backward wants live masks), 4 when Gaussians span several
+    // bricks (vpl_hint from the caller: pairs per Gaussian >= 8).
+    if (live_masks == nullptr && vpl_hint >= 4)
+      forward32_kernel<4, 64><<<(unsigned)nb, 64, 0, s>>>(
+          positions, rec32, rec64, starts, gids, *grid, *bricks, (float)cut2d,
+          cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
+          (float2*)ab, loss_part, nullptr);
+    else
+      forward32_kernel<2, 128><<<(unsigned)nb, 128, 0, s>>>(
+          positions, rec32, rec64, starts, gids, *grid, *bricks, (float)cut2d,
+          cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
+          (float2*)ab, loss_part, (uint2*)live_masks);
     GSV_CHECK_LAUNCH("forward32_kernel");
   } else {
     forward64_kernel<<<(unsigned)nb, 128, 0, s>>>(

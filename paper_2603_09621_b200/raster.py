@@ -21,6 +21,7 @@ int32 (the reference uses int64; values are identical), ``starts`` int64.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -294,6 +295,15 @@ def _records(f, grid, idx: BrickIndex, opts: RenderOptions):
 
 
 # ----------------------------------------------------------------- forward
+def _vpl_hint(idx, f) -> int:
+    """Voxels per lane for the forward's warp tiles: 4 when Gaussians span
+    several bricks (many pairs per Gaussian, e.g. HR renders), else 2."""
+    forced = os.environ.get("GSV_VPL")
+    if forced in ("2", "4"):
+        return int(forced)
+    return 4 if idx.pair_count >= 8 * max(f.count, 1) else 2
+
+
 def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_kind=0,
                   ab=None, loss_part=None, live_masks=None):
     lib = _lib.lib()
@@ -304,7 +314,7 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
-        _lib.stream_ptr()), "forward")
+        _vpl_hint(idx, f), _lib.stream_ptr()), "forward")
 
 
 def forward(f: GaussianField, grid: GridSpec, idx: BrickIndex,
