@@ -94,8 +94,9 @@ int gsv_device_sm_count(void);
  * (raster.py:175-198), computed in f64 with the reference's unfused operation
  * order (numpy einsum "nkm,nm->nk" sums (p0+p2)+p1).
  *   rec32  (N)   : gsv_record32, always written
- *   rec64  (N)   : gsv_record64, written when non-NULL (the f32 engine needs it
- *                  too: its guard-band re-decisions use the f64 factor)
+ *   rec64  (N)   : gsv_record64, written when non-NULL (required by the f64
+ *                  engine; the f32 engine recomputes the f64 factor from
+ *                  log_scales/rotations in its rare guard-band path)
  *   counts (N)   : pairs Gaussian i emits inside the slab (0 if outside)
  *   box    (N,4) : int32 {blo_x | blo_y<<16, blo_z | nb_x<<16, nb_y | nb_z<<16, 0}
  *                  brick box of Gaussian i clipped to the slab.
@@ -161,7 +162,8 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  * pays off when Gaussians span several bricks (e.g. pairs/Gaussian >= 8),
  * else 2 (4x4x4 tiles).  Ignored (2) when live_masks != NULL.
  * ------------------------------------------------------------------------ */
-int gsv_forward(const double* positions, const gsv_record32* rec32,
+int gsv_forward(const double* positions, const double* log_scales,
+                const double* rotations, const gsv_record32* rec32,
                 const gsv_record64* rec64, const int64_t* starts,
                 const int32_t* gids, const gsv_grid* grid,
                 const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
@@ -187,7 +189,8 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi,
  * ascending brick order).  partials: float (f32) or double (f64), (P,12).
  * live_masks: the masks gsv_forward wrote for the same index (f32 only), or
  * NULL to find live voxels from exact per-row spans. */
-int gsv_backward(const double* positions, const gsv_record32* rec32,
+int gsv_backward(const double* positions, const double* log_scales,
+                 const double* rotations, const gsv_record32* rec32,
                  const gsv_record64* rec64, const int64_t* starts,
                  const int32_t* gids, const int64_t* gstart,
                  const int32_t* box, const gsv_grid* grid,
@@ -245,12 +248,15 @@ typedef struct {
  * and quaternion renormalisation (field.py:100-102).  Same arithmetic as
  * gsv_merge + gsv_chain_rule + gsv_adam + gsv_normalize_rotations.
  * moments: host array of 10 device pointers {m_pos, m_ls, m_rot, m_amp,
- * m_rel, v_pos, v_ls, v_rot, v_amp, v_rel} (AdamState.m / .v). */
+ * m_rel, v_pos, v_ls, v_rot, v_amp, v_rel} (AdamState.m / .v).
+ * grad_scratch: NULL for the one-pass f32 kernel (default); else an (N,12)
+ * double workspace for the two-kernel path (merge+chain, then streaming
+ * Adam), required for precision 1. */
 int gsv_fused_update(const void* partials, const int64_t* gstart, const double* gsum,
                      int64_t n, int precision, double* positions, double* log_scales,
                      double* rotations, double* raw_amplitude, double* raw_relax,
                      double* const* moments, int amplitude_enabled, int relax_enabled,
-                     const gsv_adam_hparams* hp, void* stream);
+                     const gsv_adam_hparams* hp, double* grad_scratch, void* stream);
 
 /* q /= |q| per Gaussian (GaussianField.normalize_rotations, field.py:100). */
 int gsv_normalize_rotations(double* rotations, int64_t n, void* stream);

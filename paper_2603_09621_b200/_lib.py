@@ -58,10 +58,10 @@ _SIGS = {
     "gsv_lists_unsorted": [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp],
     "gsv_canonicalize_workspace": [c_i64, c_i32, c_szp],
     "gsv_canonicalize": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp],
-    "gsv_forward": [c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl, c_dbl, c_int,
+    "gsv_forward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl, c_dbl, c_int,
                     c_vp, c_vp, c_vp, c_vp, c_int, c_dbl, c_vp, c_vp, c_vp, c_int, c_vp],
     "gsv_backward_prep": [c_vp, c_vp, c_vp, GP, BP, c_dbl, c_int, c_vp, c_vp, c_vp],
-    "gsv_backward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl,
+    "gsv_backward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl,
                      c_int, c_vp, c_vp, c_vp, c_vp],
     "gsv_merge": [c_vp, c_vp, c_i64, c_int, c_vp, c_vp],
     "gsv_chain_rule": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp,
@@ -74,7 +74,7 @@ _SIGS = {
     "gsv_normalize_rotations": [c_vp, c_i64, c_vp],
     "gsv_fused_update": [c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                          ctypes.POINTER(c_vp), c_int, c_int, ctypes.POINTER(GsvAdamHparams),
-                         c_vp],
+                         c_vp, c_vp],
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
     # include/gsv_diag.h (measurement only)

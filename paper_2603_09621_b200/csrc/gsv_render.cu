@@ -107,13 +107,26 @@ __device__ __forceinline__ void sub_range_inv(double c, double h, double inv_s, 
 }
 
 // Exact f64 truncation decision of one (Gaussian, voxel) -- the rare
-// guard-band path -- from the f64 whitening factor written by preprocess.
-__device__ __noinline__ bool exact_live(int gid, int gx, int gy, int gz,
-                                        const double* __restrict__ pos,
-                                        const gsv_record64* __restrict__ rec64,
+// guard-band path -- with the f64 whitening factor from rec64 when the caller
+// built it (f64 engine), else recomputed from the field (f32 engine).
+struct ExactSrc {
+  const double* pos;
+  const double* ls;
+  const double* rot;
+  const gsv_record64* rec64;
+};
+
+__device__ __noinline__ bool exact_live(int gid, int gx, int gy, int gz, const ExactSrc& x,
                                         const gsv_grid& g, double cutoff2) {
-  const double* L = rec64[gid].l;
-  const double* m = pos + 3 * (int64_t)gid;
+  double Lw[9];
+  const double* L;
+  if (x.rec64 != nullptr) {
+    L = x.rec64[gid].l;
+  } else {
+    whitening_f64(x.ls + 3 * (int64_t)gid, x.rot + 4 * (int64_t)gid, Lw);
+    L = Lw;
+  }
+  const double* m = x.pos + 3 * (int64_t)gid;
   return ref_d2(L, m[0], m[1], m[2], gx, gy, gz, g) <= cutoff2;
 }
 
@@ -198,10 +211,11 @@ __device__ __forceinline__ void unit_voxel_v(int u, const gsv_bricks& k, int& x,
 
 template <int VPL, int THREADS>
 __global__ void __launch_bounds__(THREADS, 640 / THREADS)
-forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
-                 const gsv_record64* __restrict__ rec64,
+forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
+                 const gsv_record32* __restrict__ rec,
                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
-                 gsv_grid g, gsv_bricks k, float cut2, double cut2d, double eps_w,
+                 const __grid_constant__ gsv_grid g, gsv_bricks k, float cut2, double cut2d,
+                 double eps_w,
                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
                  const float* __restrict__ target, int loss_kind, double vox_count,
                  float2* __restrict__ ab, double* __restrict__ loss_part,
@@ -371,7 +385,7 @@ forward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict_
 #pragma unroll
           for (int h = 0; h < VPL; ++h)
             if (!live[h] && q[h] >= pd.x)
-              live[h] = exact_live(gidj, gx, gy, gz + h, pos, rec64, g, cut2d);
+              live[h] = exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d);
         }
 #pragma unroll
         for (int h = 0; h < VPL; ++h) {
@@ -640,11 +654,11 @@ size_t bwd_smem_bytes(int ab_voxels) {
 
 template <bool kSmem>
 __global__ void __launch_bounds__(kBwdThreads, 3)
-backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
-                  const gsv_record64* __restrict__ rec64,
+backward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
+                  const gsv_record32* __restrict__ rec,
                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                   const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
-                  gsv_grid g, gsv_bricks k, float cut2, double cut2d,
+                  const __grid_constant__ gsv_grid g, gsv_bricks k, float cut2, double cut2d,
                   const float2* __restrict__ ab, float4* __restrict__ partials, int dbg) {
   extern __shared__ __align__(16) unsigned char bwd_smem[];
   unsigned char* sspan = bwd_smem;                                       // kBwdSpanBytes
@@ -817,7 +831,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
           const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
           if (d2 > lim) continue;
           if (d2 >= lo_band &&
-              !exact_live(gid, bg.x0 + xi, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
+              !exact_live(gid, bg.x0 + xi, bg.y0 + y, bg.z0 + z, xsrc, g, cut2d))
             continue;
           bwd_accumulate(d2, C.r, C.A, v_ab, v0, v1, v2, fmaf(fx, fsx, C.c[0]), dy, dz, acc);
         }
@@ -843,7 +857,7 @@ backward32_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
               const float d2 = fmaf(v0, v0, fmaf(v1, v1, v2 * v2));
               if (d2 > lim) continue;
               if (d2 >= lo_band &&
-                  !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, pos, rec64, g, cut2d))
+                  !exact_live(gid, bg.x0 + x, bg.y0 + y, bg.z0 + z, xsrc, g, cut2d))
                 continue;
               bwd_accumulate(d2, C.r, C.A, v_ab, v0, v1, v2, fmaf(fx, fsx, C.c[0]), dy, dz, acc);
             }
@@ -1165,15 +1179,15 @@ using namespace gsv;
 
 extern "C" {
 
-int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_record64* rec64,
-                const int64_t* starts,
+int gsv_forward(const double* positions, const double* log_scales, const double* rotations,
+                const gsv_record32* rec32, const gsv_record64* rec64, const int64_t* starts,
                 const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
                 double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
                 double* loss_part, uint32_t* live_masks, int vpl_hint, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
-  GSV_REQUIRE(rec64 != nullptr, "forward needs rec64 (f64 whitening factors)");
+  GSV_REQUIRE(precision == 0 || rec64 != nullptr, "the f64 forward needs rec64");
   GSV_REQUIRE(target == nullptr || (ab != nullptr && loss_part != nullptr),
               "fused loss needs ab and loss_part");
   GSV_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (l1) or 1 (l2)");
@@ -1187,12 +1201,12 @@ int gsv_forward(const double* positions, const gsv_record32* rec32, const gsv_re
     // bricks (vpl_hint from the caller: pairs per Gaussian >= 8).
     if (live_masks == nullptr && vpl_hint >= 4)
       forward32_kernel<4, 64><<<(unsigned)nb, 64, 0, s>>>(
-          positions, rec32, rec64, starts, gids, *grid, *bricks, (float)cut2d,
+          positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, *grid, *bricks, (float)cut2d,
           cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
           (float2*)ab, loss_part, nullptr);
     else
       forward32_kernel<2, 128><<<(unsigned)nb, 128, 0, s>>>(
-          positions, rec32, rec64, starts, gids, *grid, *bricks, (float)cut2d,
+          positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, *grid, *bricks, (float)cut2d,
           cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
           (float2*)ab, loss_part, (uint2*)live_masks);
     GSV_CHECK_LAUNCH("forward32_kernel");
@@ -1232,15 +1246,15 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi, const gs
   return GSV_OK;
 }
 
-int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_record64* rec64,
-                 const int64_t* starts,
+int gsv_backward(const double* positions, const double* log_scales, const double* rotations,
+                 const gsv_record32* rec32, const gsv_record64* rec64, const int64_t* starts,
                  const int32_t* gids, const int64_t* gstart, const int32_t* box,
                  const gsv_grid* grid, const gsv_bricks* bricks, double cutoff_sigma,
                  int precision, const void* ab, const uint32_t* live_masks, void* partials,
                  void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
-  GSV_REQUIRE(rec64 != nullptr, "backward needs rec64 (f64 whitening factors)");
+  GSV_REQUIRE(precision == 0 || rec64 != nullptr, "the f64 backward needs rec64");
   const int64_t nb = slab_bricks(*bricks);
   if (nb == 0) return GSV_OK;
   const double cut2d = cutoff_sigma * cutoff_sigma;
@@ -1269,11 +1283,11 @@ int gsv_backward(const double* positions, const gsv_record32* rec32, const gsv_r
     }
     if (smem)
       backward32_kernel<true><<<(unsigned)nb, kBwdThreads, shm, s>>>(
-          positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
+          positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, gstart, box, *grid, *bricks,
           (float)cut2d, cut2d, (const float2*)ab, (float4*)partials, dbg);
     else
       backward32_kernel<false><<<(unsigned)nb, kBwdThreads, shm, s>>>(
-          positions, rec32, rec64, starts, gids, gstart, box, *grid, *bricks,
+          positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, gstart, box, *grid, *bricks,
           (float)cut2d, cut2d, (const float2*)ab, (float4*)partials, dbg);
     GSV_CHECK_LAUNCH("backward32_kernel");
   } else {

@@ -135,24 +135,17 @@ __device__ __forceinline__ double adam_one(double p, double& m, double& v, doubl
   return sub(p, __ddiv_rn(mul(lr, __ddiv_rn(m, bc1)), add(sqrt(__ddiv_rn(v, bc2)), eps)));
 }
 
-struct MomentPtrs {
-  double* p[10];
-  __device__ double* operator[](int k) const { return p[k]; }
-};
-
-// Fused optimizer tail of one fit() iteration, one thread per Gaussian:
-// merge of the pair partials in ascending brick order (raster.py:412-451)
-// [or the already all-reduced sums] -> chain rule -> Adam on every enabled
-// group (optimize.py:127-148) -> quaternion renormalisation (field.py:100).
-// Identical arithmetic to gsv_merge + gsv_chain_rule + gsv_adam x5 +
-// gsv_normalize_rotations, in one pass over the per-Gaussian state.
+// Optimizer tail, kernel 1 of 2: per Gaussian, merge its pair partials in
+// ascending brick order (raster.py:412-451) [or read the all-reduced sums],
+// then the chain rule (raster.py:524-549) -> packed f64 gradients (N,12) in
+// field order.  Kept apart from Adam so each kernel stays lean: this one is
+// latency/compute bound, the Adam pass is a pure HBM stream.
 template <typename T>
 __global__ void __launch_bounds__(128)
-fused_update_kernel(const T* __restrict__ partials, const int64_t* __restrict__ gstart,
-                    const double* __restrict__ gsum, int64_t n, double* __restrict__ pos,
-                    double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
-                    double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
-                    gsv_adam_hparams h) {
+merge_chain_kernel(const T* __restrict__ partials, const int64_t* __restrict__ gstart,
+                   const double* __restrict__ gsum, int64_t n, const double* __restrict__ ls,
+                   const double* __restrict__ rot, const double* __restrict__ ra,
+                   const double* __restrict__ rr, int relax_en, double* __restrict__ g12) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s[11];
@@ -162,20 +155,38 @@ fused_update_kernel(const T* __restrict__ partials, const int64_t* __restrict__ 
   } else {
 #pragma unroll
     for (int a = 0; a < 11; ++a) s[a] = 0.0;
-    for (int64_t e = gstart[i]; e < gstart[i + 1]; ++e) {
+    const int64_t e1 = gstart[i + 1];
+#pragma unroll 2
+    for (int64_t e = gstart[i]; e < e1; ++e) {
       const T* p = partials + 12 * e;
 #pragma unroll
       for (int a = 0; a < 11; ++a) s[a] += (double)p[a];
     }
   }
-  double q[4], l[3];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) q[a] = rot[4 * i + a];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) l[a] = ls[3 * i + a];
   double g[12];
-  chain_one(s, l, q, ra[i], rr[i], relax_en, g);
-  // mv: m_pos, m_ls, m_rot, m_amp, m_rel, v_pos, v_ls, v_rot, v_amp, v_rel
+  chain_one(s, ls + 3 * i, rot + 4 * i, ra[i], rr[i], relax_en, g);
+  double2* o = reinterpret_cast<double2*>(g12 + 12 * i);
+#pragma unroll
+  for (int a = 0; a < 6; ++a) o[a] = make_double2(g[2 * a], g[2 * a + 1]);
+}
+
+struct MomentPtrs {
+  double* p[10];
+  __device__ double* operator[](int k) const { return p[k]; }
+};
+
+// Optimizer tail, kernel 2 of 2: Adam on every enabled group from the packed
+// gradients (optimize.py:127-148, numpy operand order) + quaternion
+// renormalisation (field.py:100-102).  A streaming pass: coalesced f64
+// loads/stores, small live state, high occupancy.
+__global__ void __launch_bounds__(256)
+adam12_kernel(const double* __restrict__ g12, int64_t n, double* __restrict__ pos,
+              double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
+              double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
+              gsv_adam_hparams h) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* g = g12 + 12 * i;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double m = mv[0][3 * i + a], v = mv[5][3 * i + a];
@@ -185,15 +196,20 @@ fused_update_kernel(const T* __restrict__ partials, const int64_t* __restrict__ 
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double m = mv[1][3 * i + a], v = mv[6][3 * i + a];
-    ls[3 * i + a] = adam_one(l[a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    ls[3 * i + a] = adam_one(ls[3 * i + a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, h.bc1, h.bc2);
     mv[1][3 * i + a] = m; mv[6][3 * i + a] = v;
   }
+  double q[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     double m = mv[2][4 * i + a], v = mv[7][4 * i + a];
-    q[a] = adam_one(q[a], m, v, g[6 + a], h.lr[2], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    q[a] = adam_one(rot[4 * i + a], m, v, g[6 + a], h.lr[2], h.b1, h.b2, h.eps, h.bc1, h.bc2);
     mv[2][4 * i + a] = m; mv[7][4 * i + a] = v;
   }
+  const double nrm = sqrt(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
+                              mul(q[3], q[3])));
+#pragma unroll
+  for (int a = 0; a < 4; ++a) rot[4 * i + a] = __ddiv_rn(q[a], nrm);
   if (amp_en) {
     double m = mv[3][i], v = mv[8][i];
     ra[i] = adam_one(ra[i], m, v, g[10], h.lr[3], h.b1, h.b2, h.eps, h.bc1, h.bc2);
@@ -204,10 +220,6 @@ fused_update_kernel(const T* __restrict__ partials, const int64_t* __restrict__ 
     rr[i] = adam_one(rr[i], m, v, g[11], h.lr[4], h.b1, h.b2, h.eps, h.bc1, h.bc2);
     mv[4][i] = m; mv[9][i] = v;
   }
-  const double nrm = sqrt(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
-                              mul(q[3], q[3])));
-#pragma unroll
-  for (int a = 0; a < 4; ++a) rot[4 * i + a] = __ddiv_rn(q[a], nrm);
 }
 
 constexpr int kLossThreads = 256;
@@ -282,6 +294,92 @@ __global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ q, 
       sqrt(add(add(add(mul(qi[0], qi[0]), mul(qi[1], qi[1])), mul(qi[2], qi[2])), mul(qi[3], qi[3])));
 #pragma unroll
   for (int a = 0; a < 4; ++a) qi[a] = __ddiv_rn(qi[a], nrm);
+}
+
+// Optimizer tail in one pass (the default): a CTA owns 128 consecutive
+// Gaussians, whose pair partials are one contiguous range in gid-major
+// emission order.  The range is staged through shared memory with coalesced
+// float4 loads (in 512-pair sub-chunks); each thread sums its own segment in
+// ascending brick order (raster.py:412-451), then applies the chain rule
+// (raster.py:524-549), Adam on every enabled group (optimize.py:127-148) and
+// the quaternion renormalisation (field.py:100-102) in place.
+constexpr int kTailThreads = 128;
+constexpr int kTailSub = 512;   // pairs per smem sub-chunk (24 KB)
+
+__global__ void __launch_bounds__(kTailThreads)
+tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gstart,
+            const double* __restrict__ gsum, int64_t n, double* __restrict__ pos,
+            double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
+            double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
+            gsv_adam_hparams h) {
+  __shared__ float4 sp[kTailSub * 3];
+  const int64_t i0 = blockIdx.x * (int64_t)kTailThreads;
+  const int64_t i = i0 + threadIdx.x;
+  const bool valid = i < n;
+  double s[11];
+#pragma unroll
+  for (int a = 0; a < 11; ++a) s[a] = 0.0;
+  if (gsum != nullptr) {
+    if (valid) {
+#pragma unroll
+      for (int a = 0; a < 11; ++a) s[a] = gsum[12 * i + a];
+    }
+  } else {
+    const int64_t iend = min(n, i0 + kTailThreads);
+    const int64_t e_lo = gstart[i0], e_hi = gstart[iend];
+    const int64_t my0 = valid ? gstart[i] : 0, my1 = valid ? gstart[i + 1] : 0;
+    const float4* src = reinterpret_cast<const float4*>(partials);
+    for (int64_t c0 = e_lo; c0 < e_hi; c0 += kTailSub) {
+      const int cnt = (int)min((int64_t)kTailSub, e_hi - c0);
+      __syncthreads();
+      for (int q = threadIdx.x; q < 3 * cnt; q += kTailThreads) sp[q] = __ldg(src + 3 * c0 + q);
+      __syncthreads();
+      const int64_t a0 = max(my0, c0), a1 = min(my1, c0 + cnt);
+      for (int64_t e = a0; e < a1; ++e) {
+        const float4* pp = sp + 3 * (e - c0);
+        const float4 x = pp[0], y = pp[1], z = pp[2];
+        s[0] += (double)x.x; s[1] += (double)x.y; s[2] += (double)x.z; s[3] += (double)x.w;
+        s[4] += (double)y.x; s[5] += (double)y.y; s[6] += (double)y.z; s[7] += (double)y.w;
+        s[8] += (double)z.x; s[9] += (double)z.y; s[10] += (double)z.z;
+      }
+    }
+  }
+  if (!valid) return;
+  double g[12];
+  chain_one(s, ls + 3 * i, rot + 4 * i, ra[i], rr[i], relax_en, g);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double m = mv[0][3 * i + a], v = mv[5][3 * i + a];
+    pos[3 * i + a] = adam_one(pos[3 * i + a], m, v, g[a], h.lr[0], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[0][3 * i + a] = m; mv[5][3 * i + a] = v;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double m = mv[1][3 * i + a], v = mv[6][3 * i + a];
+    ls[3 * i + a] = adam_one(ls[3 * i + a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[1][3 * i + a] = m; mv[6][3 * i + a] = v;
+  }
+  double q[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double m = mv[2][4 * i + a], v = mv[7][4 * i + a];
+    q[a] = adam_one(rot[4 * i + a], m, v, g[6 + a], h.lr[2], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[2][4 * i + a] = m; mv[7][4 * i + a] = v;
+  }
+  const double nrm = sqrt(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
+                              mul(q[3], q[3])));
+#pragma unroll
+  for (int a = 0; a < 4; ++a) rot[4 * i + a] = __ddiv_rn(q[a], nrm);
+  if (amp_en) {
+    double m = mv[3][i], v = mv[8][i];
+    ra[i] = adam_one(ra[i], m, v, g[10], h.lr[3], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[3][i] = m; mv[8][i] = v;
+  }
+  if (relax_en) {
+    double m = mv[4][i], v = mv[9][i];
+    rr[i] = adam_one(rr[i], m, v, g[11], h.lr[4], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    mv[4][i] = m; mv[9][i] = v;
+  }
 }
 
 }  // namespace
@@ -367,24 +465,37 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
                      int64_t n, int precision, double* positions, double* log_scales,
                      double* rotations, double* raw_amplitude, double* raw_relax,
                      double* const* moments, int amplitude_enabled, int relax_enabled,
-                     const gsv_adam_hparams* hp, void* stream) {
+                     const gsv_adam_hparams* hp, double* grad_scratch, void* stream) {
   GSV_REQUIRE(hp != nullptr && moments != nullptr, "null hparams/moments");
   GSV_REQUIRE(gsum != nullptr || (partials != nullptr && gstart != nullptr),
               "need gsum or partials+gstart");
   if (n <= 0) return GSV_OK;
-  const unsigned blocks = (unsigned)((n + 127) / 128);
   cudaStream_t s = as_stream(stream);
   MomentPtrs mv;
   for (int k = 0; k < 10; ++k) mv.p[k] = moments[k];
-  if (precision == 0)
-    fused_update_kernel<float><<<blocks, 128, 0, s>>>(
-        (const float*)partials, gstart, gsum, n, positions, log_scales, rotations, raw_amplitude,
-        raw_relax, mv, amplitude_enabled, relax_enabled, *hp);
-  else
-    fused_update_kernel<double><<<blocks, 128, 0, s>>>(
-        (const double*)partials, gstart, gsum, n, positions, log_scales, rotations,
+  if (precision == 0 && grad_scratch == nullptr) {
+    // one pass: staged merge + chain rule + Adam + renorm
+    tail_kernel<<<(unsigned)((n + kTailThreads - 1) / kTailThreads), kTailThreads, 0, s>>>(
+        (const float*)partials, gstart, gsum, n, positions, log_scales, rotations,
         raw_amplitude, raw_relax, mv, amplitude_enabled, relax_enabled, *hp);
-  GSV_CHECK_LAUNCH("fused_update_kernel");
+    GSV_CHECK_LAUNCH("tail_kernel");
+    return GSV_OK;
+  }
+  GSV_REQUIRE(grad_scratch != nullptr, "the f64 tail needs grad_scratch (N,12) double");
+  const unsigned b128 = (unsigned)((n + 127) / 128), b256 = (unsigned)((n + 255) / 256);
+  if (precision == 0)
+    merge_chain_kernel<float><<<b128, 128, 0, s>>>((const float*)partials, gstart, gsum, n,
+                                                   log_scales, rotations, raw_amplitude,
+                                                   raw_relax, relax_enabled, grad_scratch);
+  else
+    merge_chain_kernel<double><<<b128, 128, 0, s>>>((const double*)partials, gstart, gsum, n,
+                                                    log_scales, rotations, raw_amplitude,
+                                                    raw_relax, relax_enabled, grad_scratch);
+  GSV_CHECK_LAUNCH("merge_chain_kernel");
+  adam12_kernel<<<b256, 256, 0, s>>>(grad_scratch, n, positions, log_scales, rotations,
+                                     raw_amplitude, raw_relax, mv, amplitude_enabled,
+                                     relax_enabled, *hp);
+  GSV_CHECK_LAUNCH("adam12_kernel");
   return GSV_OK;
 }
 

@@ -198,16 +198,17 @@ def _preprocess(f: GaussianField, grid: GridSpec, cutoff_sigma: float, brick_dim
     lib = _lib.lib()
     n, dev = f.count, f.device
     rec32 = _alloc(pool, "rec32", (n, 16), torch.float32, dev)
-    # rec64 is always built: the f64 engine uses it, and the f32 engine's
-    # guard-band re-decisions read the f64 whitening factor from it.
-    rec64 = _alloc(pool, "rec64", (n, 12), torch.float64, dev)
+    # rec64 only for the f64 engine; the f32 engine recomputes the f64 factor
+    # in its rare guard-band path
+    want64 = want64 or bool(os.environ.get("GSV_FORCE_REC64"))
+    rec64 = _alloc(pool, "rec64", (n, 12), torch.float64, dev) if want64 else None
     counts = _alloc(pool, "counts", (n,), torch.int32, dev)
     box = _alloc(pool, "box", (n, 4), torch.int32, dev)
     _lib.check(lib.gsv_preprocess(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), n, int(f.relax_enabled),
         float(cutoff_sigma), _lib.make_grid(grid), _lib.make_bricks(grid, brick_dims, slab),
-        rec32.data_ptr(), rec64.data_ptr(), counts.data_ptr(), box.data_ptr(),
+        rec32.data_ptr(), _lib.ptr(rec64), counts.data_ptr(), box.data_ptr(),
         _lib.stream_ptr()), "preprocess")
     return rec32, rec64, counts, box
 
@@ -264,7 +265,7 @@ def build_brick_index(f: GaussianField, grid: GridSpec, opts: RenderOptions = Re
     bricks = _lib.make_bricks(grid, brick_dims, slab)
     nbricks = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
     rec32, rec64, counts, box = _preprocess(f, grid, opts.cutoff_sigma, brick_dims, slab,
-                                            True, pool)
+                                            opts.precision == "f64", pool)
     gstart = _scan(counts, nbricks, pool)
     pairs = int(gstart[-1].item())  # the one host read binning needs (buffer sizing)
     starts, gids = _fill(counts, box, gstart, pairs, bricks, nbricks, pool)
@@ -288,9 +289,10 @@ def _check_index(f: GaussianField, grid: GridSpec, idx: BrickIndex, opts: Render
 def _records(f, grid, idx: BrickIndex, opts: RenderOptions):
     """rec32 (and rec64 for f64) for the current field state."""
     aux = idx._aux
-    if aux is not None and aux.field_version == f.version:
+    want64 = opts.precision == "f64"
+    if aux is not None and aux.field_version == f.version and (aux.rec64 is not None or not want64):
         return aux.rec32, aux.rec64
-    rec32, rec64, _, _ = _preprocess(f, grid, opts.cutoff_sigma, idx.brick_dims, idx.slab, True)
+    rec32, rec64, _, _ = _preprocess(f, grid, opts.cutoff_sigma, idx.brick_dims, idx.slab, want64)
     return rec32, rec64
 
 
@@ -308,8 +310,9 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
                   ab=None, loss_part=None, live_masks=None):
     lib = _lib.lib()
     _lib.check(lib.gsv_forward(
-        f.positions.data_ptr(), rec32.data_ptr(), rec64.data_ptr(), idx.starts.data_ptr(),
-        idx.gids.data_ptr(), _lib.make_grid(grid),
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        rec32.data_ptr(), _lib.ptr(rec64), idx.starts.data_ptr(), idx.gids.data_ptr(),
+        _lib.make_grid(grid),
         _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
@@ -360,8 +363,9 @@ def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: b
     if timer is not None:
         timer("backward")
     _lib.check(lib.gsv_backward(
-        f.positions.data_ptr(), rec32.data_ptr(), rec64.data_ptr(), idx.starts.data_ptr(),
-        idx.gids.data_ptr(), gstart.data_ptr(),
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        rec32.data_ptr(), _lib.ptr(rec64), idx.starts.data_ptr(), idx.gids.data_ptr(),
+        gstart.data_ptr(),
         box.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), _lib.ptr(live_masks),
         partials.data_ptr(), _lib.stream_ptr()), "backward")

@@ -178,7 +178,7 @@ class TrainStep:
 
 
 def _adam_launch(f: GaussianField, state, lrs: dict, beta1: float, beta2: float, eps: float,
-                 partials, gstart, gsum, precision_code: int) -> None:
+                 partials, gstart, gsum, precision_code: int, pool=None) -> None:
     """gsv_fused_update: merge (or pre-reduced sums) -> chain rule -> Adam ->
     renorm.  Bumps the field version twice, like step_optimizer +
     normalize_rotations (optimize.py:148, field.py:102)."""
@@ -195,11 +195,16 @@ def _adam_launch(f: GaussianField, state, lrs: dict, beta1: float, beta2: float,
     groups = ("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax")
     mv = (ctypes.c_void_p * 10)(*([state.m[g].data_ptr() for g in groups] +
                                   [state.v[g].data_ptr() for g in groups]))
+    scratch = None
+    if precision_code != 0 or os.environ.get("GSV_TAIL_SPLIT"):
+        scratch = (pool.get("grad12", (f.count, 12), torch.float64) if pool is not None
+                   else torch.empty((f.count, 12), dtype=torch.float64, device=f.device))
     _lib.check(lib.gsv_fused_update(
         _lib.ptr(partials), _lib.ptr(gstart), _lib.ptr(gsum), f.count, precision_code,
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), mv, int(f.amplitude_enabled),
-        int(f.relax_enabled), ctypes.byref(hp), _lib.stream_ptr()), "fused_update")
+        int(f.relax_enabled), ctypes.byref(hp), _lib.ptr(scratch), _lib.stream_ptr()),
+        "fused_update")
     f.bump_version()
     f.bump_version()
 
@@ -227,20 +232,22 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
         gsum[0, 11] = 0.0
         out.reduced = True
         self._mark("update")
-        _adam_launch(f, state, lrs, beta1, beta2, eps, None, None, gsum, opts.precision_code)
+        _adam_launch(f, state, lrs, beta1, beta2, eps, None, None, gsum, opts.precision_code,
+                     self.pool)
     else:
         pdt = opts.torch_dtype
         partials = _alloc(self.pool, "partials", (max(idx.pair_count, 1), 12), pdt, f.device)
         self._mark("backward")
         _lib.check(lib.gsv_backward(
-            f.positions.data_ptr(), aux.rec32.data_ptr(), aux.rec64.data_ptr(),
+            f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+            aux.rec32.data_ptr(), _lib.ptr(aux.rec64),
             idx.starts.data_ptr(), idx.gids.data_ptr(), aux.gstart.data_ptr(), aux.box.data_ptr(),
             _lib.make_grid(self.grid), _lib.make_bricks(self.grid, idx.brick_dims, idx.slab),
             float(opts.cutoff_sigma), opts.precision_code, out.ab.data_ptr(),
             _lib.ptr(self._masks), partials.data_ptr(), _lib.stream_ptr()), "backward")
         self._mark("update")
         _adam_launch(f, state, lrs, beta1, beta2, eps, partials, aux.gstart, None,
-                     opts.precision_code)
+                     opts.precision_code, self.pool)
     self._mark(None)
 
 

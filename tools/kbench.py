@@ -37,11 +37,13 @@ def main():
     if not args.no_train:
         t = PhaseTimer()
         step = gs.TrainStep(gs.Volume(p["lr_grid"], p["lr"]), opts, (8, 8, 4), "l1", timer=t)
+        state = gs.AdamState.create(f)
+        lrs = gs.FitConfig().resolved_lrs(p["lr_grid"].spacing)
         for i in range(args.iters + 1):
             if i == 1:
                 t.reset()
             out = step.forward(f)
-            step.backward(f, out)
+            step.update(f, out, state, lrs)
         print("LR train phases (ms):", {k: round(v[1], 4) for k, v in t.summary().items()})
     if args.hr:
         grid = p["render_grid"]
