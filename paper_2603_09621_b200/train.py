@@ -119,6 +119,22 @@ class TrainStep:
         if self.timer is not None:
             self.timer(name)
 
+    def _reduce_buffer(self, gsum: torch.Tensor, out: "StepOutput") -> torch.Tensor:
+        """The single collective's buffer: the merged per-Gaussian partials
+        (f32 for the f32 engine -- they are sums of f32 pair partials -- halving
+        the NVLink bytes), with this rank's loss partial in column 11."""
+        gsum[0, 11] = out.loss_sum[0]
+        if self.opts.precision == "f32":
+            return gsum.to(torch.float32)
+        return gsum
+
+    def _unpack_reduced(self, red: torch.Tensor, gsum: torch.Tensor, out: "StepOutput") -> None:
+        if red.data_ptr() != gsum.data_ptr():
+            gsum.copy_(red)
+        out.loss_sum.copy_(gsum[0, 11:12])
+        gsum[0, 11] = 0.0
+        out.reduced = True
+
     def forward(self, f: GaussianField) -> StepOutput:
         lib = _lib.lib()
         grid, opts = self.grid, self.opts
@@ -166,11 +182,9 @@ class TrainStep:
             # this rank's loss partial riding in the spare 12th column.
             import torch.distributed as dist
             self._mark("allreduce")
-            gsum[0, 11] = out.loss_sum[0]
-            dist.all_reduce(gsum, group=self.group)
-            out.loss_sum.copy_(gsum[0, 11:12])
-            gsum[0, 11] = 0.0
-            out.reduced = True
+            red = self._reduce_buffer(gsum, out)
+            dist.all_reduce(red, group=self.group)
+            self._unpack_reduced(red, gsum, out)
         self._mark("chain")
         g = _chain_rule(f, gsum, pool=self.pool)
         self._mark(None)
@@ -226,11 +240,9 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
                               live_masks=self._masks)
         import torch.distributed as dist
         self._mark("allreduce")
-        gsum[0, 11] = out.loss_sum[0]
-        dist.all_reduce(gsum, group=self.group)
-        out.loss_sum.copy_(gsum[0, 11:12])
-        gsum[0, 11] = 0.0
-        out.reduced = True
+        red = self._reduce_buffer(gsum, out)
+        dist.all_reduce(red, group=self.group)
+        self._unpack_reduced(red, gsum, out)
         self._mark("update")
         _adam_launch(f, state, lrs, beta1, beta2, eps, None, None, gsum, opts.precision_code,
                      self.pool)
