@@ -70,7 +70,8 @@ typedef struct {
   float amp;       /* A = sigmoid(raw_amplitude)                            */
   float relax;     /* r = sigmoid(raw_relax), or 1 when relax is disabled    */
   float half[3];   /* cutoff*sqrt(Sigma_kk): world-axis half extents        */
-  float _pad[2];
+  float inv_smax2; /* 1/sigma_max^2 = smallest eigenvalue of L^T L          */
+  float _pad;
 } gsv_record32;
 
 /* Per-Gaussian fp64 record for the f64 engine (precision="f64"). */

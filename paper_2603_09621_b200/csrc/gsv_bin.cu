@@ -84,8 +84,10 @@ preprocess_kernel(const double* __restrict__ pos, const double* __restrict__ ls,
   o.relax = (float)r;
 #pragma unroll
   for (int a = 0; a < 3; ++a) o.half[a] = (float)half[a];
-  o._pad[0] = 0.f;
-  o._pad[1] = 0.f;
+  // 1/sigma_max^2 = lambda_min(L^T L): d2 >= |p - mu|^2 / sigma_max^2, the
+  // forward's sphere-vs-tile culling bound.
+  o.inv_smax2 = (float)exp(-2.0 * fmax(l[0], fmax(l[1], l[2])));
+  o._pad = 0.f;
   {
     float4* dst = reinterpret_cast<float4*>(rec32 + i);
     const float4* src = reinterpret_cast<const float4*>(&o);

@@ -295,6 +295,16 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
                     hzv = fmaf(q3.y, isz, 1e-3f);
         hit = cxv + hxv >= ftxl && cxv - hxv <= ftxh && cyv + hyv >= ftyl &&
               cyv - hyv <= ftyh && czv + hzv >= ftzl && czv - hzv <= ftzh;
+        if (hit && !isinf(cut2)) {
+          // Sphere-vs-tile: d2 >= |p - mu|^2 / sigma_max^2 over the tile's
+          // voxel-centre box (world units); reject when even that bound
+          // exceeds cutoff^2 (with a 1e-4 relative margin for rounding).
+          const float ddx = fmaxf(fmaxf(ftxl - cxv, cxv - ftxh), 0.f) * fsx;
+          const float ddy = fmaxf(fmaxf(ftyl - cyv, cyv - ftyh), 0.f) * fsy;
+          const float ddz = fmaxf(fmaxf(ftzl - czv, czv - ftzh), 0.f) * fsz;
+          const float dist2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
+          hit = dist2 * q3.z <= cut2 * 1.0001f + 1e-6f;
+        }
         if (hit) {
           const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
           float u3[3], e[3][3], umax = 0.f;
