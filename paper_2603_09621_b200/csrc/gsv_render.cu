@@ -171,6 +171,20 @@ __device__ __forceinline__ float ex2_approx(float q) {
   return r;
 }
 
+// Asynchronous global->shared copies (LDGSTS): the next round's pair records
+// land in shared memory while this round is evaluated.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // exp(-d2/2) as one FMUL + MUFU.EX2 (rel. error ~2e-7, well inside the 1e-5
 // parity bar).
 __device__ __forceinline__ float exp_neg_half(float d2) {
@@ -209,8 +223,11 @@ __device__ __forceinline__ void unit_voxel_v(int u, const gsv_bricks& k, int& x,
   }
 }
 
+#ifndef GSV_FWD_OCC
+#define GSV_FWD_OCC 640
+#endif
 template <int VPL, int THREADS>
-__global__ void __launch_bounds__(THREADS, 640 / THREADS)
+__global__ void __launch_bounds__(THREADS, GSV_FWD_OCC / THREADS)
 forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
                  const gsv_record32* __restrict__ rec,
                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
@@ -221,7 +238,6 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
                  float2* __restrict__ ab, double* __restrict__ loss_part,
                  uint2* __restrict__ live_masks) {
   __shared__ Pair32 sp[THREADS];       // 32 slots per warp
-  __shared__ uint2 smask[THREADS];     // live bits of this round's pairs, per warp
   __shared__ double red[THREADS / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
@@ -355,25 +371,29 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
       // Compact this round's hits into consecutive slots (ballot rank), so the
       // evaluation loop below is a plain counter over broadcast smem records.
       const unsigned ball = __ballot_sync(kFull, hit);
-      if (hit) wsp[__popc(ball & ((1u << lane) - 1u))] = p;
-      if (want_masks) smask[(warp << 5) + lane] = make_uint2(0u, 0u);
+      const int rank = __popc(ball & ((1u << lane) - 1u));
+      if (hit) wsp[rank] = p;
       __syncwarp();
       const int nh = __popc(ball);
+      // live bits of hit jj are parked in lane jj's registers, then shuffled
+      // back to the lane that staged the pair (its ballot rank).
+      unsigned hma = 0u, hmb = 0u;
       for (int jj = 0; jj < nh; ++jj) {
         const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c;
         const float4 pd = wsp[jj].d;
         // q(X,Y,Z) for the column's first voxel, then second differences
         float q[VPL];
+        // two independent FMA chains (latency, not throughput, bounds this)
         float qa = fmaf(pa.y, mX, pa.x);
+        float qb = pb.x * mXX;
         qa = fmaf(pa.z, mY, qa);
+        qb = fmaf(pb.y, mYY, qb);
         qa = fmaf(pa.w, mZ, qa);
-        qa = fmaf(pb.x, mXX, qa);
-        qa = fmaf(pb.y, mYY, qa);
-        qa = fmaf(pb.z, mZZ, qa);
+        qb = fmaf(pb.z, mZZ, qb);
         qa = fmaf(pb.w, mXY, qa);
-        qa = fmaf(pc.x, mXZ, qa);
+        qb = fmaf(pc.x, mXZ, qb);
         qa = fmaf(pc.y, mYZ, qa);
-        q[0] = qa;
+        q[0] = qa + qb;
         float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, m2Z1, pa.w)));
         const float d2q = 2.f * pb.z;
 #pragma unroll
@@ -406,14 +426,18 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
         if (want_masks) {
           const unsigned ma = __ballot_sync(kFull, live[0] && own[0]);
           const unsigned mb = __ballot_sync(kFull, live[VPL - 1] && own[VPL - 1]);
-          if (lane == 0) smask[(warp << 5) + __float_as_int(pd.z)] = make_uint2(ma, mb);
+          if (lane == jj) {
+            hma = ma;
+            hmb = mb;
+          }
         }
       }
-      __syncwarp();
       // live-voxel masks for the backward, plane [warp][pair]: one coalesced
       // 256-byte store per warp and round (pairs missing the tile get zeros)
-      if (want_masks && gid >= 0)
-        live_masks[warp * mstride + base + lane] = smask[(warp << 5) + lane];
+      if (want_masks) {
+        const unsigned ma = __shfl_sync(kFull, hma, rank), mb = __shfl_sync(kFull, hmb, rank);
+        if (gid >= 0) live_masks[warp * mstride + base + lane] = hit ? make_uint2(ma, mb) : make_uint2(0u, 0u);
+      }
       __syncwarp();
     }
     // Epilogue: normalise, store, fused loss (optimize.py:91-103).
