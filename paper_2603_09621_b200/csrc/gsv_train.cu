@@ -74,20 +74,25 @@ __device__ __forceinline__ void chain_one(const double* s, const double* ls, con
       for (int b = 0; b < 3; ++b) t += R[3 * a + kk] * G[3 * a + b] * R[3 * b + kk];
     out[3 + kk] = -2.0 * iv[kk] * t;
   }
+  // d q_j = 2 sum_{a,c,m} G[a][c] dR_j[c][m] e^{-2 ls_m} R[a][m] = 2 <dR_j, K>
+  // with K = G P, P[a][m] = e^{-2 ls_m} R[a][m] (G symmetric).
+  double K[9];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      double t = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) t += G[3 * a + c] * (iv[m] * R[3 * a + m]);
+      K[3 * c + m] = t;
+    }
   double J[4][9];
   rotation_jacobians(q, J);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     double t = 0.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double pm = 0.0;  // pmat[c][a]
-#pragma unroll
-        for (int m = 0; m < 3; ++m) pm += J[j][3 * c + m] * iv[m] * R[3 * a + m];
-        t += G[3 * a + c] * pm;
-      }
+    for (int a = 0; a < 9; ++a) t += J[j][a] * K[a];
     out[6 + j] = 2.0 * t;
   }
   out[0] = s[2];
