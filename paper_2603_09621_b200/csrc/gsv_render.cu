@@ -932,9 +932,10 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
                    gsv_grid g, gsv_bricks k, float cut2, const uint2* __restrict__ masks,
                    const float2* __restrict__ ab, float4* __restrict__ partials) {
   __shared__ float2 sab[256];                 // brick voxels (units <= 128)
-  __shared__ unsigned sunit[128];             // unit -> lx | ly<<8 | lz0<<16
+  __shared__ float4 slut[256];                // (word << 5) | bit -> (x, y, z, sab index)
+  __shared__ unsigned swords[kBwdThreads / 32][8][32];   // per lane: its pair's 8 mask words
   __shared__ unsigned short sorder[kBwdMChunk];
-  __shared__ unsigned char scost[kBwdMChunk];
+  __shared__ unsigned short scost[kBwdMChunk];
   __shared__ int shist[kBwdBuckets];
   __shared__ int snext;
   const int lb = blockIdx.x;
@@ -948,10 +949,19 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
   const bool tiled = ((k.bdx | k.bdy | k.bdz) & 3) == 0;
   const int units = k.bdx * k.bdy * ((k.bdz + 1) >> 1);
   const int64_t mstride = starts[gridDim.x];   // mask plane stride = slab pairs
-  for (int u = tid; u < units; u += kBwdThreads) {
-    int x, y, z0;
-    unit_voxel(u, k, tiled, x, y, z0);
-    sunit[u] = (unsigned)x | ((unsigned)y << 8) | ((unsigned)z0 << 16);
+  // mask word wi = 2 * tile + half, bit = lane of the tile: voxel of unit
+  // tile * 32 + bit, z0 + half
+  for (int e = tid; e < 256; e += kBwdThreads) {
+    const int wi = e >> 5, u = ((wi >> 1) << 5) + (e & 31);
+    float4 v = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
+    if (u < units) {
+      int x, y, z0;
+      unit_voxel(u, k, tiled, x, y, z0);
+      const int z = z0 + (wi & 1);
+      if (z < k.bdz)
+        v = make_float4((float)x, (float)y, (float)z, __int_as_float(x + k.bdx * (y + k.bdy * z)));
+    }
+    slut[e] = v;
   }
   {
     const int nv = bg.ex * bg.ey * bg.ez;
@@ -974,7 +984,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
                   a2 = __ldg(masks + 2 * mstride + jt), a3 = __ldg(masks + 3 * mstride + jt);
       const int c = __popc(a0.x) + __popc(a0.y) + __popc(a1.x) + __popc(a1.y) + __popc(a2.x) +
                     __popc(a2.y) + __popc(a3.x) + __popc(a3.y);
-      scost[t] = (unsigned char)min(c, 255);
+      scost[t] = (unsigned short)c;
       atomicAdd(&shist[kBwdBuckets - 1 - min(c, kBwdBuckets - 1)], 1);
     }
     __syncthreads();
@@ -1028,27 +1038,27 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       }
       const uint2 a0 = __ldg(masks + j), a1 = __ldg(masks + mstride + j),
                   a2 = __ldg(masks + 2 * mstride + j), a3 = __ldg(masks + 3 * mstride + j);
-      const unsigned words[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+      // this lane's column of the warp's word table (conflict-free, no sync:
+      // only the lane itself reads it)
+      unsigned* myw = &swords[tid >> 5][0][lane];
+      myw[0] = a0.x; myw[32] = a0.y; myw[64] = a1.x; myw[96] = a1.y;
+      myw[128] = a2.x; myw[160] = a2.y; myw[192] = a3.x; myw[224] = a3.y;
       float acc[11];
 #pragma unroll
       for (int a = 0; a < 11; ++a) acc[a] = 0.f;
       const int cost = scost[t];
       int wi = 0;
-      unsigned cur = words[0];
+      unsigned cur = a0.x;
       for (int it = 0; it < cost; ++it) {
-        while (cur == 0u) {      // next non-empty word (static indexing)
+        while (cur == 0u) {      // next non-empty word
           ++wi;
-          cur = wi == 1 ? words[1] : wi == 2 ? words[2] : wi == 3 ? words[3] : wi == 4 ? words[4]
-              : wi == 5 ? words[5] : wi == 6 ? words[6] : words[7];
+          cur = myw[wi << 5];
         }
         const int bit = __ffs(cur) - 1;
         cur &= cur - 1u;
-        // word wi = 2*warp + half; lane bit -> unit warp*32 + bit; half -> z0 / z0+1
-        const unsigned uv = sunit[((wi >> 1) << 5) + bit];
-        const int x = uv & 255, y = (uv >> 8) & 255, z = ((uv >> 16) & 255) + (wi & 1);
-        const float2 v_ab = sab[x + k.bdx * (y + k.bdy * z)];
-        if (v_ab.x == 0.f) continue;
-        const float fx = (float)x, fy = (float)y, fz = (float)z;
+        const float4 vx = slut[(wi << 5) | bit];
+        const float2 v_ab = sab[__float_as_int(vx.w)];
+        const float fx = vx.x, fy = vx.y, fz = vx.z;
         const float v0 = fmaf(fz, ez[0], fmaf(fy, ey[0], fmaf(fx, ex[0], u[0])));
         const float v1 = fmaf(fz, ez[1], fmaf(fy, ey[1], fmaf(fx, ex[1], u[1])));
         const float v2 = fmaf(fz, ez[2], fmaf(fy, ey[2], fmaf(fx, ex[2], u[2])));
