@@ -933,7 +933,9 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
                    const float2* __restrict__ ab, float4* __restrict__ partials) {
   __shared__ float2 sab[256];                 // brick voxels (units <= 128)
   __shared__ float4 slut[256];                // (word << 5) | bit -> (x, y, z, sab index)
-  __shared__ unsigned swords[kBwdThreads / 32][8][32];   // per lane: its pair's 8 mask words
+  __shared__ unsigned swords[kBwdThreads / 32][9][32];   // per lane: its pair's non-empty
+  __shared__ unsigned short swbase[kBwdThreads / 32][9][32];  // mask words, LUT bases
+  __shared__ int sgid[kBwdMChunk];
   __shared__ unsigned short sorder[kBwdMChunk];
   __shared__ unsigned short scost[kBwdMChunk];
   __shared__ int shist[kBwdBuckets];
@@ -985,6 +987,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       const int c = __popc(a0.x) + __popc(a0.y) + __popc(a1.x) + __popc(a1.y) + __popc(a2.x) +
                     __popc(a2.y) + __popc(a3.x) + __popc(a3.y);
       scost[t] = (unsigned short)c;
+      sgid[t] = __ldg(gids + jt);
       atomicAdd(&shist[kBwdBuckets - 1 - min(c, kBwdBuckets - 1)], 1);
     }
     __syncthreads();
@@ -1020,7 +1023,10 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       if (s >= cnt) continue;
       const int t = sorder[s];
       const int64_t j = cbase + t;
-      const int gid = gids[j];
+      const int gid = sgid[t];
+      // every global load of the pair up front: one latency, hidden by the loop
+      const GBox gb = unpack_box(box, gid);
+      const int64_t gst = __ldg(gstart + gid);
       const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
       const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2);
       const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
@@ -1039,24 +1045,43 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       const uint2 a0 = __ldg(masks + j), a1 = __ldg(masks + mstride + j),
                   a2 = __ldg(masks + 2 * mstride + j), a3 = __ldg(masks + 3 * mstride + j);
       // this lane's column of the warp's word table (conflict-free, no sync:
-      // only the lane itself reads it)
+      // only the lane itself reads it): its non-empty words and their LUT
+      // bases, compacted, plus a zero sentinel
       unsigned* myw = &swords[tid >> 5][0][lane];
-      myw[0] = a0.x; myw[32] = a0.y; myw[64] = a1.x; myw[96] = a1.y;
-      myw[128] = a2.x; myw[160] = a2.y; myw[192] = a3.x; myw[224] = a3.y;
+      unsigned short* myb = &swbase[tid >> 5][0][lane];
+      {
+        const unsigned words[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+        int nw = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          if (words[w] != 0u) {
+            myw[nw << 5] = words[w];
+            myb[nw << 5] = (unsigned short)(w << 5);
+            ++nw;
+          }
+        myw[nw << 5] = 0u;
+        myb[nw << 5] = 0;
+      }
       float acc[11];
 #pragma unroll
       for (int a = 0; a < 11; ++a) acc[a] = 0.f;
       const int cost = scost[t];
-      int wi = 0;
-      unsigned cur = a0.x;
+      unsigned cur = myw[0];
+      int wb = myb[0];
+      unsigned nxt = myw[32];                   // next word, prefetched
+      int nxb = myb[32];
+      int slot = 1;
       for (int it = 0; it < cost; ++it) {
-        while (cur == 0u) {      // next non-empty word
-          ++wi;
-          cur = myw[wi << 5];
+        if (cur == 0u) {
+          cur = nxt;
+          wb = nxb;
+          ++slot;
+          nxt = myw[min(slot, 8) << 5];
+          nxb = myb[min(slot, 8) << 5];
         }
         const int bit = __ffs(cur) - 1;
         cur &= cur - 1u;
-        const float4 vx = slut[(wi << 5) | bit];
+        const float4 vx = slut[wb | bit];
         const float2 v_ab = sab[__float_as_int(vx.w)];
         const float fx = vx.x, fy = vx.y, fz = vx.z;
         const float v0 = fmaf(fz, ez[0], fmaf(fy, ey[0], fmaf(fx, ex[0], u[0])));
@@ -1069,10 +1094,9 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       const float mu0 = fmaf(q0.x, acc[2], fmaf(q0.w, acc[3], q1.z * acc[4]));
       const float mu1 = fmaf(q0.y, acc[2], fmaf(q1.x, acc[3], q1.w * acc[4]));
       const float mu2 = fmaf(q0.z, acc[2], fmaf(q1.y, acc[3], q2.x * acc[4]));
-      const GBox gb = unpack_box(box, gid);
       const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
       if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
-      const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+      const int64_t e = gst + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
       float4* dst = partials + 3 * e;
       dst[0] = make_float4(acc[0], acc[1], mu0, mu1);
       dst[1] = make_float4(mu2, acc[5], acc[6], acc[7]);
