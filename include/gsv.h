@@ -132,6 +132,22 @@ int gsv_bin_fill(const int32_t* counts, const int32_t* box,
                  int64_t* starts_out, void* workspace, size_t workspace_bytes,
                  void* stream);
 
+/* Capacity mode of gsv_bin_fill for host-sync-free (CUDA-graph) steps: the
+ * pair count P = gstart[N] is never read by the host.  Pairs fill slots
+ * [0, P) as in gsv_bin_fill, slots [P, capacity) get the sentinel brick
+ * nbricks_slab (sorted behind every list), and the sort always covers
+ * `capacity` slots.  *overflow (device int32) = P > capacity, or *dry != 0
+ * (dry may be NULL); on overflow every list is emptied (starts = 0) so the
+ * downstream kernels do no work and the caller re-bins with more capacity.
+ * Buffers as gsv_bin_fill, sized by capacity; workspace from
+ * gsv_bin_workspace(n, capacity, nbricks). */
+int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box,
+                          const int64_t* gstart, int64_t n, int64_t capacity,
+                          const gsv_bricks* bricks, int32_t* keys_tmp,
+                          int32_t* vals_tmp, int32_t* keys_out, int32_t* gids_out,
+                          int64_t* starts_out, const int32_t* dry, int32_t* overflow,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Canonical-order check and repair for caller-supplied lists
  * (BrickIndex.lists_sorted / canonicalized, raster.py:91-112).
  * gsv_lists_unsorted writes 1 to *flag (device int32) if any brick list is
@@ -258,6 +274,26 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
                      double* rotations, double* raw_amplitude, double* raw_relax,
                      double* const* moments, int amplitude_enabled, int relax_enabled,
                      const gsv_adam_hparams* hp, double* grad_scratch, void* stream);
+
+/* Device-side control of a graph-replayed fit() iteration (optimize.py:177-197
+ * with loss read before the update, as the reference: a non-finite loss
+ * raises before step_optimizer).
+ * gsv_step_gate: gate = overflow | !isfinite(*loss_sum); result[0] = loss
+ * sum, result[1] = overflow | nonfinite << 1 (the step's 16-byte D2H).
+ * gsv_fused_update_device: the one-pass f32 tail of gsv_fused_update, but a
+ * no-op when *gate != 0, with bc1 = bias_corrections[2 t], bc2 =
+ * bias_corrections[2 t + 1] for t = *step (the number of completed steps;
+ * the table holds 1 - beta^(t+1) computed on the host like the reference).
+ * gsv_step_advance: *step += 1 unless *gate. */
+int gsv_step_gate(const double* loss_sum, const int32_t* overflow, int32_t* gate,
+                  double* result, void* stream);
+int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_t n,
+                            double* positions, double* log_scales, double* rotations,
+                            double* raw_amplitude, double* raw_relax, double* const* moments,
+                            int amplitude_enabled, int relax_enabled,
+                            const gsv_adam_hparams* hp, const double* bias_corrections,
+                            const int64_t* step, const int32_t* gate, void* stream);
+int gsv_step_advance(int64_t* step, const int32_t* gate, void* stream);
 
 /* q /= |q| per Gaussian (GaussianField.normalize_rotations, field.py:100). */
 int gsv_normalize_rotations(double* rotations, int64_t n, void* stream);

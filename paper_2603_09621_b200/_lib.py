@@ -55,6 +55,8 @@ _SIGS = {
     "gsv_bin_scan": [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp],
     "gsv_bin_fill": [c_vp, c_vp, c_vp, c_i64, c_i64, BP, c_vp, c_vp, c_vp, c_vp, c_vp,
                      c_vp, ctypes.c_size_t, c_vp],
+    "gsv_bin_fill_capacity": [c_vp, c_vp, c_vp, c_i64, c_i64, BP, c_vp, c_vp, c_vp, c_vp,
+                              c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp],
     "gsv_lists_unsorted": [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp],
     "gsv_canonicalize_workspace": [c_i64, c_i32, c_szp],
     "gsv_canonicalize": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp],
@@ -75,6 +77,11 @@ _SIGS = {
     "gsv_fused_update": [c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                          ctypes.POINTER(c_vp), c_int, c_int, ctypes.POINTER(GsvAdamHparams),
                          c_vp, c_vp],
+    "gsv_step_gate": [c_vp, c_vp, c_vp, c_vp, c_vp],
+    "gsv_fused_update_device": [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                ctypes.POINTER(c_vp), c_int, c_int,
+                                ctypes.POINTER(GsvAdamHparams), c_vp, c_vp, c_vp, c_vp],
+    "gsv_step_advance": [c_vp, c_vp, c_vp],
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
     # include/gsv_diag.h (measurement only)

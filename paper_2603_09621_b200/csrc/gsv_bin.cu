@@ -165,11 +165,12 @@ __global__ void scan_tail_kernel(const int32_t* counts, int64_t n, int64_t* gsta
 __global__ void __launch_bounds__(256)
 emit_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
             const int64_t* __restrict__ gstart, int64_t n, gsv_bricks k,
-            int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+            int32_t* __restrict__ keys, int32_t* __restrict__ vals, int64_t cap) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n || counts[i] == 0) return;
   const GBox b = unpack_box(box, i);
   int64_t off = gstart[i];
+  if (off + counts[i] > cap) return;   // capacity mode: overflow is flagged by pad_kernel
   const int64_t first = (int64_t)k.bgx * k.bgy * k.bz0;
   for (int z = 0; z < b.nb_z; ++z)
     for (int y = 0; y < b.nb_y; ++y) {
@@ -183,10 +184,32 @@ emit_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
     }
 }
 
+// Capacity mode: the pair count P = gstart[n] stays on the device.  Slots
+// [P, cap) get the sentinel brick nb (sorted behind every real pair);
+// overflow = P > cap (or the caller's dry-run flag) empties every list.
+__global__ void pad_kernel(const int64_t* __restrict__ gstart, int64_t n, int64_t cap,
+                           int32_t nb, const int32_t* __restrict__ dry,
+                           int32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                           int32_t* __restrict__ overflow) {
+  const int64_t p = gstart[n];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = p + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cap; j += stride) {
+    keys[j] = nb;
+    vals[j] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    *overflow = (p > cap || (dry != nullptr && *dry != 0)) ? 1 : 0;
+}
+
 // starts[b] = first sorted position with key >= b, for b in [0, B].
 __global__ void starts_kernel(const int32_t* __restrict__ keys, int64_t p, int32_t nb,
-                              int64_t* __restrict__ starts) {
+                              int64_t* __restrict__ starts,
+                              const int32_t* __restrict__ overflow) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (overflow != nullptr && *overflow != 0) {   // capacity overflow / dry run: empty lists
+    if (j <= nb) starts[j] = 0;
+    return;
+  }
   if (j > p) return;
   const int32_t cur = j < p ? keys[j] : nb;
   const int32_t prev = j > 0 ? keys[j - 1] : -1;
@@ -290,7 +313,7 @@ int gsv_bin_fill(const int32_t* counts, const int32_t* box, const int64_t* gstar
   const int64_t nb = slab_bricks(*bricks);
   if (pairs > 0) {
     emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(counts, box, gstart, n, *bricks,
-                                                           keys_tmp, vals_tmp);
+                                                           keys_tmp, vals_tmp, INT64_MAX);
     GSV_CHECK_LAUNCH("emit_kernel");
     size_t bytes = workspace_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, bytes, keys_tmp, keys_out,
@@ -300,7 +323,38 @@ int gsv_bin_fill(const int32_t* counts, const int32_t* box, const int64_t* gstar
   }
   const int64_t threads = 256, items = pairs + 1;
   starts_kernel<<<(unsigned)((items + threads - 1) / threads), (unsigned)threads, 0, s>>>(
-      keys_out, pairs, (int32_t)nb, starts_out);
+      keys_out, pairs, (int32_t)nb, starts_out, nullptr);
+  GSV_CHECK_LAUNCH("starts_kernel");
+  return GSV_OK;
+}
+
+int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box, const int64_t* gstart,
+                          int64_t n, int64_t capacity, const gsv_bricks* bricks,
+                          int32_t* keys_tmp, int32_t* vals_tmp, int32_t* keys_out,
+                          int32_t* gids_out, int64_t* starts_out, const int32_t* dry,
+                          int32_t* overflow, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  GSV_REQUIRE(bricks != nullptr && overflow != nullptr, "null bricks/overflow");
+  GSV_REQUIRE(capacity >= 1 && capacity < (int64_t)INT32_MAX, "capacity %lld out of range",
+              (long long)capacity);
+  cudaStream_t s = as_stream(stream);
+  const int64_t nb = slab_bricks(*bricks);
+  if (n > 0) {
+    emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(counts, box, gstart, n, *bricks,
+                                                           keys_tmp, vals_tmp, capacity);
+    GSV_CHECK_LAUNCH("emit_kernel");
+  }
+  pad_kernel<<<592, 256, 0, s>>>(gstart, n, capacity, (int32_t)nb, dry, keys_tmp, vals_tmp,
+                                 overflow);
+  GSV_CHECK_LAUNCH("pad_kernel");
+  size_t bytes = workspace_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, bytes, keys_tmp, keys_out,
+                                                  vals_tmp, gids_out, (int)capacity, 0,
+                                                  key_bits(nb), s);
+  if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort::SortPairs");
+  const int64_t threads = 256, items = (capacity > nb ? capacity : nb) + 1;
+  starts_kernel<<<(unsigned)((items + threads - 1) / threads), (unsigned)threads, 0, s>>>(
+      keys_out, capacity, (int32_t)nb, starts_out, overflow);
   GSV_CHECK_LAUNCH("starts_kernel");
   return GSV_OK;
 }

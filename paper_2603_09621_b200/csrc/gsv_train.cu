@@ -308,6 +308,30 @@ __global__ void __launch_bounds__(256) normalize_kernel(double* __restrict__ q, 
 // ascending brick order (raster.py:412-451), then applies the chain rule
 // (raster.py:524-549), Adam on every enabled group (optimize.py:127-148) and
 // the quaternion renormalisation (field.py:100-102) in place.
+// Graph-replayed steps: the gate (overflow | non-finite loss) and the step
+// counter live on the device; bc holds 1 - beta^t for t = 1, 2, ... computed
+// on the host exactly as the reference does (Python float pow).
+struct StepDev {
+  const int32_t* gate;
+  const double* bc;
+  const int64_t* t;
+};
+
+__global__ void gate_kernel(const double* __restrict__ loss_sum,
+                            const int32_t* __restrict__ overflow, int32_t* __restrict__ gate,
+                            double* __restrict__ result) {
+  const double l = *loss_sum;
+  const int ovf = *overflow != 0;
+  const int bad = !isfinite(l);
+  *gate = ovf | bad;
+  result[0] = l;
+  result[1] = (double)(ovf | (bad << 1));
+}
+
+__global__ void advance_kernel(int64_t* __restrict__ t, const int32_t* __restrict__ gate) {
+  if (*gate == 0) *t += 1;
+}
+
 constexpr int kTailThreads = 128;
 constexpr int kTailSub = 512;   // pairs per smem sub-chunk (24 KB)
 
@@ -316,8 +340,14 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
             const double* __restrict__ gsum, int64_t n, double* __restrict__ pos,
             double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
             double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
-            gsv_adam_hparams h) {
+            gsv_adam_hparams h, StepDev sd) {
   __shared__ float4 sp[kTailSub * 3];
+  if (sd.gate != nullptr && *sd.gate != 0) return;   // overflow / non-finite loss: no update
+  if (sd.bc != nullptr) {                            // step number from the device
+    const int64_t t = *sd.t;
+    h.bc1 = sd.bc[2 * t];
+    h.bc2 = sd.bc[2 * t + 1];
+  }
   const int64_t i0 = blockIdx.x * (int64_t)kTailThreads;
   const int64_t i = i0 + threadIdx.x;
   const bool valid = i < n;
@@ -482,7 +512,8 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
     // one pass: staged merge + chain rule + Adam + renorm
     tail_kernel<<<(unsigned)((n + kTailThreads - 1) / kTailThreads), kTailThreads, 0, s>>>(
         (const float*)partials, gstart, gsum, n, positions, log_scales, rotations,
-        raw_amplitude, raw_relax, mv, amplitude_enabled, relax_enabled, *hp);
+        raw_amplitude, raw_relax, mv, amplitude_enabled, relax_enabled, *hp,
+        StepDev{nullptr, nullptr, nullptr});
     GSV_CHECK_LAUNCH("tail_kernel");
     return GSV_OK;
   }
@@ -501,6 +532,40 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
                                      raw_amplitude, raw_relax, mv, amplitude_enabled,
                                      relax_enabled, *hp);
   GSV_CHECK_LAUNCH("adam12_kernel");
+  return GSV_OK;
+}
+
+int gsv_step_gate(const double* loss_sum, const int32_t* overflow, int32_t* gate,
+                  double* result, void* stream) {
+  GSV_REQUIRE(loss_sum && overflow && gate && result, "null pointer argument");
+  gate_kernel<<<1, 1, 0, as_stream(stream)>>>(loss_sum, overflow, gate, result);
+  GSV_CHECK_LAUNCH("gate_kernel");
+  return GSV_OK;
+}
+
+int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_t n,
+                            double* positions, double* log_scales, double* rotations,
+                            double* raw_amplitude, double* raw_relax, double* const* moments,
+                            int amplitude_enabled, int relax_enabled,
+                            const gsv_adam_hparams* hp, const double* bias_corrections,
+                            const int64_t* step, const int32_t* gate, void* stream) {
+  GSV_REQUIRE(hp && moments && partials && gstart && bias_corrections && step && gate,
+              "null pointer argument");
+  if (n <= 0) return GSV_OK;
+  cudaStream_t s = as_stream(stream);
+  MomentPtrs mv;
+  for (int k = 0; k < 10; ++k) mv.p[k] = moments[k];
+  tail_kernel<<<(unsigned)((n + kTailThreads - 1) / kTailThreads), kTailThreads, 0, s>>>(
+      partials, gstart, nullptr, n, positions, log_scales, rotations, raw_amplitude, raw_relax,
+      mv, amplitude_enabled, relax_enabled, *hp, StepDev{gate, bias_corrections, step});
+  GSV_CHECK_LAUNCH("tail_kernel");
+  return GSV_OK;
+}
+
+int gsv_step_advance(int64_t* step, const int32_t* gate, void* stream) {
+  GSV_REQUIRE(step && gate, "null pointer argument");
+  advance_kernel<<<1, 1, 0, as_stream(stream)>>>(step, gate);
+  GSV_CHECK_LAUNCH("advance_kernel");
   return GSV_OK;
 }
 

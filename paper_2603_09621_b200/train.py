@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from .field import GaussianField
-from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule,
+from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule, _preprocess, _scan,
                      _forward_into, _pair_partials, build_brick_index)
 from .render import RenderOptions
 from .volume import Volume
@@ -264,6 +264,229 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
 
 
 TrainStep.update = _update_method
+
+
+# ------------------------------------------------------------ graph-replayed step
+_GRAPH_HEADROOM = 1.15       # pair capacity over the pair count seen at capture
+_BC_CHUNK = 16384            # bias-correction table length per capture
+
+
+def _bias_corrections(beta1: float, beta2: float, t0: int, count: int) -> torch.Tensor:
+    """[1 - beta1^t, 1 - beta2^t] for t = 1 .. t0 + count, Python float pow like
+    the reference's step_optimizer (optimize.py:141-142) -- bit-identical."""
+    vals = []
+    for t in range(1, t0 + count + 1):
+        vals.append(1.0 - beta1 ** t)
+        vals.append(1.0 - beta2 ** t)
+    return torch.tensor(vals, dtype=torch.float64)
+
+
+class _StepGraph:
+    """Buffers and the captured CUDA graph of one fused fit() iteration.
+
+    The graph holds the whole iteration -- preprocess, scan, capacity-mode
+    binning (pair count never read by the host), forward with the fused loss
+    and live masks, loss sum, gate, masked backward, the one-pass tail with
+    the step counter and bias corrections read on the device, step advance,
+    and one 16-byte D2H of {loss sum, flags} -- so a replay costs one launch
+    and one stream sync, with no per-kernel host work.
+    """
+
+    def __init__(self, key, cap: int, t_max: int):
+        self.key = key
+        self.cap = cap
+        self.t_max = t_max           # largest state.t the bias table covers
+        self.t_synced = -1
+        self.graph = None
+        self.bufs: dict = {}
+
+
+def _graph_key(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps):
+    groups = ("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax")
+    return (f.count, f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+            f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), int(f.amplitude_enabled),
+            int(f.relax_enabled), tuple(state.m[g].data_ptr() for g in groups),
+            tuple(state.v[g].data_ptr() for g in groups), self.target.data_ptr(),
+            tuple(float(lrs[g]) for g in groups), float(beta1), float(beta2), float(eps))
+
+
+def _graph_supported(self) -> bool:
+    bd = self.brick_dims
+    return (not self.sharded and self.opts.precision == "f32"
+            and bd[0] * bd[1] * ((bd[2] + 1) // 2) <= 128
+            and not os.environ.get("GSV_NO_GRAPH") and not os.environ.get("GSV_NO_LIVE_MASKS")
+            and not os.environ.get("GSV_TAIL_SPLIT"))
+
+
+def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
+    """The launch sequence captured into the graph (also run once, dry, to
+    warm every kernel up before capture)."""
+    import ctypes
+    lib = _lib.lib()
+    b = g.bufs
+    s = _lib.stream_ptr()
+    grid, opts, n = self.grid, self.opts, f.count
+    gr, br = _lib.make_grid(grid), b["bricks"]
+    cap = g.cap
+    _lib.check(lib.gsv_preprocess(
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), n, int(f.relax_enabled),
+        float(opts.cutoff_sigma), gr, br, b["rec32"].data_ptr(), None, b["counts"].data_ptr(),
+        b["box"].data_ptr(), s), "preprocess")
+    ws = b["ws"]
+    _lib.check(lib.gsv_bin_scan(b["counts"].data_ptr(), n, b["gstart"].data_ptr(),
+                                ws.data_ptr(), ws.numel(), s), "bin_scan")
+    k = b["keys"]
+    _lib.check(lib.gsv_bin_fill_capacity(
+        b["counts"].data_ptr(), b["box"].data_ptr(), b["gstart"].data_ptr(), n, cap, br,
+        k[0].data_ptr(), k[1].data_ptr(), k[2].data_ptr(), b["gids"].data_ptr(),
+        b["starts"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(), ws.data_ptr(),
+        ws.numel(), s), "bin_fill_capacity")
+    nvox = grid.num_voxels
+    _lib.check(lib.gsv_forward(
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
+        float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
+        b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(), self.loss_kind,
+        float(nvox), b["ab"].data_ptr(), b["loss_part"].data_ptr(), b["masks"].data_ptr(),
+        b["vpl"], s), "forward")
+    _lib.check(lib.gsv_sum(b["loss_part"].data_ptr(), b["nb"], b["loss_sum"].data_ptr(), s),
+               "sum")
+    _lib.check(lib.gsv_step_gate(b["loss_sum"].data_ptr(), b["overflow"].data_ptr(),
+                                 b["gate"].data_ptr(), b["result"].data_ptr(), s), "step_gate")
+    _lib.check(lib.gsv_backward(
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(),
+        b["gstart"].data_ptr(), b["box"].data_ptr(), gr, br, float(opts.cutoff_sigma), 0,
+        b["ab"].data_ptr(), b["masks"].data_ptr(), b["partials"].data_ptr(), s), "backward")
+    _lib.check(lib.gsv_fused_update_device(
+        b["partials"].data_ptr(), b["gstart"].data_ptr(), n, f.positions.data_ptr(),
+        f.log_scales.data_ptr(), f.rotations.data_ptr(), f.raw_amplitude.data_ptr(),
+        f.raw_relax.data_ptr(), b["mv"], int(f.amplitude_enabled), int(f.relax_enabled),
+        ctypes.byref(b["hp"]), b["bc"].data_ptr(), b["t"].data_ptr(), b["gate"].data_ptr(), s),
+        "fused_update_device")
+    _lib.check(lib.gsv_step_advance(b["t"].data_ptr(), b["gate"].data_ptr(), s), "step_advance")
+    b["result_host"].copy_(b["result"], non_blocking=True)
+
+
+def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, key,
+                   min_cap: int = 0) -> _StepGraph:
+    import ctypes
+    lib = _lib.lib()
+    dev = f.device
+    grid, opts, n = self.grid, self.opts, f.count
+    bricks = _lib.make_bricks(grid, self.brick_dims, self.slab)
+    nb = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
+    # the exact pair count, read once per capture (never per step)
+    rec32, _, counts, box = _preprocess(f, grid, opts.cutoff_sigma, self.brick_dims, self.slab,
+                                        False, self.pool)
+    pairs = int(_scan(counts, nb, self.pool)[-1].item())
+    cap = max(int(pairs * _GRAPH_HEADROOM) + 4096, min_cap, 1)
+    g = _StepGraph(key, cap, state.t + _BC_CHUNK - 1)
+    b = g.bufs
+    gp = _lib.BufferPool(dev)        # private: replays need fixed addresses
+    b["bricks"] = bricks
+    b["nb"] = max(nb, 1)
+    b["rec32"] = gp.get("rec32", (n, 16), torch.float32)
+    b["counts"] = gp.get("counts", (n,), torch.int32)
+    b["box"] = gp.get("box", (n, 4), torch.int32)
+    b["gstart"] = gp.get("gstart", (n + 1,), torch.int64)
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
+    b["ws"] = gp.get("ws", (nbytes.value,), torch.uint8)
+    b["keys"] = gp.get("keys", (3, cap), torch.int32)
+    b["gids"] = gp.get("gids", (cap,), torch.int32)
+    b["starts"] = gp.get("starts", (nb + 1,), torch.int64)
+    nvox = grid.num_voxels
+    for name in ("S", "W", "I"):
+        b[name] = gp.get(name, (nvox,), torch.float32)
+    b["ab"] = gp.get("ab", (nvox, 2), torch.float32)
+    b["loss_part"] = gp.get("loss_part", (max(nb, 1),), torch.float64)
+    b["loss_sum"] = gp.get("loss_sum", (1,), torch.float64)
+    b["masks"] = gp.get("masks", (4, cap, 2), torch.int32)
+    b["partials"] = gp.get("partials", (cap, 12), torch.float32)
+    b["dry"] = gp.get("dry", (1,), torch.int32)
+    b["overflow"] = gp.get("overflow", (1,), torch.int32)
+    b["gate"] = gp.get("gate", (1,), torch.int32)
+    b["result"] = gp.get("result", (2,), torch.float64)
+    b["result_host"] = torch.zeros(2, dtype=torch.float64).pin_memory()
+    b["t"] = gp.get("t", (1,), torch.int64)
+    b["bc"] = _bias_corrections(beta1, beta2, state.t, _BC_CHUNK).to(dev)
+    b["vpl"] = 4 if pairs >= 8 * max(n, 1) and not os.environ.get("GSV_VPL") else \
+        int(os.environ.get("GSV_VPL", "2"))
+    hp = _lib.GsvAdamHparams()
+    for i, name in enumerate(("positions", "log_scales", "rotations", "raw_amplitude",
+                              "raw_relax")):
+        hp.lr[i] = float(lrs[name])
+    hp.b1, hp.b2, hp.eps, hp.bc1, hp.bc2 = beta1, beta2, eps, 0.0, 0.0
+    b["hp"] = hp
+    groups = ("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax")
+    b["mv"] = (ctypes.c_void_p * 10)(*([state.m[x].data_ptr() for x in groups] +
+                                       [state.v[x].data_ptr() for x in groups]))
+    # dry run (every kernel once, empty lists, no update), then capture
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        b["dry"].fill_(1)
+        _graph_body(self, f, g)
+        b["dry"].zero_()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize(dev)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
+        _graph_body(self, f, g)
+    g.graph = graph
+    return g
+
+
+def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
+                 beta2: float = 0.999, eps: float = 1e-8) -> float:
+    """One whole fit() iteration (optimize.py:177-197): render + loss, then --
+    only if the loss is finite, as the reference raises before updating --
+    backward, chain rule, Adam and renormalisation.  Returns the mean loss
+    (a Python float: the iteration's one device->host read).
+
+    Replays a captured CUDA graph (single GPU, f32): no host work per kernel,
+    no pair-count read.  The graph is (re)captured when the field / optimizer
+    buffers, target, hyper-parameters or pair capacity change.  Elsewhere
+    (sharded, f64) it runs forward() + update() eagerly.
+    """
+    import math
+    if not _graph_supported(self):
+        out = self.forward(f)
+        loss = out.loss()
+        if math.isfinite(loss):
+            self.update(f, out, state, lrs, beta1, beta2, eps)
+        return loss
+    key = _graph_key(self, f, state, lrs, beta1, beta2, eps)
+    g = getattr(self, "_graph", None)
+    if g is None or g.key != key or state.t > g.t_max:
+        self._graph = None
+        g = self._graph = _graph_capture(self, f, state, lrs, beta1, beta2, eps, key)
+    b = g.bufs
+    if g.t_synced != state.t:
+        b["t"].fill_(int(state.t))
+        g.t_synced = state.t
+    g.graph.replay()
+    torch.cuda.current_stream(f.device).synchronize()
+    loss_sum, flags = float(b["result_host"][0]), int(b["result_host"][1])
+    if flags & 1:
+        # pair capacity overflow: nothing was updated; re-bin with more room
+        self._graph = None
+        self._graph = _graph_capture(self, f, state, lrs, beta1, beta2, eps, key,
+                                     min_cap=int(g.cap * 1.5))
+        return _step_method(self, f, state, lrs, beta1, beta2, eps)
+    loss = loss_sum / self.grid.num_voxels
+    if flags & 2:
+        return loss                      # non-finite: no update, like the reference
+    state.t += 1
+    g.t_synced = state.t
+    f.bump_version()
+    f.bump_version()
+    return loss
+
+
+TrainStep.step = _step_method
 
 
 class Renderer:

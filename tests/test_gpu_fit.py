@@ -146,3 +146,91 @@ def test_fit_quality_matches_reference_psnr_ssim():
     assert abs(got_psnr - ref["psnr"]) <= 0.05, (got_psnr, ref["psnr"])
     assert abs(got_ssim - ref["ssim"]) <= 0.001, (got_ssim, ref["ssim"])
     assert got_psnr >= ref["trilinear_psnr"] + 2.0   # criterion 5: beats trilinear by 2 dB
+
+
+# --------------------------------------------------------- graph-replayed step
+def _eager_and_graph(cfg_id=1, steps=4, loss="l1"):
+    p = make_problem(CONFIGS[cfg_id])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    ea = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), loss)
+    eb = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), loss)
+    la, lb = [], []
+    for _ in range(steps):
+        out = ea.forward(fa)
+        la.append(out.loss())
+        ea.update(fa, out, sa, lrs)
+        lb.append(eb.step(fb, sb, lrs))
+    return (fa, sa, la), (fb, sb, lb), eb
+
+
+@pytest.mark.parametrize("loss", ["l1", "l2"])
+def test_graph_step_bit_identical_to_eager(loss):
+    """Capacity-mode binning + the captured step give exactly the eager
+    forward()+update() parameters, moments, losses and step count."""
+    (fa, sa, la), (fb, sb, lb), eb = _eager_and_graph(loss=loss)
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    for k in sa.m:
+        assert torch.equal(sa.m[k], sb.m[k]) and torch.equal(sa.v[k], sb.v[k])
+    assert la == lb
+    assert sa.t == sb.t == 4 and fa.version == fb.version
+    assert eb._graph is not None and eb._graph.cap >= 1
+
+
+def test_graph_step_recovers_from_capacity_overflow(monkeypatch):
+    """A capacity below the pair count flags overflow on the device: the step
+    is not applied, the graph is re-captured with more room, and the result
+    equals the eager step."""
+    import paper_2603_09621_b200.train as train_mod
+    real = train_mod._graph_capture
+    calls = []
+
+    def tiny(self, f, state, lrs, b1, b2, eps, key, min_cap=0):
+        calls.append(min_cap)
+        if len(calls) == 1:
+            monkeypatch.setattr(train_mod, "_GRAPH_HEADROOM", 0.25)
+            g = real(self, f, state, lrs, b1, b2, eps, key, min_cap)
+            g_cap = g.cap
+            monkeypatch.setattr(train_mod, "_GRAPH_HEADROOM", 1.15)
+            assert g_cap >= 1
+            return g
+        return real(self, f, state, lrs, b1, b2, eps, key, min_cap)
+
+    monkeypatch.setattr(train_mod, "_graph_capture", tiny)
+    (fa, sa, la), (fb, sb, lb), _ = _eager_and_graph(cfg_id=2, steps=2)
+    assert len(calls) >= 2                      # overflow -> re-capture
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    assert la == lb and sa.t == sb.t == 2
+
+
+def test_graph_step_nonfinite_loss_skips_update():
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    st = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    assert math.isfinite(step.step(f, st, lrs))
+    before, t0, v0 = _pack(f), st.t, f.version
+    bad = step.target.clone()
+    bad[7] = float("nan")
+    step.set_target(bad)
+    assert math.isnan(step.step(f, st, lrs))
+    np.testing.assert_array_equal(_pack(f), before)
+    assert st.t == t0 and f.version == v0
+
+
+def test_graph_step_recaptures_on_new_hyperparameters():
+    (fa, sa, _), (fb, sb, _), eb = _eager_and_graph(steps=1)
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    lrs2 = {k: v * 0.5 for k, v in gs.FitConfig().resolved_lrs(lr.grid.spacing).items()}
+    ea = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    key0 = eb._graph.key
+    out = ea.forward(fa)
+    ea.update(fa, out, sa, lrs2)
+    eb.step(fb, sb, lrs2)
+    assert eb._graph.key != key0
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
