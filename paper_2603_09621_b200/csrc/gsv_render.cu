@@ -238,6 +238,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
                  float2* __restrict__ ab, double* __restrict__ loss_part,
                  uint2* __restrict__ live_masks) {
   __shared__ Pair32 sp[THREADS];       // 32 slots per warp
+  __shared__ uint2 smask[THREADS];     // live bits of this round's hits, per warp
   __shared__ double red[THREADS / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
@@ -283,9 +284,12 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
     const float ctx = 0.5f * (ftxl + ftxh), cty = 0.5f * (ftyl + ftyh), ctz = 0.5f * (ftzl + ftzh);
     const float ext_x = fmaxf(0.5f * (ftxh - ftxl), 0.f), ext_y = fmaxf(0.5f * (ftyh - ftyl), 0.f),
                 ext_z = fmaxf(0.5f * (ftzh - ftzl), 0.f);
-    const float mX = (float)lx - ctx, mY = (float)ly - cty, mZ = (float)lz - ctz;
+    // A voxel the lane does not own gets NaN offsets: every q is NaN, so it is
+    // never live and never enters a mask (no per-hit ownership predicates).
+    const float qnan = __int_as_float(0x7fc00000);
+    const float mX = own[0] ? (float)lx - ctx : qnan, mY = (float)ly - cty, mZ = (float)lz - ctz;
     const float mXX = mX * mX, mYY = mY * mY, mZZ = mZ * mZ, mXY = mX * mY, mXZ = mX * mZ,
-                mYZ = mY * mZ, m2Z1 = fmaf(2.f, mZ, 1.f);
+                mYZ = mY * mZ, m2Z1 = (VPL == 2 && !own[1]) ? qnan : fmaf(2.f, mZ, 1.f);
     const int gx = bg.x0 + lx, gy = bg.y0 + ly, gz = bg.z0 + lz;
     float accS[VPL], accW[VPL];
 #pragma unroll
@@ -375,12 +379,9 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
       if (hit) wsp[rank] = p;
       __syncwarp();
       const int nh = __popc(ball);
-      // live bits of hit jj are parked in lane jj's registers, then shuffled
-      // back to the lane that staged the pair (its ballot rank).
-      unsigned hma = 0u, hmb = 0u;
       for (int jj = 0; jj < nh; ++jj) {
         const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c;
-        const float4 pd = wsp[jj].d;
+        const float2 pd = *reinterpret_cast<const float2*>(&wsp[jj].d);   // qlo, gid
         // q(X,Y,Z) for the column's first voxel, then second differences
         float q[VPL];
         // two independent FMA chains (latency, not throughput, bounds this)
@@ -401,42 +402,43 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
           q[h] = q[h - 1] + dq;
           dq += d2q;
         }
-        // Branch-free accumulation; the guard band re-decides in f64 (rare,
-        // warp-voted), exactly like the reference's truncation test.
-        bool live[VPL];
+        // live: q >= thr, thr = the certain-live bound; in the guard band
+        // [qlo, qhi) the exact f64 decision (the reference's truncation test,
+        // rare and warp-voted) sets thr to -inf (live) or +inf (dead).
+        float thr[VPL];
         bool band = false;
 #pragma unroll
         for (int h = 0; h < VPL; ++h) {
-          live[h] = q[h] >= pc.w;
-          band |= !live[h] && q[h] >= pd.x;
+          thr[h] = pc.w;
+          band |= q[h] >= pd.x && q[h] < pc.w;
         }
         if (__any_sync(kFull, band)) {
           const int gidj = __float_as_int(pd.y);
 #pragma unroll
           for (int h = 0; h < VPL; ++h)
-            if (!live[h] && q[h] >= pd.x)
-              live[h] = exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d);
+            if (q[h] >= pd.x && q[h] < pc.w)
+              thr[h] = exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d) ? -INFINITY : INFINITY;
         }
+        bool live[VPL];
 #pragma unroll
         for (int h = 0; h < VPL; ++h) {
+          live[h] = q[h] >= thr[h];
           const float w = live[h] ? ex2_approx(q[h]) : 0.f;
           accS[h] = fmaf(pc.z, w, accS[h]);
           accW[h] += w;
         }
         if (want_masks) {
-          const unsigned ma = __ballot_sync(kFull, live[0] && own[0]);
-          const unsigned mb = __ballot_sync(kFull, live[VPL - 1] && own[VPL - 1]);
-          if (lane == jj) {
-            hma = ma;
-            hmb = mb;
-          }
+          const unsigned ma = __ballot_sync(kFull, live[0]);
+          const unsigned mb = __ballot_sync(kFull, live[VPL - 1]);
+          smask[(warp << 5) + jj] = make_uint2(ma, mb);   // warp-uniform: same-address store
         }
       }
       // live-voxel masks for the backward, plane [warp][pair]: one coalesced
       // 256-byte store per warp and round (pairs missing the tile get zeros)
       if (want_masks) {
-        const unsigned ma = __shfl_sync(kFull, hma, rank), mb = __shfl_sync(kFull, hmb, rank);
-        if (gid >= 0) live_masks[warp * mstride + base + lane] = hit ? make_uint2(ma, mb) : make_uint2(0u, 0u);
+        __syncwarp();
+        const uint2 mm = hit ? smask[(warp << 5) + rank] : make_uint2(0u, 0u);
+        if (gid >= 0) live_masks[warp * mstride + base + lane] = mm;
       }
       __syncwarp();
     }
