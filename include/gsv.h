@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GSV_ABI_VERSION 1
+#define GSV_ABI_VERSION 2
 
 typedef enum {
   GSV_OK = 0,
@@ -171,13 +171,16 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  *   loss_part (nbricks_slab) double : per-brick sum |I-T| (l1) or (I-T)^2.
  * loss_kind: 0 = l1, 1 = l2.  vox_count = global voxel count V, so
  * dL/dI = sign(I-T)/V (l1) or 2(I-T)/V (l2) exactly as optimize.py:99-102.
- * live_masks (optional, f32, bricks of <= 256 voxels): 4 planes of P uint2,
- * plane w = warp tile w, entry j = list entry j: {live bits of the tile's
- * voxel z0, voxel z0+1} -- the forward's exact truncation decisions, consumed
- * by gsv_backward so the backward walks only live voxels.
- * vpl_hint: voxels per lane of the f32 kernel's warp tiles; 4 (8x4x4 tiles)
- * pays off when Gaussians span several bricks (e.g. pairs/Gaussian >= 8),
- * else 2 (4x4x4 tiles).  Ignored (2) when live_masks != NULL.
+ * vpl: voxels per lane of the f32 kernel's 32-lane warp tiles: 2 (4x4x4
+ * tiles when the brick dims are multiples of 4, 4 warps per 8x8x4 brick),
+ * 4 (columns of 4 in z: 8x4x4 tiles, 2 warps), or 0 = auto (4 when
+ * bdz % 4 == 0 and the brick has <= 64 columns, else 2).
+ * live_masks (optional, f32): 4 planes of P uint2, the forward's exact
+ * truncation decisions, consumed by gsv_backward so it walks only live
+ * voxels.  Word w of a pair (plane w/2, .x/.y = w%2) holds the live bits of
+ * warp tile w/vpl at depth w%vpl, bit = lane.  Requires a brick that fills
+ * the CTA's warp tiles exactly (vpl 2: 128 columns of 2; vpl 4: 64 of 4 --
+ * e.g. 8x8x4).
  * ------------------------------------------------------------------------ */
 int gsv_forward(const double* positions, const double* log_scales,
                 const double* rotations, const gsv_record32* rec32,
@@ -186,7 +189,7 @@ int gsv_forward(const double* positions, const double* log_scales,
                 const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
                 int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, uint32_t* live_masks, int vpl_hint, void* stream);
+                double* loss_part, uint32_t* live_masks, int vpl, void* stream);
 
 /* Per-voxel backward inputs from (W, I, dL/dI) for the unfused API path
  * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) = {dL/dI / W, I}
@@ -205,7 +208,8 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi,
  * the reference merges in (raster.py:512-516: stable argsort by gid keeps
  * ascending brick order).  partials: float (f32) or double (f64), (P,12).
  * live_masks: the masks gsv_forward wrote for the same index (f32 only), or
- * NULL to find live voxels from exact per-row spans. */
+ * NULL to find live voxels from exact per-row spans; mask_vpl: the vpl that
+ * forward ran with (0 = the same auto rule). */
 int gsv_backward(const double* positions, const double* log_scales,
                  const double* rotations, const gsv_record32* rec32,
                  const gsv_record64* rec64, const int64_t* starts,
@@ -213,7 +217,7 @@ int gsv_backward(const double* positions, const double* log_scales,
                  const int32_t* box, const gsv_grid* grid,
                  const gsv_bricks* bricks, double cutoff_sigma,
                  int precision, const void* ab, const uint32_t* live_masks,
-                 void* partials, void* stream);
+                 int mask_vpl, void* partials, void* stream);
 
 /* Deterministic per-Gaussian merge of pair partials in ascending brick order
  * (_merge_pairs_kernel, raster.py:412-451).  gsum (N,12) double. */

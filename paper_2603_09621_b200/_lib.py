@@ -64,7 +64,7 @@ _SIGS = {
                     c_vp, c_vp, c_vp, c_vp, c_int, c_dbl, c_vp, c_vp, c_vp, c_int, c_vp],
     "gsv_backward_prep": [c_vp, c_vp, c_vp, GP, BP, c_dbl, c_int, c_vp, c_vp, c_vp],
     "gsv_backward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl,
-                     c_int, c_vp, c_vp, c_vp, c_vp],
+                     c_int, c_vp, c_vp, c_int, c_vp, c_vp],
     "gsv_merge": [c_vp, c_vp, c_i64, c_int, c_vp, c_vp],
     "gsv_chain_rule": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp,
                        c_vp, c_vp],
@@ -91,6 +91,7 @@ _SIGS = {
 _RESTYPES = {"gsv_last_error": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)
+ABI_VERSION = 2        # GSV_ABI_VERSION of include/gsv.h these signatures follow
 
 _lib = None
 
@@ -109,6 +110,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
             " (there is no CPU fallback)")
     lib = ctypes.CDLL(path)
+    lib.gsv_abi_version.restype = c_int
+    if lib.gsv_abi_version() != ABI_VERSION:
+        raise GsvLibraryError(f"{path} implements ABI {lib.gsv_abi_version()}, these bindings "
+                              f"expect {ABI_VERSION}: rebuild the library")
     for name, args in _SIGS.items():
         fn = getattr(lib, name)
         fn.argtypes = args

@@ -145,6 +145,16 @@ __device__ double block_sum(double v, double* sh) {
   return t;  // valid in thread 0
 }
 
+// Live-mask layouts: VPL voxels per lane, one warp tile of 32 lanes; the
+// units of a brick (column heads) must fit one CTA pass.
+__host__ __device__ inline int64_t mask_units(const gsv_bricks& k, int vpl) {
+  return (int64_t)k.bdx * k.bdy * ((k.bdz + vpl - 1) / vpl);
+}
+inline int mask_vpl_auto(const gsv_bricks& k) {
+  return (k.bdz % 4 == 0 && mask_units(k, 4) <= 64) ? 4 : 2;
+}
+// (live masks: mask_units == 128 / vpl * 2, i.e. exactly 4 planes of words)
+
 // --------------------------------------------------------------- forward f32
 // Thread -> voxel ownership.  A "unit" is a column pair of voxels (x, y, z0)
 // and (x, y, z0+1).  When the brick dims are multiples of 4 the 32 units of a
@@ -226,7 +236,7 @@ __device__ __forceinline__ void unit_voxel_v(int u, const gsv_bricks& k, int& x,
 #ifndef GSV_FWD_OCC
 #define GSV_FWD_OCC 640
 #endif
-template <int VPL, int THREADS>
+template <int VPL, int THREADS, bool MASKS>
 __global__ void __launch_bounds__(THREADS, GSV_FWD_OCC / THREADS)
 forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
                  const gsv_record32* __restrict__ rec,
@@ -238,7 +248,8 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
                  float2* __restrict__ ab, double* __restrict__ loss_part,
                  uint2* __restrict__ live_masks) {
   __shared__ Pair32 sp[THREADS];       // 32 slots per warp
-  __shared__ uint2 smask[THREADS];     // live bits of this round's hits, per warp
+  // live bits of this round's hits: per warp and hit VPL words (VPL/2 uint2)
+  __shared__ uint2 smask[MASKS ? THREADS * VPL / 2 : 1];
   __shared__ double red[THREADS / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
@@ -250,7 +261,9 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
   const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
   // masks: VPL 2, one pass over the brick's voxel units (4 warp tiles)
-  const bool want_masks = VPL == 2 && THREADS == 128 && live_masks != nullptr && units <= THREADS;
+  // masks (host-checked: units <= THREADS): per pair VPL words per warp,
+  // planes [warp * VPL/2 + k][pair] of uint2 {word 2k, word 2k+1}
+  constexpr bool want_masks = MASKS;
   const int64_t mstride = starts[gridDim.x];   // pairs of the slab: mask plane stride
   double lsum = 0.0;
 
@@ -291,6 +304,9 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
     const float mXX = mX * mX, mYY = mY * mY, mZZ = mZ * mZ, mXY = mX * mY, mXZ = mX * mZ,
                 mYZ = mY * mZ, m2Z1 = (VPL == 2 && !own[1]) ? qnan : fmaf(2.f, mZ, 1.f);
     const int gx = bg.x0 + lx, gy = bg.y0 + ly, gz = bg.z0 + lz;
+    unsigned ownb[VPL];
+#pragma unroll
+    for (int h = 0; h < VPL; ++h) ownb[h] = __ballot_sync(kFull, own[h]);
     float accS[VPL], accW[VPL];
 #pragma unroll
     for (int h = 0; h < VPL; ++h) accS[h] = accW[h] = 0.f;
@@ -428,17 +444,26 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
           accW[h] += w;
         }
         if (want_masks) {
-          const unsigned ma = __ballot_sync(kFull, live[0]);
-          const unsigned mb = __ballot_sync(kFull, live[VPL - 1]);
-          smask[(warp << 5) + jj] = make_uint2(ma, mb);   // warp-uniform: same-address store
+          unsigned mw[VPL];
+#pragma unroll
+          for (int h = 0; h < VPL; ++h) mw[h] = __ballot_sync(kFull, live[h]);
+          // warp-uniform values: every lane stores the same words (no predicate)
+#pragma unroll
+          for (int kk = 0; kk < VPL / 2; ++kk)
+            smask[((warp << 5) + jj) * (VPL / 2) + kk] = make_uint2(mw[2 * kk], mw[2 * kk + 1]);
         }
       }
       // live-voxel masks for the backward, plane [warp][pair]: one coalesced
       // 256-byte store per warp and round (pairs missing the tile get zeros)
       if (want_masks) {
         __syncwarp();
-        const uint2 mm = hit ? smask[(warp << 5) + rank] : make_uint2(0u, 0u);
-        if (gid >= 0) live_masks[warp * mstride + base + lane] = mm;
+#pragma unroll
+        for (int kk = 0; kk < VPL / 2; ++kk) {
+          uint2 mm = hit ? smask[((warp << 5) + rank) * (VPL / 2) + kk] : make_uint2(0u, 0u);
+          mm.x &= ownb[2 * kk];          // voxels outside the grid never enter a mask
+          mm.y &= ownb[2 * kk + 1];
+          if (gid >= 0) live_masks[(warp * (VPL / 2) + kk) * mstride + base + lane] = mm;
+        }
       }
       __syncwarp();
     }
@@ -932,7 +957,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
                    const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                    const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
                    gsv_grid g, gsv_bricks k, float cut2, const uint2* __restrict__ masks,
-                   const float2* __restrict__ ab, float4* __restrict__ partials) {
+                   int mvpl, const float2* __restrict__ ab, float4* __restrict__ partials) {
   __shared__ float2 sab[256];                 // brick voxels (units <= 128)
   __shared__ float4 slut[256];                // (word << 5) | bit -> (x, y, z, sab index)
   __shared__ unsigned swords[kBwdThreads / 32][9][32];   // per lane: its pair's non-empty
@@ -951,17 +976,25 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
   const int tid = threadIdx.x, lane = tid & 31;
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
   const bool tiled = ((k.bdx | k.bdy | k.bdz) & 3) == 0;
-  const int units = k.bdx * k.bdy * ((k.bdz + 1) >> 1);
+  const int units = (int)mask_units(k, mvpl);
   const int64_t mstride = starts[gridDim.x];   // mask plane stride = slab pairs
-  // mask word wi = 2 * tile + half, bit = lane of the tile: voxel of unit
-  // tile * 32 + bit, z0 + half
+  // mask word wi = VPL * warp + h, bit = lane of the warp tile: voxel of
+  // unit warp * 32 + bit, z0 + h (the forward's layout for its VPL)
+  const int wsh = mvpl == 4 ? 2 : 1;
+  // the host guarantees the brick fills all 4 planes (units = 128 / vpl * 2)
+  auto load_plane = [&](const uint2* m, int plane, int64_t j) {
+    return __ldg(m + plane * mstride + j);
+  };
   for (int e = tid; e < 256; e += kBwdThreads) {
-    const int wi = e >> 5, u = ((wi >> 1) << 5) + (e & 31);
+    const int wi = e >> 5, u = ((wi >> wsh) << 5) + (e & 31);
     float4 v = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
     if (u < units) {
       int x, y, z0;
-      unit_voxel(u, k, tiled, x, y, z0);
-      const int z = z0 + (wi & 1);
+      if (mvpl == 4)
+        unit_voxel_v<4>(u, k, x, y, z0);
+      else
+        unit_voxel(u, k, tiled, x, y, z0);
+      const int z = z0 + (wi & ((1 << wsh) - 1));
       if (z < k.bdz)
         v = make_float4((float)x, (float)y, (float)z, __int_as_float(x + k.bdx * (y + k.bdy * z)));
     }
@@ -984,8 +1017,8 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
     // (1) cost = live voxels of the pair
     for (int t = tid; t < cnt; t += kBwdThreads) {
       const int64_t jt = cbase + t;
-      const uint2 a0 = __ldg(masks + jt), a1 = __ldg(masks + mstride + jt),
-                  a2 = __ldg(masks + 2 * mstride + jt), a3 = __ldg(masks + 3 * mstride + jt);
+      const uint2 a0 = load_plane(masks, 0, jt), a1 = load_plane(masks, 1, jt),
+                  a2 = load_plane(masks, 2, jt), a3 = load_plane(masks, 3, jt);
       const int c = __popc(a0.x) + __popc(a0.y) + __popc(a1.x) + __popc(a1.y) + __popc(a2.x) +
                     __popc(a2.y) + __popc(a3.x) + __popc(a3.y);
       scost[t] = (unsigned short)c;
@@ -1044,8 +1077,8 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
         ey[a] = L[3 * a + 1] * fsy;
         ez[a] = L[3 * a + 2] * fsz;
       }
-      const uint2 a0 = __ldg(masks + j), a1 = __ldg(masks + mstride + j),
-                  a2 = __ldg(masks + 2 * mstride + j), a3 = __ldg(masks + 3 * mstride + j);
+      const uint2 a0 = load_plane(masks, 0, j), a1 = load_plane(masks, 1, j),
+                  a2 = load_plane(masks, 2, j), a3 = load_plane(masks, 3, j);
       // this lane's column of the warp's word table (conflict-free, no sync:
       // only the lane itself reads it): its non-empty words and their LUT
       // bases, compacted, plus a zero sentinel
@@ -1254,7 +1287,7 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
                 const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
                 double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
                 const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, uint32_t* live_masks, int vpl_hint, void* stream) {
+                double* loss_part, uint32_t* live_masks, int vpl, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
   GSV_REQUIRE(precision == 0 || rec64 != nullptr, "the f64 forward needs rec64");
@@ -1266,19 +1299,26 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
   const double cut2d = cutoff_sigma * cutoff_sigma;
   cudaStream_t s = as_stream(stream);
   if (precision == 0) {
-    // Column depth: 2 voxels for small Gaussians (LR train grid, and always
-    // when the backward wants live masks), 4 when Gaussians span several
-    // bricks (vpl_hint from the caller: pairs per Gaussian >= 8).
-    if (live_masks == nullptr && vpl_hint >= 4)
-      forward32_kernel<4, 64><<<(unsigned)nb, 64, 0, s>>>(
-          positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, *grid, *bricks, (float)cut2d,
-          cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
-          (float2*)ab, loss_part, nullptr);
-    else
-      forward32_kernel<2, 128><<<(unsigned)nb, 128, 0, s>>>(
-          positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, *grid, *bricks, (float)cut2d,
-          cut2d, eps_w, (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count,
-          (float2*)ab, loss_part, (uint2*)live_masks);
+    // Column depth: VPL voxels per lane (2: 4x4x4 warp tiles, 4 warps per
+    // 8x8x4 brick; 4: 8x4x4 tiles, 2 warps); 0 = auto (4 when bdz % 4 == 0).
+    GSV_REQUIRE(vpl == 0 || vpl == 2 || vpl == 4, "vpl must be 0, 2 or 4");
+    if (vpl == 0) vpl = mask_vpl_auto(*bricks);
+    if (live_masks != nullptr)
+      GSV_REQUIRE(mask_units(*bricks, vpl) == (vpl == 4 ? 64 : 128),
+                  "live masks need a brick that fills one CTA's warp tiles exactly "
+                  "(e.g. 8x8x4)");
+    const ExactSrc xs{positions, log_scales, rotations, rec64};
+#define GSV_FWD32(V, T, M)                                                                     \
+  forward32_kernel<V, T, M><<<(unsigned)nb, T, 0, s>>>(                                        \
+      positions, xs, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,          \
+      (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab, loss_part,   \
+      (uint2*)live_masks)
+    if (vpl == 4) {
+      if (live_masks) GSV_FWD32(4, 64, true); else GSV_FWD32(4, 64, false);
+    } else {
+      if (live_masks) GSV_FWD32(2, 128, true); else GSV_FWD32(2, 128, false);
+    }
+#undef GSV_FWD32
     GSV_CHECK_LAUNCH("forward32_kernel");
   } else {
     forward64_kernel<<<(unsigned)nb, 128, 0, s>>>(
@@ -1320,8 +1360,8 @@ int gsv_backward(const double* positions, const double* log_scales, const double
                  const gsv_record32* rec32, const gsv_record64* rec64, const int64_t* starts,
                  const int32_t* gids, const int64_t* gstart, const int32_t* box,
                  const gsv_grid* grid, const gsv_bricks* bricks, double cutoff_sigma,
-                 int precision, const void* ab, const uint32_t* live_masks, void* partials,
-                 void* stream) {
+                 int precision, const void* ab, const uint32_t* live_masks, int mask_vpl,
+                 void* partials, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
   GSV_REQUIRE(precision == 0 || rec64 != nullptr, "the f64 backward needs rec64");
@@ -1329,12 +1369,15 @@ int gsv_backward(const double* positions, const double* log_scales, const double
   if (nb == 0) return GSV_OK;
   const double cut2d = cutoff_sigma * cutoff_sigma;
   cudaStream_t s = as_stream(stream);
-  const int64_t units = (int64_t)bricks->bdx * bricks->bdy * ((bricks->bdz + 1) / 2);
   if (precision == 0 && live_masks != nullptr) {
-    GSV_REQUIRE(units <= kFwdThreads, "live masks need bricks of <= 256 voxels");
+    if (mask_vpl == 0) mask_vpl = mask_vpl_auto(*bricks);
+    GSV_REQUIRE(mask_vpl == 2 || mask_vpl == 4, "mask_vpl must be 0, 2 or 4");
+    GSV_REQUIRE(mask_units(*bricks, mask_vpl) == (mask_vpl == 4 ? 64 : 128),
+                "live masks need a brick that fills one CTA's warp tiles exactly "
+                "(e.g. 8x8x4)");
     backward32m_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(
         positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,
-        (const uint2*)live_masks, (const float2*)ab, (float4*)partials);
+        (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials);
     GSV_CHECK_LAUNCH("backward32m_kernel");
   } else if (precision == 0) {
     const int64_t bvox = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz;

@@ -297,13 +297,23 @@ def _records(f, grid, idx: BrickIndex, opts: RenderOptions):
 
 
 # ----------------------------------------------------------------- forward
-def _vpl_hint(idx, f) -> int:
-    """Voxels per lane for the forward's warp tiles: 4 when Gaussians span
-    several bricks (many pairs per Gaussian, e.g. HR renders), else 2."""
+def _resolve_vpl(brick_dims) -> int:
+    """Voxels per lane of the f32 forward's warp tiles (gsv_forward's vpl,
+    the same rule as its auto mode): 4 -- columns of 4 in z, 8x4x4 tiles --
+    when bdz % 4 == 0 and the brick has <= 64 columns, else 2 (4x4x4 tiles).
+    GSV_VPL=2|4 forces one (measurement)."""
     forced = os.environ.get("GSV_VPL")
     if forced in ("2", "4"):
         return int(forced)
-    return 4 if idx.pair_count >= 8 * max(f.count, 1) else 2
+    bx, by, bz = brick_dims
+    return 4 if bz % 4 == 0 and bx * by * (bz // 4) <= 64 else 2
+
+
+def _masks_fit(brick_dims, vpl: int) -> bool:
+    """Live masks need a brick that fills one CTA's warp tiles exactly (4
+    planes of mask words), e.g. the default 8x8x4."""
+    bx, by, bz = brick_dims
+    return bx * by * (-(-bz // vpl)) == (64 if vpl == 4 else 128)
 
 
 def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_kind=0,
@@ -317,7 +327,7 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
-        _vpl_hint(idx, f), _lib.stream_ptr()), "forward")
+        _resolve_vpl(idx.brick_dims), _lib.stream_ptr()), "forward")
 
 
 def forward(f: GaussianField, grid: GridSpec, idx: BrickIndex,
@@ -351,7 +361,7 @@ def _emission_layout(f, grid, idx: BrickIndex, opts: RenderOptions):
 
 
 def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: bool,
-                   timer=None, pool=None, live_masks=None):
+                   timer=None, pool=None, live_masks=None, mask_vpl: int = 0):
     lib = _lib.lib()
     n = f.count
     pdt = opts.torch_dtype
@@ -368,7 +378,7 @@ def _pair_partials(f, grid, idx, opts, rec32, rec64, ab, gstart, box, trusted: b
         gstart.data_ptr(),
         box.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), opts.precision_code, ab.data_ptr(), _lib.ptr(live_masks),
-        partials.data_ptr(), _lib.stream_ptr()), "backward")
+        int(mask_vpl), partials.data_ptr(), _lib.stream_ptr()), "backward")
     gsum = _alloc(pool, "gsum", (n, 12), torch.float64, f.device)
     if timer is not None:
         timer("merge")

@@ -25,7 +25,8 @@ import torch
 
 from . import _lib
 from .field import GaussianField
-from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule, _preprocess, _scan,
+from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule, _masks_fit,
+                     _preprocess, _resolve_vpl, _scan,
                      _forward_into, _pair_partials, build_brick_index)
 from .render import RenderOptions
 from .volume import Volume
@@ -106,6 +107,7 @@ class TrainStep:
         # Everything a step returns is a view valid until the next step.
         self.pool = _lib.BufferPool(self.target.device)
         self._masks = None
+        self._mask_vpl = 0
 
     @property
     def sharded(self) -> bool:
@@ -154,7 +156,8 @@ class TrainStep:
         # exactly the forward's live voxels
         bd = self.brick_dims
         masks = None
-        if (opts.precision == "f32" and bd[0] * bd[1] * ((bd[2] + 1) // 2) <= 128
+        self._mask_vpl = _resolve_vpl(bd)
+        if (opts.precision == "f32" and _masks_fit(bd, self._mask_vpl)
                 and not os.environ.get("GSV_NO_LIVE_MASKS")):
             masks = pool.get("live_masks", (4, max(idx.pair_count, 1), 2), torch.int32)
         self._mark("forward")
@@ -176,7 +179,7 @@ class TrainStep:
         aux = idx._aux
         gsum = _pair_partials(f, self.grid, idx, self.opts, aux.rec32, aux.rec64, out.ab,
                               aux.gstart, aux.box, True, timer=self.timer, pool=self.pool,
-                              live_masks=self._masks)
+                              live_masks=self._masks, mask_vpl=self._mask_vpl)
         if self.sharded:
             # One collective per step: the merged per-Gaussian partials, with
             # this rank's loss partial riding in the spare 12th column.
@@ -237,7 +240,7 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
     if self.sharded:
         gsum = _pair_partials(f, self.grid, idx, opts, aux.rec32, aux.rec64, out.ab, aux.gstart,
                               aux.box, True, timer=self.timer, pool=self.pool,
-                              live_masks=self._masks)
+                              live_masks=self._masks, mask_vpl=self._mask_vpl)
         import torch.distributed as dist
         self._mark("allreduce")
         red = self._reduce_buffer(gsum, out)
@@ -256,7 +259,8 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
             idx.starts.data_ptr(), idx.gids.data_ptr(), aux.gstart.data_ptr(), aux.box.data_ptr(),
             _lib.make_grid(self.grid), _lib.make_bricks(self.grid, idx.brick_dims, idx.slab),
             float(opts.cutoff_sigma), opts.precision_code, out.ab.data_ptr(),
-            _lib.ptr(self._masks), partials.data_ptr(), _lib.stream_ptr()), "backward")
+            _lib.ptr(self._masks), int(self._mask_vpl), partials.data_ptr(),
+            _lib.stream_ptr()), "backward")
         self._mark("update")
         _adam_launch(f, state, lrs, beta1, beta2, eps, partials, aux.gstart, None,
                      opts.precision_code, self.pool)
@@ -313,7 +317,7 @@ def _graph_key(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps):
 def _graph_supported(self) -> bool:
     bd = self.brick_dims
     return (not self.sharded and self.opts.precision == "f32"
-            and bd[0] * bd[1] * ((bd[2] + 1) // 2) <= 128
+            and _masks_fit(bd, _resolve_vpl(bd))
             and not os.environ.get("GSV_NO_GRAPH") and not os.environ.get("GSV_NO_LIVE_MASKS")
             and not os.environ.get("GSV_TAIL_SPLIT"))
 
@@ -358,7 +362,8 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(),
         b["gstart"].data_ptr(), b["box"].data_ptr(), gr, br, float(opts.cutoff_sigma), 0,
-        b["ab"].data_ptr(), b["masks"].data_ptr(), b["partials"].data_ptr(), s), "backward")
+        b["ab"].data_ptr(), b["masks"].data_ptr(), b["vpl"], b["partials"].data_ptr(), s),
+        "backward")
     _lib.check(lib.gsv_fused_update_device(
         b["partials"].data_ptr(), b["gstart"].data_ptr(), n, f.positions.data_ptr(),
         f.log_scales.data_ptr(), f.rotations.data_ptr(), f.raw_amplitude.data_ptr(),
@@ -412,8 +417,7 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     b["result_host"] = torch.zeros(2, dtype=torch.float64).pin_memory()
     b["t"] = gp.get("t", (1,), torch.int64)
     b["bc"] = _bias_corrections(beta1, beta2, state.t, _BC_CHUNK).to(dev)
-    b["vpl"] = 4 if pairs >= 8 * max(n, 1) and not os.environ.get("GSV_VPL") else \
-        int(os.environ.get("GSV_VPL", "2"))
+    b["vpl"] = _resolve_vpl(self.brick_dims)
     hp = _lib.GsvAdamHparams()
     for i, name in enumerate(("positions", "log_scales", "rotations", "raw_amplitude",
                               "raw_relax")):

@@ -37,7 +37,9 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel_without_gpu():
     lib = _lib.load()
-    assert lib.gsv_abi_version() == 1
+    header = open(os.path.join(ROOT, "include", "gsv.h")).read()
+    declared = int(re.search(r"#define GSV_ABI_VERSION (\d+)", header).group(1))
+    assert lib.gsv_abi_version() == declared == _lib.ABI_VERSION
     assert isinstance(lib.gsv_last_error(), bytes)
 
 

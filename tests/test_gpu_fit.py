@@ -234,3 +234,27 @@ def test_graph_step_recaptures_on_new_hyperparameters():
     eb.step(fb, sb, lrs2)
     assert eb._graph.key != key0
     np.testing.assert_array_equal(_pack(fa), _pack(fb))
+
+
+@pytest.mark.parametrize("vpl", ["2", "4"])
+def test_masked_backward_matches_span_backward(vpl, monkeypatch):
+    """The train step's backward walks the forward's live masks (either warp
+    tile layout); its merged gradients equal the public span backward's --
+    both evaluate exactly the live pair-voxels -- up to f32 rounding."""
+    monkeypatch.setenv("GSV_VPL", vpl)
+    p = make_problem(CONFIGS[2])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    out = step.forward(f)
+    assert step._masks is not None and step._mask_vpl == int(vpl)
+    gm = step.backward(f, out)
+    idx = gs.build_brick_index(f, lr.grid)
+    c = gs.forward(f, lr.grid, idx)
+    _, dl = gs.loss_and_grad(c.volume(), lr, "l1")
+    gp = gs.backward(f, lr.grid, idx, c, dl)
+    for k in GRAD_KEYS:
+        a = getattr(gm, k).double().cpu().numpy().ravel()
+        b = getattr(gp, k).double().cpu().numpy().ravel()
+        err = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+        assert err <= 1e-5, (k, err)
