@@ -952,6 +952,11 @@ backward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 // set bits of its pair -- exactly the live voxels, nothing else.
 constexpr int kBwdMChunk = 2048;
 
+// ARITH: the default 8x8x4 brick with vpl-4 masks, where word wi = 4 w + z
+// and bit b map to brick voxel index b + 32 w + 64 z -- decoded with integer
+// ops instead of the (word, bit) LUT, keeping the shared-memory pipe for the
+// {alpha, I} gathers (the kernel's bound).
+template <bool ARITH>
 __global__ void __launch_bounds__(kBwdThreads, 3)
 backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
                    const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
@@ -1091,7 +1096,9 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
         for (int w = 0; w < 8; ++w)
           if (words[w] != 0u) {
             myw[nw << 5] = words[w];
-            myb[nw << 5] = (unsigned short)(w << 5);
+            // ARITH: the word's brick-voxel base 32 (w / 4) + 64 (w % 4); else
+            // its LUT row
+            myb[nw << 5] = (unsigned short)(ARITH ? ((w >> 2) << 5) + ((w & 3) << 6) : w << 5);
             ++nw;
           }
         myw[nw << 5] = 0u;
@@ -1116,9 +1123,21 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
         }
         const int bit = __ffs(cur) - 1;
         cur &= cur - 1u;
-        const float4 vx = slut[wb | bit];
-        const float2 v_ab = sab[__float_as_int(vx.w)];
-        const float fx = vx.x, fy = vx.y, fz = vx.z;
+        float fx, fy, fz;
+        float2 v_ab;
+        if (ARITH) {
+          const int vi = wb + bit;              // x + 8 y + 64 z
+          v_ab = sab[vi];
+          fx = (float)(vi & 7);
+          fy = (float)((vi >> 3) & 7);
+          fz = (float)(vi >> 6);
+        } else {
+          const float4 vx = slut[wb | bit];
+          v_ab = sab[__float_as_int(vx.w)];
+          fx = vx.x;
+          fy = vx.y;
+          fz = vx.z;
+        }
         const float v0 = fmaf(fz, ez[0], fmaf(fy, ey[0], fmaf(fx, ex[0], u[0])));
         const float v1 = fmaf(fz, ez[1], fmaf(fy, ey[1], fmaf(fx, ex[1], u[1])));
         const float v2 = fmaf(fz, ez[2], fmaf(fy, ey[2], fmaf(fx, ex[2], u[2])));
@@ -1375,9 +1394,15 @@ int gsv_backward(const double* positions, const double* log_scales, const double
     GSV_REQUIRE(mask_units(*bricks, mask_vpl) == (mask_vpl == 4 ? 64 : 128),
                 "live masks need a brick that fills one CTA's warp tiles exactly "
                 "(e.g. 8x8x4)");
-    backward32m_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(
-        positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,
-        (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials);
+    const bool arith = mask_vpl == 4 && bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4;
+    if (arith)
+      backward32m_kernel<true><<<(unsigned)nb, kBwdThreads, 0, s>>>(
+          positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,
+          (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials);
+    else
+      backward32m_kernel<false><<<(unsigned)nb, kBwdThreads, 0, s>>>(
+          positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,
+          (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials);
     GSV_CHECK_LAUNCH("backward32m_kernel");
   } else if (precision == 0) {
     const int64_t bvox = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz;
