@@ -250,6 +250,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
   __shared__ Pair32 sp[THREADS];       // 32 slots per warp
   // live bits of this round's hits: per warp and hit VPL words (VPL/2 uint2)
   __shared__ uint2 smask[MASKS ? THREADS * VPL / 2 : 1];
+  __shared__ uint2 sxmask[MASKS ? THREADS * VPL / 2 : 1];   // guard-band additions
   __shared__ double red[THREADS / 32];
   const int lb = blockIdx.x;                               // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
@@ -301,8 +302,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
     // never live and never enters a mask (no per-hit ownership predicates).
     const float qnan = __int_as_float(0x7fc00000);
     const float mX = own[0] ? (float)lx - ctx : qnan, mY = (float)ly - cty, mZ = (float)lz - ctz;
-    const float mXX = mX * mX, mYY = mY * mY, mZZ = mZ * mZ, mXY = mX * mY, mXZ = mX * mZ,
-                mYZ = mY * mZ, m2Z1 = (VPL == 2 && !own[1]) ? qnan : fmaf(2.f, mZ, 1.f);
+    const float mZ1 = (VPL == 2 && !own[1]) ? qnan : mZ + 1.f;
     const int gx = bg.x0 + lx, gy = bg.y0 + ly, gz = bg.z0 + lz;
     unsigned ownb[VPL];
 #pragma unroll
@@ -395,53 +395,67 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
       if (hit) wsp[rank] = p;
       __syncwarp();
       const int nh = __popc(ball);
+      if (want_masks) {                 // guard-band live bits of this round's hits
+#pragma unroll
+        for (int kk = 0; kk < VPL / 2; ++kk)
+          sxmask[((warp << 5) + lane) * (VPL / 2) + kk] = make_uint2(0u, 0u);
+        __syncwarp();
+      }
       for (int jj = 0; jj < nh; ++jj) {
         const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c;
         const float2 pd = *reinterpret_cast<const float2*>(&wsp[jj].d);   // qlo, gid
-        // q(X,Y,Z) for the column's first voxel, then second differences
+        // q(X,Y,Z) of the column's first voxel in nested form -- only the
+        // lane's three offsets stay live across hits -- then differences in z
         float q[VPL];
-        // two independent FMA chains (latency, not throughput, bounds this)
-        float qa = fmaf(pa.y, mX, pa.x);
-        float qb = pb.x * mXX;
-        qa = fmaf(pa.z, mY, qa);
-        qb = fmaf(pb.y, mYY, qb);
-        qa = fmaf(pa.w, mZ, qa);
-        qb = fmaf(pb.z, mZZ, qb);
-        qa = fmaf(pb.w, mXY, qa);
-        qb = fmaf(pc.x, mXZ, qb);
-        qa = fmaf(pc.y, mYZ, qa);
-        q[0] = qa + qb;
-        float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, m2Z1, pa.w)));
+        const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
+        const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
+        const float t3 = fmaf(pb.z, mZ, pa.w);
+        q[0] = fmaf(mX, t1, fmaf(mY, t2, fmaf(mZ, t3, pa.x)));
+        float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, mZ1, t3)));
         const float d2q = 2.f * pb.z;
 #pragma unroll
         for (int h = 1; h < VPL; ++h) {
           q[h] = q[h - 1] + dq;
           dq += d2q;
         }
-        // live: q >= thr, thr = the certain-live bound; in the guard band
-        // [qlo, qhi) the exact f64 decision (the reference's truncation test,
-        // rare and warp-voted) sets thr to -inf (live) or +inf (dead).
-        float thr[VPL];
+        // Live for sure: q >= qhi.  In the guard band [qlo, qhi) the exact
+        // f64 decision (the reference's truncation test; rare, warp-voted)
+        // adds the voxel's contribution right here and records its mask bit,
+        // so the common path below carries no per-voxel state.
         bool band = false;
 #pragma unroll
-        for (int h = 0; h < VPL; ++h) {
-          thr[h] = pc.w;
-          band |= q[h] >= pd.x && q[h] < pc.w;
-        }
+        for (int h = 0; h < VPL; ++h) band |= q[h] >= pd.x && q[h] < pc.w;
         if (__any_sync(kFull, band)) {
           const int gidj = __float_as_int(pd.y);
+          bool xl[VPL];
 #pragma unroll
-          for (int h = 0; h < VPL; ++h)
-            if (q[h] >= pd.x && q[h] < pc.w)
-              thr[h] = exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d) ? -INFINITY : INFINITY;
+          for (int h = 0; h < VPL; ++h) {
+            xl[h] = q[h] >= pd.x && q[h] < pc.w &&
+                    exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d);
+            if (xl[h]) {
+              const float w = ex2_approx(q[h]);
+              accS[h] = fmaf(pc.z, w, accS[h]);
+              accW[h] += w;
+            }
+          }
+          if (want_masks) {
+            unsigned xw[VPL];
+#pragma unroll
+            for (int h = 0; h < VPL; ++h) xw[h] = __ballot_sync(kFull, xl[h]);
+#pragma unroll
+            for (int kk = 0; kk < VPL / 2; ++kk)
+              sxmask[((warp << 5) + jj) * (VPL / 2) + kk] = make_uint2(xw[2 * kk], xw[2 * kk + 1]);
+          }
         }
         bool live[VPL];
 #pragma unroll
         for (int h = 0; h < VPL; ++h) {
-          live[h] = q[h] >= thr[h];
-          const float w = live[h] ? ex2_approx(q[h]) : 0.f;
-          accS[h] = fmaf(pc.z, w, accS[h]);
-          accW[h] += w;
+          live[h] = q[h] >= pc.w;
+          const float w = ex2_approx(q[h]);
+          if (live[h]) {
+            accS[h] = fmaf(pc.z, w, accS[h]);
+            accW[h] += w;
+          }
         }
         if (want_masks) {
           unsigned mw[VPL];
@@ -459,7 +473,12 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
         __syncwarp();
 #pragma unroll
         for (int kk = 0; kk < VPL / 2; ++kk) {
-          uint2 mm = hit ? smask[((warp << 5) + rank) * (VPL / 2) + kk] : make_uint2(0u, 0u);
+          uint2 mm = make_uint2(0u, 0u);
+          if (hit) {
+            const uint2 a = smask[((warp << 5) + rank) * (VPL / 2) + kk];
+            const uint2 x = sxmask[((warp << 5) + rank) * (VPL / 2) + kk];
+            mm = make_uint2(a.x | x.x, a.y | x.y);
+          }
           mm.x &= ownb[2 * kk];          // voxels outside the grid never enter a mask
           mm.y &= ownb[2 * kk + 1];
           if (gid >= 0) live_masks[(warp * (VPL / 2) + kk) * mstride + base + lane] = mm;
