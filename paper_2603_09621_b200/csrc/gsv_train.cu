@@ -335,19 +335,14 @@ __global__ void advance_kernel(int64_t* __restrict__ t, const int32_t* __restric
 constexpr int kTailThreads = 128;
 constexpr int kTailSub = 512;   // pairs per smem sub-chunk (24 KB)
 
-__global__ void __launch_bounds__(kTailThreads)
+__global__ void __launch_bounds__(kTailThreads, 6)
 tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gstart,
             const double* __restrict__ gsum, int64_t n, double* __restrict__ pos,
             double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
             double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
-            gsv_adam_hparams h, StepDev sd) {
+            const gsv_adam_hparams h, StepDev sd) {
   __shared__ float4 sp[kTailSub * 3];
   if (sd.gate != nullptr && *sd.gate != 0) return;   // overflow / non-finite loss: no update
-  if (sd.bc != nullptr) {                            // step number from the device
-    const int64_t t = *sd.t;
-    h.bc1 = sd.bc[2 * t];
-    h.bc2 = sd.bc[2 * t + 1];
-  }
   const int64_t i0 = blockIdx.x * (int64_t)kTailThreads;
   const int64_t i = i0 + threadIdx.x;
   const bool valid = i < n;
@@ -382,23 +377,31 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
   if (!valid) return;
   double g[12];
   chain_one(s, ls + 3 * i, rot + 4 * i, ra[i], rr[i], relax_en, g);
+  // bias corrections: from the device table at the device step counter
+  // (graph replays) or the launch parameters
+  double bc1 = h.bc1, bc2 = h.bc2;
+  if (sd.bc != nullptr) {
+    const int64_t t = *sd.t;
+    bc1 = sd.bc[2 * t];
+    bc2 = sd.bc[2 * t + 1];
+  }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double m = mv[0][3 * i + a], v = mv[5][3 * i + a];
-    pos[3 * i + a] = adam_one(pos[3 * i + a], m, v, g[a], h.lr[0], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    pos[3 * i + a] = adam_one(pos[3 * i + a], m, v, g[a], h.lr[0], h.b1, h.b2, h.eps, bc1, bc2);
     mv[0][3 * i + a] = m; mv[5][3 * i + a] = v;
   }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double m = mv[1][3 * i + a], v = mv[6][3 * i + a];
-    ls[3 * i + a] = adam_one(ls[3 * i + a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    ls[3 * i + a] = adam_one(ls[3 * i + a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, bc1, bc2);
     mv[1][3 * i + a] = m; mv[6][3 * i + a] = v;
   }
   double q[4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     double m = mv[2][4 * i + a], v = mv[7][4 * i + a];
-    q[a] = adam_one(rot[4 * i + a], m, v, g[6 + a], h.lr[2], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    q[a] = adam_one(rot[4 * i + a], m, v, g[6 + a], h.lr[2], h.b1, h.b2, h.eps, bc1, bc2);
     mv[2][4 * i + a] = m; mv[7][4 * i + a] = v;
   }
   const double nrm = sqrt(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
@@ -407,12 +410,12 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
   for (int a = 0; a < 4; ++a) rot[4 * i + a] = __ddiv_rn(q[a], nrm);
   if (amp_en) {
     double m = mv[3][i], v = mv[8][i];
-    ra[i] = adam_one(ra[i], m, v, g[10], h.lr[3], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    ra[i] = adam_one(ra[i], m, v, g[10], h.lr[3], h.b1, h.b2, h.eps, bc1, bc2);
     mv[3][i] = m; mv[8][i] = v;
   }
   if (relax_en) {
     double m = mv[4][i], v = mv[9][i];
-    rr[i] = adam_one(rr[i], m, v, g[11], h.lr[4], h.b1, h.b2, h.eps, h.bc1, h.bc2);
+    rr[i] = adam_one(rr[i], m, v, g[11], h.lr[4], h.b1, h.b2, h.eps, bc1, bc2);
     mv[4][i] = m; mv[9][i] = v;
   }
 }
