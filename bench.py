@@ -328,8 +328,14 @@ def run_ours(args, dist, ws, rank, local):
     t_upd = phases.get("update", (0, float("nan")))[1]
     achieved = e_live * fl / (t_dom * 1e-3) / 1e12
     n_g = f.count
-    bytes_alg = {"forward": 48 * n_g + 4 * pairs + 12 * lr_grid.num_voxels,
-                 "backward": 96 * n_g + 4 * pairs + 12 * lr_grid.num_voxels}[dom]
+    # algorithmic bytes of the train-step kernels: forward reads rec32 + mu
+    # (88 B/Gaussian), gids (4 B/pair), target (4 B/voxel) and writes S, W, I,
+    # {alpha, I} (20 B/voxel) and the live masks (32 B/pair); the masked
+    # backward reads rec32 + mu + box + gstart (112 B/Gaussian), gids + masks
+    # (36 B/pair), {alpha, I} (8 B/voxel) and writes the partials (48 B/pair)
+    nv_lr = lr_grid.num_voxels
+    bytes_alg = {"forward": 88 * n_g + 36 * pairs + 24 * nv_lr,
+                 "backward": 112 * n_g + 84 * pairs + 8 * nv_lr}[dom]
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):

@@ -1,0 +1,96 @@
+"""Summarise an `ncu --set full` report of the hot-path kernels.
+
+python tools/ncu_summary.py REPORT.ncu-rep OUT.md [--traffic profiles/traffic.json]
+
+Writes a markdown table per kernel (duration, DRAM bytes, throughputs,
+occupancy, issue activity, registers, top stall reasons) and, with
+--traffic, the per-launch DRAM bytes (read + write) of the forward and
+backward pair kernels for bench.py's roofline.traffic.
+ncu replays each kernel with cold caches and serialised launches: durations
+are for comparison between kernels, not bench numbers.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import subprocess
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
+    ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem pipes % peak"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
+    ("launch__registers_per_thread", "registers"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+]
+
+ROLE = {"forward32_kernel": "forward", "backward32m_kernel": "backward",
+        "backward32_kernel": "backward_span", "tail_kernel": "update",
+        "preprocess_kernel": "preprocess", "emit_kernel": "emit"}
+
+
+def to_bytes(v: str, unit: str) -> float:
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    return float(v.replace(",", "")) * scale.get(unit, 1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report")
+    ap.add_argument("out")
+    ap.add_argument("--traffic", default=None)
+    args = ap.parse_args()
+    raw = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    head, units = rows[0], rows[1]
+    col = {n: i for i, n in enumerate(head)}
+    stalls = [n for n in head if n.startswith("smsp__pcsamp_warps_issue_stalled_")
+              and not n.endswith("not_issued")]
+    lines = [f"# ncu summary: `{args.report.split('/')[-1]}`", "",
+             "Cold-cache, serialised replays (`--set full --clock-control none`): use the",
+             "durations to compare kernels, not as bench numbers.", ""]
+    traffic: dict = {}
+    for r in rows[2:]:
+        name = r[col["Kernel Name"]]
+        short = name.split("(")[0].replace("void ", "").split("::")[-1]
+        base = short.split("<")[0]
+        lines.append(f"## `{short}`")
+        lines.append("")
+        lines.append("| metric | value |")
+        lines.append("|---|---|")
+        for m, label in METRICS:
+            if m in col:
+                lines.append(f"| {label} | {r[col[m]]} {units[col[m]]} |")
+        samp = {n.replace("smsp__pcsamp_warps_issue_stalled_", ""):
+                float(r[col[n]].replace(",", "") or 0) for n in stalls}
+        tot = sum(samp.values()) or 1.0
+        top = sorted(samp.items(), key=lambda x: -x[1])[:5]
+        lines.append("| top stalls (% samples) | " +
+                     ", ".join(f"{k} {100 * v / tot:.0f}" for k, v in top) + " |")
+        lines.append("")
+        role = ROLE.get(base)
+        if role and "dram__bytes_read.sum" in col and role not in traffic:
+            rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
+            wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
+            traffic[role] = rd + wr
+    with open(args.out, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+    if args.traffic:
+        traffic["source"] = args.report.split("/")[-1]
+        traffic["what"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                           "one ncu --set full capture (tools/kbench.py, config 3 LR)")
+        with open(args.traffic, "w") as fh:
+            json.dump(traffic, fh, indent=1)
+    print(f"wrote {args.out}" + (f" and {args.traffic}" if args.traffic else ""))
+
+
+if __name__ == "__main__":
+    main()
