@@ -361,22 +361,42 @@ def run_ours(args, dist, ws, rank, local):
     e2e = None
     if not args.no_e2e:
         host_t = torch.from_numpy(np.ascontiguousarray(p["lr"].ravel(order="F"))).pin_memory()
-        dev_t = torch.empty_like(host_t, device=dev)
+        # input pipeline: step k+1's target is copied H2D (pinned) on a copy
+        # stream while step k runs; each step then loads it into the step's
+        # target buffer with an 8 MB device copy (stream-ordered)
+        staging = torch.empty_like(host_t, device=dev)
+        copy_s = torch.cuda.Stream(device=dev)
+        ready, freed = torch.cuda.Event(), torch.cuda.Event()
+        cur = torch.cuda.current_stream(dev)
+
+        def prefetch():
+            copy_s.wait_event(freed)
+            with torch.cuda.stream(copy_s):
+                staging.copy_(host_t, non_blocking=True)
+                ready.record(copy_s)
+
+        def e2e_step():
+            cur.wait_event(ready)
+            step.set_target(staging)
+            freed.record(cur)
+            prefetch()                         # next step's input, overlapped
+            return step.step(f, state, lrs)    # fit()'s body, loss device -> host
+
+        freed.record(cur)
+        prefetch()
         for _ in range(min(args.warmup, 3)):
-            dev_t.copy_(host_t, non_blocking=True)
-            step.set_target(dev_t)
-            step.step(f, state, lrs)
+            e2e_step()
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            dev_t.copy_(host_t, non_blocking=True)
-            step.set_target(dev_t)
-            loss = step.step(f, state, lrs)    # fit()'s body, loss device -> host
+            loss = e2e_step()
         barrier()
         sec = max_over_ranks((time.perf_counter() - t0) / args.steps)
         e2e = {"value": 1.0 / sec, "unit": "it/s", "h2d_bytes_per_step": host_t.numel() * 4,
-               "d2h_bytes_per_step": 16, "api": "TrainStep.step (the fit() loop body: CUDA-graph "
-               "replay + loss read)", "last_loss": loss}
+               "d2h_bytes_per_step": 16, "api": "TrainStep.set_target + TrainStep.step (the "
+               "fit() loop body: CUDA-graph replay + loss read)",
+               "h2d": "pinned H2D of each step's target on a copy stream, overlapped with "
+               "the previous step (prefetch), then an 8 MB device copy into the step's buffer", "last_loss": loss}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

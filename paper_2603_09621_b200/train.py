@@ -114,8 +114,16 @@ class TrainStep:
         return self.group is not None and self.world_size > 1
 
     def set_target(self, target_linear: torch.Tensor) -> None:
-        """Swap the target buffer (e.g. after a host->device copy)."""
-        self.target = target_linear
+        """Load a new target volume (linear x-fastest, V values) into the step's
+        persistent target buffer, stream-ordered: from a device tensor (a
+        device copy) or a pinned host tensor (an asynchronous H2D).  The
+        buffer's address never changes, so a captured step graph stays valid."""
+        src = target_linear.reshape(-1)
+        if src.numel() != self.target.numel():
+            raise ValueError(f"target has {src.numel()} voxels, the grid has {self.target.numel()}")
+        if src.dtype != self.target.dtype:
+            src = src.to(self.target.dtype)
+        self.target.copy_(src, non_blocking=True)
 
     def _mark(self, name):
         if self.timer is not None:
