@@ -332,6 +332,18 @@ __global__ void advance_kernel(int64_t* __restrict__ t, const int32_t* __restric
   if (*gate == 0) *t += 1;
 }
 
+// Bulk L2 prefetch of a contiguous range (TMA unit; a hint, no registers or
+// shared memory): the address is rounded down and the size to 16 B.
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t a16 = a & ~(uintptr_t)15;
+  int64_t nb = (bytes + (int64_t)(a - a16)) & ~(int64_t)15;
+  if (nb > (1 << 20)) nb = 1 << 20;
+  if (nb > 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a16), "r"((unsigned)nb)
+                 : "memory");
+}
+
 constexpr int kTailThreads = 128;
 constexpr int kTailSub = 512;   // pairs per smem sub-chunk (24 KB)
 
@@ -346,6 +358,28 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
   const int64_t i0 = blockIdx.x * (int64_t)kTailThreads;
   const int64_t i = i0 + threadIdx.x;
   const bool valid = i < n;
+  // Pull this CTA's parameter and moment runs (and its partial segment) into
+  // L2 now, so Adam's loads after the merge + chain rule hit L2.
+  if (threadIdx.x < 11) {
+    const int64_t cnt = min((int64_t)kTailThreads, n - i0);
+    const int k = threadIdx.x;
+    if (k < 10) {
+      const int grp = k % 5;                       // pos, ls, rot, amp, rel
+      const int w = grp < 2 ? 3 : (grp == 2 ? 4 : 1);
+      const double* mom = nullptr;
+#pragma unroll
+      for (int j = 0; j < 10; ++j)                 // static indices: no local copy
+        if (j == k) mom = mv.p[j];
+      prefetch_l2(mom + w * i0, 8 * w * cnt);
+      if (k < 5) {
+        const double* prm = grp == 0 ? pos : grp == 1 ? ls : grp == 2 ? rot : grp == 3 ? ra : rr;
+        prefetch_l2(prm + w * i0, 8 * w * cnt);
+      }
+    } else if (gsum == nullptr) {
+      const int64_t e_lo = gstart[i0], e_hi = gstart[i0 + cnt];
+      prefetch_l2(partials + 12 * e_lo, 48 * (e_hi - e_lo));
+    }
+  }
   double s[11];
 #pragma unroll
   for (int a = 0; a < 11; ++a) s[a] = 0.0;
