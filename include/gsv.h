@@ -134,9 +134,9 @@ int gsv_bin_fill(const int32_t* counts, const int32_t* box,
 
 /* Capacity mode of gsv_bin_fill for host-sync-free (CUDA-graph) steps: the
  * pair count P = gstart[N] is never read by the host.  Pairs fill slots
- * [0, P) as in gsv_bin_fill, slots [P, capacity) get the sentinel brick
- * nbricks_slab (sorted behind every list), and the sort always covers
- * `capacity` slots.  *overflow (device int32) = P > capacity, or *dry != 0
+ * [0, P) as in gsv_bin_fill, slots [P, capacity) get the last brick id
+ * (the stable sort keeps them behind that brick's pairs; starts[nbricks] = P
+ * cuts them off), and the sort always covers `capacity` slots.  *overflow (device int32) = P > capacity, or *dry != 0
  * (dry may be NULL); on overflow every list is emptied (starts = 0) so the
  * downstream kernels do no work and the caller re-bins with more capacity.
  * Buffers as gsv_bin_fill, sized by capacity; workspace from

@@ -185,8 +185,10 @@ emit_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
 }
 
 // Capacity mode: the pair count P = gstart[n] stays on the device.  Slots
-// [P, cap) get the sentinel brick nb (sorted behind every real pair);
-// overflow = P > cap (or the caller's dry-run flag) empties every list.
+// [P, cap) get the last brick id nb - 1 (the stable sort keeps them behind
+// that brick's real pairs, and starts[nb] = P cuts them off), so keys stay
+// within ceil(log2 nb) bits; overflow = P > cap (or the caller's dry-run
+// flag) empties every list.
 __global__ void pad_kernel(const int64_t* __restrict__ gstart, int64_t n, int64_t cap,
                            int32_t nb, const int32_t* __restrict__ dry,
                            int32_t* __restrict__ keys, int32_t* __restrict__ vals,
@@ -194,7 +196,7 @@ __global__ void pad_kernel(const int64_t* __restrict__ gstart, int64_t n, int64_
   const int64_t p = gstart[n];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = p + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cap; j += stride) {
-    keys[j] = nb;
+    keys[j] = nb - 1;
     vals[j] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -204,7 +206,8 @@ __global__ void pad_kernel(const int64_t* __restrict__ gstart, int64_t n, int64_
 // starts[b] = first sorted position with key >= b, for b in [0, B].
 __global__ void starts_kernel(const int32_t* __restrict__ keys, int64_t p, int32_t nb,
                               int64_t* __restrict__ starts,
-                              const int32_t* __restrict__ overflow) {
+                              const int32_t* __restrict__ overflow,
+                              const int64_t* __restrict__ p_true) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (overflow != nullptr && *overflow != 0) {   // capacity overflow / dry run: empty lists
     if (j <= nb) starts[j] = 0;
@@ -214,6 +217,7 @@ __global__ void starts_kernel(const int32_t* __restrict__ keys, int64_t p, int32
   const int32_t cur = j < p ? keys[j] : nb;
   const int32_t prev = j > 0 ? keys[j - 1] : -1;
   for (int32_t b = prev + 1; b <= cur; ++b) starts[b] = j;
+  if (p_true != nullptr && j == p) starts[nb] = *p_true;   // capacity mode: drop the padding
 }
 
 __global__ void unsorted_kernel(const int64_t* __restrict__ starts,
@@ -230,7 +234,7 @@ __global__ void unsorted_kernel(const int64_t* __restrict__ starts,
 
 int key_bits(int64_t nb) {
   int bits = 1;
-  while (((int64_t)1 << bits) < nb + 1) ++bits;
+  while (((int64_t)1 << bits) < nb) ++bits;   // keys are brick ids 0 .. nb-1
   return bits;
 }
 
@@ -323,7 +327,7 @@ int gsv_bin_fill(const int32_t* counts, const int32_t* box, const int64_t* gstar
   }
   const int64_t threads = 256, items = pairs + 1;
   starts_kernel<<<(unsigned)((items + threads - 1) / threads), (unsigned)threads, 0, s>>>(
-      keys_out, pairs, (int32_t)nb, starts_out, nullptr);
+      keys_out, pairs, (int32_t)nb, starts_out, nullptr, nullptr);
   GSV_CHECK_LAUNCH("starts_kernel");
   return GSV_OK;
 }
@@ -354,7 +358,7 @@ int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box, const int64
   if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort::SortPairs");
   const int64_t threads = 256, items = (capacity > nb ? capacity : nb) + 1;
   starts_kernel<<<(unsigned)((items + threads - 1) / threads), (unsigned)threads, 0, s>>>(
-      keys_out, capacity, (int32_t)nb, starts_out, overflow);
+      keys_out, capacity, (int32_t)nb, starts_out, overflow, gstart + n);
   GSV_CHECK_LAUNCH("starts_kernel");
   return GSV_OK;
 }
