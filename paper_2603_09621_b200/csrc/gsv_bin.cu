@@ -8,11 +8,13 @@
 //                       brick box; fp32 (and optionally fp64) record for the
 //                       pair kernels.
 //   cub ExclusiveSum    counts -> gstart (gid-major emission offsets)
-//   emit_kernel         (slab-local brick id, gid) in gid-major order, each
-//                       Gaussian's bricks x-fastest (raster.py:200-209)
+//   emit_warp_kernel    (slab-local brick id, gid) in gid-major order, each
+//                       Gaussian's bricks x-fastest (raster.py:200-209);
+//                       warp-cooperative, coalesced stores
 //   cub SortPairs       stable LSD radix sort on the brick id, only
 //                       ceil(log2 B) key bits -> lists ascending in gid
-//   starts_kernel       CSR starts from the sorted keys (raster.py:213-215)
+//   starts_search_kernel CSR starts by binary search in the sorted keys
+//                       (raster.py:213-215)
 //
 // This translation unit is compiled with -fmad=false in addition to using
 // the explicit _rn intrinsics, so no f64 expression that feeds a binning
@@ -160,28 +162,85 @@ __global__ void scan_tail_kernel(const int32_t* counts, int64_t n, int64_t* gsta
   gstart[n] = n > 0 ? gstart[n - 1] + (int64_t)counts[n - 1] : 0;
 }
 
-// One thread per Gaussian writes its pairs at gstart[i]: bricks of its box
-// x-fastest, exactly the reference's emission order (raster.py:200-209).
+// Warp-cooperative emission (coalesced stores):
+// a warp owns 32 consecutive Gaussians, prefix-sums their pair counts with
+// shuffles, and each lane then produces consecutive output slots -- finding
+// the owning Gaussian by a 5-step shuffle binary search and the brick from
+// the slot's rank inside the owner's box (x fastest, raster.py:200-209).
 __global__ void __launch_bounds__(256)
-emit_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
-            const int64_t* __restrict__ gstart, int64_t n, gsv_bricks k,
-            int32_t* __restrict__ keys, int32_t* __restrict__ vals, int64_t cap) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n || counts[i] == 0) return;
-  const GBox b = unpack_box(box, i);
-  int64_t off = gstart[i];
-  if (off + counts[i] > cap) return;   // capacity mode: overflow is flagged by pad_kernel
-  const int64_t first = (int64_t)k.bgx * k.bgy * k.bz0;
-  for (int z = 0; z < b.nb_z; ++z)
-    for (int y = 0; y < b.nb_y; ++y) {
-      const int64_t row = (int64_t)(b.blo_x) +
-                          (int64_t)k.bgx * ((b.blo_y + y) + (int64_t)k.bgy * (b.blo_z + z)) - first;
-      for (int x = 0; x < b.nb_x; ++x) {
-        keys[off] = (int32_t)(row + x);
-        vals[off] = (int32_t)i;
-        ++off;
-      }
+emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
+                 const int64_t* __restrict__ gstart, int64_t n, gsv_bricks k,
+                 int32_t* __restrict__ keys, int32_t* __restrict__ vals, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31;
+  if (g0 >= n) return;                       // warp-uniform
+  const int64_t g = g0 + lane;
+  int c = 0, nbx = 1, nbxy = 1, kb = 0;
+  if (g < n) {
+    c = counts[g];
+    if (c > 0) {
+      const GBox b = unpack_box(box, g);
+      nbx = b.nb_x;
+      nbxy = b.nb_x * b.nb_y;
+      kb = b.blo_x + k.bgx * (b.blo_y + k.bgy * (b.blo_z - k.bz0));   // slab-local id
     }
+  }
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int off = incl - c;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int64_t base = gstart[g0];
+  const int bxy = k.bgx * k.bgy;
+  for (int o0 = 0; o0 < total; o0 += 32) {
+    const int o = o0 + lane;
+    // owner = the last lane whose first slot is <= o (always a lane with pairs)
+    int own = 0;
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      const int cand = own + st;
+      const int oc = __shfl_sync(0xffffffffu, off, cand & 31);
+      if (cand < 32 && oc <= o) own = cand;
+    }
+    const int r = o - __shfl_sync(0xffffffffu, off, own);
+    const int ox = __shfl_sync(0xffffffffu, nbx, own);
+    const int oxy = __shfl_sync(0xffffffffu, nbxy, own);
+    const int okb = __shfl_sync(0xffffffffu, kb, own);
+    const int rz = r / oxy, rem = r - rz * oxy;
+    const int ry = rem / ox, rx = rem - ry * ox;
+    if (o < total && base + o < cap) {
+      keys[base + o] = okb + rx + k.bgx * ry + bxy * rz;
+      vals[base + o] = (int32_t)(g0 + own);
+    }
+  }
+}
+
+// starts[b] = lower_bound(keys, b) for b < B (one thread per brick, binary
+// search over the sorted keys); starts[B] = P (capacity mode: the device
+// count, which cuts off the padding); all zero on overflow.
+__global__ void starts_search_kernel(const int32_t* __restrict__ keys, int64_t p, int32_t nb,
+                                     int64_t* __restrict__ starts,
+                                     const int32_t* __restrict__ overflow,
+                                     const int64_t* __restrict__ p_true) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b > nb) return;
+  if (overflow != nullptr && *overflow != 0) {
+    starts[b] = 0;
+    return;
+  }
+  if (b == nb) {
+    starts[b] = p_true != nullptr ? *p_true : p;
+    return;
+  }
+  int64_t lo = 0, hi = p;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(keys + mid) < (int32_t)b) lo = mid + 1; else hi = mid;
+  }
+  starts[b] = lo;
 }
 
 // Capacity mode: the pair count P = gstart[n] stays on the device.  Slots
@@ -201,23 +260,6 @@ __global__ void pad_kernel(const int64_t* __restrict__ gstart, int64_t n, int64_
   }
   if (blockIdx.x == 0 && threadIdx.x == 0)
     *overflow = (p > cap || (dry != nullptr && *dry != 0)) ? 1 : 0;
-}
-
-// starts[b] = first sorted position with key >= b, for b in [0, B].
-__global__ void starts_kernel(const int32_t* __restrict__ keys, int64_t p, int32_t nb,
-                              int64_t* __restrict__ starts,
-                              const int32_t* __restrict__ overflow,
-                              const int64_t* __restrict__ p_true) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (overflow != nullptr && *overflow != 0) {   // capacity overflow / dry run: empty lists
-    if (j <= nb) starts[j] = 0;
-    return;
-  }
-  if (j > p) return;
-  const int32_t cur = j < p ? keys[j] : nb;
-  const int32_t prev = j > 0 ? keys[j - 1] : -1;
-  for (int32_t b = prev + 1; b <= cur; ++b) starts[b] = j;
-  if (p_true != nullptr && j == p) starts[nb] = *p_true;   // capacity mode: drop the padding
 }
 
 __global__ void unsorted_kernel(const int64_t* __restrict__ starts,
@@ -316,19 +358,18 @@ int gsv_bin_fill(const int32_t* counts, const int32_t* box, const int64_t* gstar
   cudaStream_t s = as_stream(stream);
   const int64_t nb = slab_bricks(*bricks);
   if (pairs > 0) {
-    emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(counts, box, gstart, n, *bricks,
-                                                           keys_tmp, vals_tmp, INT64_MAX);
-    GSV_CHECK_LAUNCH("emit_kernel");
+    emit_warp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        counts, box, gstart, n, *bricks, keys_tmp, vals_tmp, INT64_MAX);
+    GSV_CHECK_LAUNCH("emit_warp_kernel");
     size_t bytes = workspace_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, bytes, keys_tmp, keys_out,
                                                     vals_tmp, gids_out, (int)pairs, 0,
                                                     key_bits(nb), s);
     if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort::SortPairs");
   }
-  const int64_t threads = 256, items = pairs + 1;
-  starts_kernel<<<(unsigned)((items + threads - 1) / threads), (unsigned)threads, 0, s>>>(
+  starts_search_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
       keys_out, pairs, (int32_t)nb, starts_out, nullptr, nullptr);
-  GSV_CHECK_LAUNCH("starts_kernel");
+  GSV_CHECK_LAUNCH("starts_search_kernel");
   return GSV_OK;
 }
 
@@ -344,9 +385,9 @@ int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box, const int64
   cudaStream_t s = as_stream(stream);
   const int64_t nb = slab_bricks(*bricks);
   if (n > 0) {
-    emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(counts, box, gstart, n, *bricks,
-                                                           keys_tmp, vals_tmp, capacity);
-    GSV_CHECK_LAUNCH("emit_kernel");
+    emit_warp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        counts, box, gstart, n, *bricks, keys_tmp, vals_tmp, capacity);
+    GSV_CHECK_LAUNCH("emit_warp_kernel");
   }
   pad_kernel<<<592, 256, 0, s>>>(gstart, n, capacity, (int32_t)nb, dry, keys_tmp, vals_tmp,
                                  overflow);
@@ -356,10 +397,9 @@ int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box, const int64
                                                   vals_tmp, gids_out, (int)capacity, 0,
                                                   key_bits(nb), s);
   if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort::SortPairs");
-  const int64_t threads = 256, items = (capacity > nb ? capacity : nb) + 1;
-  starts_kernel<<<(unsigned)((items + threads - 1) / threads), (unsigned)threads, 0, s>>>(
+  starts_search_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
       keys_out, capacity, (int32_t)nb, starts_out, overflow, gstart + n);
-  GSV_CHECK_LAUNCH("starts_kernel");
+  GSV_CHECK_LAUNCH("starts_search_kernel");
   return GSV_OK;
 }
 

@@ -27,19 +27,26 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--hr", action="store_true", help="trace the HR render instead")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     p = synth.make_problem(synth.CONFIGS[args.config])
     f = gs.GaussianField(*p["field"])
-    step = gs.TrainStep(gs.Volume(p["lr_grid"], p["lr"]), gs.RenderOptions(), (8, 8, 4), "l1")
-    state = gs.AdamState.create(f)
-    lrs = gs.FitConfig().resolved_lrs(p["lr_grid"].spacing)
+    if args.hr:
+        rend = gs.Renderer(p["render_grid"], gs.RenderOptions(), (8, 8, 4))
+        run = lambda: rend(f)  # noqa: E731
+    else:
+        step = gs.TrainStep(gs.Volume(p["lr_grid"], p["lr"]), gs.RenderOptions(), (8, 8, 4),
+                            "l1")
+        state = gs.AdamState.create(f)
+        lrs = gs.FitConfig().resolved_lrs(p["lr_grid"].spacing)
+        run = lambda: step.step(f, state, lrs)  # noqa: E731
     for _ in range(5):
-        step.update(f, step.forward(f), state, lrs)
+        run()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(args.steps):
-            step.update(f, step.forward(f), state, lrs)
+            run()
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     evs.sort(key=lambda e: e.time_range.start)
