@@ -302,6 +302,25 @@ int gsv_step_advance(int64_t* step, const int32_t* gate, void* stream);
 /* q /= |q| per Gaussian (GaussianField.normalize_rotations, field.py:100). */
 int gsv_normalize_rotations(double* rotations, int64_t n, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Quality metrics (metrics.py:35-77), f64 like the reference.  x, y: V
+ * values, float32 (x_f64 = 0) or float64 (1), linear x-fastest.
+ * gsv_sq_diff_sum: *out = sum (x - y)^2 (PSNR's MSE numerator) in a fixed
+ *   reduction order; partials: gsv_metric_blocks(V) doubles of scratch.
+ * gsv_ssim3d: *out = sum over voxels of the local SSIM map (divide by V for
+ *   ssim3d): the 11-tap window (window11: a HOST array of 11 doubles, built
+ *   exactly as metrics.py:45-49) applied separably along x, y, z, zero fill,
+ *   local moments divided by the window's coverage; needs nx, ny, nz >= 11.
+ *   workspace: gsv_ssim3d_workspace bytes.
+ * ------------------------------------------------------------------------ */
+int gsv_metric_blocks(int64_t v);
+int gsv_sq_diff_sum(const void* x, int x_f64, const void* y, int y_f64, int64_t v,
+                    double* partials, double* out, void* stream);
+int gsv_ssim3d_workspace(const gsv_grid* grid, size_t* bytes);
+int gsv_ssim3d(const void* x, int x_f64, const void* y, int y_f64, const gsv_grid* grid,
+               const double* window11, void* workspace, size_t workspace_bytes,
+               double* out, void* stream);
+
 /* Brute-force O(N*V) render (render_naive / _naive_kernel, render.py:84-127)
  * on the device, Sigma^-1 quadratic form, f64 math.  precision selects the
  * accumulator / output type. */

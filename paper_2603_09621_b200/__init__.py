@@ -21,6 +21,7 @@ from .raster import (DEFAULT_BRICK_DIMS, BrickIndex, GradientBuffer, RenderCache
                      worker_count)
 from .optimize import (AdamState, FitConfig, FitReport, fit, loss_and_grad, step_optimizer)
 from .train import Renderer, StepOutput, TrainStep
+from .metrics import MetricReport, psnr, ssim3d
 
 __all__ = [
     "__version__",
@@ -34,4 +35,5 @@ __all__ = [
     "forward", "backward", "merge_gradients", "set_worker_count", "worker_count",
     "FitConfig", "FitReport", "AdamState", "fit", "loss_and_grad", "step_optimizer",
     "TrainStep", "StepOutput", "Renderer",
+    "psnr", "ssim3d", "MetricReport",
 ]

@@ -25,7 +25,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
 # Per-file extra flags.  The binning TU must never contract f64 mul+add into
 # FMA (bit-exact bounds vs numpy, SURVEY.md §0 finding 1).
 EXTRA = {"gsv_bin.cu": ["-fmad=false"]}
-SOURCES = ["gsv_capi.cu", "gsv_bin.cu", "gsv_render.cu", "gsv_train.cu", "gsv_diag.cu"]
+SOURCES = ["gsv_capi.cu", "gsv_bin.cu", "gsv_render.cu", "gsv_train.cu", "gsv_metrics.cu",
+           "gsv_diag.cu"]
 
 
 def _headers():

@@ -149,6 +149,37 @@ def fit_quality(iterations=200):
             "trilinear_ssim": ssim3d(resample_trilinear(lr, hr.grid), hr)}
 
 
+METRIC_CASES = [  # (seed, dims, dtype, noise): seeded volume pairs for metrics.py
+    (11, (16, 16, 16), "float32", 0.05),
+    (12, (11, 13, 17), "float64", 0.2),
+    (13, (32, 24, 20), "float32", 0.01),
+    (14, (24, 24, 24), "float64", 0.0),      # identical: PSNR inf, SSIM 1
+]
+
+
+def metric_pair(seed, dims, dtype, noise):
+    """The inputs of one metric case, rebuilt identically on the GPU box."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0.0, 1.0, size=dims)
+    b = np.clip(a + noise * rng.standard_normal(dims), 0.0, 1.0) if noise else a.copy()
+    return a.astype(dtype), b.astype(dtype)
+
+
+def metrics():
+    """Reference psnr / ssim3d (metrics.py:35-77) on seeded volume pairs."""
+    from gsvol import Volume
+    from gsvol.metrics import psnr, ssim3d
+    out = []
+    for seed, dims, dt, noise in METRIC_CASES:
+        a, b = metric_pair(seed, dims, dt, noise)
+        g = GridSpec(dims)
+        va, vb = Volume(g, a), Volume(g, b)
+        p = psnr(va, vb)
+        out.append({"seed": seed, "dims": list(dims), "dtype": dt, "noise": noise,
+                    "psnr": None if p == float("inf") else p, "ssim": ssim3d(va, vb)})
+    return out
+
+
 def full_configs():
     """Bit-exact binning hashes at BASELINE sizes + sampled forward values."""
     res = {}
@@ -178,7 +209,7 @@ def full_configs():
 
 def main():
     meta = {"versions": versions(), "generated_by": "tests/golden/make_golden.py"}
-    which = set(sys.argv[1:]) or {"sweep", "config1", "full", "fit"}
+    which = set(sys.argv[1:]) or {"sweep", "config1", "full", "fit", "metrics"}
     if "sweep" in which:
         with open(os.path.join(HERE, "sweep.json"), "w") as fh:
             json.dump({"meta": meta, "cases": sweep()}, fh)
@@ -192,6 +223,10 @@ def main():
     if "full" in which:
         with open(os.path.join(HERE, "full_configs.json"), "w") as fh:
             json.dump({"meta": meta, "configs": full_configs()}, fh)
+    if "metrics" in which:
+        with open(os.path.join(HERE, "metrics.json"), "w") as fh:
+            json.dump({"meta": meta, "cases": metrics()}, fh, indent=1)
+        print("metrics done", flush=True)
     if "fit" in which:
         with open(os.path.join(HERE, "fit_quality.json"), "w") as fh:
             json.dump({"meta": meta, **fit_quality()}, fh, indent=1)

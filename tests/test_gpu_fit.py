@@ -146,6 +146,11 @@ def test_fit_quality_matches_reference_psnr_ssim():
     assert abs(got_psnr - ref["psnr"]) <= 0.05, (got_psnr, ref["psnr"])
     assert abs(got_ssim - ref["ssim"]) <= 0.001, (got_ssim, ref["ssim"])
     assert got_psnr >= ref["trilinear_psnr"] + 2.0   # criterion 5: beats trilinear by 2 dB
+    # the device metrics give the same numbers as the host restatement
+    hr = gs.Volume(p["hr_grid"], p["hr"])
+    srv = gs.Volume(p["hr_grid"], sr)
+    assert abs(gs.psnr(srv, hr) - got_psnr) <= 1e-9
+    assert abs(gs.ssim3d(srv, hr) - got_ssim) <= 1e-12
 
 
 # --------------------------------------------------------- graph-replayed step

@@ -113,3 +113,22 @@ def test_oracle_fast_tail_equals_numpy_tail():
         assert la == lb
     for k in oracle.GROUPS:
         np.testing.assert_allclose(fa[k], fb[k], rtol=0, atol=1e-13)
+
+
+def test_oracle_metrics_match_reference_goldens():
+    """The oracle's psnr / ssim3d (metrics.py:35-77 restated) against the
+    reference's values on the seeded pairs of tests/golden/metrics.json."""
+    import math
+    for case in load_json("metrics.json")["cases"]:
+        rng = np.random.default_rng(case["seed"])
+        dims = tuple(case["dims"])
+        a = rng.uniform(0.0, 1.0, size=dims)
+        b = (np.clip(a + case["noise"] * rng.standard_normal(dims), 0.0, 1.0)
+             if case["noise"] else a.copy())
+        a, b = a.astype(case["dtype"]), b.astype(case["dtype"])
+        p = oracle.psnr(a, b)
+        if case["psnr"] is None:
+            assert math.isinf(p)
+        else:
+            assert p == case["psnr"]
+        assert oracle.ssim3d(a, b) == case["ssim"]
