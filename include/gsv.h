@@ -288,6 +288,10 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
  * no-op when *gate != 0, with bc1 = bias_corrections[2 t], bc2 =
  * bias_corrections[2 t + 1] for t = *step (the number of completed steps;
  * the table holds 1 - beta^(t+1) computed on the host like the reference).
+ * With rec32 != NULL it also writes, from the updated parameters, the next
+ * step's gsv_preprocess outputs (rec32, counts, box for grid/bricks/cutoff),
+ * so the next step's binning starts at gsv_bin_scan; when gated it writes
+ * nothing (the parameters, hence the records, are unchanged).
  * gsv_step_advance: *step += 1 unless *gate. */
 int gsv_step_gate(const double* loss_sum, const int32_t* overflow, int32_t* gate,
                   double* result, void* stream);
@@ -296,7 +300,9 @@ int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_
                             double* raw_amplitude, double* raw_relax, double* const* moments,
                             int amplitude_enabled, int relax_enabled,
                             const gsv_adam_hparams* hp, const double* bias_corrections,
-                            const int64_t* step, const int32_t* gate, void* stream);
+                            const int64_t* step, const int32_t* gate, const gsv_grid* grid,
+                            const gsv_bricks* bricks, double cutoff_sigma,
+                            gsv_record32* rec32, int32_t* counts, int32_t* box, void* stream);
 int gsv_step_advance(int64_t* step, const int32_t* gate, void* stream);
 
 /* q /= |q| per Gaussian (GaussianField.normalize_rotations, field.py:100). */

@@ -80,7 +80,8 @@ _SIGS = {
     "gsv_step_gate": [c_vp, c_vp, c_vp, c_vp, c_vp],
     "gsv_fused_update_device": [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                 ctypes.POINTER(c_vp), c_int, c_int,
-                                ctypes.POINTER(GsvAdamHparams), c_vp, c_vp, c_vp, c_vp],
+                                ctypes.POINTER(GsvAdamHparams), c_vp, c_vp, c_vp, GP, BP,
+                                c_dbl, c_vp, c_vp, c_vp, c_vp],
     "gsv_step_advance": [c_vp, c_vp, c_vp],
     "gsv_metric_blocks": [c_i64],
     "gsv_sq_diff_sum": [c_vp, c_int, c_vp, c_int, c_i64, c_vp, c_vp, c_vp],

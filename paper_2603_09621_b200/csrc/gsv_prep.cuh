@@ -1,0 +1,146 @@
+// gsv_prep.cuh -- per-Gaussian preprocessing shared by the binning pass
+// (gsv_bin.cu: preprocess_kernel) and the graph step's fused optimizer tail
+// (gsv_train.cu: tail_kernel<PREP>), which writes the next step's records
+// straight from the updated parameters.
+//
+// Replaces _whitening_factors (raster.py:233-237), the sigmoid activations
+// (field.py:86-94) and the AABB part of build_brick_index (raster.py:160-198).
+// Every f64 operation that feeds a binning decision is an explicit _rn
+// intrinsic (or a libm call / exact scaling), so the result does not depend
+// on the translation unit's contraction flags.
+#pragma once
+
+#include "gsv_common.cuh"
+
+namespace gsv {
+
+// numpy float64 -> int64 cast on x86-64 (cvttsd2si / vcvttpd2qq): truncation,
+// with NaN and out-of-range values mapping to INT64_MIN.
+__device__ __forceinline__ int64_t np_to_int64(double x) {
+  if (!(x > -9.2233720368547758e18 && x < 9.2233720368547758e18)) return INT64_MIN;
+  return (int64_t)x;
+}
+
+__device__ __forceinline__ int64_t clip64(int64_t v, int64_t lo, int64_t hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+struct PrepArgs {
+  gsv_grid g;
+  gsv_bricks k;
+  double cutoff;
+  int dense;           // cutoff = inf: every Gaussian in every brick
+  int relax_enabled;
+  gsv_record32* rec32;
+  gsv_record64* rec64;  // optional (f64 engine)
+  int32_t* counts;
+  int32_t* box;
+};
+
+// Records, pair count and slab-clipped brick box of Gaussian i from its
+// (position, log-scales, unit quaternion, raw amplitude, raw relax).
+__device__ __forceinline__ void preprocess_one(int64_t i, const double p[3], const double l[3],
+                                               const double q[4], double ra, double rr,
+                                               const PrepArgs& pa) {
+  double R[9];
+  rotation_f64(q, R);
+  const double inv_s[3] = {exp(-l[0]), exp(-l[1]), exp(-l[2])};
+  double L[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) L[3 * a + b] = mul(inv_s[a], R[3 * b + a]);
+  const double A = expit_f64(ra);
+  const double r = pa.relax_enabled ? expit_f64(rr) : 1.0;
+
+  // Marginal variance Sigma_kk = einsum("nkm,nm->nk", R*R, exp(2 ls)); numpy
+  // 2.3 reduces the length-3 axis as (p0 + p2) + p1 (SURVEY.md §0 finding 2).
+  const double var[3] = {exp(mul(2.0, l[0])), exp(mul(2.0, l[1])), exp(mul(2.0, l[2]))};
+  double half[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double p0 = mul(mul(R[3 * a + 0], R[3 * a + 0]), var[0]);
+    const double p1 = mul(mul(R[3 * a + 1], R[3 * a + 1]), var[1]);
+    const double p2 = mul(mul(R[3 * a + 2], R[3 * a + 2]), var[2]);
+    const double skk = add(add(p0, p2), p1);
+    half[a] = pa.dense ? __longlong_as_double(0x7ff0000000000000ULL) : mul(pa.cutoff, sqrt(skk));
+  }
+
+  gsv_record32 o;
+#pragma unroll
+  for (int a = 0; a < 9; ++a) o.l[a] = (float)L[a];
+  o.amp = (float)A;
+  o.relax = (float)r;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) o.half[a] = (float)half[a];
+  // 1/sigma_max^2 = lambda_min(L^T L): d2 >= |p - mu|^2 / sigma_max^2, the
+  // forward's sphere-vs-tile culling bound.
+  o.inv_smax2 = (float)exp(-2.0 * fmax(l[0], fmax(l[1], l[2])));
+  o._pad = 0.f;
+  {
+    float4* dst = reinterpret_cast<float4*>(pa.rec32 + i);
+    const float4* src = reinterpret_cast<const float4*>(&o);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) dst[a] = src[a];
+  }
+  if (pa.rec64) {
+    gsv_record64 d;
+#pragma unroll
+    for (int a = 0; a < 9; ++a) d.l[a] = L[a];
+    d.amp = A;
+    d.relax = r;
+    d._pad = 0.0;
+    pa.rec64[i] = d;
+  }
+
+  // ---- brick box (raster.py:160-198), clipped to the slab [bz0, bz1).
+  const gsv_grid& g = pa.g;
+  const gsv_bricks& k = pa.k;
+  const int dims[3] = {g.nx, g.ny, g.nz};
+  const int bd[3] = {k.bdx, k.bdy, k.bdz};
+  const int bg[3] = {k.bgx, k.bgy, k.bgz};
+  int64_t blo[3], bhi[3];
+  bool inside = true;
+  if (pa.dense) {
+    // cutoff = inf: every Gaussian in every brick (raster.py:166-171).
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      blo[a] = 0;
+      bhi[a] = bg[a] - 1;
+    }
+  } else {
+    const double org[3] = {g.ox, g.oy, g.oz};
+    const double spc[3] = {g.sx, g.sy, g.sz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double glo = __ddiv_rn(sub(sub(p[a], half[a]), org[a]), spc[a]);
+      const double ghi = __ddiv_rn(sub(add(p[a], half[a]), org[a]), spc[a]);
+      int64_t vlo = np_to_int64(ceil(sub(glo, 0.5)));
+      int64_t vhi = np_to_int64(floor(add(ghi, 0.5)));
+      vlo = clip64(vlo, 0, dims[a] - 1);
+      vhi = clip64(vhi, 0, dims[a] - 1);
+      inside = inside && (ghi >= -0.5) && (glo <= (double)dims[a] - 0.5);
+      blo[a] = vlo / bd[a];
+      bhi[a] = vhi / bd[a];
+    }
+  }
+  // z-slab clip: the slab owns brick layers [bz0, bz1).
+  if (blo[2] < k.bz0) blo[2] = k.bz0;
+  if (bhi[2] > k.bz1 - 1) bhi[2] = k.bz1 - 1;
+  int64_t cnt = 0;
+  int nb[3] = {0, 0, 0};
+  if (inside && bhi[2] >= blo[2]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) nb[a] = (int)(bhi[a] - blo[a] + 1);
+    cnt = (int64_t)nb[0] * nb[1] * nb[2];
+  }
+  pa.counts[i] = (int32_t)cnt;
+  int4 bx;
+  bx.x = (int)(blo[0] & 0xFFFF) | ((int)(blo[1] & 0xFFFF) << 16);
+  bx.y = (int)(blo[2] & 0xFFFF) | ((nb[0] & 0xFFFF) << 16);
+  bx.z = (nb[1] & 0xFFFF) | ((nb[2] & 0xFFFF) << 16);
+  bx.w = 0;
+  reinterpret_cast<int4*>(pa.box)[i] = bx;
+}
+
+}  // namespace gsv

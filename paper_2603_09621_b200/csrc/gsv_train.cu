@@ -8,7 +8,7 @@
 //   adam_kernel       step_optimizer (optimize.py:127-148), numpy operand order
 //   normalize_kernel  GaussianField.normalize_rotations (field.py:100-102)
 // f64 throughout; reductions are fixed-order (bit-reproducible).
-#include "gsv_common.cuh"
+#include "gsv_prep.cuh"
 
 namespace gsv {
 namespace {
@@ -347,12 +347,16 @@ __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
 constexpr int kTailThreads = 128;
 constexpr int kTailSub = 512;   // pairs per smem sub-chunk (24 KB)
 
-__global__ void __launch_bounds__(kTailThreads, 6)
+// PREP (graph step): also write the next step's records, pair count and
+// brick box from the updated parameters (preprocess_one), replacing the
+// binning pass's separate preprocess of the whole field.
+template <bool PREP>
+__global__ void __launch_bounds__(kTailThreads, PREP ? 5 : 6)
 tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gstart,
             const double* __restrict__ gsum, int64_t n, double* __restrict__ pos,
             double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
             double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
-            const gsv_adam_hparams h, StepDev sd) {
+            const gsv_adam_hparams h, StepDev sd, PrepArgs pa) {
   __shared__ float4 sp[kTailSub * 3];
   if (sd.gate != nullptr && *sd.gate != 0) return;   // overflow / non-finite loss: no update
   const int64_t i0 = blockIdx.x * (int64_t)kTailThreads;
@@ -420,15 +424,18 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
     bc2 = sd.bc[2 * t + 1];
   }
 #pragma unroll
+  double pn[3], ln[3], qn[4];
   for (int a = 0; a < 3; ++a) {
     double m = mv[0][3 * i + a], v = mv[5][3 * i + a];
-    pos[3 * i + a] = adam_one(pos[3 * i + a], m, v, g[a], h.lr[0], h.b1, h.b2, h.eps, bc1, bc2);
+    pn[a] = adam_one(pos[3 * i + a], m, v, g[a], h.lr[0], h.b1, h.b2, h.eps, bc1, bc2);
+    pos[3 * i + a] = pn[a];
     mv[0][3 * i + a] = m; mv[5][3 * i + a] = v;
   }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double m = mv[1][3 * i + a], v = mv[6][3 * i + a];
-    ls[3 * i + a] = adam_one(ls[3 * i + a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, bc1, bc2);
+    ln[a] = adam_one(ls[3 * i + a], m, v, g[3 + a], h.lr[1], h.b1, h.b2, h.eps, bc1, bc2);
+    ls[3 * i + a] = ln[a];
     mv[1][3 * i + a] = m; mv[6][3 * i + a] = v;
   }
   double q[4];
@@ -441,17 +448,24 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
   const double nrm = sqrt(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
                               mul(q[3], q[3])));
 #pragma unroll
-  for (int a = 0; a < 4; ++a) rot[4 * i + a] = __ddiv_rn(q[a], nrm);
+  for (int a = 0; a < 4; ++a) {
+    qn[a] = __ddiv_rn(q[a], nrm);
+    rot[4 * i + a] = qn[a];
+  }
+  double ran = ra[i], rrn = rr[i];
   if (amp_en) {
     double m = mv[3][i], v = mv[8][i];
-    ra[i] = adam_one(ra[i], m, v, g[10], h.lr[3], h.b1, h.b2, h.eps, bc1, bc2);
+    ran = adam_one(ran, m, v, g[10], h.lr[3], h.b1, h.b2, h.eps, bc1, bc2);
+    ra[i] = ran;
     mv[3][i] = m; mv[8][i] = v;
   }
   if (relax_en) {
     double m = mv[4][i], v = mv[9][i];
-    rr[i] = adam_one(rr[i], m, v, g[11], h.lr[4], h.b1, h.b2, h.eps, bc1, bc2);
+    rrn = adam_one(rrn, m, v, g[11], h.lr[4], h.b1, h.b2, h.eps, bc1, bc2);
+    rr[i] = rrn;
     mv[4][i] = m; mv[9][i] = v;
   }
+  if (PREP) preprocess_one(i, pn, ln, qn, ran, rrn, pa);
 }
 
 }  // namespace
@@ -547,10 +561,10 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
   for (int k = 0; k < 10; ++k) mv.p[k] = moments[k];
   if (precision == 0 && grad_scratch == nullptr) {
     // one pass: staged merge + chain rule + Adam + renorm
-    tail_kernel<<<(unsigned)((n + kTailThreads - 1) / kTailThreads), kTailThreads, 0, s>>>(
+    tail_kernel<false><<<(unsigned)((n + kTailThreads - 1) / kTailThreads), kTailThreads, 0, s>>>(
         (const float*)partials, gstart, gsum, n, positions, log_scales, rotations,
         raw_amplitude, raw_relax, mv, amplitude_enabled, relax_enabled, *hp,
-        StepDev{nullptr, nullptr, nullptr});
+        StepDev{nullptr, nullptr, nullptr}, PrepArgs{});
     GSV_CHECK_LAUNCH("tail_kernel");
     return GSV_OK;
   }
@@ -585,16 +599,31 @@ int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_
                             double* raw_amplitude, double* raw_relax, double* const* moments,
                             int amplitude_enabled, int relax_enabled,
                             const gsv_adam_hparams* hp, const double* bias_corrections,
-                            const int64_t* step, const int32_t* gate, void* stream) {
+                            const int64_t* step, const int32_t* gate, const gsv_grid* grid,
+                            const gsv_bricks* bricks, double cutoff_sigma,
+                            gsv_record32* rec32, int32_t* counts, int32_t* box, void* stream) {
   GSV_REQUIRE(hp && moments && partials && gstart && bias_corrections && step && gate,
               "null pointer argument");
+  GSV_REQUIRE(rec32 == nullptr || (grid && bricks && counts && box && cutoff_sigma > 0),
+              "records need grid, bricks, counts, box and a positive cutoff");
   if (n <= 0) return GSV_OK;
   cudaStream_t s = as_stream(stream);
   MomentPtrs mv;
   for (int k = 0; k < 10; ++k) mv.p[k] = moments[k];
-  tail_kernel<<<(unsigned)((n + kTailThreads - 1) / kTailThreads), kTailThreads, 0, s>>>(
-      partials, gstart, nullptr, n, positions, log_scales, rotations, raw_amplitude, raw_relax,
-      mv, amplitude_enabled, relax_enabled, *hp, StepDev{gate, bias_corrections, step});
+  const unsigned blocks = (unsigned)((n + kTailThreads - 1) / kTailThreads);
+  const StepDev sd{gate, bias_corrections, step};
+  if (rec32 != nullptr) {
+    if (int st = validate_grid_bricks(grid, bricks)) return st;
+    const PrepArgs pa{*grid, *bricks, cutoff_sigma, isinf(cutoff_sigma) ? 1 : 0, relax_enabled,
+                      rec32, nullptr, counts, box};
+    tail_kernel<true><<<blocks, kTailThreads, 0, s>>>(
+        partials, gstart, nullptr, n, positions, log_scales, rotations, raw_amplitude,
+        raw_relax, mv, amplitude_enabled, relax_enabled, *hp, sd, pa);
+  } else {
+    tail_kernel<false><<<blocks, kTailThreads, 0, s>>>(
+        partials, gstart, nullptr, n, positions, log_scales, rotations, raw_amplitude,
+        raw_relax, mv, amplitude_enabled, relax_enabled, *hp, sd, PrepArgs{});
+  }
   GSV_CHECK_LAUNCH("tail_kernel");
   return GSV_OK;
 }

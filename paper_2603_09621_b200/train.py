@@ -309,6 +309,7 @@ class _StepGraph:
         self.cap = cap
         self.t_max = t_max           # largest state.t the bias table covers
         self.t_synced = -1
+        self.prep_version = -1
         self.graph = None
         self.bufs: dict = {}
 
@@ -340,11 +341,8 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
     grid, opts, n = self.grid, self.opts, f.count
     gr, br = _lib.make_grid(grid), b["bricks"]
     cap = g.cap
-    _lib.check(lib.gsv_preprocess(
-        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
-        f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), n, int(f.relax_enabled),
-        float(opts.cutoff_sigma), gr, br, b["rec32"].data_ptr(), None, b["counts"].data_ptr(),
-        b["box"].data_ptr(), s), "preprocess")
+    # rec32 / counts / box for this step were written by the previous replay's
+    # tail (or by _graph_preprocess): binning starts at the scan
     ws = b["ws"]
     _lib.check(lib.gsv_bin_scan(b["counts"].data_ptr(), n, b["gstart"].data_ptr(),
                                 ws.data_ptr(), ws.numel(), s), "bin_scan")
@@ -376,10 +374,23 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         b["partials"].data_ptr(), b["gstart"].data_ptr(), n, f.positions.data_ptr(),
         f.log_scales.data_ptr(), f.rotations.data_ptr(), f.raw_amplitude.data_ptr(),
         f.raw_relax.data_ptr(), b["mv"], int(f.amplitude_enabled), int(f.relax_enabled),
-        ctypes.byref(b["hp"]), b["bc"].data_ptr(), b["t"].data_ptr(), b["gate"].data_ptr(), s),
-        "fused_update_device")
+        ctypes.byref(b["hp"]), b["bc"].data_ptr(), b["t"].data_ptr(), b["gate"].data_ptr(), gr,
+        br, float(opts.cutoff_sigma), b["rec32"].data_ptr(), b["counts"].data_ptr(),
+        b["box"].data_ptr(), s), "fused_update_device")
     _lib.check(lib.gsv_step_advance(b["t"].data_ptr(), b["gate"].data_ptr(), s), "step_advance")
     b["result_host"].copy_(b["result"], non_blocking=True)
+
+
+def _graph_preprocess(self, f: GaussianField, b: dict) -> None:
+    """gsv_preprocess into the graph's buffers: before the first replay, and
+    whenever the field was changed outside the graph (version mismatch)."""
+    lib = _lib.lib()
+    _lib.check(lib.gsv_preprocess(
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), f.count, int(f.relax_enabled),
+        float(self.opts.cutoff_sigma), _lib.make_grid(self.grid), b["bricks"],
+        b["rec32"].data_ptr(), None, b["counts"].data_ptr(), b["box"].data_ptr(),
+        _lib.stream_ptr()), "preprocess")
 
 
 def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, key,
@@ -390,20 +401,24 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     grid, opts, n = self.grid, self.opts, f.count
     bricks = _lib.make_bricks(grid, self.brick_dims, self.slab)
     nb = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
-    # the exact pair count, read once per capture (never per step)
-    rec32, _, counts, box = _preprocess(f, grid, opts.cutoff_sigma, self.brick_dims, self.slab,
-                                        False, self.pool)
-    pairs = int(_scan(counts, nb, self.pool)[-1].item())
+    gp = _lib.BufferPool(dev)        # private: replays need fixed addresses
+    b = {"bricks": bricks, "nb": max(nb, 1),
+         "rec32": gp.get("rec32", (n, 16), torch.float32),
+         "counts": gp.get("counts", (n,), torch.int32),
+         "box": gp.get("box", (n, 4), torch.int32),
+         "gstart": gp.get("gstart", (n + 1,), torch.int64)}
+    # records for the first replay, and the exact pair count -- read once per
+    # capture, never per step
+    _graph_preprocess(self, f, b)
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.gsv_bin_workspace(n, 1, nb, ctypes.byref(nbytes)), "bin_workspace")
+    ws0 = _lib.workspace(nbytes.value, dev, "bin")
+    _lib.check(lib.gsv_bin_scan(b["counts"].data_ptr(), n, b["gstart"].data_ptr(),
+                                ws0.data_ptr(), ws0.numel(), _lib.stream_ptr()), "bin_scan")
+    pairs = int(b["gstart"][-1].item())
     cap = max(int(pairs * _GRAPH_HEADROOM) + 4096, min_cap, 1)
     g = _StepGraph(key, cap, state.t + _BC_CHUNK - 1)
-    b = g.bufs
-    gp = _lib.BufferPool(dev)        # private: replays need fixed addresses
-    b["bricks"] = bricks
-    b["nb"] = max(nb, 1)
-    b["rec32"] = gp.get("rec32", (n, 16), torch.float32)
-    b["counts"] = gp.get("counts", (n,), torch.int32)
-    b["box"] = gp.get("box", (n, 4), torch.int32)
-    b["gstart"] = gp.get("gstart", (n + 1,), torch.int64)
+    g.bufs = b
     nbytes = ctypes.c_size_t(0)
     _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
     b["ws"] = gp.get("ws", (nbytes.value,), torch.uint8)
@@ -448,6 +463,7 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
         _graph_body(self, f, g)
     g.graph = graph
+    g.prep_version = f.version
     return g
 
 
@@ -479,6 +495,9 @@ def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
     if g.t_synced != state.t:
         b["t"].fill_(int(state.t))
         g.t_synced = state.t
+    if g.prep_version != f.version:
+        _graph_preprocess(self, f, b)      # the field changed outside the graph
+        g.prep_version = f.version
     g.graph.replay()
     torch.cuda.current_stream(f.device).synchronize()
     loss_sum, flags = float(b["result_host"][0]), int(b["result_host"][1])
@@ -495,6 +514,7 @@ def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
     g.t_synced = state.t
     f.bump_version()
     f.bump_version()
+    g.prep_version = f.version             # the replay's tail wrote the new records
     return loss
 
 
