@@ -340,7 +340,9 @@ def run_ours(args, dist, ws, rank, local):
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         with open(tf) as fh:
-            traffic = json.load(fh).get(dom)
+            tj = json.load(fh)
+        if tj.get("config") == args.config:   # measured for this workload only
+            traffic = tj.get(dom)
     hbm_peak = 6552.0  # MEASURED_PEAKS.json (driver-written) when present
     mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(mp):

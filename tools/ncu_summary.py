@@ -46,6 +46,7 @@ def main():
     ap.add_argument("report")
     ap.add_argument("out")
     ap.add_argument("--traffic", default=None)
+    ap.add_argument("--config", type=int, default=3, help="BASELINE config the capture ran")
     args = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"],
                          capture_output=True, text=True, check=True).stdout
@@ -85,6 +86,7 @@ def main():
         fh.write("\n".join(lines) + "\n")
     if args.traffic:
         traffic["source"] = args.report.split("/")[-1]
+        traffic["config"] = args.config
         traffic["what"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, "
                            "one ncu --set full capture (tools/kbench.py, config 3 LR)")
         with open(args.traffic, "w") as fh:
