@@ -990,7 +990,6 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
   __shared__ unsigned short sorder[kBwdMChunk];
   __shared__ unsigned short scost[kBwdMChunk];
   __shared__ int shist[kBwdBuckets];
-  __shared__ int snext;
   const int lb = blockIdx.x;
   const int b = (int)slab_first(k) + lb;
   const int64_t lbeg = starts[lb], lend = starts[lb + 1];
@@ -1036,17 +1035,18 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
   for (int64_t cbase = lbeg; cbase < lend; cbase += kBwdMChunk) {
     const int cnt = (int)min((int64_t)kBwdMChunk, lend - cbase);
     if (tid < kBwdBuckets) shist[tid] = 0;
-    if (tid == 0) snext = 0;
     __syncthreads();
-    // (1) cost = live voxels of the pair
+    // (1) cost = live voxels of the pair; 4 pairs' loads in flight per thread
+#pragma unroll 4
     for (int t = tid; t < cnt; t += kBwdThreads) {
       const int64_t jt = cbase + t;
       const uint2 a0 = load_plane(masks, 0, jt), a1 = load_plane(masks, 1, jt),
                   a2 = load_plane(masks, 2, jt), a3 = load_plane(masks, 3, jt);
+      const int gj = __ldg(gids + jt);
       const int c = __popc(a0.x) + __popc(a0.y) + __popc(a1.x) + __popc(a1.y) + __popc(a2.x) +
                     __popc(a2.y) + __popc(a3.x) + __popc(a3.y);
       scost[t] = (unsigned short)c;
-      sgid[t] = __ldg(gids + jt);
+      sgid[t] = gj;
       atomicAdd(&shist[kBwdBuckets - 1 - min(c, kBwdBuckets - 1)], 1);
     }
     __syncthreads();
@@ -1072,12 +1072,10 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
     }
     __syncthreads();
     // (3) warps pull groups; each lane walks its pair's live voxels
+    // groups of 32 pairs of similar cost (heaviest first), dealt round-robin
+    // to the warps: balanced without a work queue
     const int ngroups = (cnt + 31) >> 5;
-    for (;;) {
-      int grp = 0;
-      if (lane == 0) grp = atomicAdd(&snext, 1);
-      grp = __shfl_sync(kFull, grp, 0);
-      if (grp >= ngroups) break;
+    for (int grp = tid >> 5; grp < ngroups; grp += kBwdThreads / 32) {
       const int s = (grp << 5) + lane;
       if (s >= cnt) continue;
       const int t = sorder[s];

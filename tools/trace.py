@@ -28,11 +28,12 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--hr", action="store_true", help="trace the HR render instead")
+    ap.add_argument("--grid512", action="store_true", help="HR render at config 5's 512^3")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     p = synth.make_problem(synth.CONFIGS[args.config])
     f = gs.GaussianField(*p["field"])
-    if args.hr:
+    if args.hr or args.grid512:
         rend = gs.Renderer(p["render_grid"], gs.RenderOptions(), (8, 8, 4))
         run = lambda: rend(f)  # noqa: E731
     else:
