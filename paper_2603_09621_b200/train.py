@@ -18,6 +18,7 @@ chain rule and Adam step, so parameters stay replicated.
 
 from __future__ import annotations
 
+import math
 import os
 from dataclasses import dataclass
 
@@ -235,7 +236,8 @@ def _adam_launch(f: GaussianField, state, lrs: dict, beta1: float, beta2: float,
 
 
 def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
-                   beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> None:
+                   beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                   skip_nonfinite: bool = False) -> None:
     """Backward + fused optimizer tail of one fit() iteration: pair partials ->
     [merge -> all_reduce when sharded] -> chain rule -> Adam -> renorm, without
     materialising a GradientBuffer (the public backward/step_optimizer path
@@ -254,6 +256,9 @@ def _update_method(self, f: GaussianField, out: StepOutput, state, lrs: dict,
         red = self._reduce_buffer(gsum, out)
         dist.all_reduce(red, group=self.group)
         self._unpack_reduced(red, gsum, out)
+        if skip_nonfinite and not math.isfinite(out.loss()):
+            self._mark(None)           # the global loss is known only now: no update
+            return
         self._mark("update")
         _adam_launch(f, state, lrs, beta1, beta2, eps, None, None, gsum, opts.precision_code,
                      self.pool)
@@ -479,9 +484,13 @@ def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
     buffers, target, hyper-parameters or pair capacity change.  Elsewhere
     (sharded, f64) it runs forward() + update() eagerly.
     """
-    import math
     if not _graph_supported(self):
         out = self.forward(f)
+        if self.sharded:
+            # the global loss rides the step's one all_reduce, inside update():
+            # it is checked there, before Adam
+            self.update(f, out, state, lrs, beta1, beta2, eps, skip_nonfinite=True)
+            return out.loss()
         loss = out.loss()
         if math.isfinite(loss):
             self.update(f, out, state, lrs, beta1, beta2, eps)
