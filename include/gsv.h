@@ -295,7 +295,8 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
  * gsv_step_advance: *step += 1 unless *gate. */
 int gsv_step_gate(const double* loss_sum, const int32_t* overflow, int32_t* gate,
                   double* result, void* stream);
-int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_t n,
+int gsv_fused_update_device(const float* partials, const int64_t* gstart, const double* gsum,
+                            int64_t n,
                             double* positions, double* log_scales, double* rotations,
                             double* raw_amplitude, double* raw_relax, double* const* moments,
                             int amplitude_enabled, int relax_enabled,
@@ -304,6 +305,17 @@ int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_
                             const gsv_bricks* bricks, double cutoff_sigma,
                             gsv_record32* rec32, int32_t* counts, int32_t* box, void* stream);
 int gsv_step_advance(int64_t* step, const int32_t* gate, void* stream);
+
+/* Sharded graph step: the one all_reduce buffer red (N x 12
+ * float) = the merged per-Gaussian partials gsum (gsv_merge, N x 12 double)
+ * with this rank's loss sum in red[11] and its capacity overflow flag in
+ * red[23]; after the all_reduce, gsv_shard_unpack restores gsum (double, the
+ * two slots zeroed), the global loss sum and the global overflow flag (any
+ * rank).  gsv_fused_update_device then takes gsum instead of partials. */
+int gsv_shard_pack(const double* gsum, int64_t n, const double* loss_sum,
+                   const int32_t* overflow, float* red, void* stream);
+int gsv_shard_unpack(const float* red, int64_t n, double* gsum, double* loss_sum,
+                     int32_t* overflow, void* stream);
 
 /* q /= |q| per Gaussian (GaussianField.normalize_rotations, field.py:100). */
 int gsv_normalize_rotations(double* rotations, int64_t n, void* stream);

@@ -78,7 +78,9 @@ _SIGS = {
                          ctypes.POINTER(c_vp), c_int, c_int, ctypes.POINTER(GsvAdamHparams),
                          c_vp, c_vp],
     "gsv_step_gate": [c_vp, c_vp, c_vp, c_vp, c_vp],
-    "gsv_fused_update_device": [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+    "gsv_shard_pack": [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "gsv_shard_unpack": [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "gsv_fused_update_device": [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                 ctypes.POINTER(c_vp), c_int, c_int,
                                 ctypes.POINTER(GsvAdamHparams), c_vp, c_vp, c_vp, GP, BP,
                                 c_dbl, c_vp, c_vp, c_vp, c_vp],

@@ -332,6 +332,37 @@ __global__ void advance_kernel(int64_t* __restrict__ t, const int32_t* __restric
   if (*gate == 0) *t += 1;
 }
 
+// Sharded graph step: the one all_reduce carries the merged partials (f32,
+// N x 12; column 11 is free), this rank's loss in [0][11] and its capacity
+// overflow flag in [1][11].
+__global__ void shard_pack_kernel(const double* __restrict__ gsum, int64_t n12,
+                                  const double* __restrict__ loss_sum,
+                                  const int32_t* __restrict__ overflow, float* __restrict__ red) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n12) return;
+  float v = (float)gsum[i];
+  if (i == 11) v = (float)*loss_sum;
+  if (i == 23) v = *overflow != 0 ? 1.f : 0.f;
+  red[i] = v;
+}
+
+__global__ void shard_unpack_kernel(const float* __restrict__ red, int64_t n12,
+                                    double* __restrict__ gsum, double* __restrict__ loss_sum,
+                                    int32_t* __restrict__ overflow) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n12) return;
+  const float v = red[i];
+  if (i == 11) {
+    *loss_sum = (double)v;
+    gsum[i] = 0.0;
+  } else if (i == 23) {
+    *overflow = v > 0.f ? 1 : 0;
+    gsum[i] = 0.0;
+  } else {
+    gsum[i] = (double)v;
+  }
+}
+
 // Bulk L2 prefetch of a contiguous range (TMA unit; a hint, no registers or
 // shared memory): the address is rounded down and the size to 16 B.
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
@@ -594,7 +625,30 @@ int gsv_step_gate(const double* loss_sum, const int32_t* overflow, int32_t* gate
   return GSV_OK;
 }
 
-int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_t n,
+int gsv_shard_pack(const double* gsum, int64_t n, const double* loss_sum, const int32_t* overflow,
+                   float* red, void* stream) {
+  GSV_REQUIRE(gsum && loss_sum && overflow && red, "null pointer argument");
+  GSV_REQUIRE(n >= 2, "the sharded reduce buffer needs N >= 2 Gaussians");
+  const int64_t n12 = 12 * n;
+  shard_pack_kernel<<<(unsigned)((n12 + 255) / 256), 256, 0, as_stream(stream)>>>(
+      gsum, n12, loss_sum, overflow, red);
+  GSV_CHECK_LAUNCH("shard_pack_kernel");
+  return GSV_OK;
+}
+
+int gsv_shard_unpack(const float* red, int64_t n, double* gsum, double* loss_sum,
+                     int32_t* overflow, void* stream) {
+  GSV_REQUIRE(gsum && loss_sum && overflow && red, "null pointer argument");
+  GSV_REQUIRE(n >= 2, "the sharded reduce buffer needs N >= 2 Gaussians");
+  const int64_t n12 = 12 * n;
+  shard_unpack_kernel<<<(unsigned)((n12 + 255) / 256), 256, 0, as_stream(stream)>>>(
+      red, n12, gsum, loss_sum, overflow);
+  GSV_CHECK_LAUNCH("shard_unpack_kernel");
+  return GSV_OK;
+}
+
+int gsv_fused_update_device(const float* partials, const int64_t* gstart, const double* gsum,
+                            int64_t n,
                             double* positions, double* log_scales, double* rotations,
                             double* raw_amplitude, double* raw_relax, double* const* moments,
                             int amplitude_enabled, int relax_enabled,
@@ -602,8 +656,8 @@ int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_
                             const int64_t* step, const int32_t* gate, const gsv_grid* grid,
                             const gsv_bricks* bricks, double cutoff_sigma,
                             gsv_record32* rec32, int32_t* counts, int32_t* box, void* stream) {
-  GSV_REQUIRE(hp && moments && partials && gstart && bias_corrections && step && gate,
-              "null pointer argument");
+  GSV_REQUIRE(hp && moments && bias_corrections && step && gate, "null pointer argument");
+  GSV_REQUIRE(gsum != nullptr || (partials && gstart), "need gsum or partials + gstart");
   GSV_REQUIRE(rec32 == nullptr || (grid && bricks && counts && box && cutoff_sigma > 0),
               "records need grid, bricks, counts, box and a positive cutoff");
   if (n <= 0) return GSV_OK;
@@ -617,11 +671,11 @@ int gsv_fused_update_device(const float* partials, const int64_t* gstart, int64_
     const PrepArgs pa{*grid, *bricks, cutoff_sigma, isinf(cutoff_sigma) ? 1 : 0, relax_enabled,
                       rec32, nullptr, counts, box};
     tail_kernel<true><<<blocks, kTailThreads, 0, s>>>(
-        partials, gstart, nullptr, n, positions, log_scales, rotations, raw_amplitude,
+        partials, gstart, gsum, n, positions, log_scales, rotations, raw_amplitude,
         raw_relax, mv, amplitude_enabled, relax_enabled, *hp, sd, pa);
   } else {
     tail_kernel<false><<<blocks, kTailThreads, 0, s>>>(
-        partials, gstart, nullptr, n, positions, log_scales, rotations, raw_amplitude,
+        partials, gstart, gsum, n, positions, log_scales, rotations, raw_amplitude,
         raw_relax, mv, amplitude_enabled, relax_enabled, *hp, sd, PrepArgs{});
   }
   GSV_CHECK_LAUNCH("tail_kernel");

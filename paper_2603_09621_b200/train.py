@@ -112,7 +112,9 @@ class TrainStep:
 
     @property
     def sharded(self) -> bool:
-        return self.group is not None and self.world_size > 1
+        """A process group was given: the step all_reduces over it (also at
+        world size 1, where the reduction is the identity)."""
+        return self.group is not None
 
     def set_target(self, target_linear: torch.Tensor) -> None:
         """Load a new target volume (linear x-fastest, V values) into the step's
@@ -329,8 +331,18 @@ def _graph_key(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps):
 
 
 def _graph_supported(self) -> bool:
+    if self.sharded:
+        # the all_reduce is captured too: NCCL collectives are graph-capturable
+        import torch.distributed as dist
+        try:
+            if dist.get_backend(self.group) != "nccl":
+                return False
+        except (RuntimeError, ValueError):
+            return False
+        if os.environ.get("GSV_NO_SHARD_GRAPH"):
+            return False
     bd = self.brick_dims
-    return (not self.sharded and self.opts.precision == "f32"
+    return (self.opts.precision == "f32"
             and _masks_fit(bd, _resolve_vpl(bd))
             and not os.environ.get("GSV_NO_GRAPH") and not os.environ.get("GSV_NO_LIVE_MASKS")
             and not os.environ.get("GSV_TAIL_SPLIT"))
@@ -367,16 +379,39 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         b["vpl"], s), "forward")
     _lib.check(lib.gsv_sum(b["loss_part"].data_ptr(), b["nb"], b["loss_sum"].data_ptr(), s),
                "sum")
-    _lib.check(lib.gsv_step_gate(b["loss_sum"].data_ptr(), b["overflow"].data_ptr(),
-                                 b["gate"].data_ptr(), b["result"].data_ptr(), s), "step_gate")
+    if not self.sharded:
+        _lib.check(lib.gsv_step_gate(b["loss_sum"].data_ptr(), b["overflow"].data_ptr(),
+                                     b["gate"].data_ptr(), b["result"].data_ptr(), s),
+                   "step_gate")
     _lib.check(lib.gsv_backward(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(),
         b["gstart"].data_ptr(), b["box"].data_ptr(), gr, br, float(opts.cutoff_sigma), 0,
         b["ab"].data_ptr(), b["masks"].data_ptr(), b["vpl"], b["partials"].data_ptr(), s),
         "backward")
+    gsum = None
+    if self.sharded:
+        # merge this slab's pair partials per Gaussian, then the step's one
+        # collective: partials + loss + overflow flag in a single all_reduce;
+        # the gate then sees the global loss and any rank's overflow
+        import torch.distributed as dist
+        _lib.check(lib.gsv_merge(b["partials"].data_ptr(), b["gstart"].data_ptr(), n, 0,
+                                 b["gsum"].data_ptr(), s), "merge")
+        _lib.check(lib.gsv_shard_pack(b["gsum"].data_ptr(), n, b["loss_sum"].data_ptr(),
+                                      b["overflow"].data_ptr(), b["red"].data_ptr(), s),
+                   "shard_pack")
+        dist.all_reduce(b["red"], group=self.group)
+        _lib.check(lib.gsv_shard_unpack(b["red"].data_ptr(), n, b["gsum"].data_ptr(),
+                                        b["gloss"].data_ptr(), b["govf"].data_ptr(), s),
+                   "shard_unpack")
+        _lib.check(lib.gsv_step_gate(b["gloss"].data_ptr(), b["govf"].data_ptr(),
+                                     b["gate"].data_ptr(), b["result"].data_ptr(), s),
+                   "step_gate")
+        gsum = b["gsum"]
     _lib.check(lib.gsv_fused_update_device(
-        b["partials"].data_ptr(), b["gstart"].data_ptr(), n, f.positions.data_ptr(),
+        None if gsum is not None else b["partials"].data_ptr(),
+        None if gsum is not None else b["gstart"].data_ptr(), _lib.ptr(gsum), n,
+        f.positions.data_ptr(),
         f.log_scales.data_ptr(), f.rotations.data_ptr(), f.raw_amplitude.data_ptr(),
         f.raw_relax.data_ptr(), b["mv"], int(f.amplitude_enabled), int(f.relax_enabled),
         ctypes.byref(b["hp"]), b["bc"].data_ptr(), b["t"].data_ptr(), b["gate"].data_ptr(), gr,
@@ -443,6 +478,11 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     b["gate"] = gp.get("gate", (1,), torch.int32)
     b["result"] = gp.get("result", (2,), torch.float64)
     b["result_host"] = torch.zeros(2, dtype=torch.float64).pin_memory()
+    if self.sharded:
+        b["gsum"] = gp.get("gsum", (n, 12), torch.float64)
+        b["red"] = gp.get("red", (n, 12), torch.float32)
+        b["gloss"] = gp.get("gloss", (1,), torch.float64)
+        b["govf"] = gp.get("govf", (1,), torch.int32)
     b["t"] = gp.get("t", (1,), torch.int64)
     b["bc"] = _bias_corrections(beta1, beta2, state.t, _BC_CHUNK).to(dev)
     b["vpl"] = _resolve_vpl(self.brick_dims)
@@ -479,12 +519,13 @@ def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
     backward, chain rule, Adam and renormalisation.  Returns the mean loss
     (a Python float: the iteration's one device->host read).
 
-    Replays a captured CUDA graph (single GPU, f32): no host work per kernel,
-    no pair-count read.  The graph is (re)captured when the field / optimizer
-    buffers, target, hyper-parameters or pair capacity change.  Elsewhere
-    (sharded, f64) it runs forward() + update() eagerly.
+    Replays a captured CUDA graph (f32; single GPU, or sharded over an NCCL
+    group with the step's one all_reduce captured too): no host work per
+    kernel, no pair-count read.  The graph is (re)captured when the field /
+    optimizer buffers, target, hyper-parameters or pair capacity change.
+    Elsewhere (gloo groups, f64) it runs forward() + update() eagerly.
     """
-    if not _graph_supported(self):
+    if not _graph_supported(self) or (self.sharded and f.count < 2):
         out = self.forward(f)
         if self.sharded:
             # the global loss rides the step's one all_reduce, inside update():
@@ -511,10 +552,13 @@ def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
     torch.cuda.current_stream(f.device).synchronize()
     loss_sum, flags = float(b["result_host"][0]), int(b["result_host"][1])
     if flags & 1:
-        # pair capacity overflow: nothing was updated; re-bin with more room
+        # pair capacity overflow (on any rank, when sharded): nothing was
+        # updated.  Every rank re-captures -- the capture's collectives must
+        # match across ranks -- with more room where this rank overflowed.
+        local = bool(int(b["overflow"].item())) if self.sharded else True
         self._graph = None
         self._graph = _graph_capture(self, f, state, lrs, beta1, beta2, eps, key,
-                                     min_cap=int(g.cap * 1.5))
+                                     min_cap=int(g.cap * 1.5) if local else g.cap)
         return _step_method(self, f, state, lrs, beta1, beta2, eps)
     loss = loss_sum / self.grid.num_voxels
     if flags & 2:

@@ -87,3 +87,39 @@ def test_two_rank_nonfinite_loss_skips_update():
         mp.spawn(_run, args=(2, _free_port(), 1, d, True), nprocs=2, join=True)
         r = np.load(os.path.join(d, "r0.npz"))
         assert np.isnan(r["losses"][-1]) and int(r["t"]) == STEPS
+
+
+def _run_nccl(rank, world, port, cfg_id, out_dir):
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world, device_id=torch.device("cuda", 0))
+    torch.cuda.set_device(0)
+    p = make_problem(CONFIGS[cfg_id])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    st = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1",
+                        slab=slab_for_rank(lr.grid, (8, 8, 4), rank, world),
+                        process_group=dist.group.WORLD, world_size=world)
+    losses = [step.step(f, st, lrs) for _ in range(STEPS)]
+    captured = getattr(step, "_graph", None) is not None
+    np.savez(os.path.join(out_dir, "r0.npz"), losses=np.array(losses), t=st.t,
+             captured=captured, **{k: getattr(f, k).detach().cpu().numpy() for k in F})
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2])
+def test_sharded_graph_step_with_captured_nccl_all_reduce(cfg_id):
+    """The sharded step over an NCCL group replays one CUDA graph that holds
+    the all_reduce (world size 1 here: this box has one GPU, so the reduction
+    is the identity).  It equals the single-GPU step up to the f32 cast of
+    the reduced partials."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_run_nccl, args=(1, _free_port(), cfg_id, d), nprocs=1, join=True)
+        r = np.load(os.path.join(d, "r0.npz"))
+        f1, l1 = _single(cfg_id)
+        assert bool(r["captured"]) and int(r["t"]) == STEPS
+        np.testing.assert_allclose(r["losses"], l1, rtol=1e-6)
+        for k in F:
+            np.testing.assert_allclose(r[k], getattr(f1, k).cpu().numpy(), rtol=0, atol=2e-6,
+                                       err_msg=k)
