@@ -739,7 +739,7 @@ backward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                   const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
                   const __grid_constant__ gsv_grid g, gsv_bricks k, float cut2, double cut2d,
-                  const float2* __restrict__ ab, float4* __restrict__ partials, int dbg) {
+                  const float2* __restrict__ ab, float4* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char bwd_smem[];
   unsigned char* sspan = bwd_smem;                                       // kBwdSpanBytes
   uint4* smeta = reinterpret_cast<uint4*>(bwd_smem + kBwdSpanBytes);     // per pair
@@ -854,7 +854,7 @@ backward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
     }
     __syncthreads();
     // ---- (3) warps pull 32-pair groups, heaviest first
-    const int ngroups = dbg == 3 ? 0 : (cnt + 31) >> 5;
+    const int ngroups = (cnt + 31) >> 5;
     for (;;) {
       int grp = 0;
       if (lane == 0) grp = atomicAdd(snextp, 1);
@@ -1425,7 +1425,6 @@ int gsv_backward(const double* positions, const double* log_scales, const double
     const int64_t bvox = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz;
     const bool smem = bvox <= kBwdSmemVoxels;
     const size_t shm = bwd_smem_bytes(smem ? (int)bvox : 0);
-    static const int dbg = getenv("GSV_DEBUG_BWD") ? atoi(getenv("GSV_DEBUG_BWD")) : 0;
     static bool attr_set[2] = {false, false};
     if (!attr_set[smem]) {
       const int maxb = (int)bwd_smem_bytes(smem ? kBwdSmemVoxels : 0);
@@ -1439,11 +1438,11 @@ int gsv_backward(const double* positions, const double* log_scales, const double
     if (smem)
       backward32_kernel<true><<<(unsigned)nb, kBwdThreads, shm, s>>>(
           positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, gstart, box, *grid, *bricks,
-          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials, dbg);
+          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
     else
       backward32_kernel<false><<<(unsigned)nb, kBwdThreads, shm, s>>>(
           positions, ExactSrc{positions, log_scales, rotations, rec64}, rec32, starts, gids, gstart, box, *grid, *bricks,
-          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials, dbg);
+          (float)cut2d, cut2d, (const float2*)ab, (float4*)partials);
     GSV_CHECK_LAUNCH("backward32_kernel");
   } else {
     backward64_kernel<<<(unsigned)nb, kBwdThreads, 0, s>>>(

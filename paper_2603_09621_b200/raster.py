@@ -200,7 +200,6 @@ def _preprocess(f: GaussianField, grid: GridSpec, cutoff_sigma: float, brick_dim
     rec32 = _alloc(pool, "rec32", (n, 16), torch.float32, dev)
     # rec64 only for the f64 engine; the f32 engine recomputes the f64 factor
     # in its rare guard-band path
-    want64 = want64 or bool(os.environ.get("GSV_FORCE_REC64"))
     rec64 = _alloc(pool, "rec64", (n, 12), torch.float64, dev) if want64 else None
     counts = _alloc(pool, "counts", (n,), torch.int32, dev)
     box = _alloc(pool, "box", (n, 4), torch.int32, dev)
