@@ -263,3 +263,31 @@ def test_masked_backward_matches_span_backward(vpl, monkeypatch):
         b = getattr(gp, k).double().cpu().numpy().ravel()
         err = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
         assert err <= 1e-5, (k, err)
+
+
+@pytest.mark.parametrize("bd,prec", [((8, 8, 8), "f32"), ((4, 4, 4), "f32"), ((8, 8, 4), "f64"),
+                                     ((16, 8, 4), "f32")])
+def test_train_step_other_bricks_and_precision_match_public_api(bd, prec):
+    """TrainStep.step off the default path -- bricks without live masks (span
+    backward, eager step), VPL-4 tiles at partial occupancy, the f64 engine
+    (split tail) -- against build_brick_index/forward/backward/step_optimizer."""
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    opts = gs.RenderOptions(precision=prec)
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    step = gs.TrainStep(lr, opts, bd, "l1")
+    la, lb = [], []
+    for _ in range(3):
+        la.append(step.step(fa, sa, lrs))
+        idx = gs.build_brick_index(fb, lr.grid, opts, bd)
+        c = gs.forward(fb, lr.grid, idx, opts)
+        loss, dl = gs.loss_and_grad(c.volume(), lr, "l1")
+        lb.append(loss)
+        g = gs.backward(fb, lr.grid, idx, c, dl, opts)
+        gs.step_optimizer(fb, g, sb, lrs)
+        fb.normalize_rotations()
+    np.testing.assert_allclose(la, lb, rtol=1e-5 if prec == "f32" else 1e-10)
+    np.testing.assert_allclose(_pack(fa), _pack(fb), rtol=0, atol=5e-6 if prec == "f32" else 1e-9)
+    assert sa.t == sb.t == 3
