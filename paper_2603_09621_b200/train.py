@@ -287,6 +287,7 @@ TrainStep.update = _update_method
 
 # ------------------------------------------------------------ graph-replayed step
 _GRAPH_HEADROOM = 1.15       # pair capacity over the pair count seen at capture
+_RESULT_SLOTS = 4            # pinned result slots (at most 2 steps are in flight)
 _BC_CHUNK = 16384            # bias-correction table length per capture
 
 
@@ -418,7 +419,6 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         br, float(opts.cutoff_sigma), b["rec32"].data_ptr(), b["counts"].data_ptr(),
         b["box"].data_ptr(), s), "fused_update_device")
     _lib.check(lib.gsv_step_advance(b["t"].data_ptr(), b["gate"].data_ptr(), s), "step_advance")
-    b["result_host"].copy_(b["result"], non_blocking=True)
 
 
 def _graph_preprocess(self, f: GaussianField, b: dict) -> None:
@@ -477,7 +477,9 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     b["overflow"] = gp.get("overflow", (1,), torch.int32)
     b["gate"] = gp.get("gate", (1,), torch.int32)
     b["result"] = gp.get("result", (2,), torch.float64)
-    b["result_host"] = torch.zeros(2, dtype=torch.float64).pin_memory()
+    # results leave the device outside the graph, into a ring of pinned slots,
+    # so a step in flight never overwrites the one being read
+    b["result_host"] = torch.zeros((_RESULT_SLOTS, 2), dtype=torch.float64).pin_memory()
     if self.sharded:
         b["gsum"] = gp.get("gsum", (n, 12), torch.float64)
         b["red"] = gp.get("red", (n, 12), torch.float32)
@@ -509,7 +511,110 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
         _graph_body(self, f, g)
     g.graph = graph
     g.prep_version = f.version
+    b["t"].fill_(int(state.t))
+    g.t_synced = state.t
     return g
+
+
+class StepHandle:
+    """One launched fit() iteration.  ``loss()`` waits for it, commits its
+    bookkeeping (step count, field version) and returns the mean loss; a step
+    that hit the pair capacity is re-run there.  Steps are committed in launch
+    order: a step whose loss is non-finite or that overflowed applied nothing,
+    so the step queued behind it sees the same field and is gated the same
+    way (the device gate makes the one-step-ahead pipeline safe)."""
+
+    def __init__(self, step, f, state, lrs, hyper, g=None, slot=None, event=None,
+                 value=None):
+        self._step, self._f, self._state, self._lrs, self._hyper = step, f, state, lrs, hyper
+        self._g, self._slot, self._event = g, slot, event
+        self._value = value
+
+    def loss(self) -> float:
+        if self._value is not None:
+            return self._value
+        step, f, state, g = self._step, self._f, self._state, self._g
+        if step._pending and step._pending[0] is not self:
+            step._pending[0].loss()              # commit in launch order
+        self._event.synchronize()
+        step._pending.remove(self)
+        row = g.bufs["result_host"][self._slot]
+        loss_sum, flags = float(row[0]), int(row[1])
+        if flags & 1:
+            # pair capacity overflow (on any rank, when sharded): nothing was
+            # applied, by this step or by those queued behind it.  Drain them,
+            # re-capture with more room (every rank: the capture's collectives
+            # must match across ranks; more room where this rank overflowed),
+            # then run this step and the drained ones again, in launch order.
+            drained = []
+            while step._pending:
+                p = step._pending.pop(0)
+                p._event.synchronize()
+                drained.append(p)
+            if step._graph is g:
+                b = g.bufs
+                local = bool(int(b["overflow"].item())) if step.sharded else True
+                step._graph = None
+                step._graph = _graph_capture(step, f, state, self._lrs, *self._hyper, g.key,
+                                             min_cap=int(g.cap * 1.5) if local else g.cap)
+            self._value = _step_launch(step, f, state, self._lrs, *self._hyper).loss()
+            for p in drained:
+                p._value = _step_launch(step, p._f, p._state, p._lrs, *p._hyper).loss()
+            return self._value
+        loss = loss_sum / step.grid.num_voxels
+        if not flags & 2:                        # applied (finite loss)
+            state.t += 1
+            g.t_synced = state.t
+            f.bump_version()
+            f.bump_version()
+            g.prep_version = f.version           # the replay's tail wrote the new records
+        self._value = loss
+        return loss
+
+
+def _step_launch(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
+                 beta2: float = 0.999, eps: float = 1e-8) -> StepHandle:
+    """Enqueue one whole fit() iteration (see _step_method) and return its
+    handle without waiting.  Graph path only asynchronous; elsewhere the step
+    runs to completion and the handle is already resolved."""
+    hyper = (beta1, beta2, eps)
+    if not _graph_supported(self) or (self.sharded and f.count < 2):
+        out = self.forward(f)
+        if self.sharded:
+            # the global loss rides the step's one all_reduce, inside update():
+            # it is checked there, before Adam
+            self.update(f, out, state, lrs, beta1, beta2, eps, skip_nonfinite=True)
+            return StepHandle(self, f, state, lrs, hyper, value=out.loss())
+        loss = out.loss()
+        if math.isfinite(loss):
+            self.update(f, out, state, lrs, beta1, beta2, eps)
+        return StepHandle(self, f, state, lrs, hyper, value=loss)
+    pending = self.__dict__.setdefault("_pending", [])
+    key = _graph_key(self, f, state, lrs, beta1, beta2, eps)
+    g = getattr(self, "_graph", None)
+    if g is None or g.key != key or state.t > g.t_max:
+        while pending:                           # captures start from committed state
+            pending[0].loss()
+        self._graph = None
+        g = self._graph = _graph_capture(self, f, state, lrs, beta1, beta2, eps, key)
+    b = g.bufs
+    if not pending:
+        # the field / step count were changed outside the graph
+        if g.t_synced != state.t:
+            b["t"].fill_(int(state.t))
+            g.t_synced = state.t
+        if g.prep_version != f.version:
+            _graph_preprocess(self, f, b)
+            g.prep_version = f.version
+    g.graph.replay()
+    slot = self.__dict__.get("_launches", 0) % _RESULT_SLOTS
+    self._launches = self.__dict__.get("_launches", 0) + 1
+    b["result_host"][slot].copy_(b["result"], non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(f.device))
+    h = StepHandle(self, f, state, lrs, hyper, g=g, slot=slot, event=ev)
+    pending.append(h)
+    return h
 
 
 def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
@@ -524,54 +629,14 @@ def _step_method(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
     kernel, no pair-count read.  The graph is (re)captured when the field /
     optimizer buffers, target, hyper-parameters or pair capacity change.
     Elsewhere (gloo groups, f64) it runs forward() + update() eagerly.
+    ``step_async`` is the same iteration without the wait (one step can be
+    queued behind another; see StepHandle).
     """
-    if not _graph_supported(self) or (self.sharded and f.count < 2):
-        out = self.forward(f)
-        if self.sharded:
-            # the global loss rides the step's one all_reduce, inside update():
-            # it is checked there, before Adam
-            self.update(f, out, state, lrs, beta1, beta2, eps, skip_nonfinite=True)
-            return out.loss()
-        loss = out.loss()
-        if math.isfinite(loss):
-            self.update(f, out, state, lrs, beta1, beta2, eps)
-        return loss
-    key = _graph_key(self, f, state, lrs, beta1, beta2, eps)
-    g = getattr(self, "_graph", None)
-    if g is None or g.key != key or state.t > g.t_max:
-        self._graph = None
-        g = self._graph = _graph_capture(self, f, state, lrs, beta1, beta2, eps, key)
-    b = g.bufs
-    if g.t_synced != state.t:
-        b["t"].fill_(int(state.t))
-        g.t_synced = state.t
-    if g.prep_version != f.version:
-        _graph_preprocess(self, f, b)      # the field changed outside the graph
-        g.prep_version = f.version
-    g.graph.replay()
-    torch.cuda.current_stream(f.device).synchronize()
-    loss_sum, flags = float(b["result_host"][0]), int(b["result_host"][1])
-    if flags & 1:
-        # pair capacity overflow (on any rank, when sharded): nothing was
-        # updated.  Every rank re-captures -- the capture's collectives must
-        # match across ranks -- with more room where this rank overflowed.
-        local = bool(int(b["overflow"].item())) if self.sharded else True
-        self._graph = None
-        self._graph = _graph_capture(self, f, state, lrs, beta1, beta2, eps, key,
-                                     min_cap=int(g.cap * 1.5) if local else g.cap)
-        return _step_method(self, f, state, lrs, beta1, beta2, eps)
-    loss = loss_sum / self.grid.num_voxels
-    if flags & 2:
-        return loss                      # non-finite: no update, like the reference
-    state.t += 1
-    g.t_synced = state.t
-    f.bump_version()
-    f.bump_version()
-    g.prep_version = f.version             # the replay's tail wrote the new records
-    return loss
+    return _step_launch(self, f, state, lrs, beta1, beta2, eps).loss()
 
 
 TrainStep.step = _step_method
+TrainStep.step_async = _step_launch
 
 
 class Renderer:

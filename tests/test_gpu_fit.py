@@ -291,3 +291,44 @@ def test_train_step_other_bricks_and_precision_match_public_api(bd, prec):
     np.testing.assert_allclose(la, lb, rtol=1e-5 if prec == "f32" else 1e-10)
     np.testing.assert_allclose(_pack(fa), _pack(fb), rtol=0, atol=5e-6 if prec == "f32" else 1e-9)
     assert sa.t == sb.t == 3
+
+
+def test_pipelined_steps_recover_from_overflow_and_match_eager(monkeypatch):
+    """step_async with one step queued ahead (fit()'s loop): a capacity
+    overflow in the first step gates it and the queued step; both re-run on
+    a larger capture, and the field equals the eager step's bit for bit."""
+    import paper_2603_09621_b200.train as train_mod
+    real = train_mod._graph_capture
+    calls = []
+
+    def tiny_first(self, f, state, lrs, b1, b2, eps, key, min_cap=0):
+        calls.append(min_cap)
+        if len(calls) == 1:
+            monkeypatch.setattr(train_mod, "_GRAPH_HEADROOM", 0.25)
+            try:
+                return real(self, f, state, lrs, b1, b2, eps, key, min_cap)
+            finally:
+                monkeypatch.setattr(train_mod, "_GRAPH_HEADROOM", 1.15)
+        return real(self, f, state, lrs, b1, b2, eps, key, min_cap)
+
+    monkeypatch.setattr(train_mod, "_graph_capture", tiny_first)
+    p = make_problem(CONFIGS[2])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    ea = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    eb = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    la = []
+    for _ in range(4):
+        out = ea.forward(fa)
+        la.append(out.loss())
+        ea.update(fa, out, sa, lrs)
+    lb, h = [], eb.step_async(fb, sb, lrs)
+    for i in range(4):
+        nxt = eb.step_async(fb, sb, lrs) if i + 1 < 4 else None
+        lb.append(h.loss())
+        h = nxt
+    assert len(calls) >= 2
+    assert la == lb and sa.t == sb.t == 4 and fa.version == fb.version
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
