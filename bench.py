@@ -274,8 +274,7 @@ def run_ours(args, dist, ws, rank, local):
     hr_renderer = gs.Renderer(hr_grid, opts, bd, slab=my_hr_slab, device=dev)
 
     def render_iter(grid, slab):
-        c = hr_renderer(f)
-        return c, hr_renderer.last_index
+        return hr_renderer(f)
 
     kr = max(1, min(args.steps, 10))
     for _ in range(min(args.warmup, 3)):
@@ -283,13 +282,15 @@ def run_ours(args, dist, ws, rank, local):
     barrier()
     e0.record(s)
     for _ in range(kr):
-        _, hidx = render_iter(hr_grid, my_hr_slab)
+        render_iter(hr_grid, my_hr_slab)
     e1.record(s)
     barrier()
     ms_r = max_over_ranks(e0.elapsed_time(e1) / kr)
     render = {"grid": list(hr_grid.dims), "value": hr_grid.num_voxels / (ms_r * 1e-3) / 1e9,
               "unit": "Gvoxel/s", "ms_per_render": ms_r, "renders": kr,
-              "pairs": hidx.pair_count if ws == 1 else None}
+              "pairs": hr_renderer.pair_count() if ws == 1 else None,
+              "path": "Renderer: one CUDA-graph replay per render (preprocess, scan, capacity "
+              "binning, forward) + the 4-byte overflow-flag read"}
 
     render512 = None
     if not args.no_render512:
@@ -302,21 +303,21 @@ def run_ours(args, dist, ws, rank, local):
         r5_renderer = gs.Renderer(g5, opts, bd, slab=slab5, device=dev)
 
         def r5():
-            c = r5_renderer(f5)
-            return c, r5_renderer.last_index
+            return r5_renderer(f5)
         r5()
         barrier()
         k5 = max(1, min(args.steps, 5))
         e0.record(s)
         for _ in range(k5):
-            _, i5 = r5()
+            r5()
         e1.record(s)
         barrier()
         ms5 = max_over_ranks(e0.elapsed_time(e1) / k5)
         render512 = {"grid": [512, 512, 512], "value": g5.num_voxels / (ms5 * 1e-3) / 1e9,
                      "unit": "Gvoxel/s", "ms_per_render": ms5, "renders": k5,
-                     "pairs": i5.pair_count if ws == 1 else None, "field": "config-5 jittered"}
-        del f5, i5, r5_renderer
+                     "pairs": r5_renderer.pair_count() if ws == 1 else None,
+                     "field": "config-5 jittered"}
+        del f5, r5_renderer
     clocks = sampler.stop()
 
     # ---------------- roofline of the dominant pair kernel (live pair-voxels)

@@ -643,7 +643,12 @@ class Renderer:
     """Repeated renders of fields at one grid with reusable buffers: the
     render path of the reference (build_brick_index + forward, cli.py:231-233)
     without per-call allocations.  Returned tensors are views valid until the
-    next call."""
+    next call.
+
+    f32 renders replay a captured CUDA graph (preprocess -> scan -> capacity
+    binning -> forward): no pair-count read and no per-kernel host work; the
+    only host read is the overflow flag, and an overflow re-captures with more
+    room.  The graph is re-captured when the field's buffers change."""
 
     def __init__(self, grid, opts: RenderOptions = RenderOptions(), brick_dims=(8, 8, 4),
                  slab=None, device=None):
@@ -652,9 +657,41 @@ class Renderer:
         self.brick_dims = tuple(brick_dims)
         self.slab = slab
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
         self.pool = _lib.BufferPool(dev)
+        self.last_index = None
+        self._graph = None
+
+    def pair_count(self) -> int:
+        """Pairs of the last render (one device read)."""
+        if self.last_index is not None:
+            return self.last_index.pair_count
+        return int(self._graph.bufs["gstart"][-1].item())
 
     def __call__(self, f: GaussianField) -> RenderCache:
+        if self.opts.precision != "f32" or os.environ.get("GSV_NO_GRAPH"):
+            return self._eager(f)
+        key = (f.count, f.positions.data_ptr(), f.log_scales.data_ptr(),
+               f.rotations.data_ptr(), f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(),
+               int(f.relax_enabled))
+        g = self._graph
+        if g is None or g.key != key:
+            self._graph = None
+            g = self._graph = self._capture(f, key)
+        b = g.bufs
+        g.graph.replay()
+        b["ovf_host"].copy_(b["overflow"], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        ev.synchronize()
+        if int(b["ovf_host"][0]):
+            self._graph = None
+            self._graph = self._capture(f, key, min_cap=int(g.cap * 1.5))
+            return self(f)
+        self.last_index = None
+        return RenderCache(self.grid, b["S"], b["W"], b["I"], f.version)
+
+    def _eager(self, f: GaussianField) -> RenderCache:
         idx = build_brick_index(f, self.grid, self.opts, self.brick_dims, slab=self.slab,
                                 pool=self.pool)
         n = self.grid.num_voxels
@@ -665,3 +702,75 @@ class Renderer:
         _forward_into(f, self.grid, idx, self.opts, idx._aux.rec32, idx._aux.rec64, S, W, I)
         self.last_index = idx
         return RenderCache(self.grid, S, W, I, f.version)
+
+    def _body(self, f: GaussianField, g) -> None:
+        lib = _lib.lib()
+        b, s, n = g.bufs, _lib.stream_ptr(), f.count
+        gr, br, opts = _lib.make_grid(self.grid), b["bricks"], self.opts
+        _lib.check(lib.gsv_preprocess(
+            f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+            f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), n, int(f.relax_enabled),
+            float(opts.cutoff_sigma), gr, br, b["rec32"].data_ptr(), None,
+            b["counts"].data_ptr(), b["box"].data_ptr(), s), "preprocess")
+        ws, k = b["ws"], b["keys"]
+        _lib.check(lib.gsv_bin_scan(b["counts"].data_ptr(), n, b["gstart"].data_ptr(),
+                                    ws.data_ptr(), ws.numel(), s), "bin_scan")
+        _lib.check(lib.gsv_bin_fill_capacity(
+            b["counts"].data_ptr(), b["box"].data_ptr(), b["gstart"].data_ptr(), n, g.cap, br,
+            k[0].data_ptr(), k[1].data_ptr(), k[2].data_ptr(), b["gids"].data_ptr(),
+            b["starts"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(),
+            ws.data_ptr(), ws.numel(), s), "bin_fill_capacity")
+        _lib.check(lib.gsv_forward(
+            f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+            b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
+            float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
+            b["W"].data_ptr(), b["I"].data_ptr(), None, 0, float(self.grid.num_voxels), None,
+            None, None, _resolve_vpl(self.brick_dims), s), "forward")
+
+    def _capture(self, f: GaussianField, key, min_cap: int = 0):
+        import ctypes
+        lib = _lib.lib()
+        dev, n = self.device, f.count
+        bricks = _lib.make_bricks(self.grid, self.brick_dims, self.slab)
+        nb = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
+        gp = _lib.BufferPool(dev)
+        b = {"bricks": bricks,
+             "rec32": gp.get("rec32", (n, 16), torch.float32),
+             "counts": gp.get("counts", (n,), torch.int32),
+             "box": gp.get("box", (n, 4), torch.int32),
+             "gstart": gp.get("gstart", (n + 1,), torch.int64)}
+        _lib.check(lib.gsv_preprocess(
+            f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+            f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), n, int(f.relax_enabled),
+            float(self.opts.cutoff_sigma), _lib.make_grid(self.grid), bricks,
+            b["rec32"].data_ptr(), None, b["counts"].data_ptr(), b["box"].data_ptr(),
+            _lib.stream_ptr()), "preprocess")
+        pairs = int(_scan(b["counts"], nb, self.pool)[-1].item())
+        cap = max(int(pairs * _GRAPH_HEADROOM) + 4096, min_cap, 1)
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
+        nv = self.grid.num_voxels
+        b.update({"ws": gp.get("ws", (nbytes.value,), torch.uint8),
+                  "keys": gp.get("keys", (3, cap), torch.int32),
+                  "gids": gp.get("gids", (cap,), torch.int32),
+                  "starts": gp.get("starts", (nb + 1,), torch.int64),
+                  "S": gp.get("S", (nv,), torch.float32), "W": gp.get("W", (nv,), torch.float32),
+                  "I": gp.get("I", (nv,), torch.float32),
+                  "dry": gp.get("dry", (1,), torch.int32),
+                  "overflow": gp.get("overflow", (1,), torch.int32),
+                  "ovf_host": torch.zeros(1, dtype=torch.int32).pin_memory()})
+        g = _StepGraph(key, cap, 0)
+        g.bufs = b
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            b["dry"].fill_(1)
+            self._body(f, g)
+            b["dry"].zero_()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
+            self._body(f, g)
+        g.graph = graph
+        return g

@@ -14,7 +14,7 @@ import oracle
 import paper_2603_09621_b200 as gs
 from paper_2603_09621_b200.field import random_field_arrays
 from paper_2603_09621_b200.raster import RenderCache
-from paper_2603_09621_b200.synth import sha256
+from paper_2603_09621_b200.synth import CONFIGS, make_problem, sha256
 
 from conftest import GRAD_KEYS, SWEEP_GRIDS, field_dict, load_json
 
@@ -478,3 +478,66 @@ def test_slabs_reassemble_the_full_index_render_and_gradients():
     assert abs(loss_total / grid.num_voxels - out.loss()) <= 1e-12
     a, b = np_(total[:, :11]), np_(g_full[:, :11])
     assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b) + 1e-30
+
+
+# ------------------------------------------------------------------ Renderer
+def _renders_equal(a, b):
+    for k in ("S", "W", "I"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2])
+def test_renderer_graph_equals_index_plus_forward(cfg_id):
+    """The graph-replayed Renderer (capacity binning, no pair-count read) is
+    bit-identical to build_brick_index + forward, follows in-place field
+    updates without re-capturing, and reports the pair count."""
+    p = make_problem(CONFIGS[cfg_id])
+    f = gs.GaussianField(*p["field"])
+    grid = p["hr_grid"]
+    r = gs.Renderer(grid)
+    c = r(f)
+    idx = gs.build_brick_index(f, grid)
+    _renders_equal(c, gs.forward(f, grid, idx))
+    assert r.pair_count() == idx.pair_count
+    g0 = r._graph
+    with torch.no_grad():
+        f.positions.add_(0.05)
+        f.raw_amplitude.mul_(0.9)
+    f.bump_version()
+    c = r(f)
+    assert r._graph is g0
+    idx = gs.build_brick_index(f, grid)
+    _renders_equal(c, gs.forward(f, grid, idx))
+
+
+def test_renderer_recovers_from_capacity_overflow(monkeypatch):
+    """A first capture with too little pair capacity overflows on the device;
+    the Renderer re-captures with more room and the render is still exact."""
+    import paper_2603_09621_b200.train as train_mod
+    p = make_problem(CONFIGS[1])
+    f = gs.GaussianField(*p["field"])
+    grid = p["hr_grid"]
+    r = gs.Renderer(grid)
+    real = gs.Renderer._capture
+    calls = []
+
+    def capture(self, f, key, min_cap=0):
+        calls.append(min_cap)
+        monkeypatch.setattr(train_mod, "_GRAPH_HEADROOM", 0.1 if len(calls) == 1 else 1.15)
+        return real(self, f, key, min_cap)
+
+    monkeypatch.setattr(gs.Renderer, "_capture", capture)
+    c = r(f)
+    assert len(calls) >= 2
+    _renders_equal(c, gs.forward(f, grid, gs.build_brick_index(f, grid)))
+
+
+def test_renderer_f64_is_the_eager_path():
+    p = make_problem(CONFIGS[1])
+    f = gs.GaussianField(*p["field"])
+    opts = gs.RenderOptions(precision="f64")
+    r = gs.Renderer(p["hr_grid"], opts)
+    c = r(f)
+    assert r.last_index is not None
+    _renders_equal(c, gs.forward(f, p["hr_grid"], gs.build_brick_index(f, p["hr_grid"], opts),
+                                 opts))
