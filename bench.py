@@ -321,14 +321,14 @@ def run_ours(args, dist, ws, rank, local):
     clocks = sampler.stop()
 
     # ---------------- roofline of the dominant pair kernel (live pair-voxels)
-    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(3, dtype=torch.int64, device=dev)
     out_idx = out.idx
     _lib.check(lib.gsv_diag_count_live(
         f.positions.data_ptr(), out_idx._aux.rec32.data_ptr(), f.log_scales.data_ptr(),
         f.rotations.data_ptr(), out_idx.starts.data_ptr(), out_idx.gids.data_ptr(),
         _lib.make_grid(lr_grid), _lib.make_bricks(lr_grid, bd, my_slab), 3.0, cnt.data_ptr(),
         _lib.stream_ptr()), "count_live")
-    e_live, e_brick = (int(x) for x in cnt.tolist())
+    e_live, e_brick, e_tile = (int(x) for x in cnt.tolist())
     peak = fp32_peak(lib, dev)
     t_fwd = phases.get("forward", (0, float("nan")))[1]
     t_bwd = phases.get("backward", (0, float("nan")))[1]
@@ -345,12 +345,14 @@ def run_ours(args, dist, ws, rank, local):
     bytes_alg = {"forward": 88 * n_g + 36 * pairs + 24 * nv_lr,
                  "backward": 112 * n_g + 84 * pairs + 8 * nv_lr}[dom]
     traffic = None
+    issue = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         with open(tf) as fh:
             tj = json.load(fh)
         if tj.get("config") == args.config:   # measured for this workload only
             traffic = tj.get(dom)
+            issue = tj.get(dom + "_issue_active_pct")
     hbm_peak = 6552.0  # MEASURED_PEAKS.json (driver-written) when present
     mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(mp):
@@ -358,7 +360,16 @@ def run_ours(args, dist, ws, rank, local):
             hbm_peak = float(json.load(fh).get("hbm_gbs", hbm_peak))
     roofline = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": peak["tflops"],
                 "unit": "TFLOP/s", "frac": achieved / peak["tflops"], "traffic": traffic,
-                "peak_source": peak["source"], "work": {"E_live": e_live, "E_brick": e_brick,
+                "peak_source": peak["source"],
+                "evaluated": {
+                    "E_tile": e_tile if dom == "forward" else None,
+                    "live_fraction": (e_live / e_tile) if (dom == "forward" and e_tile) else None,
+                    "issue_active_pct": issue,
+                    "note": "the forward evaluates every (pair, voxel) slot of each warp tile "
+                            "a pair's 3-sigma box and sphere bound reach (E_tile); frac counts "
+                            "live pair-voxels only (SURVEY 8d's unit), issue_active_pct is the "
+                            "kernel's issue-slot use from the ncu capture in profiles/"},
+                "work": {"E_live": e_live, "E_brick": e_brick,
                 "flop_per_live_pair_voxel": fl, "ms_per_launch": t_dom},
                 "hbm": {"algorithmic_bytes": bytes_alg,
                         "achieved_gbs": bytes_alg / (t_dom * 1e-3) / 1e9, "peak_gbs": hbm_peak,

@@ -20,14 +20,40 @@ count_live_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
   const int ex = min(k.bdx, g.nx - x0), ey = min(k.bdy, g.ny - y0), ez = min(k.bdz, g.nz - z0);
   const double px = g.ox + (double)x0 * g.sx, py = g.oy + (double)y0 * g.sy,
                pz = g.oz + (double)z0 * g.sz;
-  unsigned long long live = 0, evals = 0;
+  unsigned long long live = 0, evals = 0, tiled = 0;
   const int nv = ex * ey * ez;
+  // warp tiles of the forward's default layout (8x8x4 bricks, VPL 4): warp w
+  // owns y in [4w, 4w + 4); its tile box is the bounding box of its voxels
+  const bool tiles8 = k.bdx == 8 && k.bdy == 8 && k.bdz == 4;
+  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
   for (int64_t j = starts[lb] + threadIdx.x; j < starts[lb + 1]; j += blockDim.x) {
     const int gid = gids[j];
     const gsv_record32 r = rec[gid];
     const double* m = pos + 3 * (int64_t)gid;
     const float c0 = (float)(px - m[0]), c1 = (float)(py - m[1]), c2 = (float)(pz - m[2]);
     evals += nv;
+    if (tiles8) {
+      // the forward's staging tests: 3-sigma box, then the sphere bound
+      const float cxv = -c0 * isx, cyv = -c1 * isy, czv = -c2 * isz;
+      const float hxv = fmaf(r.half[0], isx, 1e-3f), hyv = fmaf(r.half[1], isy, 1e-3f),
+                  hzv = fmaf(r.half[2], isz, 1e-3f);
+      for (int w = 0; w < 2; ++w) {
+        const int yl = 4 * w, yh = min(4 * w + 3, ey - 1);
+        if (yl > yh) continue;
+        const float fxl = 0.f, fxh = (float)(ex - 1), fyl = (float)yl, fyh = (float)yh,
+                    fzl = 0.f, fzh = (float)(ez - 1);
+        bool hit = cxv + hxv >= fxl && cxv - hxv <= fxh && cyv + hyv >= fyl &&
+                   cyv - hyv <= fyh && czv + hzv >= fzl && czv - hzv <= fzh;
+        if (hit && !isinf(cut2)) {
+          const float ddx = fmaxf(fmaxf(fxl - cxv, cxv - fxh), 0.f) * fsx;
+          const float ddy = fmaxf(fmaxf(fyl - cyv, cyv - fyh), 0.f) * fsy;
+          const float ddz = fmaxf(fmaxf(fzl - czv, czv - fzh), 0.f) * fsz;
+          hit = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz)) * r.inv_smax2 <= cut2 * 1.0001f + 1e-6f;
+        }
+        tiled += hit ? 128ull : 0ull;              // 32 lanes x 4 voxels per hit
+      }
+    }
     for (int z = 0; z < ez; ++z)
       for (int y = 0; y < ey; ++y)
         for (int x = 0; x < ex; ++x) {
@@ -49,6 +75,7 @@ count_live_kernel(const double* __restrict__ pos, const gsv_record32* __restrict
   }
   atomicAdd(&counters[0], live);
   atomicAdd(&counters[1], evals);
+  atomicAdd(&counters[2], tiled);
 }
 
 __global__ void __launch_bounds__(256) fma_probe_kernel(int iters, float* out) {

@@ -82,6 +82,9 @@ def main():
             rd = to_bytes(r[col["dram__bytes_read.sum"]], units[col["dram__bytes_read.sum"]])
             wr = to_bytes(r[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
             traffic[role] = rd + wr
+            ia = "smsp__issue_active.avg.pct_of_peak_sustained_active"
+            if ia in col:
+                traffic[role + "_issue_active_pct"] = float(r[col[ia]].replace(",", ""))
     with open(args.out, "w") as fh:
         fh.write("\n".join(lines) + "\n")
     if args.traffic:
