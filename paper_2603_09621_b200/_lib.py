@@ -199,10 +199,9 @@ class BufferPool:
         numel = 1
         for s in shape:
             numel *= s
-        numel = max(numel, 1)
         key = (name, dtype)
         buf = self._bufs.get(key)
-        if buf is None or buf.numel() < numel:
-            buf = torch.empty(int(numel * 1.1) + 64, dtype=dtype, device=self.device)
+        if buf is None or buf.numel() < max(numel, 1):
+            buf = torch.empty(int(max(numel, 1) * 1.1) + 64, dtype=dtype, device=self.device)
             self._bufs[key] = buf
         return buf[:numel].view(shape) if shape else buf[:1].view(())

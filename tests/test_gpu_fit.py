@@ -332,3 +332,30 @@ def test_pipelined_steps_recover_from_overflow_and_match_eager(monkeypatch):
     assert len(calls) >= 2
     assert la == lb and sa.t == sb.t == 4 and fa.version == fb.version
     np.testing.assert_array_equal(_pack(fa), _pack(fb))
+
+
+@pytest.mark.parametrize("case", ["outside", "single"])
+def test_graph_step_degenerate_fields_match_eager(case):
+    """P = 0 (every Gaussian outside the grid) and N = 1: the captured step
+    equals the eager forward()+update() (losses, parameters, step count)."""
+    grid = gs.GridSpec((16, 16, 16))
+    rng = np.random.default_rng(5)
+    n = 1 if case == "single" else 40
+    pos = rng.uniform(4.0, 12.0, (n, 3))
+    if case == "outside":
+        pos += 100.0
+    arrs = (pos, np.log(np.full((n, 3), 1.2)), np.tile([1.0, 0, 0, 0], (n, 1)),
+            rng.normal(size=n), rng.normal(size=n))
+    target = gs.Volume(grid, rng.uniform(size=grid.dims).astype(np.float32))
+    fa, fb = gs.GaussianField(*arrs), gs.GaussianField(*arrs)
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = gs.FitConfig().resolved_lrs(grid.spacing)
+    ea = gs.TrainStep(target, gs.RenderOptions(), (8, 8, 4), "l2")
+    eb = gs.TrainStep(target, gs.RenderOptions(), (8, 8, 4), "l2")
+    for _ in range(3):
+        out = ea.forward(fa)
+        la = out.loss()
+        ea.update(fa, out, sa, lrs)
+        assert eb.step(fb, sb, lrs) == la
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    assert sa.t == sb.t == 3

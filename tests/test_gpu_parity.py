@@ -541,3 +541,14 @@ def test_renderer_f64_is_the_eager_path():
     assert r.last_index is not None
     _renders_equal(c, gs.forward(f, p["hr_grid"], gs.build_brick_index(f, p["hr_grid"], opts),
                                  opts))
+
+
+def test_renderer_with_no_pairs_renders_zero():
+    grid = gs.GridSpec((16, 16, 16))
+    n = 10
+    arrs = (np.full((n, 3), 500.0), np.zeros((n, 3)), np.tile([1.0, 0, 0, 0], (n, 1)),
+            np.zeros(n), np.zeros(n))
+    f = gs.GaussianField(*arrs)
+    c = gs.Renderer(grid)(f)
+    for k in ("S", "W", "I"):
+        assert float(getattr(c, k).abs().max()) == 0.0, k
