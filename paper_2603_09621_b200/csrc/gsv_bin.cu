@@ -51,26 +51,31 @@ __global__ void scan_tail_kernel(const int32_t* counts, int64_t n, int64_t* gsta
   gstart[n] = n > 0 ? gstart[n - 1] + (int64_t)counts[n - 1] : 0;
 }
 
-// Warp-cooperative emission (coalesced stores):
-// a warp owns 32 consecutive Gaussians, prefix-sums their pair counts with
-// shuffles, and each lane then produces consecutive output slots -- finding
-// the owning Gaussian by a 5-step shuffle binary search and the brick from
-// the slot's rank inside the owner's box (x fastest, raster.py:200-209).
+// Warp-cooperative emission through shared memory: a warp owns 32
+// consecutive Gaussians, prefix-sums their pair counts with shuffles, and
+// fills its output range window by window (kEmitWin slots): each lane writes
+// its own Gaussian's bricks of the window into shared memory, walking the box
+// x-fastest with incremental counters (raster.py:200-209; one division per
+// lane and window, none per pair), then the warp copies the window out with
+// coalesced stores.
+constexpr int kEmitWin = 512;
+
 __global__ void __launch_bounds__(256)
 emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
                  const int64_t* __restrict__ gstart, int64_t n, gsv_bricks k,
                  int32_t* __restrict__ keys, int32_t* __restrict__ vals, int64_t cap) {
-  const int lane = threadIdx.x & 31;
+  __shared__ int2 swin[8][kEmitWin];          // per warp: (key, gid) of one window
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31;
   if (g0 >= n) return;                       // warp-uniform
   const int64_t g = g0 + lane;
-  int c = 0, nbx = 1, nbxy = 1, kb = 0;
+  int c = 0, nbx = 1, nby = 1, kb = 0;
   if (g < n) {
     c = counts[g];
     if (c > 0) {
       const GBox b = unpack_box(box, g);
       nbx = b.nb_x;
-      nbxy = b.nb_x * b.nb_y;
+      nby = b.nb_y;
       kb = b.blo_x + k.bgx * (b.blo_y + k.bgy * (b.blo_z - k.bz0));   // slab-local id
     }
   }
@@ -84,26 +89,40 @@ emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   const int64_t base = gstart[g0];
   const int bxy = k.bgx * k.bgy;
-  for (int o0 = 0; o0 < total; o0 += 32) {
-    const int o = o0 + lane;
-    // owner = the last lane whose first slot is <= o (always a lane with pairs)
-    int own = 0;
-#pragma unroll
-    for (int st = 16; st > 0; st >>= 1) {
-      const int cand = own + st;
-      const int oc = __shfl_sync(0xffffffffu, off, cand & 31);
-      if (cand < 32 && oc <= o) own = cand;
+  int2* win = swin[warp];
+  for (int w0 = 0; w0 < total; w0 += kEmitWin) {
+    // this lane's pairs inside [w0, w0 + kEmitWin)
+    const int r0 = max(0, w0 - off), r1 = min(c, w0 + kEmitWin - off);
+    if (r0 < r1) {
+      int rx = r0 % nbx;
+      const int t = r0 / nbx;
+      int ry = t % nby, rz = t / nby;
+      int key = kb + rx + k.bgx * ry + bxy * rz;
+      const int gid = (int)g;
+      for (int r = r0; r < r1; ++r) {
+        win[off + r - w0] = make_int2(key, gid);
+        ++key;
+        if (++rx == nbx) {                   // next row, then next layer
+          rx = 0;
+          key += k.bgx - nbx;
+          if (++ry == nby) {
+            ry = 0;
+            key += bxy - k.bgx * nby;
+          }
+        }
+      }
     }
-    const int r = o - __shfl_sync(0xffffffffu, off, own);
-    const int ox = __shfl_sync(0xffffffffu, nbx, own);
-    const int oxy = __shfl_sync(0xffffffffu, nbxy, own);
-    const int okb = __shfl_sync(0xffffffffu, kb, own);
-    const int rz = r / oxy, rem = r - rz * oxy;
-    const int ry = rem / ox, rx = rem - ry * ox;
-    if (o < total && base + o < cap) {
-      keys[base + o] = okb + rx + k.bgx * ry + bxy * rz;
-      vals[base + o] = (int32_t)(g0 + own);
+    __syncwarp();
+    const int cnt = min(kEmitWin, total - w0);
+    for (int q = lane; q < cnt; q += 32) {
+      const int64_t o = base + w0 + q;
+      if (o < cap) {
+        const int2 e = win[q];
+        keys[o] = e.x;
+        vals[o] = e.y;
+      }
     }
+    __syncwarp();
   }
 }
 
