@@ -20,6 +20,7 @@
 // the explicit _rn intrinsics, so no f64 expression that feeds a binning
 // decision can be contracted.
 #include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "gsv_prep.cuh"
 
@@ -225,7 +226,7 @@ int gsv_bin_workspace(int64_t n, int64_t max_pairs, int32_t nbricks, size_t* byt
   GSV_REQUIRE(max_pairs < (int64_t)INT32_MAX, "pair count %lld exceeds int32",
               (long long)max_pairs);
   size_t scan_bytes = 0, sort_bytes = 0;
-  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(nullptr, ToI64());
+  thrust::transform_iterator<ToI64, const int32_t*, int64_t> it(nullptr, ToI64());
   cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, it, (int64_t*)nullptr,
                                                 (int)(n > 0 ? n : 1));
   if (e != cudaSuccess) return cuda_status(e, "DeviceScan sizing");
@@ -247,7 +248,7 @@ int gsv_bin_scan(const int32_t* counts, int64_t n, int64_t* gstart, void* worksp
     if (e != cudaSuccess) return cuda_status(e, "memset gstart");
     return GSV_OK;
   }
-  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(counts, ToI64());
+  thrust::transform_iterator<ToI64, const int32_t*, int64_t> it(counts, ToI64());
   size_t bytes = workspace_bytes;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(workspace, bytes, it, gstart, (int)n, s);
   if (e != cudaSuccess) return cuda_status(e, "DeviceScan::ExclusiveSum");

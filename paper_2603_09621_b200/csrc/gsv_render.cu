@@ -26,7 +26,6 @@
 namespace gsv {
 namespace {
 
-constexpr int kFwdThreads = 128;     // 4 warps; each warp owns one voxel tile
 constexpr int kBwdThreads = 256;
 constexpr int kBwdSmemVoxels = 2048; // brick voxels staged in smem by the backward
 // f32 truncation guard band.  Each v component is u + x e_x + y e_y + z e_z
@@ -90,21 +89,6 @@ __device__ __forceinline__ void sub_range(double c, double h, double s, int n,
   hi = (int)b;
 }
 
-// sub_range with precomputed 1/s (no f64 division on the staging path).
-__device__ __forceinline__ void sub_range_inv(double c, double h, double inv_s, int n, int& lo,
-                                              int& hi) {
-  const double ctr = c * inv_s, hv = h * inv_s;
-  double a = ceil(ctr - hv - 1e-3), b = floor(ctr + hv + 1e-3);
-  a = fmax(a, 0.0);
-  b = fmin(b, (double)(n - 1));
-  if (!(a <= b)) {
-    lo = 1 << 20;
-    hi = -1;
-    return;
-  }
-  lo = (int)a;
-  hi = (int)b;
-}
 
 // Exact f64 truncation decision of one (Gaussian, voxel) -- the rare
 // guard-band path -- with the f64 whitening factor from rec64 when the caller
@@ -181,27 +165,6 @@ __device__ __forceinline__ float ex2_approx(float q) {
   return r;
 }
 
-// Asynchronous global->shared copies (LDGSTS): the next round's pair records
-// land in shared memory while this round is evaluated.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// exp(-d2/2) as one FMUL + MUFU.EX2 (rel. error ~2e-7, well inside the 1e-5
-// parity bar).
-__device__ __forceinline__ float exp_neg_half(float d2) {
-  float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d2 * -0.72134752044448170f));
-  return r;
-}
 
 // One CTA per brick.  Each lane owns a z-column of VPL voxels; a warp's 32
 // lanes form one voxel tile (VPL = 2: 4x4x4 tiles, 4 warps per 8x8x4 brick --

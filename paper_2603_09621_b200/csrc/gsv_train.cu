@@ -454,8 +454,8 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
     bc1 = sd.bc[2 * t];
     bc2 = sd.bc[2 * t + 1];
   }
-#pragma unroll
   double pn[3], ln[3], qn[4];
+#pragma unroll
   for (int a = 0; a < 3; ++a) {
     double m = mv[0][3 * i + a], v = mv[5][3 * i + a];
     pn[a] = adam_one(pos[3 * i + a], m, v, g[a], h.lr[0], h.b1, h.b2, h.eps, bc1, bc2);
