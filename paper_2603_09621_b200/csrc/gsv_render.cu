@@ -199,7 +199,11 @@ __device__ __forceinline__ void unit_voxel_v(int u, const gsv_bricks& k, int& x,
 #ifndef GSV_FWD_OCC
 #define GSV_FWD_OCC 640
 #endif
-template <int VPL, int THREADS, bool MASKS>
+// SPLIT: one 32-thread CTA per warp tile of a brick with exactly two tiles
+// (VPL 4, e.g. 8x8x4): no CTA waits for its slower tile, the scheduler refills
+// the SM as soon as a tile is done.  The brick's loss partial then gets two
+// atomic adds onto a zeroed slot -- order-independent, so still deterministic.
+template <int VPL, int THREADS, bool MASKS, bool SPLIT = false>
 __global__ void __launch_bounds__(THREADS, GSV_FWD_OCC / THREADS)
 forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
                  const gsv_record32* __restrict__ rec,
@@ -215,12 +219,17 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
   __shared__ uint2 smask[MASKS ? THREADS * VPL / 2 : 1];
   __shared__ uint2 sxmask[MASKS ? THREADS * VPL / 2 : 1];   // guard-band additions
   __shared__ double red[THREADS / 32];
-  const int lb = blockIdx.x;                               // slab-local brick
+  static_assert(!SPLIT || THREADS == 32, "split tiles run one warp per CTA");
+  const int lb = SPLIT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // slab-local brick
   const int b = (int)slab_first(k) + lb;                   // global brick id
   const BrickGeom bg = brick_geom(b, g, k);
   const int64_t lbeg = starts[lb], lend = starts[lb + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  Pair32* wsp = sp + (warp << 5);
+  // tid / warp: the thread's place in the brick's tiling; swarp: its warp's
+  // slot in this CTA's shared memory
+  const int warp = SPLIT ? (int)(blockIdx.x & 1) : (int)(threadIdx.x >> 5);
+  const int tid = (int)threadIdx.x + (SPLIT ? (warp << 5) : 0), lane = threadIdx.x & 31;
+  const int swarp = SPLIT ? 0 : warp;
+  Pair32* wsp = sp + (swarp << 5);
   const int units = k.bdx * k.bdy * ((k.bdz + VPL - 1) / VPL);
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
   const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
@@ -228,10 +237,11 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
   // masks (host-checked: units <= THREADS): per pair VPL words per warp,
   // planes [warp * VPL/2 + k][pair] of uint2 {word 2k, word 2k+1}
   constexpr bool want_masks = MASKS;
-  const int64_t mstride = starts[gridDim.x];   // pairs of the slab: mask plane stride
+  // pairs of the slab: the mask plane stride (starts[nbricks_slab])
+  const int64_t mstride = starts[SPLIT ? (gridDim.x >> 1) : gridDim.x];
   double lsum = 0.0;
 
-  for (int ubase = 0; ubase < units; ubase += THREADS) {
+  for (int ubase = 0; ubase < units; ubase += SPLIT ? units : THREADS) {
     const int u = ubase + tid;
     int lx = 0, ly = 0, lz = 0;
     if (u < units) unit_voxel_v<VPL>(u, k, lx, ly, lz);
@@ -361,7 +371,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
       if (want_masks) {                 // guard-band live bits of this round's hits
 #pragma unroll
         for (int kk = 0; kk < VPL / 2; ++kk)
-          sxmask[((warp << 5) + lane) * (VPL / 2) + kk] = make_uint2(0u, 0u);
+          sxmask[((swarp << 5) + lane) * (VPL / 2) + kk] = make_uint2(0u, 0u);
         __syncwarp();
       }
       for (int jj = 0; jj < nh; ++jj) {
@@ -407,7 +417,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
             for (int h = 0; h < VPL; ++h) xw[h] = __ballot_sync(kFull, xl[h]);
 #pragma unroll
             for (int kk = 0; kk < VPL / 2; ++kk)
-              sxmask[((warp << 5) + jj) * (VPL / 2) + kk] = make_uint2(xw[2 * kk], xw[2 * kk + 1]);
+              sxmask[((swarp << 5) + jj) * (VPL / 2) + kk] = make_uint2(xw[2 * kk], xw[2 * kk + 1]);
           }
         }
         bool live[VPL];
@@ -427,7 +437,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
           // warp-uniform values: every lane stores the same words (no predicate)
 #pragma unroll
           for (int kk = 0; kk < VPL / 2; ++kk)
-            smask[((warp << 5) + jj) * (VPL / 2) + kk] = make_uint2(mw[2 * kk], mw[2 * kk + 1]);
+            smask[((swarp << 5) + jj) * (VPL / 2) + kk] = make_uint2(mw[2 * kk], mw[2 * kk + 1]);
         }
       }
       // live-voxel masks for the backward, plane [warp][pair]: one coalesced
@@ -438,8 +448,8 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
         for (int kk = 0; kk < VPL / 2; ++kk) {
           uint2 mm = make_uint2(0u, 0u);
           if (hit) {
-            const uint2 a = smask[((warp << 5) + rank) * (VPL / 2) + kk];
-            const uint2 x = sxmask[((warp << 5) + rank) * (VPL / 2) + kk];
+            const uint2 a = smask[((swarp << 5) + rank) * (VPL / 2) + kk];
+            const uint2 x = sxmask[((swarp << 5) + rank) * (VPL / 2) + kk];
             mm = make_uint2(a.x | x.x, a.y | x.y);
           }
           mm.x &= ownb[2 * kk];          // voxels outside the grid never enter a mask
@@ -475,8 +485,15 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
     }
   }
   if (target) {
-    const double t = block_sum<THREADS>(lsum, red);
-    if (tid == 0) loss_part[lb] = t;
+    if (SPLIT) {
+      double t = lsum;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(kFull, t, o);
+      if (lane == 0) atomicAdd(loss_part + lb, t);   // 2 adds onto 0: order-independent
+    } else {
+      const double t = block_sum<THREADS>(lsum, red);
+      if (threadIdx.x == 0) loss_part[lb] = t;
+    }
   }
 }
 
@@ -1300,6 +1317,9 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
   if (precision == 0) {
     // Column depth: VPL voxels per lane (2: 4x4x4 warp tiles, 4 warps per
     // 8x8x4 brick; 4: 8x4x4 tiles, 2 warps); 0 = auto (4 when bdz % 4 == 0).
+    // vpl | 0x200: keep the two tiles of a VPL-4 brick in one CTA (measurement)
+    const bool no_split = (vpl & 0x200) != 0;
+    vpl &= 0xff;
     GSV_REQUIRE(vpl == 0 || vpl == 2 || vpl == 4, "vpl must be 0, 2 or 4");
     if (vpl == 0) vpl = mask_vpl_auto(*bricks);
     if (live_masks != nullptr)
@@ -1312,7 +1332,20 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
       positions, xs, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,          \
       (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab, loss_part,   \
       (uint2*)live_masks)
-    if (vpl == 4) {
+    const bool split = vpl == 4 && !no_split && mask_units(*bricks, 4) == 64;
+    if (split) {
+      if (target) {
+        cudaError_t e = cudaMemsetAsync(loss_part, 0, (size_t)nb * sizeof(double), s);
+        if (e != cudaSuccess) return cuda_status(e, "memset loss_part");
+      }
+#define GSV_FWD32S(M)                                                                          \
+  forward32_kernel<4, 32, M, true><<<(unsigned)(2 * nb), 32, 0, s>>>(                          \
+      positions, xs, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,          \
+      (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab, loss_part,   \
+      (uint2*)live_masks)
+      if (live_masks) GSV_FWD32S(true); else GSV_FWD32S(false);
+#undef GSV_FWD32S
+    } else if (vpl == 4) {
       if (live_masks) GSV_FWD32(4, 64, true); else GSV_FWD32(4, 64, false);
     } else {
       if (live_masks) GSV_FWD32(2, 128, true); else GSV_FWD32(2, 128, false);

@@ -308,6 +308,12 @@ def _resolve_vpl(brick_dims) -> int:
     return 4 if bz % 4 == 0 and bx * by * (bz // 4) <= 64 else 2
 
 
+def _forward_vpl_arg(brick_dims) -> int:
+    """gsv_forward's vpl argument: the resolved depth, | 0x200 to keep a
+    brick's two VPL-4 tiles in one CTA when GSV_NO_SPLIT is set (measurement)."""
+    return _resolve_vpl(brick_dims) | (0x200 if os.environ.get("GSV_NO_SPLIT") else 0)
+
+
 def _masks_fit(brick_dims, vpl: int) -> bool:
     """Live masks need a brick that fills one CTA's warp tiles exactly (4
     planes of mask words), e.g. the default 8x8x4."""
@@ -326,7 +332,7 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
-        _resolve_vpl(idx.brick_dims), _lib.stream_ptr()), "forward")
+        _forward_vpl_arg(idx.brick_dims), _lib.stream_ptr()), "forward")
 
 
 def forward(f: GaussianField, grid: GridSpec, idx: BrickIndex,

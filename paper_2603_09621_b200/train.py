@@ -26,7 +26,8 @@ import torch
 
 from . import _lib
 from .field import GaussianField
-from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule, _masks_fit,
+from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule,
+                     _forward_vpl_arg, _masks_fit,
                      _preprocess, _resolve_vpl, _scan,
                      _forward_into, _pair_partials, build_brick_index)
 from .render import RenderOptions
@@ -377,7 +378,7 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
         b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(), self.loss_kind,
         float(nvox), b["ab"].data_ptr(), b["loss_part"].data_ptr(), b["masks"].data_ptr(),
-        b["vpl"], s), "forward")
+        _forward_vpl_arg(self.brick_dims), s), "forward")
     _lib.check(lib.gsv_sum(b["loss_part"].data_ptr(), b["nb"], b["loss_sum"].data_ptr(), s),
                "sum")
     if not self.sharded:
@@ -725,7 +726,7 @@ class Renderer:
             b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
             float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
             b["W"].data_ptr(), b["I"].data_ptr(), None, 0, float(self.grid.num_voxels), None,
-            None, None, _resolve_vpl(self.brick_dims), s), "forward")
+            None, None, _forward_vpl_arg(self.brick_dims), s), "forward")
 
     def _capture(self, f: GaussianField, key, min_cap: int = 0):
         import ctypes
