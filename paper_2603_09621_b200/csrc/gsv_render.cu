@@ -497,6 +497,204 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
   }
 }
 
+// ------------------------------------------- forward f32, one warp per brick
+// Renders with large Gaussians (pairs >= 8 N: nearly every pair hits both
+// 8x4x4 tiles of a brick): one 32-thread CTA per 8x8x4 brick, lane l owns
+// the columns (x, y) = (l & 7, l >> 3) and (x, y + 4), all 4 z.  A pair is
+// staged and its quadratic built once per brick; column B's start value and
+// z-step follow from column A's in 5 FMAs.  No live masks (renders only).
+__global__ void __launch_bounds__(32, GSV_FWD_OCC / 32)
+forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
+                  const gsv_record32* __restrict__ rec,
+                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
+                  const __grid_constant__ gsv_grid g, gsv_bricks k, float cut2, double cut2d,
+                  double eps_w,
+                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
+                  const float* __restrict__ target, int loss_kind, double vox_count,
+                  float2* __restrict__ ab, double* __restrict__ loss_part) {
+  constexpr int Z = 4;
+  __shared__ Pair32 wsp[32];
+  const int lb = blockIdx.x;
+  const int b = (int)slab_first(k) + lb;
+  const BrickGeom bg = brick_geom(b, g, k);
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  const int lane = threadIdx.x;
+  const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
+  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  const int lx = lane & 7, lyA = lane >> 3, lyB = lyA + 4;
+  // the brick's owned voxel box and centre (brick-local voxel coordinates)
+  const float ftxh = (float)(bg.ex - 1), ftyh = (float)(bg.ey - 1), ftzh = (float)(bg.ez - 1);
+  const float ftxl = 0.f, ftyl = 0.f, ftzl = 0.f;
+  const float ctx = 0.5f * ftxh, cty = 0.5f * ftyh, ctz = 0.5f * ftzh;
+  const float ext_x = ctx, ext_y = cty, ext_z = ctz;
+  const float mX = (float)lx - ctx, mY = (float)lyA - cty, mZ = -ctz, mZ1 = mZ + 1.f;
+  const float twoY4 = fmaf(2.f, mY, 4.f);      // column B = column A + 4 in y
+  const int gx = bg.x0 + lx, gyA = bg.y0 + lyA, gyB = bg.y0 + lyB, gz = bg.z0;
+  float aS[2][Z], aW[2][Z];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int h = 0; h < Z; ++h) aS[c][h] = aW[c][h] = 0.f;
+  double lsum = 0.0;
+
+  int gid_next = (lbeg + lane < lend) ? __ldg(gids + lbeg + lane) : -1;
+  for (int64_t base = lbeg; base < lend; base += 32) {
+    const int gid = gid_next;
+    gid_next = (base + 32 + lane < lend) ? __ldg(gids + base + 32 + lane) : -1;
+    bool hit = false;
+    Pair32 p;
+    if (gid >= 0) {
+      const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+      const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
+      const double* m = pos + 3 * (int64_t)gid;
+      const float mx = (float)(__ldg(m) - bg.px), my = (float)(__ldg(m + 1) - bg.py),
+                  mz = (float)(__ldg(m + 2) - bg.pz);
+      const float cxv = mx * isx, cyv = my * isy, czv = mz * isz;
+      const float hxv = fmaf(q2.w, isx, 1e-3f), hyv = fmaf(q3.x, isy, 1e-3f),
+                  hzv = fmaf(q3.y, isz, 1e-3f);
+      hit = cxv + hxv >= ftxl && cxv - hxv <= ftxh && cyv + hyv >= ftyl &&
+            cyv - hyv <= ftyh && czv + hzv >= ftzl && czv - hzv <= ftzh;
+      if (hit && !isinf(cut2)) {
+        const float ddx = fmaxf(fmaxf(ftxl - cxv, cxv - ftxh), 0.f) * fsx;
+        const float ddy = fmaxf(fmaxf(ftyl - cyv, cyv - ftyh), 0.f) * fsy;
+        const float ddz = fmaxf(fmaxf(ftzl - czv, czv - ftzh), 0.f) * fsz;
+        const float dist2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
+        hit = dist2 * q3.z <= cut2 * 1.0001f + 1e-6f;
+      }
+      if (hit) {
+        const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+        float u3[3], e[3][3], umax = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          u3[a] = -fmaf(L[3 * a + 0], mx, fmaf(L[3 * a + 1], my, L[3 * a + 2] * mz));
+          e[0][a] = L[3 * a + 0] * fsx;
+          e[1][a] = L[3 * a + 1] * fsy;
+          e[2][a] = L[3 * a + 2] * fsz;
+          umax = fmaxf(umax, fabsf(u3[a]) + fabsf(e[0][a]) * k.bdx +
+                                 fabsf(e[1][a]) * k.bdy + fabsf(e[2][a]) * k.bdz);
+        }
+        float uc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          uc[a] = fmaf(ctz, e[2][a], fmaf(cty, e[1][a], fmaf(ctx, e[0][a], u3[a])));
+        const float sc = -0.72134752044448170f;   // -(1/2) log2(e)
+        const float lr2 = __log2f(q2.z);
+        const float d00 = fmaf(uc[0], uc[0], fmaf(uc[1], uc[1], uc[2] * uc[2]));
+        p.a.x = fmaf(sc, d00, lr2);
+        p.a.y = 2.f * sc * fmaf(uc[0], e[0][0], fmaf(uc[1], e[0][1], uc[2] * e[0][2]));
+        p.a.z = 2.f * sc * fmaf(uc[0], e[1][0], fmaf(uc[1], e[1][1], uc[2] * e[1][2]));
+        p.a.w = 2.f * sc * fmaf(uc[0], e[2][0], fmaf(uc[1], e[2][1], uc[2] * e[2][2]));
+        p.b.x = sc * fmaf(e[0][0], e[0][0], fmaf(e[0][1], e[0][1], e[0][2] * e[0][2]));
+        p.b.y = sc * fmaf(e[1][0], e[1][0], fmaf(e[1][1], e[1][1], e[1][2] * e[1][2]));
+        p.b.z = sc * fmaf(e[2][0], e[2][0], fmaf(e[2][1], e[2][1], e[2][2] * e[2][2]));
+        p.b.w = 2.f * sc * fmaf(e[0][0], e[1][0], fmaf(e[0][1], e[1][1], e[0][2] * e[1][2]));
+        p.c.x = 2.f * sc * fmaf(e[0][0], e[2][0], fmaf(e[0][1], e[2][1], e[0][2] * e[2][2]));
+        p.c.y = 2.f * sc * fmaf(e[1][0], e[2][0], fmaf(e[1][1], e[2][1], e[1][2] * e[2][2]));
+        p.c.z = q2.y;
+        const float qmag = fabsf(p.a.x) + ext_x * fabsf(p.a.y) + ext_y * fabsf(p.a.z) +
+                           ext_z * fabsf(p.a.w) + ext_x * ext_x * fabsf(p.b.x) +
+                           ext_y * ext_y * fabsf(p.b.y) + ext_z * ext_z * fabsf(p.b.z) +
+                           ext_x * ext_y * fabsf(p.b.w) + ext_x * ext_z * fabsf(p.c.x) +
+                           ext_y * ext_z * fabsf(p.c.y);
+        const float guard = isinf(cut2) ? 0.f
+                            : 0.72134752f * (kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2)) +
+                                  2.5e-6f * qmag;
+        const float qcut = isinf(cut2) ? -INFINITY : fmaf(sc, cut2, lr2);
+        p.c.w = qcut + guard;
+        p.d = make_float4(qcut - guard, __int_as_float(gid), 0.f, 0.f);
+      }
+    }
+    const unsigned ball = __ballot_sync(kFull, hit);
+    if (hit) wsp[__popc(ball & ((1u << lane) - 1u))] = p;
+    __syncwarp();
+    const int nh = __popc(ball);
+    for (int jj = 0; jj < nh; ++jj) {
+      const float4 pa = wsp[jj].a, pb = wsp[jj].b, pc = wsp[jj].c;
+      const float2 pd = *reinterpret_cast<const float2*>(&wsp[jj].d);   // qlo, gid
+      float q[2][Z];
+      const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
+      const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
+      const float t3 = fmaf(pb.z, mZ, pa.w);
+      q[0][0] = fmaf(mX, t1, fmaf(mY, t2, fmaf(mZ, t3, pa.x)));
+      // column B (y + 4): q += 4 (a_z + b_w X + c_y Z + b_y (2Y + 4)); dq += 4 c_y
+      q[1][0] = fmaf(4.f, fmaf(pb.y, twoY4, fmaf(pc.y, mZ, fmaf(pb.w, mX, pa.z))), q[0][0]);
+      float dqA = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, mZ1, t3)));
+      float dqB = fmaf(4.f, pc.y, dqA);
+      const float d2q = 2.f * pb.z;
+#pragma unroll
+      for (int h = 1; h < Z; ++h) {
+        q[0][h] = q[0][h - 1] + dqA;
+        q[1][h] = q[1][h - 1] + dqB;
+        dqA += d2q;
+        dqB += d2q;
+      }
+      bool live[2][Z];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int h = 0; h < Z; ++h) {
+          live[c][h] = q[c][h] >= pc.w;
+          const float w = ex2_approx(q[c][h]);
+          if (live[c][h]) {
+            aS[c][h] = fmaf(pc.z, w, aS[c][h]);
+            aW[c][h] += w;
+          }
+        }
+      bool band = false;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int h = 0; h < Z; ++h) band |= !live[c][h] && q[c][h] >= pd.x;
+      if (__any_sync(kFull, band)) {
+        const int gidj = __float_as_int(pd.y);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int h = 0; h < Z; ++h)
+            if (!live[c][h] && q[c][h] >= pd.x &&
+                exact_live(gidj, gx, c ? gyB : gyA, gz + h, xsrc, g, cut2d)) {
+              const float w = ex2_approx(q[c][h]);
+              aS[c][h] = fmaf(pc.z, w, aS[c][h]);
+              aW[c][h] += w;
+            }
+      }
+    }
+    __syncwarp();
+  }
+  // Epilogue: normalise, store, fused loss (optimize.py:91-103).
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int h = 0; h < Z; ++h) {
+      const int ly = c ? lyB : lyA;
+      if (!(lx < bg.ex && ly < bg.ey && h < bg.ez)) continue;
+      const int64_t lin = (int64_t)gx + (int64_t)g.nx * ((bg.y0 + ly) + (int64_t)g.ny * (gz + h));
+      const bool cov = (double)aW[c][h] >= eps_w;
+      const float iv = cov ? __fdiv_rn(aS[c][h], aW[c][h]) : 0.f;
+      S[lin] = aS[c][h];
+      W[lin] = aW[c][h];
+      I[lin] = iv;
+      if (target) {
+        const double d = (double)iv - (double)target[lin];
+        double dl;
+        if (loss_kind == 0) {
+          lsum += fabs(d);
+          dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / vox_count;
+        } else {
+          lsum += d * d;
+          dl = 2.0 * d / vox_count;
+        }
+        const float alpha = (cov && dl != 0.0) ? (float)(dl / (double)aW[c][h]) : 0.f;
+        ab[lin] = make_float2(alpha, iv);
+      }
+    }
+  if (target) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(kFull, lsum, o);
+    if (lane == 0) loss_part[lb] = lsum;
+  }
+}
+
 // --------------------------------------------------------------- forward f64
 struct __align__(16) Pair64 {
   double l[9];
@@ -1321,7 +1519,19 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
     // vpl | 0x200: keep the two tiles of a VPL-4 brick in one CTA (measurement)
     const bool no_split = (vpl & 0x200) != 0;
     vpl &= 0xff;
-    GSV_REQUIRE(vpl == 0 || vpl == 2 || vpl == 4, "vpl must be 0, 2 or 4");
+    GSV_REQUIRE(vpl == 0 || vpl == 2 || vpl == 4 || vpl == 8, "vpl must be 0, 2, 4 or 8");
+    if (vpl == 8) {
+      // one warp per 8x8x4 brick, two 4-voxel columns per lane (renders)
+      GSV_REQUIRE(bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4 &&
+                      live_masks == nullptr,
+                  "vpl 8 needs 8x8x4 bricks and no live masks");
+      const ExactSrc xw{positions, log_scales, rotations, rec64};
+      forward32w_kernel<<<(unsigned)nb, 32, 0, s>>>(
+          positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
+          (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab, loss_part);
+      GSV_CHECK_LAUNCH("forward32w_kernel");
+      return GSV_OK;
+    }
     if (vpl == 0) vpl = mask_vpl_auto(*bricks);
     if (live_masks != nullptr)
       GSV_REQUIRE(mask_units(*bricks, vpl) == (vpl == 4 ? 64 : 128),

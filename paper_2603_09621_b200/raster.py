@@ -308,9 +308,15 @@ def _resolve_vpl(brick_dims) -> int:
     return 4 if bz % 4 == 0 and bx * by * (bz // 4) <= 64 else 2
 
 
-def _forward_vpl_arg(brick_dims) -> int:
-    """gsv_forward's vpl argument: the resolved depth, | 0x200 to keep a
-    brick's two VPL-4 tiles in one CTA when GSV_NO_SPLIT is set (measurement)."""
+def _forward_vpl_arg(brick_dims, pairs: int = 0, n: int = 0, masks: bool = True) -> int:
+    """gsv_forward's vpl argument.  Renders (no live masks) of large Gaussians
+    on 8x8x4 bricks -- pairs >= 8 N, so nearly every pair covers the whole
+    brick -- use 8: one warp per brick, two columns per lane.  Otherwise the
+    resolved depth, | 0x200 to keep a brick's two VPL-4 tiles in one CTA when
+    GSV_NO_SPLIT is set (measurement; GSV_NO_WHOLE disables vpl 8)."""
+    if (not masks and tuple(brick_dims) == (8, 8, 4) and n > 0 and pairs >= 8 * n
+            and not os.environ.get("GSV_NO_WHOLE") and not os.environ.get("GSV_VPL")):
+        return 8
     return _resolve_vpl(brick_dims) | (0x200 if os.environ.get("GSV_NO_SPLIT") else 0)
 
 
@@ -332,7 +338,8 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
-        _forward_vpl_arg(idx.brick_dims), _lib.stream_ptr()), "forward")
+        _forward_vpl_arg(idx.brick_dims, idx.pair_count, f.count, live_masks is not None),
+        _lib.stream_ptr()), "forward")
 
 
 def forward(f: GaussianField, grid: GridSpec, idx: BrickIndex,

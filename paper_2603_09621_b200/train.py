@@ -726,7 +726,8 @@ class Renderer:
             b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
             float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
             b["W"].data_ptr(), b["I"].data_ptr(), None, 0, float(self.grid.num_voxels), None,
-            None, None, _forward_vpl_arg(self.brick_dims), s), "forward")
+            None, None, _forward_vpl_arg(self.brick_dims, b["pairs"], n, masks=False), s),
+            "forward")
 
     def _capture(self, f: GaussianField, key, min_cap: int = 0):
         import ctypes
@@ -751,6 +752,7 @@ class Renderer:
         nbytes = ctypes.c_size_t(0)
         _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
         nv = self.grid.num_voxels
+        b["pairs"] = pairs                   # picks the forward's tiling (vpl 8 for large)
         b.update({"ws": gp.get("ws", (nbytes.value,), torch.uint8),
                   "keys": gp.get("keys", (3, cap), torch.int32),
                   "gids": gp.get("gids", (cap,), torch.int32),
