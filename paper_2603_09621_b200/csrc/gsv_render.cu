@@ -503,7 +503,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
 // the columns (x, y) = (l & 7, l >> 3) and (x, y + 4), all 4 z.  A pair is
 // staged and its quadratic built once per brick; column B's start value and
 // z-step follow from column A's in 5 FMAs.  No live masks (renders only).
-__global__ void __launch_bounds__(32, GSV_FWD_OCC / 32)
+__global__ void __launch_bounds__(32, 16)
 forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
                   const gsv_record32* __restrict__ rec,
                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
