@@ -339,6 +339,19 @@ int gsv_ssim3d(const void* x, int x_f64, const void* y, int y_f64, const gsv_gri
                const double* window11, void* workspace, size_t workspace_bytes,
                double* out, void* stream);
 
+/* Per-Gaussian geometry helpers of the reference API, f64 on the device:
+ * gsv_rotation_matrices: R (N,3,3) from the stored quaternions, verbatim
+ *   (field.py:141-154).
+ * gsv_sigma_inv: Sigma^-1 = R diag(exp(-2 ls)) R^T (N,3,3) (render.py:67-71).
+ * gsv_weight: *out = weight of Gaussian i at world point p, 0 beyond the
+ *   cutoff (render.py:74-81). */
+int gsv_rotation_matrices(const double* rotations, int64_t n, double* R, void* stream);
+int gsv_sigma_inv(const double* log_scales, const double* rotations, int64_t n, double* out,
+                  void* stream);
+int gsv_weight(const double* positions, const double* log_scales, const double* rotations,
+               const double* raw_relax, int64_t n, int64_t i, int relax_enabled, double px,
+               double py, double pz, double cutoff_sigma, double* out, void* stream);
+
 /* Brute-force O(N*V) render (render_naive / _naive_kernel, render.py:84-127)
  * on the device, Sigma^-1 quadratic form, f64 math.  precision selects the
  * accumulator / output type. */

@@ -12,7 +12,8 @@ __version__ = "0.1.0"
 from .errors import (FormatError, GridMismatchError, GsvolError, NumericalError,
                      StaleIndexError)
 from .volume import (GridSpec, Volume, downsample_grid, ensure_unit_range,
-                     grid_covering_extent, normalize_intensity, resample_trilinear)
+                     grid_covering_extent, load_volume, normalize_intensity,
+                     resample_trilinear, save_volume)
 from .field import (GaussianField, InitConfig, init_from_volume, load_field, random_field,
                     save_field)
 from .render import RenderOptions, render_naive, weight
@@ -27,7 +28,7 @@ __all__ = [
     "__version__",
     "GsvolError", "FormatError", "GridMismatchError", "StaleIndexError", "NumericalError",
     "GridSpec", "Volume", "normalize_intensity", "ensure_unit_range", "resample_trilinear",
-    "grid_covering_extent", "downsample_grid",
+    "grid_covering_extent", "downsample_grid", "save_volume", "load_volume",
     "GaussianField", "InitConfig", "init_from_volume", "random_field", "save_field",
     "load_field",
     "RenderOptions", "render_naive", "weight",

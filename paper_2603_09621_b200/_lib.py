@@ -89,6 +89,10 @@ _SIGS = {
     "gsv_sq_diff_sum": [c_vp, c_int, c_vp, c_int, c_i64, c_vp, c_vp, c_vp],
     "gsv_ssim3d_workspace": [GP, c_szp],
     "gsv_ssim3d": [c_vp, c_int, c_vp, c_int, GP, c_vp, c_vp, ctypes.c_size_t, c_vp, c_vp],
+    "gsv_rotation_matrices": [c_vp, c_i64, c_vp, c_vp],
+    "gsv_sigma_inv": [c_vp, c_vp, c_i64, c_vp, c_vp],
+    "gsv_weight": [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_int, c_dbl, c_dbl, c_dbl, c_dbl,
+                   c_vp, c_vp],
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
     # include/gsv_diag.h (measurement only)

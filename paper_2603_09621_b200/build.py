@@ -26,7 +26,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
 # FMA (bit-exact bounds vs numpy, SURVEY.md §0 finding 1).
 EXTRA = {"gsv_bin.cu": ["-fmad=false"]}
 SOURCES = ["gsv_capi.cu", "gsv_bin.cu", "gsv_render.cu", "gsv_train.cu", "gsv_metrics.cu",
-           "gsv_diag.cu"]
+           "gsv_util.cu", "gsv_diag.cu"]
 
 
 def _headers():

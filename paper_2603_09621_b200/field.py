@@ -140,6 +140,21 @@ class GaussianField:
         return [getattr(self, name) for name in PARAM_NAMES]
 
 
+def rotation_matrices(quats) -> torch.Tensor:
+    """(N,4) w,x,y,z quaternions -> (N,3,3) rotation matrices, applied
+    verbatim without normalisation (field.py:141-154); f64 on the device
+    (gsv_rotation_matrices)."""
+    lib = _lib.lib()
+    q = torch.as_tensor(quats, dtype=torch.float64)
+    if q.device.type != "cuda":
+        q = q.to(torch.device("cuda", torch.cuda.current_device()))
+    q = q.reshape(-1, 4).contiguous()
+    out = torch.empty((q.shape[0], 3, 3), dtype=torch.float64, device=q.device)
+    _lib.check(lib.gsv_rotation_matrices(q.data_ptr(), q.shape[0], out.data_ptr(),
+                                         _lib.stream_ptr()), "rotation_matrices")
+    return out
+
+
 @dataclass(frozen=True)
 class InitConfig:
     """Initialization knobs (field.py:191-209)."""

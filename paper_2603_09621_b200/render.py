@@ -7,7 +7,6 @@ API-compatible cross-check of the brick engine.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -64,25 +63,24 @@ def render_naive(f: GaussianField, grid: GridSpec, opts: RenderOptions = RenderO
     return Volume.from_linear(grid, out)
 
 
-def weight(f: GaussianField, i: int, p, opts: RenderOptions = RenderOptions()) -> float:
-    """Spatial weight of Gaussian i at world point p (render.py:74-81).
+def field_sigma_inv(f: GaussianField) -> torch.Tensor:
+    """Per-Gaussian inverse covariances R diag(s^-2) R^T, (N,3,3) f64 on the
+    device (render.py:67-71; gsv_sigma_inv)."""
+    lib = _lib.lib()
+    out = torch.empty((f.count, 3, 3), dtype=torch.float64, device=f.device)
+    _lib.check(lib.gsv_sigma_inv(f.log_scales.data_ptr(), f.rotations.data_ptr(), f.count,
+                                 out.data_ptr(), _lib.stream_ptr()), "sigma_inv")
+    return out
 
-    A scalar API helper (one Gaussian, one point) evaluated from that
-    Gaussian's parameters; not part of the rendering path.
-    """
-    q = f.rotations[i].detach().cpu().numpy()
-    ls = f.log_scales[i].detach().cpu().numpy()
-    mu = f.positions[i].detach().cpu().numpy()
-    w, x, y, z = q
-    r = np.array([
-        [1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
-        [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
-        [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)],
-    ])
-    sigma_inv = r @ np.diag(np.exp(-2.0 * ls)) @ r.T
-    delta = np.asarray(p, dtype=np.float64) - mu
-    d2 = float(delta @ sigma_inv @ delta)
-    if d2 > opts.cutoff_sq:
-        return 0.0
-    relax = 1.0 if not f.relax_enabled else 1.0 / (1.0 + math.exp(-float(f.raw_relax[i])))
-    return math.exp(-0.5 * d2) * relax
+
+def weight(f: GaussianField, i: int, p, opts: RenderOptions = RenderOptions()) -> float:
+    """Spatial weight of Gaussian i at world point p, truncation included
+    (render.py:74-81), evaluated on the device (gsv_weight)."""
+    lib = _lib.lib()
+    px, py, pz = (float(v) for v in np.asarray(p, dtype=np.float64).reshape(3))
+    out = torch.empty(1, dtype=torch.float64, device=f.device)
+    _lib.check(lib.gsv_weight(
+        f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+        f.raw_relax.data_ptr(), f.count, int(i), int(f.relax_enabled), px, py, pz,
+        float(opts.cutoff_sigma), out.data_ptr(), _lib.stream_ptr()), "weight")
+    return float(out.item())

@@ -221,3 +221,15 @@ def downsample_grid(ref: GridSpec, factor) -> GridSpec:
     size_lr = np.asarray(dims) * np.asarray(spacing)
     origin = lo + 0.5 * (size_ref - size_lr) + 0.5 * np.asarray(spacing)
     return GridSpec(dims, spacing, tuple(origin))
+
+
+def save_volume(v: Volume, path: str, format: str | None = None) -> None:
+    """Reference location of the volume writer (volume.py:208-217); see volume_io."""
+    from .volume_io import save_volume as _save
+    _save(v, path, format)
+
+
+def load_volume(path: str, format: str | None = None) -> Volume:
+    """Reference location of the volume reader (volume.py:220-229); see volume_io."""
+    from .volume_io import load_volume as _load
+    return _load(path, format)

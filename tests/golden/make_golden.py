@@ -180,6 +180,79 @@ def metrics():
     return out
 
 
+IO_DIR = os.path.join(HERE, "io")
+
+
+def volume_io():
+    """Files written by the reference's save_volume (raw_json, NIfTI-1), and a
+    big-endian int16 NIfTI with scl_slope/scl_inter read by its load_volume."""
+    import hashlib
+    import struct
+    from gsvol import Volume
+    from gsvol.volume import load_volume, save_volume
+    os.makedirs(IO_DIR, exist_ok=True)
+    rng = np.random.default_rng(17)
+    g = GridSpec((7, 5, 4), (0.8, 1.1, 2.5), (-3.0, 0.25, 10.0))
+    v = Volume(g, rng.uniform(0.0, 1.0, g.dims).astype(np.float32))
+    save_volume(v, os.path.join(IO_DIR, "ref.json"))
+    save_volume(v, os.path.join(IO_DIR, "ref.nii"))
+    # int16, big endian, slope 0.5 intercept -2, identity qform with offsets
+    h = bytearray(348)
+    struct.pack_into(">i", h, 0, 348)
+    struct.pack_into(">8h", h, 40, 3, 6, 4, 3, 1, 1, 1, 1)
+    struct.pack_into(">h", h, 70, 4)
+    struct.pack_into(">h", h, 72, 16)
+    struct.pack_into(">8f", h, 76, 1.0, 1.5, 2.0, 0.5, 0, 0, 0, 0)
+    struct.pack_into(">f", h, 108, 352.0)
+    struct.pack_into(">f", h, 112, 0.5)
+    struct.pack_into(">f", h, 116, -2.0)
+    struct.pack_into(">h", h, 252, 1)
+    struct.pack_into(">3f", h, 268, 1.0, -2.0, 3.0)
+    struct.pack_into(">4s", h, 344, b"n+1\x00")
+    vals = rng.integers(-300, 300, size=6 * 4 * 3).astype(">i2")
+    with open(os.path.join(IO_DIR, "i16_be.nii"), "wb") as fh:
+        fh.write(bytes(h) + bytes(4) + vals.tobytes())
+    w = load_volume(os.path.join(IO_DIR, "i16_be.nii"))
+    import tempfile
+    from gsvol.errors import FormatError
+    sys.path.insert(0, HERE)
+    import io_cases
+    errors, accepted = {}, {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, make in io_cases.cases(IO_DIR).items():
+            p = make(td)
+            try:
+                load_volume(p)
+                errors[name] = None
+            except FormatError as exc:
+                errors[name] = str(exc).replace(p, "<path>").replace(
+                    os.path.join(td, "case.bin"), "<bin>")
+        for name, make in io_cases.accepted(IO_DIR).items():
+            a = load_volume(make(td))
+            accepted[name] = {"spacing": list(a.grid.spacing), "origin": list(a.grid.origin),
+                              "sha256": hashlib.sha256(
+                                  np.ascontiguousarray(a.linear(), "<f4").tobytes()).hexdigest()}
+    from gsvol.field import load_field as ref_load_field, random_field as ref_random_field
+    from gsvol.field import save_field as ref_save_field
+    fl = ref_random_field(9, g, seed=23)
+    fl.raw_relax[:] = np.linspace(-2.0, 2.0, 9)
+    ref_save_field(fl, os.path.join(IO_DIR, "ref_relax.gsv"))
+    fl.relax_enabled = False
+    ref_save_field(fl, os.path.join(IO_DIR, "ref_norelax.gsv"))
+    back = ref_load_field(os.path.join(IO_DIR, "ref_relax.gsv"))
+    field_values = {k: np.asarray(getattr(back, k)).tolist() for k in
+                    ("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax")}
+    digest = lambda p: hashlib.sha256(open(os.path.join(IO_DIR, p), "rb").read()).hexdigest()
+    return {"volume_seed": 17, "dims": list(g.dims), "spacing": list(g.spacing),
+            "origin": list(g.origin),
+            "sha256": {n: digest(n) for n in ("ref.json", "ref.bin", "ref.nii", "ref_relax.gsv",
+                                              "ref_norelax.gsv")},
+            "field_seed": 23, "field_loaded": field_values,
+            "i16_be": {"dims": list(w.grid.dims), "spacing": list(w.grid.spacing),
+                       "origin": list(w.grid.origin), "linear": w.linear().tolist()},
+            "errors": errors, "accepted": accepted}
+
+
 def full_configs():
     """Bit-exact binning hashes at BASELINE sizes + sampled forward values."""
     res = {}
@@ -209,7 +282,7 @@ def full_configs():
 
 def main():
     meta = {"versions": versions(), "generated_by": "tests/golden/make_golden.py"}
-    which = set(sys.argv[1:]) or {"sweep", "config1", "full", "fit", "metrics"}
+    which = set(sys.argv[1:]) or {"sweep", "config1", "full", "fit", "metrics", "io"}
     if "sweep" in which:
         with open(os.path.join(HERE, "sweep.json"), "w") as fh:
             json.dump({"meta": meta, "cases": sweep()}, fh)
@@ -223,6 +296,10 @@ def main():
     if "full" in which:
         with open(os.path.join(HERE, "full_configs.json"), "w") as fh:
             json.dump({"meta": meta, "configs": full_configs()}, fh)
+    if "io" in which:
+        with open(os.path.join(HERE, "volume_io.json"), "w") as fh:
+            json.dump({"meta": meta, **volume_io()}, fh, indent=1)
+        print("io done", flush=True)
     if "metrics" in which:
         with open(os.path.join(HERE, "metrics.json"), "w") as fh:
             json.dump({"meta": meta, "cases": metrics()}, fh, indent=1)
