@@ -12,7 +12,8 @@ CUDA events, inputs resident in HBM.  The same line carries the 256^3 render
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1: launched by torch.distributed.run, one rank per GPU; each rank owns a
-contiguous z-slab of brick layers; one NCCL all_reduce per train step.
+contiguous brick-id range (cuts balanced by pairs per brick, mid-layer cuts
+allowed); one NCCL all_reduce per train step.
 --impl reference: the reference's CPU algorithm (oracle/ port, OpenMP, all
 host cores) on the same config, rank 0 only.
 """
@@ -128,7 +129,7 @@ def dist_setup(args):
     return None, 1, 0, 0
 
 
-from paper_2603_09621_b200.distributed import slab_ranges  # noqa: E402
+from paper_2603_09621_b200.distributed import pair_weights, slab_for_rank  # noqa: E402
 
 
 def problem_for(cfg_id):
@@ -182,7 +183,8 @@ def _config_dict(args, p, pairs, ws):
                         f"(x2 -> {p['hr_grid'].dims} HR), N={p['field'][0].shape[0]} Gaussians",
             "lr_dims": list(p["lr_grid"].dims), "hr_dims": list(p["hr_grid"].dims),
             "N": int(p["field"][0].shape[0]), "pairs_lr": pairs, "brick_dims": [8, 8, 4],
-            "loss": "l1", "optimizer": "Adam (f64 master)", "parallelism": f"z-slab x{ws}",
+            "loss": "l1", "optimizer": "Adam (f64 master)",
+            "parallelism": f"brick-range slabs x{ws} (pair-balanced)",
             "l2": "inputs larger than L2 (f64 field + Adam moments = 0.7 GB, pairs 0.1 GB)"}
 
 
@@ -200,13 +202,15 @@ def run_ours(args, dist, ws, rank, local):
     lr = gs.Volume(lr_grid, p["lr"])
     opts = gs.RenderOptions()
     bd = (8, 8, 4)
-    lr_layers = -(-lr_grid.dims[2] // bd[2])
-    hr_layers = -(-hr_grid.dims[2] // bd[2])
-    my_slab = slab_ranges(lr_layers, ws)[rank] if ws > 1 else None
-    my_hr_slab = slab_ranges(hr_layers, ws)[rank] if ws > 1 else None
     group = dist.group.WORLD if dist else None
 
     f = gs.GaussianField(*p["field"], device=dev)
+    # slabs: contiguous brick-id ranges balanced by the pair count per brick
+    # (one whole-grid binning pass at setup, identical on every rank)
+    my_slab = slab_for_rank(lr_grid, bd, rank, ws, pair_weights(f, lr_grid, opts, bd)) \
+        if ws > 1 else None
+    my_hr_slab = slab_for_rank(hr_grid, bd, rank, ws, pair_weights(f, hr_grid, opts, bd)) \
+        if ws > 1 else None
     state = gs.AdamState.create(f)
     lrs = gs.FitConfig().resolved_lrs(lr_grid.spacing)
     timer = PhaseTimer()
@@ -298,7 +302,8 @@ def run_ours(args, dist, ws, rank, local):
         arr5 = synth.jitter_field([np.asarray(a) for a in p["field"]], lr_grid)
         f5 = gs.GaussianField(*arr5, device=dev)
         g5 = gs.grid_covering_extent(lr_grid, (512, 512, 512))
-        slab5 = slab_ranges(-(-512 // bd[2]), ws)[rank] if ws > 1 else None
+        slab5 = slab_for_rank(g5, bd, rank, ws, pair_weights(f5, g5, opts, bd)) \
+            if ws > 1 else None
 
         r5_renderer = gs.Renderer(g5, opts, bd, slab=slab5, device=dev)
 

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GSV_ABI_VERSION 2
+#define GSV_ABI_VERSION 3
 
 typedef enum {
   GSV_OK = 0,
@@ -54,14 +54,16 @@ typedef struct {
   double sx, sy, sz;
 } gsv_grid;
 
-/* Brick decomposition (raster.py:152-156) plus the z-slab [bz0, bz1) of brick
- * layers this call owns.  A whole-grid call uses bz0 = 0, bz1 = bgz.  The
- * slab's bricks are the contiguous brick-id range [bgx*bgy*bz0, bgx*bgy*bz1)
- * (SURVEY.md §8e), so a slab index is an exact slice of the global index. */
+/* Brick decomposition (raster.py:152-156) plus the slab this call owns: the
+ * contiguous brick-id range [b0, b1) (bricks numbered x-fastest,
+ * raster.py:209).  A whole-grid call uses b0 = 0, b1 = bgx*bgy*bgz.  Any
+ * contiguous range is an exact slice of the global index, so
+ * slabs may cut a brick layer anywhere: whole z-layers are the special case
+ * b0, b1 multiples of bgx*bgy. */
 typedef struct {
   int32_t bdx, bdy, bdz;
   int32_t bgx, bgy, bgz;
-  int32_t bz0, bz1;
+  int32_t b0, b1;
 } gsv_bricks;
 
 /* Per-Gaussian fp32 record consumed by the pair kernels (64 bytes). */

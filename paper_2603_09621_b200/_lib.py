@@ -33,7 +33,7 @@ class GsvGrid(ctypes.Structure):
 class GsvBricks(ctypes.Structure):
     _fields_ = [("bdx", c_i32), ("bdy", c_i32), ("bdz", c_i32),
                 ("bgx", c_i32), ("bgy", c_i32), ("bgz", c_i32),
-                ("bz0", c_i32), ("bz1", c_i32)]
+                ("b0", c_i32), ("b1", c_i32)]
 
 
 class GsvAdamHparams(ctypes.Structure):
@@ -102,7 +102,7 @@ _SIGS = {
 _RESTYPES = {"gsv_last_error": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 2        # GSV_ABI_VERSION of include/gsv.h these signatures follow
+ABI_VERSION = 3        # GSV_ABI_VERSION of include/gsv.h these signatures follow
 
 _lib = None
 
@@ -169,8 +169,8 @@ def make_bricks(grid, brick_dims, slab=None) -> GsvBricks:
     bdx, bdy, bdz = brick_dims
     nx, ny, nz = grid.dims
     bgx, bgy, bgz = -(-nx // bdx), -(-ny // bdy), -(-nz // bdz)
-    bz0, bz1 = (0, bgz) if slab is None else slab
-    return GsvBricks(bdx, bdy, bdz, bgx, bgy, bgz, bz0, bz1)
+    b0, b1 = (0, bgx * bgy * bgz) if slab is None else slab
+    return GsvBricks(bdx, bdy, bdz, bgx, bgy, bgz, b0, b1)
 
 
 _ws_cache: dict = {}

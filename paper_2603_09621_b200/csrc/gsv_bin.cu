@@ -70,14 +70,15 @@ emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__
   const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31;
   if (g0 >= n) return;                       // warp-uniform
   const int64_t g = g0 + lane;
-  int c = 0, nbx = 1, nby = 1, kb = 0;
+  int c = 0, nbx = 1, nby = 1, kb = 0, k0 = 0;
   if (g < n) {
     c = counts[g];
     if (c > 0) {
       const GBox b = unpack_box(box, g);
       nbx = b.nb_x;
       nby = b.nb_y;
-      kb = b.blo_x + k.bgx * (b.blo_y + k.bgy * (b.blo_z - k.bz0));   // slab-local id
+      k0 = b.k0;                            // the slab's run starts k0 into the box
+      kb = b.blo_x + k.bgx * (b.blo_y + k.bgy * b.blo_z) - k.b0;   // slab-local id
     }
   }
   int incl = c;
@@ -95,8 +96,8 @@ emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__
     // this lane's pairs inside [w0, w0 + kEmitWin)
     const int r0 = max(0, w0 - off), r1 = min(c, w0 + kEmitWin - off);
     if (r0 < r1) {
-      int rx = r0 % nbx;
-      const int t = r0 / nbx;
+      int rx = (r0 + k0) % nbx;
+      const int t = (r0 + k0) / nbx;
       int ry = t % nby, rz = t / nby;
       int key = kb + rx + k.bgx * ry + bxy * rz;
       const int gid = (int)g;

@@ -35,10 +35,10 @@ int validate_grid_bricks(const gsv_grid* g, const gsv_bricks* k) {
               "brick grid does not match ceil(dims / brick_dims)");
   GSV_REQUIRE(k->bgx <= 65535 && k->bgy <= 65535 && k->bgz <= 65535,
               "brick grid above 65535 per axis is not supported");
-  GSV_REQUIRE(0 <= k->bz0 && k->bz0 <= k->bz1 && k->bz1 <= k->bgz,
-              "slab [%d,%d) outside brick layers [0,%d)", k->bz0, k->bz1, k->bgz);
   GSV_REQUIRE((int64_t)k->bgx * k->bgy * k->bgz < (int64_t)INT32_MAX,
               "too many bricks");
+  GSV_REQUIRE(0 <= k->b0 && k->b0 <= k->b1 && k->b1 <= k->bgx * k->bgy * k->bgz,
+              "slab [%d,%d) outside brick ids [0,%d)", k->b0, k->b1, k->bgx * k->bgy * k->bgz);
   return GSV_OK;
 }
 

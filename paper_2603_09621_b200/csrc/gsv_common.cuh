@@ -104,8 +104,12 @@ __device__ __forceinline__ BrickXYZ brick_xyz(int b, const gsv_bricks& k) {
 }
 
 // Unpack the per-Gaussian slab-clipped brick box written by preprocess.
+// k0 = box-order index (x-fastest within the box) of the first brick inside
+// the slab's id range; the slab's bricks of the box are box-order
+// [k0, k0 + counts[i]) (box order and brick-id order are both lexicographic
+// in (z, y, x), so an id range meets a box in one contiguous run).
 struct GBox {
-  int blo_x, blo_y, blo_z, nb_x, nb_y, nb_z;
+  int blo_x, blo_y, blo_z, nb_x, nb_y, nb_z, k0;
 };
 __device__ __forceinline__ GBox unpack_box(const int32_t* box, int64_t i) {
   const int4 b = reinterpret_cast<const int4*>(box)[i];
@@ -116,14 +120,23 @@ __device__ __forceinline__ GBox unpack_box(const int32_t* box, int64_t i) {
   r.nb_x = (b.y >> 16) & 0xFFFF;
   r.nb_y = b.z & 0xFFFF;
   r.nb_z = (b.z >> 16) & 0xFFFF;
+  r.k0 = b.w;
   return r;
+}
+// Slot of brick (bx, by, bz) in the Gaussian's run of pair slots (the order
+// binning emitted them: box order from k0), or -1 if binning emitted none.
+__device__ __forceinline__ int64_t box_slot(const GBox& gb, int bx, int by, int bz) {
+  const int rx = bx - gb.blo_x, ry = by - gb.blo_y, rz = bz - gb.blo_z;
+  if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) return -1;
+  const int64_t k = rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz) - gb.k0;
+  return k >= 0 ? k : -1;
 }
 
 __host__ __device__ inline int64_t slab_bricks(const gsv_bricks& k) {
-  return (int64_t)k.bgx * k.bgy * (k.bz1 - k.bz0);
+  return (int64_t)k.b1 - k.b0;
 }
 __host__ __device__ inline int64_t slab_first(const gsv_bricks& k) {
-  return (int64_t)k.bgx * k.bgy * k.bz0;
+  return k.b0;
 }
 
 int validate_grid_bricks(const gsv_grid* g, const gsv_bricks* k);

@@ -37,6 +37,23 @@ struct PrepArgs {
   int32_t* box;
 };
 
+// Number of bricks of the box (origin blo, extent nb) whose brick id is < b;
+// the box's bricks in x-fastest order have increasing ids.  Brick ids fit in
+// int32 (validate_grid_bricks).
+__device__ __forceinline__ int box_rank(int b, const int64_t blo[3], const int nb[3], int bgx,
+                                        int plane) {
+  const int z = b / plane, rem = b - z * plane;
+  const int y = rem / bgx, x = rem - y * bgx;
+  const int dz = z - (int)blo[2], dy = y - (int)blo[1], dx = x - (int)blo[0];
+  if (dz < 0) return 0;
+  if (dz >= nb[2]) return nb[0] * nb[1] * nb[2];
+  int r = nb[0] * nb[1] * dz;
+  if (dy < 0) return r;
+  if (dy >= nb[1]) return r + nb[0] * nb[1];
+  r += nb[0] * dy;
+  return r + (dx < 0 ? 0 : (dx >= nb[0] ? nb[0] : dx));
+}
+
 // Records, pair count and slab-clipped brick box of Gaussian i from its
 // (position, log-scales, unit quaternion, raw amplitude, raw relax).
 __device__ __forceinline__ void preprocess_one(int64_t i, const double p[3], const double l[3],
@@ -93,7 +110,7 @@ __device__ __forceinline__ void preprocess_one(int64_t i, const double p[3], con
     pa.rec64[i] = d;
   }
 
-  // ---- brick box (raster.py:160-198), clipped to the slab [bz0, bz1).
+  // ---- brick box (raster.py:160-198), clipped to the slab below.
   const gsv_grid& g = pa.g;
   const gsv_bricks& k = pa.k;
   const int dims[3] = {g.nx, g.ny, g.nz};
@@ -124,22 +141,38 @@ __device__ __forceinline__ void preprocess_one(int64_t i, const double p[3], con
       bhi[a] = vhi / bd[a];
     }
   }
-  // z-slab clip: the slab owns brick layers [bz0, bz1).
-  if (blo[2] < k.bz0) blo[2] = k.bz0;
-  if (bhi[2] > k.bz1 - 1) bhi[2] = k.bz1 - 1;
-  int64_t cnt = 0;
+  // Slab clip: the slab owns brick ids [b0, b1).  First the
+  // box is clipped to the brick layers the range touches; then, since box
+  // order and id order are both lexicographic in (z, y, x), the slab's bricks
+  // of the box are the box-order run [k0, k1) with k = #box bricks of id < b.
+  const int plane = bg[0] * bg[1];
+  int cnt = 0, k0 = 0;
   int nb[3] = {0, 0, 0};
-  if (inside && bhi[2] >= blo[2]) {
+  if (k.b1 > k.b0) {
+    const bool whole = k.b0 == 0 && k.b1 == plane * bg[2];
+    if (!whole) {
+      const int zlo = k.b0 / plane, zhi = (k.b1 - 1) / plane;
+      if (blo[2] < zlo) blo[2] = zlo;
+      if (bhi[2] > zhi) bhi[2] = zhi;
+    }
+    if (inside && bhi[2] >= blo[2]) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) nb[a] = (int)(bhi[a] - blo[a] + 1);
-    cnt = (int64_t)nb[0] * nb[1] * nb[2];
+      for (int a = 0; a < 3; ++a) nb[a] = (int)(bhi[a] - blo[a] + 1);
+      if (whole) {
+        cnt = nb[0] * nb[1] * nb[2];
+      } else {
+        k0 = box_rank(k.b0, blo, nb, bg[0], plane);
+        cnt = box_rank(k.b1, blo, nb, bg[0], plane) - k0;
+      }
+    }
   }
-  pa.counts[i] = (int32_t)cnt;
+  if (cnt == 0) nb[0] = nb[1] = nb[2] = 0;
+  pa.counts[i] = cnt;
   int4 bx;
   bx.x = (int)(blo[0] & 0xFFFF) | ((int)(blo[1] & 0xFFFF) << 16);
   bx.y = (int)(blo[2] & 0xFFFF) | ((nb[0] & 0xFFFF) << 16);
   bx.z = (nb[1] & 0xFFFF) | ((nb[2] & 0xFFFF) << 16);
-  bx.w = 0;
+  bx.w = k0;
   reinterpret_cast<int4*>(pa.box)[i] = bx;
 }
 

@@ -810,11 +810,17 @@ forward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict_
 // ------------------------------------------------------------- backward prep
 template <typename T, typename T2>
 __global__ void backward_prep_kernel(const T* __restrict__ W, const T* __restrict__ I,
-                                     const double* __restrict__ dldi, gsv_grid g,
+                                     const double* __restrict__ dldi, gsv_grid g, gsv_bricks k,
                                      int64_t v0, int64_t v1, double eps_w, T2* __restrict__ ab,
                                      unsigned long long* bad) {
   const int64_t lin = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (lin >= v1) return;
+  {  // only the slab's voxels: brick id of the voxel in [b0, b1)
+    const int64_t x = lin % g.nx, t = lin / g.nx;
+    const int64_t y = t % g.ny, z = t / g.ny;
+    const int64_t b = x / k.bdx + k.bgx * (y / k.bdy + (int64_t)k.bgy * (z / k.bdz));
+    if (b < k.b0 || b >= k.b1) return;
+  }
   const double dl = dldi[lin];
   if (!isfinite(dl)) atomicMin(bad, (unsigned long long)lin);
   const double w = (double)W[lin];
@@ -1128,10 +1134,10 @@ backward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
       const float mu1 = fmaf(q0.y, acc[2], fmaf(q1.x, acc[3], q1.w * acc[4]));
       const float mu2 = fmaf(q0.z, acc[2], fmaf(q1.y, acc[3], q2.x * acc[4]));
       const GBox gb = unpack_box(box, gid);
-      const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
+      const int64_t slot = box_slot(gb, bc.bx, bc.by, bc.bz);
       // A caller-built list may hold a pair the binning would not emit: skip it.
-      if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
-      const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+      if (slot < 0) continue;
+      const int64_t e = gstart[gid] + slot;
       float4* dst = partials + 3 * e;
       dst[0] = make_float4(acc[0], acc[1], mu0, mu1);
       dst[1] = make_float4(mu2, acc[5], acc[6], acc[7]);
@@ -1344,9 +1350,10 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       const float mu0 = fmaf(q0.x, acc[2], fmaf(q0.w, acc[3], q1.z * acc[4]));
       const float mu1 = fmaf(q0.y, acc[2], fmaf(q1.x, acc[3], q1.w * acc[4]));
       const float mu2 = fmaf(q0.z, acc[2], fmaf(q1.y, acc[3], q2.x * acc[4]));
-      const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
-      if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
-      const int64_t e = gst + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+      const int64_t bs = box_slot(gb, bc.bx, bc.by, bc.bz);
+      // A caller-built list may hold a pair the binning would not emit: skip it.
+      if (bs < 0) continue;
+      const int64_t e = gst + bs;
       float4* dst = partials + 3 * e;
       dst[0] = make_float4(acc[0], acc[1], mu0, mu1);
       dst[1] = make_float4(mu2, acc[5], acc[6], acc[7]);
@@ -1420,10 +1427,10 @@ backward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict
       }
     }
     const GBox gb = unpack_box(box, gid);
-    const int rx = bc.bx - gb.blo_x, ry = bc.by - gb.blo_y, rz = bc.bz - gb.blo_z;
+    const int64_t slot = box_slot(gb, bc.bx, bc.by, bc.bz);
     // A caller-built list may hold a pair the binning would not emit: skip it.
-    if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z) continue;
-    const int64_t e = gstart[gid] + rx + (int64_t)gb.nb_x * (ry + (int64_t)gb.nb_y * rz);
+    if (slot < 0) continue;
+    const int64_t e = gstart[gid] + slot;
     double* dst = partials + 12 * e;
     dst[0] = acc_a; dst[1] = acc_r; dst[2] = mu0; dst[3] = mu1; dst[4] = mu2;
     dst[5] = g00; dst[6] = g11; dst[7] = g22; dst[8] = g01; dst[9] = g02; dst[10] = g12;
@@ -1580,20 +1587,23 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi, const gs
   cudaStream_t s = as_stream(stream);
   cudaError_t e = cudaMemsetAsync(bad, 0x7F, sizeof(int64_t), s);
   if (e != cudaSuccess) return cuda_status(e, "memset bad");
-  // The slab's voxels: whole z-layers [bz0*bdz, min(bz1*bdz, nz)).
+  if (bricks->b1 <= bricks->b0) return GSV_OK;
+  // The voxel planes of the brick layers the slab touches; the kernel keeps
+  // only the voxels of the slab's bricks.
   const int64_t plane = (int64_t)grid->nx * grid->ny;
-  const int64_t v0 = plane * ((int64_t)bricks->bz0 * bricks->bdz);
-  const int64_t zend = (int64_t)bricks->bz1 * bricks->bdz;
+  const int64_t bplane = (int64_t)bricks->bgx * bricks->bgy;
+  const int64_t v0 = plane * ((bricks->b0 / bplane) * bricks->bdz);
+  const int64_t zend = ((bricks->b1 - 1) / bplane + 1) * bricks->bdz;
   const int64_t v1 = plane * (zend < grid->nz ? zend : (int64_t)grid->nz);
   if (v1 <= v0) return GSV_OK;
   const unsigned blocks = (unsigned)((v1 - v0 + 255) / 256);
   if (precision == 0)
     backward_prep_kernel<float, float2><<<blocks, 256, 0, s>>>(
-        (const float*)W, (const float*)I, dldi, *grid, v0, v1, eps_w, (float2*)ab,
+        (const float*)W, (const float*)I, dldi, *grid, *bricks, v0, v1, eps_w, (float2*)ab,
         (unsigned long long*)bad);
   else
     backward_prep_kernel<double, double2><<<blocks, 256, 0, s>>>(
-        (const double*)W, (const double*)I, dldi, *grid, v0, v1, eps_w, (double2*)ab,
+        (const double*)W, (const double*)I, dldi, *grid, *bricks, v0, v1, eps_w, (double2*)ab,
         (unsigned long long*)bad);
   GSV_CHECK_LAUNCH("backward_prep_kernel");
   return GSV_OK;

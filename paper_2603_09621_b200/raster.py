@@ -11,8 +11,8 @@ raster.py:55-570; every computation runs in libgsv_b200.so (include/gsv.h):
                      gsv_merge (ascending brick order) -> gsv_chain_rule
 
 Extensions (keyword-only, defaults keep the reference behaviour):
-``slab=(bz0, bz1)`` restricts binning/render/backward to a contiguous range
-of brick layers -- the z-slab sharding unit of the multi-GPU path.
+``slab=(b0, b1)`` restricts binning/render/backward to the contiguous brick-id
+range [b0, b1) -- the sharding unit of the multi-GPU path (distributed.py).
 
 Arrays are torch tensors on the field's CUDA device.  ``BrickIndex.gids`` is
 int32 (the reference uses int64; values are identical), ``starts`` int64.
@@ -72,8 +72,8 @@ class BrickIndex:
     """CSR layout of per-brick Gaussian lists (raster.py:66-112).
 
     gids[starts[b]:starts[b+1]] are the Gaussians binned to brick b,
-    ascending; bricks x-fastest.  With ``slab=(bz0, bz1)`` the index covers
-    only brick layers [bz0, bz1) and ``starts`` has one entry per slab brick.
+    ascending; bricks x-fastest.  With ``slab=(b0, b1)`` the index covers
+    only bricks [b0, b1) and ``starts`` has one entry per slab brick.
     """
     grid: GridSpec
     brick_dims: tuple
@@ -108,7 +108,8 @@ class BrickIndex:
 
     @property
     def slab_range(self) -> tuple:
-        return self.slab if self.slab is not None else (0, self.brick_grid[2])
+        bg = self.brick_grid
+        return self.slab if self.slab is not None else (0, bg[0] * bg[1] * bg[2])
 
     def lists_sorted(self) -> bool:
         """True when every brick's list is ascending (canonical order)."""
@@ -262,7 +263,7 @@ def build_brick_index(f: GaussianField, grid: GridSpec, opts: RenderOptions = Re
         raise ValueError(f"brick_dims must be positive, got {brick_dims}")
     brick_dims = tuple(int(d) for d in brick_dims)
     bricks = _lib.make_bricks(grid, brick_dims, slab)
-    nbricks = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
+    nbricks = bricks.b1 - bricks.b0
     rec32, rec64, counts, box = _preprocess(f, grid, opts.cutoff_sigma, brick_dims, slab,
                                             opts.precision == "f64", pool)
     gstart = _scan(counts, nbricks, pool)
@@ -368,7 +369,7 @@ def _emission_layout(f, grid, idx: BrickIndex, opts: RenderOptions):
         return aux.gstart, aux.box, True
     _, _, counts, box = _preprocess(f, grid, opts.cutoff_sigma, idx.brick_dims, idx.slab, False)
     b = _lib.make_bricks(grid, idx.brick_dims, idx.slab)
-    gstart = _scan(counts, b.bgx * b.bgy * (b.bz1 - b.bz0))
+    gstart = _scan(counts, b.b1 - b.b0)
     return gstart, box, False
 
 

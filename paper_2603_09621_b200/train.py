@@ -9,8 +9,8 @@
                N x 12 partial sums, the only collective, when sharded] ->
                gsv_chain_rule.
 
-Sharding: with ``slab=(bz0, bz1)`` a rank bins, renders and
-back-propagates only its contiguous range of brick layers; the per-Gaussian
+Sharding: with ``slab=(b0, b1)`` a rank bins, renders and
+back-propagates only its contiguous brick-id range; the per-Gaussian
 merged partials (and the loss, carried in the spare 12th column) are summed
 across ranks by one NCCL all_reduce, after which every rank applies the same
 chain rule and Adam step, so parameters stay replicated.
@@ -441,7 +441,7 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     dev = f.device
     grid, opts, n = self.grid, self.opts, f.count
     bricks = _lib.make_bricks(grid, self.brick_dims, self.slab)
-    nb = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
+    nb = bricks.b1 - bricks.b0
     gp = _lib.BufferPool(dev)        # private: replays need fixed addresses
     b = {"bricks": bricks, "nb": max(nb, 1),
          "rec32": gp.get("rec32", (n, 16), torch.float32),
@@ -734,7 +734,7 @@ class Renderer:
         lib = _lib.lib()
         dev, n = self.device, f.count
         bricks = _lib.make_bricks(self.grid, self.brick_dims, self.slab)
-        nb = bricks.bgx * bricks.bgy * (bricks.bz1 - bricks.bz0)
+        nb = bricks.b1 - bricks.b0
         gp = _lib.BufferPool(dev)
         b = {"bricks": bricks,
              "rec32": gp.get("rec32", (n, 16), torch.float32),

@@ -75,9 +75,9 @@ int main(int argc, char** argv) {
   k.bgx = (dims[0] + bd[0] - 1) / bd[0];
   k.bgy = (dims[1] + bd[1] - 1) / bd[1];
   k.bgz = (dims[2] + bd[2] - 1) / bd[2];
-  k.bz0 = 0;
-  k.bz1 = k.bgz;
   const int32_t nb = k.bgx * k.bgy * k.bgz;
+  k.b0 = 0; /* the whole grid: brick ids [0, nb) */
+  k.b1 = nb;
   const int64_t nv = (int64_t)dims[0] * dims[1] * dims[2];
 
   double* pos = (double*)dev_copy(h, (size_t)(3 * n) * 8);

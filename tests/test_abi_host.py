@@ -10,8 +10,8 @@ import torch
 
 import paper_2603_09621_b200 as gs
 from paper_2603_09621_b200 import _lib
-from paper_2603_09621_b200.distributed import (brick_layers, slab_for_rank, slab_ranges,
-                                               slab_voxel_range)
+from paper_2603_09621_b200.distributed import (brick_layers, layer_slab_ranges, slab_for_rank,
+                                               slab_ranges, slab_voxel_mask)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADERS = [os.path.join(ROOT, "include", h) for h in ("gsv.h", "gsv_diag.h")]
@@ -154,16 +154,51 @@ def test_brick_index_accepts_host_lists():
     assert idx.gids.dtype == torch.int32 and idx.starts.dtype == torch.int64
 
 
-def test_slab_partition_covers_every_layer_once():
-    for layers in (1, 7, 10, 32, 128):
+def _check_partition(r, n):
+    assert r[0][0] == 0 and r[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+    assert all(a <= b for a, b in r)
+
+
+def test_slab_partition_covers_every_brick_once():
+    for n in (1, 7, 10, 32, 128, 8192):
         for ws in (1, 2, 3, 4, 8):
-            r = slab_ranges(layers, ws)
-            assert r[0][0] == 0 and r[-1][1] == layers
-            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            r = slab_ranges(n, ws)
+            _check_partition(r, n)
             sizes = [b - a for a, b in r]
             assert max(sizes) - min(sizes) <= 1
     g = gs.GridSpec((16, 16, 20))
     assert brick_layers(g, (8, 8, 4)) == 5
     assert slab_for_rank(g, (8, 8, 4), 0, 1) is None
-    spans = [slab_voxel_range(g, (8, 8, 4), slab_for_rank(g, (8, 8, 4), r, 2)) for r in range(2)]
-    assert spans[0][0] == 0 and spans[0][1] == spans[1][0] and spans[1][1] == g.num_voxels
+    # whole-layer slabs are the aligned special case
+    lay = layer_slab_ranges(g, (8, 8, 4), 2)
+    _check_partition(lay, 20)
+    assert sorted(b - a for a, b in lay) == [8, 12] and all(b % 4 == 0 for _, b in lay)
+    # mid-layer cuts: 20 bricks over 3 ranks
+    r = [slab_for_rank(g, (8, 8, 4), k, 3) for k in range(3)]
+    _check_partition(r, 20)
+    assert any(b % 4 for _, b in r[:-1])
+    masks = [slab_voxel_mask(g, (8, 8, 4), s) for s in r]
+    assert (sum(m.astype(int) for m in masks) == 1).all()
+
+
+def test_slab_partition_balances_weights():
+    rng = np.random.default_rng(3)
+    w = rng.integers(0, 50, size=1000).astype(np.float64)
+    w[:300] *= 10                                   # a heavy front
+    for ws in (2, 3, 5, 8):
+        r = slab_ranges(1000, ws, weights=w)
+        _check_partition(r, 1000)
+        loads = [w[a:b].sum() for a, b in r]
+        assert max(loads) <= w.sum() / ws + w.max() + 1e-9
+    # 10 layers of 64 bricks over 8 ranks: whole layers cap the balance at
+    # 2 layers per rank on the heaviest; mid-layer cuts do not
+    w = np.ones(640)
+    lay = slab_ranges(640, 8, weights=w, align=64)
+    mid = slab_ranges(640, 8, weights=w)
+    assert max(b - a for a, b in lay) == 128
+    assert max(b - a for a, b in mid) == 80
+    with pytest.raises(ValueError):
+        slab_ranges(10, 2, weights=np.ones(9))
+    with pytest.raises(ValueError):
+        slab_ranges(10, 2, weights=-np.ones(10))

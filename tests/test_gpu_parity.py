@@ -440,12 +440,16 @@ def test_train_step_matches_unfused_api():
 
 
 # ------------------------------------------------------------ z-slab sharding
-def test_slabs_reassemble_the_full_index_render_and_gradients():
-    """Two ranks emulated sequentially on one GPU: per-slab lists are exact
-    slices of the global lists, per-slab renders are bit-identical on their
-    voxels, and the sum of per-slab merged partials (what the NCCL all_reduce
+@pytest.mark.parametrize("cuts", ["layers", "balanced3", "odd"])
+def test_slabs_reassemble_the_full_index_render_and_gradients(cuts):
+    """Ranks emulated sequentially on one GPU, slabs = contiguous brick-id
+    ranges (whole layers, pair-balanced mid-layer cuts, and odd ranges: one
+    brick, empty, a layer remainder): per-slab lists are exact slices of the
+    global lists, per-slab renders are bit-identical on their bricks' voxels,
+    and the sum of per-slab merged partials (what the NCCL all_reduce
     computes) equals the single-index merge."""
-    from paper_2603_09621_b200.distributed import slab_ranges, slab_voxel_range
+    from paper_2603_09621_b200.distributed import (layer_slab_ranges, pair_weights,
+                                                   slab_ranges, slab_voxel_mask)
     from paper_2603_09621_b200.raster import _pair_partials
     from paper_2603_09621_b200.synth import CONFIGS, make_problem
     p = make_problem(CONFIGS[1])
@@ -460,16 +464,28 @@ def test_slabs_reassemble_the_full_index_render_and_gradients():
                             live_masks=full._masks).clone()
     I_full = np_(out.cache.I).copy()
     starts_full, gids_full = np_(out.idx.starts), np_(out.idx.gids)
-    layers = -(-grid.dims[2] // bd[2])
+    nb = len(starts_full) - 1
+    layer = out.idx.brick_grid[0] * out.idx.brick_grid[1]
+    if cuts == "layers":
+        slabs = layer_slab_ranges(grid, bd, 2)
+    elif cuts == "balanced3":
+        slabs = slab_ranges(nb, 3, weights=pair_weights(f, grid, gs.RenderOptions(), bd))
+        assert any(b % layer for _, b in slabs[:-1]), "expected a mid-layer cut"
+    else:
+        c = [0, 1, 1, layer + 5, 3 * layer - 7, nb]
+        slabs = list(zip(c, c[1:]))
     total = torch.zeros_like(g_full)
     loss_total = 0.0
     pieces = []
-    for slab in slab_ranges(layers, 2):
+    for slab in slabs:
         st = gs.TrainStep(lr, gs.RenderOptions(), bd, "l1", slab=slab)
         o = st.forward(f)
+        s0, s1 = starts_full[slab[0]], starts_full[slab[1]]
+        np.testing.assert_array_equal(np_(o.idx.starts), starts_full[slab[0]:slab[1] + 1] - s0)
+        np.testing.assert_array_equal(np_(o.idx.gids), gids_full[s0:s1])
         pieces.append(np_(o.idx.gids))
-        v0, v1 = slab_voxel_range(grid, bd, slab)
-        np.testing.assert_array_equal(np_(o.cache.I)[v0:v1], I_full[v0:v1])
+        own = slab_voxel_mask(grid, bd, slab)
+        np.testing.assert_array_equal(np_(o.cache.I)[own], I_full[own])
         g = _pair_partials(f, grid, o.idx, st.opts, o.idx._aux.rec32, None, o.ab,
                            o.idx._aux.gstart, o.idx._aux.box, True, live_masks=st._masks)
         total += g
@@ -478,6 +494,34 @@ def test_slabs_reassemble_the_full_index_render_and_gradients():
     assert abs(loss_total / grid.num_voxels - out.loss()) <= 1e-12
     a, b = np_(total[:, :11]), np_(g_full[:, :11])
     assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b) + 1e-30
+
+
+def test_slab_backward_api_mid_layer():
+    """The reference-shaped backward() on a mid-layer slab index: the
+    backward_prep step touches only the slab's bricks (voxels outside keep
+    their zero W without tripping the coverage check), and the two slabs'
+    gradients sum to the whole-grid gradient."""
+    from paper_2603_09621_b200.synth import CONFIGS, make_problem
+    p = make_problem(CONFIGS[1])
+    grid = p["lr_grid"]
+    f = gs.GaussianField(*p["field"])
+    opts = gs.RenderOptions()
+    idx = gs.build_brick_index(f, grid, opts)
+    cache = gs.forward(f, grid, idx)
+    rng = np.random.default_rng(4)
+    dldi = torch.as_tensor(rng.standard_normal(grid.num_voxels), device=cache.I.device)
+    ref = gs.backward(f, grid, idx, cache, dldi)
+    nb = idx.brick_count
+    cut = (nb // 2) | 3
+    acc = None
+    for slab in ((0, cut), (cut, nb)):
+        si = gs.build_brick_index(f, grid, opts, slab=slab)
+        sc = gs.forward(f, grid, si)
+        gb = [t.clone() for t in gs.backward(f, grid, si, sc, dldi).tensors()]
+        acc = gb if acc is None else [x + y for x, y in zip(acc, gb)]
+    for x, y in zip(acc, ref.tensors()):      # gradients are linear in the partial sums
+        a, b = np_(x), np_(y)
+        assert np.linalg.norm(a - b) <= 1e-9 * (np.linalg.norm(b) + 1e-30)
 
 
 # ------------------------------------------------------------------ Renderer
