@@ -10,6 +10,8 @@
 // f64 throughout; reductions are fixed-order (bit-reproducible).
 #include "gsv_prep.cuh"
 
+#include <cstdlib>
+
 namespace gsv {
 namespace {
 
@@ -499,10 +501,326 @@ tail_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gsta
   if (PREP) preprocess_one(i, pn, ln, qn, ran, rrn, pa);
 }
 
+// ---------------------------------------------------------------- TMA tail
+// The same one-pass tail with its memory traffic on the bulk-copy (TMA)
+// engine: a CTA's 128 Gaussians own contiguous runs of every parameter and
+// moment array (15 runs, 36 KB) and one contiguous range of pair partials.
+// One thread issues 1-D bulk copies global -> shared for all of them at
+// once, signalled on mbarriers: the parameter/moment runs land while the
+// merge walks the partials (double-buffered 128-pair chunks).  Adam and the
+// renormalisation then run out of shared memory and the updated runs go back
+// with bulk stores.  No per-thread strided f64 loads waiting on L2/HBM one
+// dependent round trip after another (the old tail's long-scoreboard stalls).
+// The last, partial CTA and misaligned caller pointers take a generic path
+// into the same shared layout.
+namespace tma {
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(su32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void store_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// wait until the committed bulk stores have READ shared memory (the CTA may
+// then exit; the global writes complete asynchronously, as in CUTLASS's
+// TMA-store epilogues)
+__device__ __forceinline__ void store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+}  // namespace tma
+
+#ifndef GSV_TMA_CHUNK
+#define GSV_TMA_CHUNK 64
+#endif
+constexpr int kTmaChunk = GSV_TMA_CHUNK;       // pairs per staging buffer (48 B each)
+// shared layout (doubles): per array family (params, m, v) the runs
+// pos(3T) ls(3T) rot(4T) ra(T) rr(T), T = kTailThreads
+__host__ __device__ constexpr int run_w(int g) { return g < 2 ? 3 : (g == 2 ? 4 : 1); }
+template <int NT>
+__host__ __device__ constexpr int run_off(int g) {
+  return NT * (g == 0 ? 0 : g == 1 ? 3 : g == 2 ? 6 : g == 3 ? 10 : 11);
+}
+#ifndef GSV_TMA_THREADS
+#define GSV_TMA_THREADS 64
+#endif
+constexpr int kTmaThreads = GSV_TMA_THREADS;   // Gaussians (= threads) per CTA
+template <int NT>
+constexpr size_t tma_smem() {
+  return 3 * 12 * NT * sizeof(double) + 2 * kTmaChunk * 48 + 4 * sizeof(uint64_t);
+}
+
+#ifndef GSV_TMA_WARPS_PER_SM
+#define GSV_TMA_WARPS_PER_SM 20
+#endif
+template <int NT>
+__global__ void __launch_bounds__(NT, GSV_TMA_WARPS_PER_SM * 32 / NT)
+tail_tma_kernel(const float* __restrict__ partials, const int64_t* __restrict__ gstart,
+                const double* __restrict__ gsum, int64_t n, double* __restrict__ pos,
+                double* __restrict__ ls, double* __restrict__ rot, double* __restrict__ ra,
+                double* __restrict__ rr, MomentPtrs mv, int amp_en, int relax_en,
+                const gsv_adam_hparams h, StepDev sd, int aligned) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sprm = reinterpret_cast<double*>(smem_raw);
+  double* sm = sprm + 12 * NT;
+  double* sv = sm + 12 * NT;
+  float4* spart = reinterpret_cast<float4*>(sv + 12 * NT);            // [2][kTmaChunk * 3]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(spart + 2 * 3 * kTmaChunk);
+  if (sd.gate != nullptr && *sd.gate != 0) return;   // overflow / non-finite loss: no update
+  const int tid = threadIdx.x;
+  const int64_t i0 = blockIdx.x * (int64_t)NT;
+  const int cnt = (int)min((int64_t)NT, n - i0);
+  const int64_t i = i0 + tid;
+  const bool valid = tid < cnt;
+  const bool tma = aligned && cnt == NT;
+  double* const gprm[5] = {pos, ls, rot, ra, rr};
+  const bool en[5] = {true, true, true, amp_en != 0, relax_en != 0};
+  const bool merge = gsum == nullptr;
+  const int64_t e_lo = merge ? gstart[i0] : 0, e_hi = merge ? gstart[i0 + cnt] : 0;
+  const int nch = (int)((e_hi - e_lo + kTmaChunk - 1) / kTmaChunk);
+  const float4* src = reinterpret_cast<const float4*>(partials);
+
+  auto chunk_pairs = [&](int c) {
+    return (int)min((int64_t)kTmaChunk, e_hi - (e_lo + (int64_t)c * kTmaChunk));
+  };
+  auto issue_chunk = [&](int c) {   // thread 0, TMA path
+    const int np = chunk_pairs(c);
+    uint64_t* b = bar + 1 + (c & 1);
+    tma::expect_tx(b, (uint32_t)(48 * np));
+    tma::g2s(spart + (c & 1) * 3 * kTmaChunk, src + 3 * (e_lo + (int64_t)c * kTmaChunk),
+             (uint32_t)(48 * np), b);
+  };
+
+  if (tma) {
+    if (tid == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) tma::mbar_init(bar + k);
+      tma::fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t bytes = 0;
+#pragma unroll
+      for (int g = 0; g < 5; ++g) {
+        const uint32_t b = (uint32_t)(8 * run_w(g) * NT);
+        bytes += b;
+        if (mv[g] != nullptr) bytes += b;
+        if (mv[g + 5] != nullptr) bytes += b;
+      }
+      tma::expect_tx(bar, bytes);
+#pragma unroll
+      for (int g = 0; g < 5; ++g) {
+        const uint32_t b = (uint32_t)(8 * run_w(g) * NT);
+        const int64_t off = run_w(g) * i0;
+        tma::g2s(sprm + run_off<NT>(g), gprm[g] + off, b, bar);
+        if (mv[g] != nullptr) tma::g2s(sm + run_off<NT>(g), mv[g] + off, b, bar);
+        if (mv[g + 5] != nullptr) tma::g2s(sv + run_off<NT>(g), mv[g + 5] + off, b, bar);
+      }
+      if (merge) {
+        if (nch > 0) issue_chunk(0);
+        if (nch > 1) issue_chunk(1);
+      }
+    }
+  } else {
+    // generic path: the same shared layout filled by plain loads
+#pragma unroll
+    for (int g = 0; g < 5; ++g) {
+      const int w = run_w(g);
+      const int64_t off = w * i0;
+      for (int q = tid; q < w * cnt; q += NT) {
+        sprm[run_off<NT>(g) + q] = gprm[g][off + q];
+        if (mv[g] != nullptr) sm[run_off<NT>(g) + q] = mv[g][off + q];
+        if (mv[g + 5] != nullptr) sv[run_off<NT>(g) + q] = mv[g + 5][off + q];
+      }
+    }
+  }
+
+  // ---- merge this thread's pair partials in ascending brick order
+  double s[11];
+#pragma unroll
+  for (int a = 0; a < 11; ++a) s[a] = 0.0;
+  if (!merge) {
+    if (valid) {
+#pragma unroll
+      for (int a = 0; a < 11; ++a) s[a] = gsum[12 * i + a];
+    }
+  } else {
+    const int64_t my0 = valid ? gstart[i] : 0, my1 = valid ? gstart[i + 1] : 0;
+    for (int c = 0; c < nch; ++c) {
+      const int64_t c0 = e_lo + (int64_t)c * kTmaChunk;
+      const int np = chunk_pairs(c);
+      const float4* buf = spart + (tma ? (c & 1) * 3 * kTmaChunk : 0);
+      if (tma) {
+        tma::wait(bar + 1 + (c & 1), (uint32_t)((c >> 1) & 1));
+      } else {
+        __syncthreads();
+        for (int q = tid; q < 3 * np; q += NT) spart[q] = __ldg(src + 3 * c0 + q);
+        __syncthreads();
+      }
+      const int64_t a0 = max(my0, c0), a1 = min(my1, c0 + np);
+      for (int64_t e = a0; e < a1; ++e) {
+        const float4* pp = buf + 3 * (e - c0);
+        const float4 x = pp[0], y = pp[1], z = pp[2];
+        s[0] += (double)x.x; s[1] += (double)x.y; s[2] += (double)x.z; s[3] += (double)x.w;
+        s[4] += (double)y.x; s[5] += (double)y.y; s[6] += (double)y.z; s[7] += (double)y.w;
+        s[8] += (double)z.x; s[9] += (double)z.y; s[10] += (double)z.z;
+      }
+      if (tma) {
+        __syncthreads();                       // buffer (c & 1) free again
+        if (tid == 0 && c + 2 < nch) issue_chunk(c + 2);
+      }
+    }
+  }
+  if (tma) tma::wait(bar, 0);                  // parameter and moment runs
+  else __syncthreads();
+
+  if (valid) {
+    double* P[5];
+    double* M[5];
+    double* V[5];
+#pragma unroll
+    for (int g = 0; g < 5; ++g) {
+      P[g] = sprm + run_off<NT>(g) + run_w(g) * tid;
+      M[g] = sm + run_off<NT>(g) + run_w(g) * tid;
+      V[g] = sv + run_off<NT>(g) + run_w(g) * tid;
+    }
+    double g[12];
+    chain_one(s, P[1], P[2], P[3][0], P[4][0], relax_en, g);
+    double bc1 = h.bc1, bc2 = h.bc2;
+    if (sd.bc != nullptr) {
+      const int64_t t = *sd.t;
+      bc1 = sd.bc[2 * t];
+      bc2 = sd.bc[2 * t + 1];
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      P[0][a] = adam_one(P[0][a], M[0][a], V[0][a], g[a], h.lr[0], h.b1, h.b2, h.eps, bc1, bc2);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      P[1][a] = adam_one(P[1][a], M[1][a], V[1][a], g[3 + a], h.lr[1], h.b1, h.b2, h.eps, bc1,
+                         bc2);
+    double q[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      q[a] = adam_one(P[2][a], M[2][a], V[2][a], g[6 + a], h.lr[2], h.b1, h.b2, h.eps, bc1, bc2);
+    const double nrm = sqrt(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
+                                mul(q[3], q[3])));
+#pragma unroll
+    for (int a = 0; a < 4; ++a) P[2][a] = __ddiv_rn(q[a], nrm);
+    if (amp_en)
+      P[3][0] = adam_one(P[3][0], M[3][0], V[3][0], g[10], h.lr[3], h.b1, h.b2, h.eps, bc1, bc2);
+    if (relax_en)
+      P[4][0] = adam_one(P[4][0], M[4][0], V[4][0], g[11], h.lr[4], h.b1, h.b2, h.eps, bc1, bc2);
+  }
+
+  // ---- write the updated runs back (enabled groups only)
+  if (tma) {
+    tma::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int g = 0; g < 5; ++g) {
+        if (!en[g]) continue;
+        const uint32_t b = (uint32_t)(8 * run_w(g) * NT);
+        const int64_t off = run_w(g) * i0;
+        tma::s2g(gprm[g] + off, sprm + run_off<NT>(g), b);
+        if (mv[g] != nullptr) tma::s2g(mv[g] + off, sm + run_off<NT>(g), b);
+        if (mv[g + 5] != nullptr) tma::s2g(mv[g + 5] + off, sv + run_off<NT>(g), b);
+      }
+      tma::store_commit();
+    }
+  } else {
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < 5; ++g) {
+      if (!en[g]) continue;
+      const int w = run_w(g);
+      const int64_t off = w * i0;
+      for (int q = tid; q < w * cnt; q += NT) {
+        gprm[g][off + q] = sprm[run_off<NT>(g) + q];
+        if (mv[g] != nullptr) mv[g][off + q] = sm[run_off<NT>(g) + q];
+        if (mv[g + 5] != nullptr) mv[g + 5][off + q] = sv[run_off<NT>(g) + q];
+      }
+    }
+  }
+  if (tma && tid == 0) tma::store_wait_read();
+}
+
 }  // namespace
 }  // namespace gsv
 
 using namespace gsv;
+
+namespace {
+// TMA tail (default for the tail without PREP) or the per-thread-load tail
+// (GSV_TAIL_V1=1, for A/B runs).
+bool use_tma_tail() {
+  static const bool v = [] {
+    const char* e = getenv("GSV_TAIL_V1");
+    return !(e != nullptr && e[0] == '1');
+  }();
+  return v;
+}
+
+bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int launch_tail_tma(cudaStream_t s, const float* partials,
+                    const int64_t* gstart, const double* gsum, int64_t n, double* pos,
+                    double* ls, double* rot, double* ra, double* rr, const MomentPtrs& mv,
+                    int amp_en, int relax_en, const gsv_adam_hparams& h, const StepDev& sd) {
+  constexpr size_t smem = tma_smem<kTmaThreads>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tail_tma_kernel<kTmaThreads>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "tail_tma_kernel smem attribute");
+    attr = true;
+  }
+  int ok = aligned16(partials) && aligned16(pos) && aligned16(ls) && aligned16(rot) &&
+           aligned16(ra) && aligned16(rr);
+  for (int k = 0; k < 10; ++k) ok = ok && aligned16(mv.p[k]);
+  const unsigned blocks = (unsigned)((n + kTmaThreads - 1) / kTmaThreads);
+  tail_tma_kernel<kTmaThreads><<<blocks, kTmaThreads, smem, s>>>(
+      partials, gstart, gsum, n, pos, ls, rot, ra, rr, mv, amp_en, relax_en, h, sd, ok);
+  GSV_CHECK_LAUNCH("tail_tma_kernel");
+  return GSV_OK;
+}
+}  // namespace
 
 extern "C" {
 
@@ -592,6 +910,12 @@ int gsv_fused_update(const void* partials, const int64_t* gstart, const double* 
   for (int k = 0; k < 10; ++k) mv.p[k] = moments[k];
   if (precision == 0 && grad_scratch == nullptr) {
     // one pass: staged merge + chain rule + Adam + renorm
+    if (use_tma_tail())
+      return launch_tail_tma(s,
+                                    (const float*)partials, gstart, gsum, n, positions,
+                                    log_scales, rotations, raw_amplitude, raw_relax, mv,
+                                    amplitude_enabled, relax_enabled, *hp,
+                                    StepDev{nullptr, nullptr, nullptr});
     tail_kernel<false><<<(unsigned)((n + kTailThreads - 1) / kTailThreads), kTailThreads, 0, s>>>(
         (const float*)partials, gstart, gsum, n, positions, log_scales, rotations,
         raw_amplitude, raw_relax, mv, amplitude_enabled, relax_enabled, *hp,
@@ -670,10 +994,17 @@ int gsv_fused_update_device(const float* partials, const int64_t* gstart, const 
     if (int st = validate_grid_bricks(grid, bricks)) return st;
     const PrepArgs pa{*grid, *bricks, cutoff_sigma, isinf(cutoff_sigma) ? 1 : 0, relax_enabled,
                       rec32, nullptr, counts, box};
+    // PREP stays on the L2-prefetch tail: measured faster there (0.49 vs
+    // 0.55 ms at config 3), its f64 preprocessing wants the warps that the
+    // TMA tail's shared staging takes away.
     tail_kernel<true><<<blocks, kTailThreads, 0, s>>>(
         partials, gstart, gsum, n, positions, log_scales, rotations, raw_amplitude,
         raw_relax, mv, amplitude_enabled, relax_enabled, *hp, sd, pa);
   } else {
+    if (use_tma_tail())
+      return launch_tail_tma(s, partials, gstart, gsum, n, positions, log_scales,
+                                    rotations, raw_amplitude, raw_relax, mv, amplitude_enabled,
+                                    relax_enabled, *hp, sd);
     tail_kernel<false><<<blocks, kTailThreads, 0, s>>>(
         partials, gstart, gsum, n, positions, log_scales, rotations, raw_amplitude,
         raw_relax, mv, amplitude_enabled, relax_enabled, *hp, sd, PrepArgs{});

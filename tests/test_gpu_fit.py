@@ -359,3 +359,56 @@ def test_graph_step_degenerate_fields_match_eager(case):
         assert eb.step(fb, sb, lrs) == la
     np.testing.assert_array_equal(_pack(fa), _pack(fb))
     assert sa.t == sb.t == 3
+
+
+@pytest.mark.parametrize("n", [4096, 1000])
+def test_fused_update_tma_generic_and_split_paths_agree(n):
+    """gsv_fused_update's one-pass tail moves each CTA's parameter/moment runs
+    with TMA bulk copies when every pointer is 16-byte aligned and the CTA is
+    full; otherwise (here: all arrays shifted by one double, and n = 1000
+    leaving a partial last CTA) it fills the same shared layout with plain
+    loads.  Both must give bit-identical parameters and moments, and so must
+    the two-kernel split tail (merge+chain, then Adam)."""
+    import ctypes
+    from paper_2603_09621_b200 import _lib
+    lib = _lib.lib()
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(n)
+    widths = (3, 3, 4, 1, 1)
+    pairs = rng.integers(0, 7, size=n)
+    gstart = torch.as_tensor(np.concatenate([[0], np.cumsum(pairs)]), dtype=torch.int64,
+                             device=dev)
+    P = int(pairs.sum())
+    partials = torch.as_tensor(rng.standard_normal((P, 12)).astype(np.float32) * 1e-3,
+                               device=dev)
+    base = [rng.standard_normal((n, w)) for w in widths]
+    base[2] /= np.linalg.norm(base[2], axis=1, keepdims=True)
+    mom = ([rng.standard_normal((n, w)) * 1e-4 for w in widths] +            # m
+           [np.abs(rng.standard_normal((n, w))) * 1e-6 for w in widths])     # v
+
+    def run(shift, split=False):
+        def put(a):
+            buf = torch.zeros(a.size + 2, dtype=torch.float64, device=dev)
+            v = buf[shift:shift + a.size]
+            v.copy_(torch.as_tensor(a.reshape(-1), device=dev))
+            return v
+        prm = [put(a) for a in base]
+        mv = [put(a) for a in mom]
+        hp = _lib.GsvAdamHparams()
+        for k in range(5):
+            hp.lr[k] = 1e-3 * (k + 1)
+        hp.b1, hp.b2, hp.eps = 0.9, 0.999, 1e-8
+        hp.bc1, hp.bc2 = 1 - 0.9 ** 3, 1 - 0.999 ** 3
+        scratch = torch.empty((n, 12), dtype=torch.float64, device=dev) if split else None
+        mvp = (ctypes.c_void_p * 10)(*[t.data_ptr() for t in mv])
+        _lib.check(lib.gsv_fused_update(
+            partials.data_ptr(), gstart.data_ptr(), None, n, 0,
+            *[t.data_ptr() for t in prm], mvp, 1, 1, ctypes.byref(hp), _lib.ptr(scratch),
+            _lib.stream_ptr()), "fused_update")
+        torch.cuda.synchronize()
+        return [t.cpu().numpy().copy() for t in prm + mv]
+
+    a, b, c = run(0), run(1), run(0, split=True)
+    for x, y, z in zip(a, b, c):
+        np.testing.assert_array_equal(x, y)
+        np.testing.assert_array_equal(x, z)
