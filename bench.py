@@ -138,6 +138,23 @@ def problem_for(cfg_id):
 
 
 # ----------------------------------------------------------------- CPU arm
+def host_threads() -> int:
+    """Pin the oracle's OpenMP team to every usable host core and return the
+    count.  torchrun exports OMP_NUM_THREADS=1 to each rank, so the CPU arm
+    sets the thread count explicitly on the libgomp the oracle links."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        n = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(n)
+    try:
+        import ctypes
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(n)
+    except OSError:
+        pass
+    return n
+
+
 def cpu_train_step_seconds(p, steps: int, warmup: int):
     """Oracle (port of the reference CPU path) train iterations on this host."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -162,10 +179,10 @@ def run_reference(args, dist, rank):
     if rank != 0:
         return
     p = problem_for(args.config)
+    cores = host_threads()
     sec = cpu_train_step_seconds(p, args.steps, args.warmup)
-    cores = os.cpu_count()
     v = 1.0 / sec
-    cfg = _config_dict(args, p, None, 1)
+    cfg = _config_dict(args, p, None, int(os.environ.get("WORLD_SIZE", "1")))
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "it/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -355,7 +372,8 @@ def run_ours(args, dist, ws, rank, local):
     if os.path.exists(tf):
         with open(tf) as fh:
             tj = json.load(fh)
-        if tj.get("config") == args.config:   # measured for this workload only
+        # measured for this workload at N=1 only (a rank of N>1 renders a slab)
+        if tj.get("config") == args.config and ws == 1:
             traffic = tj.get(dom)
             issue = tj.get(dom + "_issue_active_pct")
     hbm_peak = 6552.0  # MEASURED_PEAKS.json (driver-written) when present
@@ -425,8 +443,9 @@ def run_ours(args, dist, ws, rank, local):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
+        cores = host_threads()
         sec = cpu_train_step_seconds(p, 1, 0)
-        cpu = {"value": 1.0 / sec, "unit": "it/s", "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": 1.0 / sec, "unit": "it/s", "cores": cores, "kind": "port",
                "sample": f"1 full config-{args.config} train iteration on the host "
                          "(oracle/: numpy binning + OpenMP C loops, all cores)"}
 
@@ -485,6 +504,11 @@ def count_launches(fn) -> int:
 
 def main():
     args = parse()
+    if args.impl == "reference":
+        # the CPU reference arm needs no process group: rank 0 runs, the
+        # other ranks exit 0 without work
+        run_reference(args, None, int(os.environ.get("RANK", "0")))
+        return
     dist, ws, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":
