@@ -196,6 +196,17 @@ __device__ __forceinline__ void unit_voxel_v(int u, const gsv_bricks& k, int& x,
   }
 }
 
+// One hit's VPL live words into its shared slot (16-byte store at VPL 4).
+template <int VPL>
+__device__ __forceinline__ void store_mask_words(uint2* dst, const unsigned* w) {
+  if constexpr (VPL == 4) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+#pragma unroll
+    for (int kk = 0; kk < VPL / 2; ++kk) dst[kk] = make_uint2(w[2 * kk], w[2 * kk + 1]);
+  }
+}
+
 #ifndef GSV_FWD_OCC
 #define GSV_FWD_OCC 640
 #endif
@@ -216,8 +227,8 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
                  uint2* __restrict__ live_masks) {
   __shared__ Pair32 sp[THREADS];       // 32 slots per warp
   // live bits of this round's hits: per warp and hit VPL words (VPL/2 uint2)
-  __shared__ uint2 smask[MASKS ? THREADS * VPL / 2 : 1];
-  __shared__ uint2 sxmask[MASKS ? THREADS * VPL / 2 : 1];   // guard-band additions
+  __shared__ __align__(16) uint2 smask[MASKS ? THREADS * VPL / 2 : 1];
+  __shared__ __align__(16) uint2 sxmask[MASKS ? THREADS * VPL / 2 : 1];   // guard-band additions
   __shared__ double red[THREADS / 32];
   static_assert(!SPLIT || THREADS == 32, "split tiles run one warp per CTA");
   const int lb = SPLIT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // slab-local brick
@@ -391,35 +402,13 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
           q[h] = q[h - 1] + dq;
           dq += d2q;
         }
-        // Live for sure: q >= qhi.  In the guard band [qlo, qhi) the exact
-        // f64 decision (the reference's truncation test; rare, warp-voted)
-        // adds the voxel's contribution right here and records its mask bit,
-        // so the common path below carries no per-voxel state.
-        bool band = false;
-#pragma unroll
-        for (int h = 0; h < VPL; ++h) band |= q[h] >= pd.x && q[h] < pc.w;
-        if (__any_sync(kFull, band)) {
-          const int gidj = __float_as_int(pd.y);
-          bool xl[VPL];
-#pragma unroll
-          for (int h = 0; h < VPL; ++h) {
-            xl[h] = q[h] >= pd.x && q[h] < pc.w &&
-                    exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d);
-            if (xl[h]) {
-              const float w = ex2_approx(q[h]);
-              accS[h] = fmaf(pc.z, w, accS[h]);
-              accW[h] += w;
-            }
-          }
-          if (want_masks) {
-            unsigned xw[VPL];
-#pragma unroll
-            for (int h = 0; h < VPL; ++h) xw[h] = __ballot_sync(kFull, xl[h]);
-#pragma unroll
-            for (int kk = 0; kk < VPL / 2; ++kk)
-              sxmask[((swarp << 5) + jj) * (VPL / 2) + kk] = make_uint2(xw[2 * kk], xw[2 * kk + 1]);
-          }
-        }
+        // Live for sure: q >= qhi -- accumulated first, branch-free.  Then
+        // the guard band [qlo, qhi): the exact f64 decision (the reference's
+        // truncation test; rare, warp-voted) adds those voxels' contributions
+        // and records their mask bits.  A voxel is live or in the band, never
+        // both, so its per-voxel order of additions is the list order either
+        // way.  The band compare reuses the live predicate (NaN -- a voxel
+        // the lane does not own -- is neither live nor in the band).
         bool live[VPL];
 #pragma unroll
         for (int h = 0; h < VPL; ++h) {
@@ -435,26 +424,61 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
 #pragma unroll
           for (int h = 0; h < VPL; ++h) mw[h] = __ballot_sync(kFull, live[h]);
           // warp-uniform values: every lane stores the same words (no predicate)
+          store_mask_words<VPL>(smask + ((swarp << 5) + jj) * (VPL / 2), mw);
+        }
+        bool inband[VPL], band = false;
 #pragma unroll
-          for (int kk = 0; kk < VPL / 2; ++kk)
-            smask[((swarp << 5) + jj) * (VPL / 2) + kk] = make_uint2(mw[2 * kk], mw[2 * kk + 1]);
+        for (int h = 0; h < VPL; ++h) {
+          inband[h] = !live[h] && q[h] >= pd.x;
+          band |= inband[h];
+        }
+        if (__any_sync(kFull, band)) {
+          const int gidj = __float_as_int(pd.y);
+          bool xl[VPL];
+#pragma unroll
+          for (int h = 0; h < VPL; ++h) {
+            xl[h] = inband[h] && exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d);
+            if (xl[h]) {
+              const float w = ex2_approx(q[h]);
+              accS[h] = fmaf(pc.z, w, accS[h]);
+              accW[h] += w;
+            }
+          }
+          if (want_masks) {
+            unsigned xw[VPL];
+#pragma unroll
+            for (int h = 0; h < VPL; ++h) xw[h] = __ballot_sync(kFull, xl[h]);
+            store_mask_words<VPL>(sxmask + ((swarp << 5) + jj) * (VPL / 2), xw);
+          }
         }
       }
       // live-voxel masks for the backward, plane [warp][pair]: one coalesced
       // 256-byte store per warp and round (pairs missing the tile get zeros)
       if (want_masks) {
         __syncwarp();
+        uint2 mm[VPL / 2];
+#pragma unroll
+        for (int kk = 0; kk < VPL / 2; ++kk) mm[kk] = make_uint2(0u, 0u);
+        if (hit) {
+          const int slot = ((swarp << 5) + rank) * (VPL / 2);
+          if constexpr (VPL == 4) {
+            const uint4 a = *reinterpret_cast<const uint4*>(smask + slot);
+            const uint4 x = *reinterpret_cast<const uint4*>(sxmask + slot);
+            mm[0] = make_uint2(a.x | x.x, a.y | x.y);
+            mm[1] = make_uint2(a.z | x.z, a.w | x.w);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < VPL / 2; ++kk) {
+              const uint2 a = smask[slot + kk], x = sxmask[slot + kk];
+              mm[kk] = make_uint2(a.x | x.x, a.y | x.y);
+            }
+          }
+        }
 #pragma unroll
         for (int kk = 0; kk < VPL / 2; ++kk) {
-          uint2 mm = make_uint2(0u, 0u);
-          if (hit) {
-            const uint2 a = smask[((swarp << 5) + rank) * (VPL / 2) + kk];
-            const uint2 x = sxmask[((swarp << 5) + rank) * (VPL / 2) + kk];
-            mm = make_uint2(a.x | x.x, a.y | x.y);
-          }
-          mm.x &= ownb[2 * kk];          // voxels outside the grid never enter a mask
-          mm.y &= ownb[2 * kk + 1];
-          if (gid >= 0) live_masks[(warp * (VPL / 2) + kk) * mstride + base + lane] = mm;
+          mm[kk].x &= ownb[2 * kk];      // voxels outside the grid never enter a mask
+          mm[kk].y &= ownb[2 * kk + 1];
+          if (gid >= 0) live_masks[(warp * (VPL / 2) + kk) * mstride + base + lane] = mm[kk];
         }
       }
       __syncwarp();
