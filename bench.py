@@ -388,10 +388,18 @@ def run_ours(args, dist, ws, rank, local):
                     "E_tile": e_tile if dom == "forward" else None,
                     "live_fraction": (e_live / e_tile) if (dom == "forward" and e_tile) else None,
                     "issue_active_pct": issue,
+                    # the same 28 FLOP counted per evaluated slot: what the kernel
+                    # sustains; frac above is that times the live fraction
+                    "achieved_evaluated": (e_tile * fl / (t_dom * 1e-3) / 1e12)
+                    if (dom == "forward" and e_tile) else None,
+                    "frac_evaluated": (e_tile * fl / (t_dom * 1e-3) / 1e12 / peak["tflops"])
+                    if (dom == "forward" and e_tile) else None,
                     "note": "the forward evaluates every (pair, voxel) slot of each warp tile "
-                            "a pair's 3-sigma box and sphere bound reach (E_tile); frac counts "
-                            "live pair-voxels only (SURVEY 8d's unit), issue_active_pct is the "
-                            "kernel's issue-slot use from the ncu capture in profiles/"},
+                            "a pair's 3-sigma box and sphere bound reach (E_tile; every such "
+                            "hit has a live voxel, tools/deadhits.py); frac counts live "
+                            "pair-voxels only (SURVEY 8d's unit), frac_evaluated every "
+                            "evaluated slot; issue_active_pct is the kernel's issue-slot use "
+                            "from the ncu capture in profiles/"},
                 "work": {"E_live": e_live, "E_brick": e_brick,
                 "flop_per_live_pair_voxel": fl, "ms_per_launch": t_dom},
                 "hbm": {"algorithmic_bytes": bytes_alg,

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--hr", action="store_true")
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="also run graph-replayed train steps (TrainStep.step), e.g. under ncu")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     p = synth.make_problem(synth.CONFIGS[args.config])
@@ -45,6 +47,16 @@ def main():
             out = step.forward(f)
             step.update(f, out, state, lrs)
         print("LR train phases (ms):", {k: round(v[1], 4) for k, v in t.summary().items()})
+        if args.graph:
+            step.timer = None
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            for i in range(args.iters + 3):
+                if i == 3:
+                    ev[0].record()
+                step.step(f, state, lrs)
+            ev[1].record()
+            torch.cuda.synchronize()
+            print("graph step ms:", round(ev[0].elapsed_time(ev[1]) / max(args.iters, 1), 4))
     if args.hr:
         grid = p["render_grid"]
         t = PhaseTimer()

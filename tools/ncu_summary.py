@@ -33,7 +33,8 @@ METRICS = [
 
 ROLE = {"forward32_kernel": "forward", "backward32m_kernel": "backward",
         "backward32_kernel": "backward_span", "tail_kernel": "update",
-        "preprocess_kernel": "preprocess", "emit_kernel": "emit"}
+        "tail_tma_kernel": "update_eager", "forward32w_kernel": "render_forward",
+        "preprocess_kernel": "preprocess", "emit_kernel": "emit", "emit_warp_kernel": "emit"}
 
 
 def to_bytes(v: str, unit: str) -> float:
