@@ -527,6 +527,59 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
 // the columns (x, y) = (l & 7, l >> 3) and (x, y + 4), all 4 z.  A pair is
 // staged and its quadratic built once per brick; column B's start value and
 // z-step follow from column A's in 5 FMAs.  No live masks (renders only).
+// Evaluate one column (4 voxels in z) of a lane against a compacted hit list
+// (the two-list whole-brick forward): q in nested form at the column's first
+// voxel, then second differences; live accumulation, then the guard band.
+__device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits, int nh,
+                                                 float mX, float mY, float mZ, float mZ1,
+                                                 int gx, int gy, int gz, const ExactSrc& xsrc,
+                                                 const gsv_grid& g, double cut2d,
+                                                 float* aS, float* aW) {
+  constexpr int Z = 4;
+  for (int jj = 0; jj < nh; ++jj) {
+    const float4 pa = hits[jj].a, pb = hits[jj].b, pc = hits[jj].c;
+    const float2 pd = *reinterpret_cast<const float2*>(&hits[jj].d);   // qlo, gid
+    float q[Z];
+    const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
+    const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
+    const float t3 = fmaf(pb.z, mZ, pa.w);
+    q[0] = fmaf(mX, t1, fmaf(mY, t2, fmaf(mZ, t3, pa.x)));
+    float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, mZ1, t3)));
+    const float d2q = 2.f * pb.z;
+#pragma unroll
+    for (int h = 1; h < Z; ++h) {
+      q[h] = q[h - 1] + dq;
+      dq += d2q;
+    }
+    bool live[Z], band = false;
+#pragma unroll
+    for (int h = 0; h < Z; ++h) {
+      live[h] = q[h] >= pc.w;
+      const float w = ex2_approx(q[h]);
+      if (live[h]) {
+        aS[h] = fmaf(pc.z, w, aS[h]);
+        aW[h] += w;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < Z; ++h) band |= !live[h] && q[h] >= pd.x;
+    if (__any_sync(kFull, band)) {
+      const int gidj = __float_as_int(pd.y);
+#pragma unroll
+      for (int h = 0; h < Z; ++h)
+        if (!live[h] && q[h] >= pd.x && exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d)) {
+          const float w = ex2_approx(q[h]);
+          aS[h] = fmaf(pc.z, w, aS[h]);
+          aW[h] += w;
+        }
+    }
+  }
+}
+
+// TWO: per 32-pair round, the hits are compacted into one list per y-half of
+// the brick (each half's own box and sphere cull) and each list is evaluated
+// for that half's column only -- a pair that reaches one half costs half.
+template <bool TWO>
 __global__ void __launch_bounds__(32, 16)
 forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
                   const gsv_record32* __restrict__ rec,
@@ -537,7 +590,7 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
                   const float* __restrict__ target, int loss_kind, double vox_count,
                   float2* __restrict__ ab, double* __restrict__ loss_part) {
   constexpr int Z = 4;
-  __shared__ Pair32 wsp[32];
+  __shared__ Pair32 wsp[TWO ? 64 : 32];
   const int lb = blockIdx.x;
   const int b = (int)slab_first(k) + lb;
   const BrickGeom bg = brick_geom(b, g, k);
@@ -565,7 +618,7 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
   for (int64_t base = lbeg; base < lend; base += 32) {
     const int gid = gid_next;
     gid_next = (base + 32 + lane < lend) ? __ldg(gids + base + 32 + lane) : -1;
-    bool hit = false;
+    bool hit = false, hitA = false, hitB = false;
     Pair32 p;
     if (gid >= 0) {
       const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
@@ -578,12 +631,29 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
                   hzv = fmaf(q3.y, isz, 1e-3f);
       hit = cxv + hxv >= ftxl && cxv - hxv <= ftxh && cyv + hyv >= ftyl &&
             cyv - hyv <= ftyh && czv + hzv >= ftzl && czv - hzv <= ftzh;
+      if (TWO && hit) {                        // y-half boxes: [0, 3] and [4, ey - 1]
+        hitA = cyv - hyv <= fminf(3.f, ftyh);
+        hitB = ftyh >= 4.f && cyv + hyv >= 4.f;
+      }
       if (hit && !isinf(cut2)) {
         const float ddx = fmaxf(fmaxf(ftxl - cxv, cxv - ftxh), 0.f) * fsx;
         const float ddy = fmaxf(fmaxf(ftyl - cyv, cyv - ftyh), 0.f) * fsy;
         const float ddz = fmaxf(fmaxf(ftzl - czv, czv - ftzh), 0.f) * fsz;
         const float dist2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
-        hit = dist2 * q3.z <= cut2 * 1.0001f + 1e-6f;
+        const float lim = cut2 * 1.0001f + 1e-6f;
+        hit = dist2 * q3.z <= lim;
+        if (TWO) {
+          const float ddyA = fmaxf(fmaxf(-cyv, cyv - fminf(3.f, ftyh)), 0.f) * fsy;
+          const float ddyB = fmaxf(fmaxf(4.f - cyv, cyv - ftyh), 0.f) * fsy;
+          const float xz = fmaf(ddx, ddx, ddz * ddz);
+          hitA = hitA && fmaf(ddyA, ddyA, xz) * q3.z <= lim;
+          hitB = hitB && fmaf(ddyB, ddyB, xz) * q3.z <= lim;
+        }
+      }
+      if (TWO) {
+        hitA = hitA && hit;
+        hitB = hitB && hit;
+        hit = hitA || hitB;
       }
       if (hit) {
         const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
@@ -627,6 +697,19 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
         p.c.w = qcut + guard;
         p.d = make_float4(qcut - guard, __int_as_float(gid), 0.f, 0.f);
       }
+    }
+    if (TWO) {
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned ballA = __ballot_sync(kFull, hitA), ballB = __ballot_sync(kFull, hitB);
+      if (hitA) wsp[__popc(ballA & lt)] = p;
+      if (hitB) wsp[32 + __popc(ballB & lt)] = p;
+      __syncwarp();
+      eval_column_hits(wsp, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g, cut2d, aS[0],
+                       aW[0]);
+      eval_column_hits(wsp + 32, __popc(ballB), mX, mY + 4.f, mZ, mZ1, gx, gyB, gz, xsrc, g,
+                       cut2d, aS[1], aW[1]);
+      __syncwarp();
+      continue;
     }
     const unsigned ball = __ballot_sync(kFull, hit);
     if (hit) wsp[__popc(ball & ((1u << lane) - 1u))] = p;
@@ -1557,9 +1640,20 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
                       live_masks == nullptr,
                   "vpl 8 needs 8x8x4 bricks and no live masks");
       const ExactSrc xw{positions, log_scales, rotations, rec64};
-      forward32w_kernel<<<(unsigned)nb, 32, 0, s>>>(
-          positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
-          (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab, loss_part);
+      static const bool one_list = [] {
+        const char* e = getenv("GSV_WHOLE_ONE_LIST");
+        return e != nullptr && e[0] == '1';
+      }();
+      if (one_list)
+        forward32w_kernel<false><<<(unsigned)nb, 32, 0, s>>>(
+            positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
+            (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab,
+            loss_part);
+      else
+        forward32w_kernel<true><<<(unsigned)nb, 32, 0, s>>>(
+            positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
+            (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab,
+            loss_part);
       GSV_CHECK_LAUNCH("forward32w_kernel");
       return GSV_OK;
     }
