@@ -288,6 +288,10 @@ TrainStep.update = _update_method
 
 # ------------------------------------------------------------ graph-replayed step
 _GRAPH_HEADROOM = 1.15       # pair capacity over the pair count seen at capture
+# Renderer graphs: less room -- the sort runs over the whole capacity, and a
+# render's field moves less between calls than a fit step's (an overflow
+# still re-captures with 1.5x)
+_RENDER_HEADROOM = 1.05
 _RESULT_SLOTS = 4            # pinned result slots (at most 2 steps are in flight)
 _BC_CHUNK = 16384            # bias-correction table length per capture
 
@@ -756,7 +760,7 @@ class Renderer:
             b["rec32"].data_ptr(), None, b["counts"].data_ptr(), b["box"].data_ptr(),
             _lib.stream_ptr()), "preprocess")
         pairs = int(_scan(b["counts"], nb, self.pool)[-1].item())
-        cap = max(int(pairs * _GRAPH_HEADROOM) + 4096, min_cap, 1)
+        cap = max(int(pairs * _RENDER_HEADROOM) + 4096, min_cap, 1)
         nbytes = ctypes.c_size_t(0)
         _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
         nv = self.grid.num_voxels

@@ -567,7 +567,7 @@ def test_renderer_recovers_from_capacity_overflow(monkeypatch):
 
     def capture(self, f, key, min_cap=0):
         calls.append(min_cap)
-        monkeypatch.setattr(train_mod, "_GRAPH_HEADROOM", 0.1 if len(calls) == 1 else 1.15)
+        monkeypatch.setattr(train_mod, "_RENDER_HEADROOM", 0.1 if len(calls) == 1 else 1.05)
         return real(self, f, key, min_cap)
 
     monkeypatch.setattr(gs.Renderer, "_capture", capture)

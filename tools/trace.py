@@ -33,7 +33,15 @@ def main():
     torch.cuda.set_device(0)
     p = synth.make_problem(synth.CONFIGS[args.config])
     f = gs.GaussianField(*p["field"])
-    if args.hr or args.grid512:
+    if args.grid512:
+        # bench.py's config-5 render: the jittered trained-size field at 512^3
+        import numpy as np
+        f = gs.GaussianField(*synth.jitter_field([np.asarray(a) for a in p["field"]],
+                                                 p["lr_grid"]))
+        rend = gs.Renderer(gs.grid_covering_extent(p["lr_grid"], (512, 512, 512)),
+                           gs.RenderOptions(), (8, 8, 4))
+        run = lambda: rend(f)  # noqa: E731
+    elif args.hr:
         rend = gs.Renderer(p["render_grid"], gs.RenderOptions(), (8, 8, 4))
         run = lambda: rend(f)  # noqa: E731
     else:
