@@ -36,6 +36,9 @@
 extern "C" {
 #endif
 
+/* ABI history: 2 -- graph step, metrics, geometry helpers; 3 -- gsv_bricks
+ * carries a brick-id range [b0, b1) instead of whole z-layers [bz0, bz1),
+ * and the box record's 4th word holds k0 (see gsv_preprocess). */
 #define GSV_ABI_VERSION 3
 
 typedef enum {
@@ -101,8 +104,12 @@ int gsv_device_sm_count(void);
  *                  engine; the f32 engine recomputes the f64 factor from
  *                  log_scales/rotations in its rare guard-band path)
  *   counts (N)   : pairs Gaussian i emits inside the slab (0 if outside)
- *   box    (N,4) : int32 {blo_x | blo_y<<16, blo_z | nb_x<<16, nb_y | nb_z<<16, 0}
- *                  brick box of Gaussian i clipped to the slab.
+ *   box    (N,4) : int32 {blo_x | blo_y<<16, blo_z | nb_x<<16, nb_y | nb_z<<16, k0}
+ *                  brick box of Gaussian i clipped to the slab's brick layers;
+ *                  k0 = box-order (x-fastest) index of its first brick inside
+ *                  [b0, b1): the slab's bricks of the box are the box-order
+ *                  run [k0, k0 + counts[i]) (box order and brick-id order are
+ *                  both lexicographic in (z, y, x)).
  * cutoff_sigma may be +inf (dense lists, raster.py:166-171).
  * ------------------------------------------------------------------------ */
 int gsv_preprocess(const double* positions, const double* log_scales,
@@ -196,7 +203,7 @@ int gsv_forward(const double* positions, const double* log_scales,
 /* Per-voxel backward inputs from (W, I, dL/dI) for the unfused API path
  * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) = {dL/dI / W, I}
  * in the precision's type and *bad (device int64) = first non-finite voxel index or
- * -1.  Slab voxels only. */
+ * -1.  Slab voxels only (the voxels of bricks [b0, b1)). */
 int gsv_backward_prep(const void* W, const void* I, const double* dldi,
                       const gsv_grid* grid, const gsv_bricks* bricks,
                       double eps_w, int precision, void* ab, int64_t* bad,
