@@ -65,6 +65,7 @@ class _Aux:
     gstart: torch.Tensor
     field_version: int
     canonical: bool = True
+    active: int | None = None        # Gaussians with >= 1 pair (the forward's tiling choice)
 
 
 @dataclass(frozen=True)
@@ -267,9 +268,12 @@ def build_brick_index(f: GaussianField, grid: GridSpec, opts: RenderOptions = Re
     rec32, rec64, counts, box = _preprocess(f, grid, opts.cutoff_sigma, brick_dims, slab,
                                             opts.precision == "f64", pool)
     gstart = _scan(counts, nbricks, pool)
-    pairs = int(gstart[-1].item())  # the one host read binning needs (buffer sizing)
+    # the one host read binning needs (buffer sizing), with the number of
+    # Gaussians that reach the slab
+    pairs, active = (int(v) for v in torch.stack(
+        [gstart[-1], torch.count_nonzero(counts)]).tolist())
     starts, gids = _fill(counts, box, gstart, pairs, bricks, nbricks, pool)
-    aux = _Aux(rec32, rec64, counts, box, gstart, f.version, True)
+    aux = _Aux(rec32, rec64, counts, box, gstart, f.version, True, active)
     return BrickIndex(grid, brick_dims, (bricks.bgx, bricks.bgy, bricks.bgz), starts, gids,
                       f.version, f.count, opts.cutoff_sigma, slab, aux)
 
@@ -310,6 +314,8 @@ def _resolve_vpl(brick_dims) -> int:
 
 
 def _forward_vpl_arg(brick_dims, pairs: int = 0, n: int = 0, masks: bool = True) -> int:
+    # n: the Gaussians that reach the index's bricks (pairs / n = mean bricks
+    # per Gaussian, the same for a slab as for the whole grid)
     """gsv_forward's vpl argument.  Renders (no live masks) of large Gaussians
     on 8x8x4 bricks -- pairs >= 8 N, so nearly every pair covers the whole
     brick -- use 8: one warp per brick, two columns per lane.  Otherwise the
@@ -339,7 +345,9 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
-        _forward_vpl_arg(idx.brick_dims, idx.pair_count, f.count, live_masks is not None),
+        _forward_vpl_arg(idx.brick_dims, idx.pair_count,
+                         idx._aux.active if (idx._aux is not None and idx._aux.active is not None)
+                         else f.count, live_masks is not None),
         _lib.stream_ptr()), "forward")
 
 

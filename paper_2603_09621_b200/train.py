@@ -738,7 +738,7 @@ class Renderer:
             b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
             float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
             b["W"].data_ptr(), b["I"].data_ptr(), None, 0, float(self.grid.num_voxels), None,
-            None, None, _forward_vpl_arg(self.brick_dims, b["pairs"], n, masks=False), s),
+            None, None, _forward_vpl_arg(self.brick_dims, b["pairs"], b["active"], masks=False), s),
             "forward")
 
     def _capture(self, f: GaussianField, key, min_cap: int = 0):
@@ -759,12 +759,15 @@ class Renderer:
             float(self.opts.cutoff_sigma), _lib.make_grid(self.grid), bricks,
             b["rec32"].data_ptr(), None, b["counts"].data_ptr(), b["box"].data_ptr(),
             _lib.stream_ptr()), "preprocess")
-        pairs = int(_scan(b["counts"], nb, self.pool)[-1].item())
+        gst = _scan(b["counts"], nb, self.pool)
+        pairs, active = (int(v) for v in torch.stack(
+            [gst[-1], torch.count_nonzero(b["counts"])]).tolist())
         cap = max(int(pairs * _RENDER_HEADROOM) + 4096, min_cap, 1)
         nbytes = ctypes.c_size_t(0)
         _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
         nv = self.grid.num_voxels
-        b["pairs"] = pairs                   # picks the forward's tiling (vpl 8 for large)
+        b["pairs"] = pairs                   # with b["active"], picks the forward's tiling
+        b["active"] = active
         b.update({"ws": gp.get("ws", (nbytes.value,), torch.uint8),
                   "keys": gp.get("keys", (3, cap), torch.int32),
                   "gids": gp.get("gids", (cap,), torch.int32),

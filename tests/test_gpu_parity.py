@@ -596,3 +596,34 @@ def test_renderer_with_no_pairs_renders_zero():
     c = gs.Renderer(grid)(f)
     for k in ("S", "W", "I"):
         assert float(getattr(c, k).abs().max()) == 0.0, k
+
+
+def test_renderer_slabs_reassemble_the_full_render():
+    """Renderer(slab=...) -- the N>1 render path -- on pair-balanced brick-id
+    ranges with mid-layer cuts: each slab's voxels match the whole-grid render
+    (to f32 rounding: a slab may pick the other warp tiling when its pairs per
+    Gaussian sit near the whole-brick threshold), and the slabs' pair counts
+    add up exactly to the whole-grid count."""
+    from paper_2603_09621_b200.distributed import pair_weights, slab_ranges, slab_voxel_mask
+    p = make_problem(CONFIGS[1])
+    f = gs.GaussianField(*p["field"])
+    grid = p["hr_grid"]
+    bd = (8, 8, 4)
+    full = gs.Renderer(grid)
+    I_full = np_(full(f).I).copy()
+    P_full = full.pair_count()
+    w = pair_weights(f, grid, gs.RenderOptions(), bd)
+    slabs = slab_ranges(len(w), 3, weights=w)
+    layer = (-(-grid.dims[0] // 8)) * (-(-grid.dims[1] // 8))
+    assert any(b % layer for _, b in slabs[:-1])
+    got = np.zeros_like(I_full)
+    pairs = 0
+    for slab in slabs:
+        r = gs.Renderer(grid, slab=slab)
+        c = r(f)
+        own = slab_voxel_mask(grid, bd, slab)
+        np.testing.assert_allclose(np_(c.I)[own], I_full[own], rtol=4e-6, atol=1e-9)
+        got[own] = np_(c.I)[own]
+        pairs += r.pair_count()
+    np.testing.assert_allclose(got, I_full, rtol=4e-6, atol=1e-9)
+    assert pairs == P_full == int(w.sum())
