@@ -268,12 +268,9 @@ def build_brick_index(f: GaussianField, grid: GridSpec, opts: RenderOptions = Re
     rec32, rec64, counts, box = _preprocess(f, grid, opts.cutoff_sigma, brick_dims, slab,
                                             opts.precision == "f64", pool)
     gstart = _scan(counts, nbricks, pool)
-    # the one host read binning needs (buffer sizing), with the number of
-    # Gaussians that reach the slab
-    pairs, active = (int(v) for v in torch.stack(
-        [gstart[-1], torch.count_nonzero(counts)]).tolist())
+    pairs = int(gstart[-1].item())  # the one host read binning needs (buffer sizing)
     starts, gids = _fill(counts, box, gstart, pairs, bricks, nbricks, pool)
-    aux = _Aux(rec32, rec64, counts, box, gstart, f.version, True, active)
+    aux = _Aux(rec32, rec64, counts, box, gstart, f.version, True)
     return BrickIndex(grid, brick_dims, (bricks.bgx, bricks.bgy, bricks.bgz), starts, gids,
                       f.version, f.count, opts.cutoff_sigma, slab, aux)
 
@@ -301,6 +298,17 @@ def _records(f, grid, idx: BrickIndex, opts: RenderOptions):
 
 
 # ----------------------------------------------------------------- forward
+def _reaching(f: GaussianField, idx: BrickIndex) -> int:
+    """Gaussians that reach the index's bricks: N for a whole-grid index
+    (Gaussians outside the grid are few), counted once for a slab index."""
+    aux = idx._aux
+    if idx.slab is None or aux is None:
+        return f.count
+    if aux.active is None:
+        aux.active = int(torch.count_nonzero(aux.counts).item())
+    return aux.active
+
+
 def _resolve_vpl(brick_dims) -> int:
     """Voxels per lane of the f32 forward's warp tiles (gsv_forward's vpl,
     the same rule as its auto mode): 4 -- columns of 4 in z, 8x4x4 tiles --
@@ -345,9 +353,8 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
         S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
-        _forward_vpl_arg(idx.brick_dims, idx.pair_count,
-                         idx._aux.active if (idx._aux is not None and idx._aux.active is not None)
-                         else f.count, live_masks is not None),
+        _forward_vpl_arg(idx.brick_dims, idx.pair_count, _reaching(f, idx),
+                         live_masks is not None),
         _lib.stream_ptr()), "forward")
 
 

@@ -760,8 +760,10 @@ class Renderer:
             b["rec32"].data_ptr(), None, b["counts"].data_ptr(), b["box"].data_ptr(),
             _lib.stream_ptr()), "preprocess")
         gst = _scan(b["counts"], nb, self.pool)
-        pairs, active = (int(v) for v in torch.stack(
-            [gst[-1], torch.count_nonzero(b["counts"])]).tolist())
+        pairs = int(gst[-1].item())
+        # Gaussians that reach the bricks (as raster._reaching): N for the
+        # whole grid, counted for a slab
+        active = n if self.slab is None else int(torch.count_nonzero(b["counts"]).item())
         cap = max(int(pairs * _RENDER_HEADROOM) + 4096, min_cap, 1)
         nbytes = ctypes.c_size_t(0)
         _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
