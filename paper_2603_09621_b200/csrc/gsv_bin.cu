@@ -27,7 +27,7 @@
 namespace gsv {
 namespace {
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 preprocess_kernel(const double* __restrict__ pos, const double* __restrict__ ls,
                   const double* __restrict__ rot, const double* __restrict__ ra,
                   const double* __restrict__ rr, int64_t n, PrepArgs pa) {
