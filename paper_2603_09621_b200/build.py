@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
           f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
+# measurement builds only: extra nvcc flags, e.g. GSV_NVCC_EXTRA="-DGSV_FWD_PREFETCH=1"
+COMMON += os.environ.get("GSV_NVCC_EXTRA", "").split()
 # Per-file extra flags.  The binning TU must never contract f64 mul+add into
 # FMA (bit-exact bounds vs numpy, SURVEY.md §0 finding 1).
 EXTRA = {"gsv_bin.cu": ["-fmad=false"]}

@@ -159,6 +159,17 @@ __device__ __forceinline__ void unit_voxel(int u, const gsv_bricks& k, bool tile
   }
 }
 
+#ifndef GSV_FWD_PREFETCH
+#define GSV_FWD_PREFETCH 1      // LR forward: 0 off, 1 L1 (-0.5%), 2 L2 (measurement builds)
+#endif
+__device__ __forceinline__ void prefetch_line(const void* p) {
+#if GSV_FWD_PREFETCH == 1
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#elif GSV_FWD_PREFETCH == 2
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#endif
+}
+
 __device__ __forceinline__ float ex2_approx(float q) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
@@ -296,9 +307,18 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
     for (int h = 0; h < VPL; ++h) accS[h] = accW[h] = 0.f;
 
     int gid_next = (lbeg + lane < lend) ? __ldg(gids + lbeg + lane) : -1;
+    int gid_next2 = (lbeg + 32 + lane < lend) ? __ldg(gids + lbeg + 32 + lane) : -1;
     for (int64_t base = lbeg; base < lend; base += 32) {
       const int gid = gid_next;
-      gid_next = (base + 32 + lane < lend) ? __ldg(gids + base + 32 + lane) : -1;
+      gid_next = gid_next2;
+      gid_next2 = (base + 64 + lane < lend) ? __ldg(gids + base + 64 + lane) : -1;
+#if GSV_FWD_PREFETCH
+      // next round's record and position lines, in flight during this round
+      if (gid_next >= 0) {
+        prefetch_line(rec + gid_next);
+        prefetch_line(pos + 3 * (int64_t)gid_next);
+      }
+#endif
       bool hit = false;
       Pair32 p;
       if (gid >= 0) {
