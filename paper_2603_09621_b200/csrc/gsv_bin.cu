@@ -61,10 +61,11 @@ __global__ void scan_tail_kernel(const int32_t* counts, int64_t n, int64_t* gsta
 // coalesced stores.
 constexpr int kEmitWin = 512;
 
+template <typename K>
 __global__ void __launch_bounds__(256)
 emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
                  const int64_t* __restrict__ gstart, int64_t n, gsv_bricks k,
-                 int32_t* __restrict__ keys, int32_t* __restrict__ vals, int64_t cap) {
+                 K* __restrict__ keys, int32_t* __restrict__ vals, int64_t cap) {
   __shared__ int2 swin[8][kEmitWin];          // per warp: (key, gid) of one window
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31;
@@ -120,7 +121,7 @@ emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__
       const int64_t o = base + w0 + q;
       if (o < cap) {
         const int2 e = win[q];
-        keys[o] = e.x;
+        keys[o] = (K)e.x;
         vals[o] = e.y;
       }
     }
@@ -131,7 +132,8 @@ emit_warp_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__
 // starts[b] = lower_bound(keys, b) for b < B (one thread per brick, binary
 // search over the sorted keys); starts[B] = P (capacity mode: the device
 // count, which cuts off the padding); all zero on overflow.
-__global__ void starts_search_kernel(const int32_t* __restrict__ keys, int64_t p, int32_t nb,
+template <typename K>
+__global__ void starts_search_kernel(const K* __restrict__ keys, int64_t p, int32_t nb,
                                      int64_t* __restrict__ starts,
                                      const int32_t* __restrict__ overflow,
                                      const int64_t* __restrict__ p_true) {
@@ -148,7 +150,7 @@ __global__ void starts_search_kernel(const int32_t* __restrict__ keys, int64_t p
   int64_t lo = 0, hi = p;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(keys + mid) < (int32_t)b) lo = mid + 1; else hi = mid;
+    if ((int32_t)__ldg(keys + mid) < (int32_t)b) lo = mid + 1; else hi = mid;
   }
   starts[b] = lo;
 }
@@ -158,14 +160,15 @@ __global__ void starts_search_kernel(const int32_t* __restrict__ keys, int64_t p
 // that brick's real pairs, and starts[nb] = P cuts them off), so keys stay
 // within ceil(log2 nb) bits; overflow = P > cap (or the caller's dry-run
 // flag) empties every list.
+template <typename K>
 __global__ void pad_kernel(const int64_t* __restrict__ gstart, int64_t n, int64_t cap,
                            int32_t nb, const int32_t* __restrict__ dry,
-                           int32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                           K* __restrict__ keys, int32_t* __restrict__ vals,
                            int32_t* __restrict__ overflow) {
   const int64_t p = gstart[n];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = p + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cap; j += stride) {
-    keys[j] = nb - 1;
+    keys[j] = (K)(nb - 1);
     vals[j] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -182,6 +185,19 @@ __global__ void unsorted_kernel(const int64_t* __restrict__ starts,
       *flag = 1;
       return;
     }
+}
+
+// Slabs of at most 65536 bricks sort 16-bit keys: a quarter less traffic
+// per radix pass (the key buffers, allocated for int32, are used at half width).
+inline bool keys16(int64_t nb) { return nb <= 65536; }
+
+template <typename K>
+cudaError_t sort_pairs(void* ws, size_t& bytes, const int32_t* keys_in, int32_t* keys_out,
+                       const int32_t* vals_in, int32_t* vals_out, int count, int bits,
+                       cudaStream_t s) {
+  return cub::DeviceRadixSort::SortPairs(ws, bytes, reinterpret_cast<const K*>(keys_in),
+                                         reinterpret_cast<K*>(keys_out), vals_in, vals_out,
+                                         count, 0, bits, s);
 }
 
 int key_bits(int64_t nb) {
@@ -231,10 +247,14 @@ int gsv_bin_workspace(int64_t n, int64_t max_pairs, int32_t nbricks, size_t* byt
   cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, it, (int64_t*)nullptr,
                                                 (int)(n > 0 ? n : 1));
   if (e != cudaSuccess) return cuda_status(e, "DeviceScan sizing");
-  e = cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int32_t*)nullptr,
-                                      (int32_t*)nullptr, (const int32_t*)nullptr,
-                                      (int32_t*)nullptr, (int)(max_pairs > 0 ? max_pairs : 1),
-                                      0, key_bits(nbricks));
+  {
+    const int cnt = (int)(max_pairs > 0 ? max_pairs : 1);
+    e = keys16(nbricks)
+            ? sort_pairs<uint16_t>(nullptr, sort_bytes, nullptr, nullptr, nullptr, nullptr, cnt,
+                                   key_bits(nbricks), nullptr)
+            : sort_pairs<int32_t>(nullptr, sort_bytes, nullptr, nullptr, nullptr, nullptr, cnt,
+                                  key_bits(nbricks), nullptr);
+  }
   if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort sizing");
   *bytes = (scan_bytes > sort_bytes ? scan_bytes : sort_bytes) + 256;
   return GSV_OK;
@@ -268,18 +288,30 @@ int gsv_bin_fill(const int32_t* counts, const int32_t* box, const int64_t* gstar
               (long long)pairs);
   cudaStream_t s = as_stream(stream);
   const int64_t nb = slab_bricks(*bricks);
+  const bool k16 = keys16(nb);
   if (pairs > 0) {
-    emit_warp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-        counts, box, gstart, n, *bricks, keys_tmp, vals_tmp, INT64_MAX);
+    if (k16)
+      emit_warp_kernel<uint16_t><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+          counts, box, gstart, n, *bricks, reinterpret_cast<uint16_t*>(keys_tmp), vals_tmp,
+          INT64_MAX);
+    else
+      emit_warp_kernel<int32_t><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+          counts, box, gstart, n, *bricks, keys_tmp, vals_tmp, INT64_MAX);
     GSV_CHECK_LAUNCH("emit_warp_kernel");
     size_t bytes = workspace_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, bytes, keys_tmp, keys_out,
-                                                    vals_tmp, gids_out, (int)pairs, 0,
-                                                    key_bits(nb), s);
+    cudaError_t e = k16 ? sort_pairs<uint16_t>(workspace, bytes, keys_tmp, keys_out, vals_tmp,
+                                               gids_out, (int)pairs, key_bits(nb), s)
+                        : sort_pairs<int32_t>(workspace, bytes, keys_tmp, keys_out, vals_tmp,
+                                              gids_out, (int)pairs, key_bits(nb), s);
     if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort::SortPairs");
   }
-  starts_search_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
-      keys_out, pairs, (int32_t)nb, starts_out, nullptr, nullptr);
+  if (k16)
+    starts_search_kernel<uint16_t><<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const uint16_t*>(keys_out), pairs, (int32_t)nb, starts_out, nullptr,
+        nullptr);
+  else
+    starts_search_kernel<int32_t><<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
+        keys_out, pairs, (int32_t)nb, starts_out, nullptr, nullptr);
   GSV_CHECK_LAUNCH("starts_search_kernel");
   return GSV_OK;
 }
@@ -295,21 +327,37 @@ int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box, const int64
               (long long)capacity);
   cudaStream_t s = as_stream(stream);
   const int64_t nb = slab_bricks(*bricks);
+  const bool k16 = keys16(nb);
+  uint16_t* kt16 = reinterpret_cast<uint16_t*>(keys_tmp);
   if (n > 0) {
-    emit_warp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-        counts, box, gstart, n, *bricks, keys_tmp, vals_tmp, capacity);
+    if (k16)
+      emit_warp_kernel<uint16_t><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+          counts, box, gstart, n, *bricks, kt16, vals_tmp, capacity);
+    else
+      emit_warp_kernel<int32_t><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+          counts, box, gstart, n, *bricks, keys_tmp, vals_tmp, capacity);
     GSV_CHECK_LAUNCH("emit_warp_kernel");
   }
-  pad_kernel<<<592, 256, 0, s>>>(gstart, n, capacity, (int32_t)nb, dry, keys_tmp, vals_tmp,
-                                 overflow);
+  if (k16)
+    pad_kernel<uint16_t><<<592, 256, 0, s>>>(gstart, n, capacity, (int32_t)nb, dry, kt16,
+                                             vals_tmp, overflow);
+  else
+    pad_kernel<int32_t><<<592, 256, 0, s>>>(gstart, n, capacity, (int32_t)nb, dry, keys_tmp,
+                                            vals_tmp, overflow);
   GSV_CHECK_LAUNCH("pad_kernel");
   size_t bytes = workspace_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, bytes, keys_tmp, keys_out,
-                                                  vals_tmp, gids_out, (int)capacity, 0,
-                                                  key_bits(nb), s);
+  cudaError_t e = k16 ? sort_pairs<uint16_t>(workspace, bytes, keys_tmp, keys_out, vals_tmp,
+                                             gids_out, (int)capacity, key_bits(nb), s)
+                      : sort_pairs<int32_t>(workspace, bytes, keys_tmp, keys_out, vals_tmp,
+                                            gids_out, (int)capacity, key_bits(nb), s);
   if (e != cudaSuccess) return cuda_status(e, "DeviceRadixSort::SortPairs");
-  starts_search_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
-      keys_out, capacity, (int32_t)nb, starts_out, overflow, gstart + n);
+  if (k16)
+    starts_search_kernel<uint16_t><<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
+        reinterpret_cast<const uint16_t*>(keys_out), capacity, (int32_t)nb, starts_out,
+        overflow, gstart + n);
+  else
+    starts_search_kernel<int32_t><<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(
+        keys_out, capacity, (int32_t)nb, starts_out, overflow, gstart + n);
   GSV_CHECK_LAUNCH("starts_search_kernel");
   return GSV_OK;
 }

@@ -87,6 +87,25 @@ def test_binning_matches_oracle_any_brick_dims(bd):
     np.testing.assert_array_equal(np_(idx.gids), gi)
 
 
+@pytest.mark.parametrize("dims", [(128, 128, 256), (136, 128, 256)])
+def test_binning_at_the_16_bit_key_boundary(dims):
+    """Slabs of <= 65536 bricks sort 16-bit keys, larger ones 32-bit: 128x128x256
+    voxels (8x8x4 bricks) is exactly 65536 bricks, 136x128x256 is 69632.  Both
+    widths match the oracle bit for bit, through the eager index and through
+    the capacity-mode (graph) binning of the Renderer."""
+    grid = gs.GridSpec(dims, (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    arrs = random_field_arrays(3000, grid, 5, 0.5, 2.0)
+    f = gs.GaussianField(*arrs)
+    idx = gs.build_brick_index(f, grid)
+    st, gi = oracle.build_index(field_dict(arrs), grid.dims, grid.spacing, grid.origin,
+                                (8, 8, 4), 3.0)
+    assert len(st) - 1 == (dims[0] // 8) * (dims[1] // 8) * (dims[2] // 4)
+    np.testing.assert_array_equal(np_(idx.starts), st)
+    np.testing.assert_array_equal(np_(idx.gids), gi)
+    r = gs.Renderer(grid)
+    _renders_equal(r(f), gs.forward(f, grid, idx))
+
+
 # ------------------------------------------------------------ forward
 @pytest.mark.parametrize("precision", ["f32", "f64"])
 def test_sweep_forward_vs_oracle(precision):
