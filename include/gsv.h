@@ -184,9 +184,10 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  * tiles when the brick dims are multiples of 4, 4 warps per 8x8x4 brick),
  * 4 (columns of 4 in z: 8x4x4 tiles, 2 warps), or 0 = auto (4 when
  * bdz % 4 == 0 and the brick has <= 64 columns, else 2).
- * live_masks (optional, f32): 4 planes of P uint2, the forward's exact
- * truncation decisions, consumed by gsv_backward so it walks only live
- * voxels.  Word w of a pair (plane w/2, .x/.y = w%2) holds the live bits of
+ * live_masks (optional, f32): P x 4 uint2 (pair-major: a pair's 8 words are
+ * 32 contiguous bytes), the forward's exact truncation decisions, consumed by
+ * gsv_backward so it walks only live voxels.  Word w of a pair (uint2 w/2,
+ * .x/.y = w%2) holds the live bits of
  * warp tile w/vpl at depth w%vpl, bit = lane.  Requires a brick that fills
  * the CTA's warp tiles exactly (vpl 2: 128 columns of 2; vpl 4: 64 of 4 --
  * e.g. 8x8x4).

@@ -259,8 +259,6 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
   // masks (host-checked: units <= THREADS): per pair VPL words per warp,
   // planes [warp * VPL/2 + k][pair] of uint2 {word 2k, word 2k+1}
   constexpr bool want_masks = MASKS;
-  // pairs of the slab: the mask plane stride (starts[nbricks_slab])
-  const int64_t mstride = starts[SPLIT ? (gridDim.x >> 1) : gridDim.x];
   double lsum = 0.0;
 
   for (int ubase = 0; ubase < units; ubase += SPLIT ? units : THREADS) {
@@ -498,7 +496,16 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
         for (int kk = 0; kk < VPL / 2; ++kk) {
           mm[kk].x &= ownb[2 * kk];      // voxels outside the grid never enter a mask
           mm[kk].y &= ownb[2 * kk + 1];
-          if (gid >= 0) live_masks[(warp * (VPL / 2) + kk) * mstride + base + lane] = mm[kk];
+        }
+        // pair-major: the pair's 4 planes are 32 contiguous bytes
+        if (gid >= 0) {
+          uint2* dst = live_masks + 4 * (base + lane) + warp * (VPL / 2);
+          if constexpr (VPL == 4) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(mm[0].x, mm[0].y, mm[1].x, mm[1].y);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < VPL / 2; ++kk) dst[kk] = mm[kk];
+          }
         }
       }
       __syncwarp();
@@ -1312,13 +1319,18 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
   const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
   const bool tiled = ((k.bdx | k.bdy | k.bdz) & 3) == 0;
   const int units = (int)mask_units(k, mvpl);
-  const int64_t mstride = starts[gridDim.x];   // mask plane stride = slab pairs
+  // pair-major masks: pair j's 4 planes {a0, a1, a2, a3} are 32 contiguous bytes
   // mask word wi = VPL * warp + h, bit = lane of the warp tile: voxel of
   // unit warp * 32 + bit, z0 + h (the forward's layout for its VPL)
   const int wsh = mvpl == 4 ? 2 : 1;
   // the host guarantees the brick fills all 4 planes (units = 128 / vpl * 2)
-  auto load_plane = [&](const uint2* m, int plane, int64_t j) {
-    return __ldg(m + plane * mstride + j);
+  auto load_masks = [&](int64_t j, uint2& a0, uint2& a1, uint2& a2, uint2& a3) {
+    const uint4* p = reinterpret_cast<const uint4*>(masks + 4 * j);
+    const uint4 m01 = __ldg(p), m23 = __ldg(p + 1);
+    a0 = make_uint2(m01.x, m01.y);
+    a1 = make_uint2(m01.z, m01.w);
+    a2 = make_uint2(m23.x, m23.y);
+    a3 = make_uint2(m23.z, m23.w);
   };
   for (int e = tid; e < 256; e += kBwdThreads) {
     const int wi = e >> 5, u = ((wi >> wsh) << 5) + (e & 31);
@@ -1352,8 +1364,8 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
 #pragma unroll 4
     for (int t = tid; t < cnt; t += kBwdThreads) {
       const int64_t jt = cbase + t;
-      const uint2 a0 = load_plane(masks, 0, jt), a1 = load_plane(masks, 1, jt),
-                  a2 = load_plane(masks, 2, jt), a3 = load_plane(masks, 3, jt);
+      uint2 a0, a1, a2, a3;
+      load_masks(jt, a0, a1, a2, a3);
       const int gj = __ldg(gids + jt);
       const int c = __popc(a0.x) + __popc(a0.y) + __popc(a1.x) + __popc(a1.y) + __popc(a2.x) +
                     __popc(a2.y) + __popc(a3.x) + __popc(a3.y);
@@ -1411,8 +1423,8 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
         ey[a] = L[3 * a + 1] * fsy;
         ez[a] = L[3 * a + 2] * fsz;
       }
-      const uint2 a0 = load_plane(masks, 0, j), a1 = load_plane(masks, 1, j),
-                  a2 = load_plane(masks, 2, j), a3 = load_plane(masks, 3, j);
+      uint2 a0, a1, a2, a3;
+      load_masks(j, a0, a1, a2, a3);
       // this lane's column of the warp's word table (conflict-free, no sync:
       // only the lane itself reads it): its non-empty words and their LUT
       // bases, compacted, plus a zero sentinel

@@ -171,7 +171,7 @@ class TrainStep:
         self._mask_vpl = _resolve_vpl(bd)
         if (opts.precision == "f32" and _masks_fit(bd, self._mask_vpl)
                 and not os.environ.get("GSV_NO_LIVE_MASKS")):
-            masks = pool.get("live_masks", (4, max(idx.pair_count, 1), 2), torch.int32)
+            masks = pool.get("live_masks", (max(idx.pair_count, 1), 4, 2), torch.int32)
         self._mark("forward")
         _forward_into(f, grid, idx, opts, aux.rec32, aux.rec64, S, W, I, target=self.target,
                       loss_kind=self.loss_kind, ab=ab, loss_part=loss_part, live_masks=masks)
@@ -484,7 +484,7 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     b["ab"] = gp.get("ab", (nvox, 2), torch.float32)
     b["loss_part"] = gp.get("loss_part", (max(nb, 1),), torch.float64)
     b["loss_sum"] = gp.get("loss_sum", (1,), torch.float64)
-    b["masks"] = gp.get("masks", (4, cap, 2), torch.int32)
+    b["masks"] = gp.get("masks", (cap, 4, 2), torch.int32)
     b["partials"] = gp.get("partials", (cap, 12), torch.float32)
     b["dry"] = gp.get("dry", (1,), torch.int32)
     b["overflow"] = gp.get("overflow", (1,), torch.int32)

@@ -34,7 +34,7 @@ def main():
     out = step.forward(f)
     torch.cuda.synchronize()
     P = out.idx.pair_count
-    words = step._masks[:, :P, :].cpu().numpy()                 # (4, P, 2) int32
+    words = step._masks[:P].permute(1, 0, 2).cpu().numpy()    # (P, 4, 2) -> (4, P, 2)
     bits = np.unpackbits(np.ascontiguousarray(words).view(np.uint8), axis=-1)
     bits = bits.reshape(4, P, -1)
     per_tile = [bits[2 * t:2 * t + 2].transpose(1, 0, 2).reshape(P, -1).sum(1)
