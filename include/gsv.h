@@ -38,8 +38,9 @@ extern "C" {
 
 /* ABI history: 2 -- graph step, metrics, geometry helpers; 3 -- gsv_bricks
  * carries a brick-id range [b0, b1) instead of whole z-layers [bz0, bz1),
- * and the box record's 4th word holds k0 (see gsv_preprocess). */
-#define GSV_ABI_VERSION 3
+ * and the box record's 4th word holds k0 (see gsv_preprocess); 4 -- live
+ * masks are pair-major (P x 4 uint2, see gsv_forward). */
+#define GSV_ABI_VERSION 4
 
 typedef enum {
   GSV_OK = 0,

@@ -102,7 +102,7 @@ _SIGS = {
 _RESTYPES = {"gsv_last_error": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 3        # GSV_ABI_VERSION of include/gsv.h these signatures follow
+ABI_VERSION = 4        # GSV_ABI_VERSION of include/gsv.h these signatures follow
 
 _lib = None
 
