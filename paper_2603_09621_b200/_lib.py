@@ -198,7 +198,9 @@ class BufferPool:
         self.device = device
         self._bufs: dict = {}
 
-    def get(self, name: str, shape, dtype) -> torch.Tensor:
+    def get(self, name: str, shape, dtype, zeroed: bool = False) -> torch.Tensor:
+        """``zeroed``: a newly allocated buffer starts at zero (slab outputs, whose
+        voxels outside the slab are never written)."""
         shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
         numel = 1
         for s in shape:
@@ -206,6 +208,7 @@ class BufferPool:
         key = (name, dtype)
         buf = self._bufs.get(key)
         if buf is None or buf.numel() < max(numel, 1):
-            buf = torch.empty(int(max(numel, 1) * 1.1) + 64, dtype=dtype, device=self.device)
+            alloc = torch.zeros if zeroed else torch.empty
+            buf = alloc(int(max(numel, 1) * 1.1) + 64, dtype=dtype, device=self.device)
             self._bufs[key] = buf
         return buf[:numel].view(shape) if shape else buf[:1].view(())

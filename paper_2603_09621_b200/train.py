@@ -158,9 +158,10 @@ class TrainStep:
         nvox = grid.num_voxels
         dt = opts.torch_dtype
         pool = self.pool
-        S = pool.get("S", (nvox,), dt)
-        W = pool.get("W", (nvox,), dt)
-        I = pool.get("I", (nvox,), dt)
+        z = self.slab is not None          # voxels outside a slab stay zero
+        S = pool.get("S", (nvox,), dt, zeroed=z)
+        W = pool.get("W", (nvox,), dt, zeroed=z)
+        I = pool.get("I", (nvox,), dt, zeroed=z)
         ab = pool.get("ab", (nvox, 2), dt)
         nb = max(idx.brick_count, 1)
         loss_part = pool.get("loss_part", (nb,), torch.float64)
@@ -479,8 +480,8 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     b["gids"] = gp.get("gids", (cap,), torch.int32)
     b["starts"] = gp.get("starts", (nb + 1,), torch.int64)
     nvox = grid.num_voxels
-    for name in ("S", "W", "I"):
-        b[name] = gp.get(name, (nvox,), torch.float32)
+    for name in ("S", "W", "I"):               # voxels outside a slab stay zero
+        b[name] = gp.get(name, (nvox,), torch.float32, zeroed=self.slab is not None)
     b["ab"] = gp.get("ab", (nvox, 2), torch.float32)
     b["loss_part"] = gp.get("loss_part", (max(nb, 1),), torch.float64)
     b["loss_sum"] = gp.get("loss_sum", (1,), torch.float64)
@@ -709,9 +710,10 @@ class Renderer:
                                 pool=self.pool)
         n = self.grid.num_voxels
         dt = self.opts.torch_dtype
-        S = self.pool.get("S", (n,), dt)
-        W = self.pool.get("W", (n,), dt)
-        I = self.pool.get("I", (n,), dt)
+        z = self.slab is not None          # voxels outside a slab stay zero
+        S = self.pool.get("S", (n,), dt, zeroed=z)
+        W = self.pool.get("W", (n,), dt, zeroed=z)
+        I = self.pool.get("I", (n,), dt, zeroed=z)
         _forward_into(f, self.grid, idx, self.opts, idx._aux.rec32, idx._aux.rec64, S, W, I)
         self.last_index = idx
         return RenderCache(self.grid, S, W, I, f.version)
@@ -774,8 +776,9 @@ class Renderer:
                   "keys": gp.get("keys", (3, cap), torch.int32),
                   "gids": gp.get("gids", (cap,), torch.int32),
                   "starts": gp.get("starts", (nb + 1,), torch.int64),
-                  "S": gp.get("S", (nv,), torch.float32), "W": gp.get("W", (nv,), torch.float32),
-                  "I": gp.get("I", (nv,), torch.float32),
+                  "S": gp.get("S", (nv,), torch.float32, zeroed=self.slab is not None),
+                  "W": gp.get("W", (nv,), torch.float32, zeroed=self.slab is not None),
+                  "I": gp.get("I", (nv,), torch.float32, zeroed=self.slab is not None),
                   "dry": gp.get("dry", (1,), torch.int32),
                   "overflow": gp.get("overflow", (1,), torch.int32),
                   "ovf_host": torch.zeros(1, dtype=torch.int32).pin_memory()})

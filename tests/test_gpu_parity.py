@@ -642,6 +642,7 @@ def test_renderer_slabs_reassemble_the_full_render():
         c = r(f)
         own = slab_voxel_mask(grid, bd, slab)
         np.testing.assert_allclose(np_(c.I)[own], I_full[own], rtol=4e-6, atol=1e-9)
+        assert not np_(c.I)[~own].any()          # voxels outside the slab stay zero
         got[own] = np_(c.I)[own]
         pairs += r.pair_count()
     np.testing.assert_allclose(got, I_full, rtol=4e-6, atol=1e-9)
