@@ -323,11 +323,13 @@ def run_ours(args, dist, ws, rank, local):
         barrier()
         # wall clock: at least 100 steps (~0.2 s) so host jitter averages out
         k_e2e = max(args.steps, 100)
+        caps0 = getattr(step, "graph_captures", 0)
         t0 = time.perf_counter()
         loss = run_fit_steps(k_e2e, e2e_launch)[-1]   # loss device -> host each step
         barrier()
         sec = max_over_ranks((time.perf_counter() - t0) / k_e2e)
         e2e = {"value": 1.0 / sec, "unit": "it/s", "steps": k_e2e,
+               "graph_captures": getattr(step, "graph_captures", 0) - caps0,
                "h2d_bytes_per_step": host_t.numel() * 4,
                "d2h_bytes_per_step": 16, "api": "TrainStep.set_target + TrainStep.step_async/"
                "StepHandle.loss (fit()'s loop body: CUDA-graph replay + 16-byte loss read, "

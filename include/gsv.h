@@ -181,10 +181,11 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  *   loss_part (nbricks_slab) double : per-brick sum |I-T| (l1) or (I-T)^2.
  * loss_kind: 0 = l1, 1 = l2.  vox_count = global voxel count V, so
  * dL/dI = sign(I-T)/V (l1) or 2(I-T)/V (l2) exactly as optimize.py:99-102.
- * vpl: voxels per lane of the f32 kernel's 32-lane warp tiles: 2 (4x4x4
- * tiles when the brick dims are multiples of 4, 4 warps per 8x8x4 brick),
- * 4 (columns of 4 in z: 8x4x4 tiles, 2 warps), or 0 = auto (4 when
- * bdz % 4 == 0 and the brick has <= 64 columns, else 2).
+ * vpl: voxels per lane of the f32 kernel: 2 (4x4x4 warp tiles when the
+ * brick dims are multiples of 4, 4 warps per 8x8x4 brick), 4 (columns of 4
+ * in z: 8x4x4 tiles, 2 warps), 8 (8x8x4 bricks only: one warp per brick,
+ * two columns per lane, one hit list per y-half), or 0 = auto (8 for 8x8x4
+ * bricks, else 4 when bdz % 4 == 0 and the brick has <= 64 columns, else 2).
  * live_masks (optional, f32): P x 4 uint2 (pair-major: a pair's 8 words are
  * 32 contiguous bytes), the forward's exact truncation decisions, consumed by
  * gsv_backward so it walks only live voxels.  Word w of a pair (uint2 w/2,

@@ -554,14 +554,13 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
 // the columns (x, y) = (l & 7, l >> 3) and (x, y + 4), all 4 z.  A pair is
 // staged and its quadratic built once per brick; column B's start value and
 // z-step follow from column A's in 5 FMAs.  No live masks (renders only).
-// Evaluate one column (4 voxels in z) of a lane against a compacted hit list
-// (the two-list whole-brick forward): q in nested form at the column's first
-// voxel, then second differences; live accumulation, then the guard band.
-__device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits, int nh,
-                                                 float mX, float mY, float mZ, float mZ1,
-                                                 int gx, int gy, int gz, const ExactSrc& xsrc,
-                                                 const gsv_grid& g, double cut2d,
-                                                 float* aS, float* aW) {
+// Render form (no live masks): kept as its own function -- sharing the
+// masked template measurably changed the render kernel's scheduling (+1.5%).
+__device__ __forceinline__ void eval_column_hits_plain(const Pair32* __restrict__ hits, int nh,
+                                                       float mX, float mY, float mZ, float mZ1,
+                                                       int gx, int gy, int gz,
+                                                       const ExactSrc& xsrc, const gsv_grid& g,
+                                                       double cut2d, float* aS, float* aW) {
   constexpr int Z = 4;
   for (int jj = 0; jj < nh; ++jj) {
     const float4 pa = hits[jj].a, pb = hits[jj].b, pc = hits[jj].c;
@@ -603,10 +602,84 @@ __device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits
   }
 }
 
+// Evaluate one column (4 voxels in z) of a lane against a compacted hit list
+// (the two-list whole-brick forward): q in nested form at the column's first
+// voxel, then second differences; live accumulation, then the guard band.
+template <bool MASKS>
+__device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits, int nh,
+                                                 float mX, float mY, float mZ, float mZ1,
+                                                 int gx, int gy, int gz, const ExactSrc& xsrc,
+                                                 const gsv_grid& g, double cut2d,
+                                                 float* aS, float* aW, uint4* smw) {
+  constexpr int Z = 4;
+  for (int jj = 0; jj < nh; ++jj) {
+    const float4 pa = hits[jj].a, pb = hits[jj].b, pc = hits[jj].c;
+    const float2 pd = *reinterpret_cast<const float2*>(&hits[jj].d);   // qlo, gid
+    float q[Z];
+    const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
+    const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
+    const float t3 = fmaf(pb.z, mZ, pa.w);
+    q[0] = fmaf(mX, t1, fmaf(mY, t2, fmaf(mZ, t3, pa.x)));
+    float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, mZ1, t3)));
+    const float d2q = 2.f * pb.z;
+#pragma unroll
+    for (int h = 1; h < Z; ++h) {
+      q[h] = q[h - 1] + dq;
+      dq += d2q;
+    }
+    bool live[Z], band = false;
+#pragma unroll
+    for (int h = 0; h < Z; ++h) {
+      live[h] = q[h] >= pc.w;
+      const float w = ex2_approx(q[h]);
+      if (live[h]) {
+        aS[h] = fmaf(pc.z, w, aS[h]);
+        aW[h] += w;
+      }
+    }
+    if constexpr (MASKS)   // the column's live words of this hit (warp-uniform stores)
+      smw[jj] = make_uint4(__ballot_sync(kFull, live[0]), __ballot_sync(kFull, live[1]),
+                           __ballot_sync(kFull, live[2]), __ballot_sync(kFull, live[3]));
+#pragma unroll
+    for (int h = 0; h < Z; ++h) band |= !live[h] && q[h] >= pd.x;
+    if (__any_sync(kFull, band)) {
+      const int gidj = __float_as_int(pd.y);
+      if constexpr (MASKS) {
+        bool xl[Z];
+#pragma unroll
+        for (int h = 0; h < Z; ++h) {
+          xl[h] = !live[h] && q[h] >= pd.x && exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d);
+          if (xl[h]) {
+            const float w = ex2_approx(q[h]);
+            aS[h] = fmaf(pc.z, w, aS[h]);
+            aW[h] += w;
+          }
+        }
+        const uint4 x = make_uint4(__ballot_sync(kFull, xl[0]), __ballot_sync(kFull, xl[1]),
+                                   __ballot_sync(kFull, xl[2]), __ballot_sync(kFull, xl[3]));
+        const uint4 a = smw[jj];
+        __syncwarp();
+        smw[jj] = make_uint4(a.x | x.x, a.y | x.y, a.z | x.z, a.w | x.w);
+      } else {
+#pragma unroll
+        for (int h = 0; h < Z; ++h)
+          if (!live[h] && q[h] >= pd.x && exact_live(gidj, gx, gy, gz + h, xsrc, g, cut2d)) {
+            const float w = ex2_approx(q[h]);
+            aS[h] = fmaf(pc.z, w, aS[h]);
+            aW[h] += w;
+          }
+      }
+    }
+  }
+}
+
 // TWO: per 32-pair round, the hits are compacted into one list per y-half of
 // the brick (each half's own box and sphere cull) and each list is evaluated
 // for that half's column only -- a pair that reaches one half costs half.
-template <bool TWO>
+// MASKS (two-list form, the train step): the pair's live-voxel words in the
+// backward's VPL-4 pair-major layout -- column A (y < 4) is tile 0, column B
+// tile 1, word = 4 tile + z, bit = lane -- one 32-byte store per pair.
+template <bool TWO, bool MASKS = false>
 __global__ void __launch_bounds__(32, 16)
 forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
                   const gsv_record32* __restrict__ rec,
@@ -615,9 +688,12 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
                   double eps_w,
                   float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
                   const float* __restrict__ target, int loss_kind, double vox_count,
-                  float2* __restrict__ ab, double* __restrict__ loss_part) {
+                  float2* __restrict__ ab, double* __restrict__ loss_part,
+                  uint2* __restrict__ live_masks = nullptr) {
+  static_assert(!MASKS || TWO, "live masks need the two-list form");
   constexpr int Z = 4;
   __shared__ Pair32 wsp[TWO ? 64 : 32];
+  __shared__ uint4 smw[MASKS ? 64 : 1];      // per hit slot: its column's 4 live words
   const int lb = blockIdx.x;
   const int b = (int)slab_first(k) + lb;
   const BrickGeom bg = brick_geom(b, g, k);
@@ -634,6 +710,14 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
   const float mX = (float)lx - ctx, mY = (float)lyA - cty, mZ = -ctz, mZ1 = mZ + 1.f;
   const float twoY4 = fmaf(2.f, mY, 4.f);      // column B = column A + 4 in y
   const int gx = bg.x0 + lx, gyA = bg.y0 + lyA, gyB = bg.y0 + lyB, gz = bg.z0;
+  unsigned ownA[Z], ownB[Z];                   // voxels inside the grid (mask words)
+  if constexpr (MASKS) {
+#pragma unroll
+    for (int h = 0; h < Z; ++h) {
+      ownA[h] = __ballot_sync(kFull, lx < bg.ex && lyA < bg.ey && h < bg.ez);
+      ownB[h] = __ballot_sync(kFull, lx < bg.ex && lyB < bg.ey && h < bg.ez);
+    }
+  }
   float aS[2][Z], aW[2][Z];
 #pragma unroll
   for (int c = 0; c < 2; ++c)
@@ -731,10 +815,28 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
       if (hitA) wsp[__popc(ballA & lt)] = p;
       if (hitB) wsp[32 + __popc(ballB & lt)] = p;
       __syncwarp();
-      eval_column_hits(wsp, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g, cut2d, aS[0],
-                       aW[0]);
-      eval_column_hits(wsp + 32, __popc(ballB), mX, mY + 4.f, mZ, mZ1, gx, gyB, gz, xsrc, g,
-                       cut2d, aS[1], aW[1]);
+      if constexpr (MASKS) {
+        eval_column_hits<true>(wsp, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g, cut2d,
+                               aS[0], aW[0], smw);
+        eval_column_hits<true>(wsp + 32, __popc(ballB), mX, mY + 4.f, mZ, mZ1, gx, gyB, gz,
+                               xsrc, g, cut2d, aS[1], aW[1], smw + 32);
+      } else {
+        eval_column_hits_plain(wsp, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g, cut2d,
+                               aS[0], aW[0]);
+        eval_column_hits_plain(wsp + 32, __popc(ballB), mX, mY + 4.f, mZ, mZ1, gx, gyB, gz, xsrc,
+                               g, cut2d, aS[1], aW[1]);
+      }
+      __syncwarp();
+      if (MASKS && gid >= 0) {
+        const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+        uint4 wa = hitA ? smw[__popc(ballA & lt)] : zero;
+        uint4 wb = hitB ? smw[32 + __popc(ballB & lt)] : zero;
+        wa = make_uint4(wa.x & ownA[0], wa.y & ownA[1], wa.z & ownA[2], wa.w & ownA[3]);
+        wb = make_uint4(wb.x & ownB[0], wb.y & ownB[1], wb.z & ownB[2], wb.w & ownB[3]);
+        uint4* dst = reinterpret_cast<uint4*>(live_masks + 4 * (base + lane));
+        dst[0] = wa;
+        dst[1] = wb;
+      }
       __syncwarp();
       continue;
     }
@@ -1661,22 +1763,31 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
   cudaStream_t s = as_stream(stream);
   if (precision == 0) {
     // Column depth: VPL voxels per lane (2: 4x4x4 warp tiles, 4 warps per
-    // 8x8x4 brick; 4: 8x4x4 tiles, 2 warps); 0 = auto (4 when bdz % 4 == 0).
+    // 8x8x4 brick; 4: 8x4x4 tiles, 2 warps; 8: whole brick per warp).
     // vpl | 0x200: keep the two tiles of a VPL-4 brick in one CTA (measurement)
     const bool no_split = (vpl & 0x200) != 0;
     vpl &= 0xff;
     GSV_REQUIRE(vpl == 0 || vpl == 2 || vpl == 4 || vpl == 8, "vpl must be 0, 2, 4 or 8");
+    // auto: the whole-brick two-list kernel for 8x8x4 bricks (fastest at every
+    // pair density measured), else the warp-tile kernels
+    if (vpl == 0 && bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4) vpl = 8;
     if (vpl == 8) {
-      // one warp per 8x8x4 brick, two 4-voxel columns per lane (renders)
-      GSV_REQUIRE(bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4 &&
-                      live_masks == nullptr,
-                  "vpl 8 needs 8x8x4 bricks and no live masks");
+      // one warp per 8x8x4 brick, two 4-voxel columns per lane, a hit list per
+      // y-half; with live masks for the train step
+      GSV_REQUIRE(bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4,
+                  "vpl 8 needs 8x8x4 bricks");
       const ExactSrc xw{positions, log_scales, rotations, rec64};
       static const bool one_list = [] {
         const char* e = getenv("GSV_WHOLE_ONE_LIST");
         return e != nullptr && e[0] == '1';
       }();
-      if (one_list)
+      GSV_REQUIRE(live_masks == nullptr || !one_list, "live masks need the two-list form");
+      if (live_masks != nullptr)
+        forward32w_kernel<true, true><<<(unsigned)nb, 32, 0, s>>>(
+            positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
+            (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab,
+            loss_part, (uint2*)live_masks);
+      else if (one_list)
         forward32w_kernel<false><<<(unsigned)nb, 32, 0, s>>>(
             positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
             (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab,

@@ -322,15 +322,19 @@ def _resolve_vpl(brick_dims) -> int:
 
 
 def _forward_vpl_arg(brick_dims, pairs: int = 0, n: int = 0, masks: bool = True) -> int:
-    # n: the Gaussians that reach the index's bricks (pairs / n = mean bricks
-    # per Gaussian, the same for a slab as for the whole grid)
-    """gsv_forward's vpl argument.  Renders (no live masks) of large Gaussians
-    on 8x8x4 bricks -- pairs >= 8 N, so nearly every pair covers the whole
-    brick -- use 8: one warp per brick, two columns per lane.  Otherwise the
-    resolved depth, | 0x200 to keep a brick's two VPL-4 tiles in one CTA when
-    GSV_NO_SPLIT is set (measurement; GSV_NO_WHOLE disables vpl 8)."""
-    if (not masks and tuple(brick_dims) == (8, 8, 4) and n > 0 and pairs >= 8 * n
-            and not os.environ.get("GSV_NO_WHOLE") and not os.environ.get("GSV_VPL")):
+    """gsv_forward's vpl argument.  8x8x4 bricks (the default) use 8: one warp
+    per brick, two columns per lane, the pairs of each 32-pair round compacted
+    into one hit list per y-half (with live masks for the train step).  It is
+    the fastest form at every pair density measured (LR train forward 0.99 ->
+    0.91 ms, 256^3 render 2.26 -> 2.01 ms), and using it for every path keeps
+    the train step, forward() and Renderer bit-identical.  Other bricks use the
+    warp-tile kernels (_resolve_vpl); GSV_NO_WHOLE=1 or GSV_VPL=2|4 force those
+    (measurement), GSV_NO_SPLIT keeps a brick's two tiles in one CTA.
+    pairs / n (the Gaussians reaching the index) are kept for callers and
+    tools that report the density."""
+    del pairs, n, masks
+    if (tuple(brick_dims) == (8, 8, 4) and not os.environ.get("GSV_NO_WHOLE")
+            and not os.environ.get("GSV_VPL")):
         return 8
     return _resolve_vpl(brick_dims) | (0x200 if os.environ.get("GSV_NO_SPLIT") else 0)
 

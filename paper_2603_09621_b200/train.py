@@ -451,6 +451,7 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
                    min_cap: int = 0) -> _StepGraph:
     import ctypes
     lib = _lib.lib()
+    self.graph_captures = getattr(self, "graph_captures", 0) + 1     # diagnostics
     dev = f.device
     grid, opts, n = self.grid, self.opts, f.count
     bricks = _lib.make_bricks(grid, self.brick_dims, self.slab)
