@@ -679,8 +679,11 @@ __device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits
 // MASKS (two-list form, the train step): the pair's live-voxel words in the
 // backward's VPL-4 pair-major layout -- column A (y < 4) is tile 0, column B
 // tile 1, word = 4 tile + z, bit = lane -- one 32-byte store per pair.
+#ifndef GSV_WHOLE_MINB
+#define GSV_WHOLE_MINB 16       // CTAs (warps) per SM the whole-brick kernel is built for
+#endif
 template <bool TWO, bool MASKS = false>
-__global__ void __launch_bounds__(32, 16)
+__global__ void __launch_bounds__(32, GSV_WHOLE_MINB)
 forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
                   const gsv_record32* __restrict__ rec,
                   const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
