@@ -1,5 +1,7 @@
-"""2000-iteration fit on config 3 through the public fit() (development check):
-loss trace, graph recaptures, wall time, and PSNR/SSIM of the 256^3 render."""
+"""Long fit through the public fit() (development check): loss trace, graph
+recaptures, wall time, and PSNR/SSIM of the HR render.
+
+python tools/longfit.py [iterations] [config]"""
 
 from __future__ import annotations
 
@@ -19,8 +21,9 @@ import paper_2603_09621_b200.train as train_mod  # noqa: E402
 
 def main():
     iters = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+    cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     torch.cuda.set_device(0)
-    p = synth.make_problem(synth.CONFIGS[3])
+    p = synth.make_problem(synth.CONFIGS[cfg])
     lr = gs.Volume(p["lr_grid"], p["lr"])
     captures = [0]
     real = train_mod._graph_capture
