@@ -39,8 +39,9 @@ extern "C" {
 /* ABI history: 2 -- graph step, metrics, geometry helpers; 3 -- gsv_bricks
  * carries a brick-id range [b0, b1) instead of whole z-layers [bz0, bz1),
  * and the box record's 4th word holds k0 (see gsv_preprocess); 4 -- live
- * masks are pair-major (P x 4 uint2, see gsv_forward). */
-#define GSV_ABI_VERSION 4
+ * masks are pair-major (P x 4 uint2, see gsv_forward); 5 -- gsv_forward takes
+ * the fused loss's target as float32 or float64 (target_dtype). */
+#define GSV_ABI_VERSION 5
 
 typedef enum {
   GSV_OK = 0,
@@ -179,6 +180,9 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  *   ab (V,2) float : {alpha, I} with alpha = dL/dI / W (0 where W < eps_w or
  *                    dL/dI == 0), the backward's per-voxel inputs;
  *   loss_part (nbricks_slab) double : per-brick sum |I-T| (l1) or (I-T)^2.
+ * target_dtype: 0 = target is float32 (V), 1 = float64 (V); the difference
+ * I - T is taken in float64 either way, as optimize.py:97 does with the
+ * target volume's own dtype.
  * loss_kind: 0 = l1, 1 = l2.  vox_count = global voxel count V, so
  * dL/dI = sign(I-T)/V (l1) or 2(I-T)/V (l2) exactly as optimize.py:99-102.
  * vpl: voxels per lane of the f32 kernel: 2 (4x4x4 warp tiles when the
@@ -200,8 +204,9 @@ int gsv_forward(const double* positions, const double* log_scales,
                 const int32_t* gids, const gsv_grid* grid,
                 const gsv_bricks* bricks, double cutoff_sigma, double eps_w,
                 int precision, void* S, void* W, void* I,
-                const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, uint32_t* live_masks, int vpl, void* stream);
+                const void* target, int target_dtype, int loss_kind,
+                double vox_count, float* ab, double* loss_part,
+                uint32_t* live_masks, int vpl, void* stream);
 
 /* Per-voxel backward inputs from (W, I, dL/dI) for the unfused API path
  * (raster.py:484-508).  dldi is float64 (V).  Writes ab (V,2) = {dL/dI / W, I}

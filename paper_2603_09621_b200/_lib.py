@@ -61,7 +61,7 @@ _SIGS = {
     "gsv_canonicalize_workspace": [c_i64, c_i32, c_szp],
     "gsv_canonicalize": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp],
     "gsv_forward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl, c_dbl, c_int,
-                    c_vp, c_vp, c_vp, c_vp, c_int, c_dbl, c_vp, c_vp, c_vp, c_int, c_vp],
+                    c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_dbl, c_vp, c_vp, c_vp, c_int, c_vp],
     "gsv_backward_prep": [c_vp, c_vp, c_vp, GP, BP, c_dbl, c_int, c_vp, c_vp, c_vp],
     "gsv_backward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl,
                      c_int, c_vp, c_vp, c_int, c_vp, c_vp],
@@ -102,7 +102,7 @@ _SIGS = {
 _RESTYPES = {"gsv_last_error": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 4        # GSV_ABI_VERSION of include/gsv.h these signatures follow
+ABI_VERSION = 5        # GSV_ABI_VERSION of include/gsv.h these signatures follow
 
 _lib = None
 
@@ -177,8 +177,18 @@ _ws_cache: dict = {}
 
 
 def workspace(nbytes: int, device, key: str = "default") -> torch.Tensor:
-    """Grow-only scratch buffer per (device, key) for CUB temp storage."""
-    k = (str(device), key)
+    """Grow-only scratch buffer per (device, stream, key) for CUB temp storage.
+
+    Keyed by the stream the work is enqueued on (the current stream), so
+    two callers on different streams (two Renderers, a TrainStep beside an
+    eager render) never share scratch that both may be using at once.  On
+    one stream, launches are ordered and the reuse is safe.  The buffer is
+    allocated while that stream is current, so the caching allocator orders
+    its eventual reuse after the stream's pending work.
+    """
+    dev = torch.device(device)
+    s = torch.cuda.current_stream(dev) if dev.type == "cuda" else None
+    k = (str(dev), 0 if s is None else s.cuda_stream, key)
     buf = _ws_cache.get(k)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes * 1.25), 1 << 16), dtype=torch.uint8, device=device)

@@ -114,6 +114,13 @@ __device__ __noinline__ bool exact_live(int gid, int gx, int gy, int gz, const E
   return ref_d2(L, m[0], m[1], m[2], gx, gy, gz, g) <= cutoff2;
 }
 
+// One target voxel as double: the fused loss subtracts in f64 like
+// loss_and_grad (optimize.py:97), from a float32 or float64 target.
+__device__ __forceinline__ double target_value(const void* t, int f64, int64_t lin) {
+  return f64 ? __ldg(static_cast<const double*>(t) + lin)
+             : (double)__ldg(static_cast<const float*>(t) + lin);
+}
+
 // Deterministic block reduction of one double (fixed tree).
 template <int THREADS>
 __device__ double block_sum(double v, double* sh) {
@@ -233,7 +240,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
                  const __grid_constant__ gsv_grid g, gsv_bricks k, float cut2, double cut2d,
                  double eps_w,
                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
-                 const float* __restrict__ target, int loss_kind, double vox_count,
+                 const void* __restrict__ target, int target_f64, int loss_kind, double vox_count,
                  float2* __restrict__ ab, double* __restrict__ loss_part,
                  uint2* __restrict__ live_masks) {
   __shared__ Pair32 sp[THREADS];       // 32 slots per warp
@@ -521,7 +528,7 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
       W[lin] = accW[h];
       I[lin] = iv;
       if (target) {
-        const double d = (double)iv - (double)target[lin];
+        const double d = (double)iv - target_value(target, target_f64, lin);
         double dl;
         if (loss_kind == 0) {
           lsum += fabs(d);
@@ -690,7 +697,7 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
                   const __grid_constant__ gsv_grid g, gsv_bricks k, float cut2, double cut2d,
                   double eps_w,
                   float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
-                  const float* __restrict__ target, int loss_kind, double vox_count,
+                  const void* __restrict__ target, int target_f64, int loss_kind, double vox_count,
                   float2* __restrict__ ab, double* __restrict__ loss_part,
                   uint2* __restrict__ live_masks = nullptr) {
   static_assert(!MASKS || TWO, "live masks need the two-list form");
@@ -914,7 +921,7 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
       W[lin] = aW[c][h];
       I[lin] = iv;
       if (target) {
-        const double d = (double)iv - (double)target[lin];
+        const double d = (double)iv - target_value(target, target_f64, lin);
         double dl;
         if (loss_kind == 0) {
           lsum += fabs(d);
@@ -948,7 +955,7 @@ forward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict_
                  const double* __restrict__ half_src, const int64_t* __restrict__ starts,
                  const int32_t* __restrict__ gids, gsv_grid g, gsv_bricks k, double cut2,
                  double eps_w, double* __restrict__ S, double* __restrict__ W,
-                 double* __restrict__ I, const float* __restrict__ target, int loss_kind,
+                 double* __restrict__ I, const void* __restrict__ target, int target_f64, int loss_kind,
                  double vox_count, double2* __restrict__ ab, double* __restrict__ loss_part,
                  const gsv_record32* __restrict__ rec32) {
   constexpr int T = 128;
@@ -1026,7 +1033,7 @@ forward64_kernel(const double* __restrict__ pos, const gsv_record64* __restrict_
       W[lin] = accW;
       I[lin] = iv;
       if (target) {
-        const double d = iv - (double)target[lin];
+        const double d = iv - target_value(target, target_f64, lin);
         double dl;
         if (loss_kind == 0) {
           lsum += fabs(d);
@@ -1752,14 +1759,17 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
                 const gsv_record32* rec32, const gsv_record64* rec64, const int64_t* starts,
                 const int32_t* gids, const gsv_grid* grid, const gsv_bricks* bricks,
                 double cutoff_sigma, double eps_w, int precision, void* S, void* W, void* I,
-                const float* target, int loss_kind, double vox_count, float* ab,
-                double* loss_part, uint32_t* live_masks, int vpl, void* stream) {
+                const void* target, int target_dtype, int loss_kind, double vox_count,
+                float* ab, double* loss_part, uint32_t* live_masks, int vpl, void* stream) {
   if (int s = validate_grid_bricks(grid, bricks)) return s;
   GSV_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (f32) or 1 (f64)");
   GSV_REQUIRE(precision == 0 || rec64 != nullptr, "the f64 forward needs rec64");
   GSV_REQUIRE(target == nullptr || (ab != nullptr && loss_part != nullptr),
               "fused loss needs ab and loss_part");
   GSV_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (l1) or 1 (l2)");
+  GSV_REQUIRE(target_dtype == 0 || target_dtype == 1,
+              "target_dtype must be 0 (float32) or 1 (float64)");
+  const int target_f64 = target_dtype;
   const int64_t nb = slab_bricks(*bricks);
   if (nb == 0) return GSV_OK;
   const double cut2d = cutoff_sigma * cutoff_sigma;
@@ -1788,17 +1798,17 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
       if (live_masks != nullptr)
         forward32w_kernel<true, true><<<(unsigned)nb, 32, 0, s>>>(
             positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
-            (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab,
+            (float*)S, (float*)W, (float*)I, target, target_f64, loss_kind, vox_count, (float2*)ab,
             loss_part, (uint2*)live_masks);
       else if (one_list)
         forward32w_kernel<false><<<(unsigned)nb, 32, 0, s>>>(
             positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
-            (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab,
+            (float*)S, (float*)W, (float*)I, target, target_f64, loss_kind, vox_count, (float2*)ab,
             loss_part);
       else
         forward32w_kernel<true><<<(unsigned)nb, 32, 0, s>>>(
             positions, xw, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
-            (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab,
+            (float*)S, (float*)W, (float*)I, target, target_f64, loss_kind, vox_count, (float2*)ab,
             loss_part);
       GSV_CHECK_LAUNCH("forward32w_kernel");
       return GSV_OK;
@@ -1812,7 +1822,7 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
 #define GSV_FWD32(V, T, M)                                                                     \
   forward32_kernel<V, T, M><<<(unsigned)nb, T, 0, s>>>(                                        \
       positions, xs, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,          \
-      (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab, loss_part,   \
+      (float*)S, (float*)W, (float*)I, target, target_f64, loss_kind, vox_count, (float2*)ab, loss_part,   \
       (uint2*)live_masks)
     const bool split = vpl == 4 && !no_split && mask_units(*bricks, 4) == 64;
     if (split) {
@@ -1823,7 +1833,7 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
 #define GSV_FWD32S(M)                                                                          \
   forward32_kernel<4, 32, M, true><<<(unsigned)(2 * nb), 32, 0, s>>>(                          \
       positions, xs, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,          \
-      (float*)S, (float*)W, (float*)I, target, loss_kind, vox_count, (float2*)ab, loss_part,   \
+      (float*)S, (float*)W, (float*)I, target, target_f64, loss_kind, vox_count, (float2*)ab, loss_part,   \
       (uint2*)live_masks)
       if (live_masks) GSV_FWD32S(true); else GSV_FWD32S(false);
 #undef GSV_FWD32S
@@ -1837,7 +1847,7 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
   } else {
     forward64_kernel<<<(unsigned)nb, 128, 0, s>>>(
         positions, rec64, nullptr, starts, gids, *grid, *bricks, cut2d, eps_w, (double*)S,
-        (double*)W, (double*)I, target, loss_kind, vox_count, (double2*)ab, loss_part, rec32);
+        (double*)W, (double*)I, target, target_f64, loss_kind, vox_count, (double2*)ab, loss_part, rec32);
     GSV_CHECK_LAUNCH("forward64_kernel");
   }
   return GSV_OK;

@@ -355,7 +355,8 @@ def _forward_into(f, grid, idx, opts, rec32, rec64, S, W, I, target=None, loss_k
         _lib.make_grid(grid),
         _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.cutoff_sigma), float(opts.epsilon_w), opts.precision_code,
-        S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target), int(loss_kind),
+        S.data_ptr(), W.data_ptr(), I.data_ptr(), _lib.ptr(target),
+        int(target is not None and target.dtype == torch.float64), int(loss_kind),
         float(grid.num_voxels), _lib.ptr(ab), _lib.ptr(loss_part), _lib.ptr(live_masks),
         _forward_vpl_arg(idx.brick_dims, idx.pair_count, _reaching(f, idx),
                          live_masks is not None),
@@ -459,12 +460,17 @@ def backward(f: GaussianField, grid: GridSpec, idx: BrickIndex, cache: RenderCac
     pdt = opts.torch_dtype
     ab = torch.zeros((nvox, 2), dtype=pdt, device=f.device)
     bad = torch.empty(1, dtype=torch.int64, device=f.device)
+    # Converted copies must stay referenced until the launch is enqueued: a
+    # temporary freed after data_ptr() can be handed straight to the next
+    # conversion by the caching allocator, aliasing W and I.
+    Wc = cache.W if cache.W.dtype == pdt else cache.W.to(pdt)
+    Ic = cache.I if cache.I.dtype == pdt else cache.I.to(pdt)
     _lib.check(lib.gsv_backward_prep(
-        cache.W.to(pdt).data_ptr() if cache.W.dtype != pdt else cache.W.data_ptr(),
-        cache.I.to(pdt).data_ptr() if cache.I.dtype != pdt else cache.I.data_ptr(),
+        Wc.data_ptr(), Ic.data_ptr(),
         dl.data_ptr(), _lib.make_grid(grid), _lib.make_bricks(grid, idx.brick_dims, idx.slab),
         float(opts.epsilon_w), opts.precision_code, ab.data_ptr(), bad.data_ptr(),
         _lib.stream_ptr()), "backward_prep")
+    del Wc, Ic
     k = int(bad.item())
     if k < nvox:
         raise NumericalError(f"non-finite dL_dI at voxel index {k}")

@@ -97,7 +97,10 @@ class TrainStep:
         lin = target.linear()
         if lin.device.type != "cuda":
             lin = lin.to(torch.device("cuda", torch.cuda.current_device()))
-        self.target = lin.to(torch.float32).contiguous()
+        # the fused loss subtracts in f64 from the target's own values, like
+        # loss_and_grad (optimize.py:97): an f64 volume keeps its f64 target
+        tdt = torch.float64 if lin.dtype == torch.float64 else torch.float32
+        self.target = lin.to(tdt).contiguous()
         self.opts = opts
         self.brick_dims = tuple(brick_dims)
         self.loss_kind = LOSS_KINDS[loss]
@@ -381,7 +384,8 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
         float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
-        b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(), self.loss_kind,
+        b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(),
+        int(self.target.dtype == torch.float64), self.loss_kind,
         float(nvox), b["ab"].data_ptr(), b["loss_part"].data_ptr(), b["masks"].data_ptr(),
         _forward_vpl_arg(self.brick_dims), s), "forward")
     _lib.check(lib.gsv_sum(b["loss_part"].data_ptr(), b["nb"], b["loss_sum"].data_ptr(), s),
@@ -484,7 +488,9 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     for name in ("S", "W", "I"):               # voxels outside a slab stay zero
         b[name] = gp.get(name, (nvox,), torch.float32, zeroed=self.slab is not None)
     b["ab"] = gp.get("ab", (nvox, 2), torch.float32)
-    b["loss_part"] = gp.get("loss_part", (max(nb, 1),), torch.float64)
+    # zeroed: an empty slab (b0 == b1) never writes its loss partial, and the
+    # loss sum still reads entry 0
+    b["loss_part"] = gp.get("loss_part", (max(nb, 1),), torch.float64, zeroed=True)
     b["loss_sum"] = gp.get("loss_sum", (1,), torch.float64)
     b["masks"] = gp.get("masks", (cap, 4, 2), torch.int32)
     b["partials"] = gp.get("partials", (cap, 12), torch.float32)
@@ -605,9 +611,16 @@ def _step_launch(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
             self.update(f, out, state, lrs, beta1, beta2, eps)
         return StepHandle(self, f, state, lrs, hyper, value=loss)
     pending = self.__dict__.setdefault("_pending", [])
+    # the result ring has _RESULT_SLOTS pinned slots: commit the oldest step
+    # before a new replay could overwrite a slot whose result is unread
+    while len(pending) >= _RESULT_SLOTS - 1:
+        pending[0].loss()
     key = _graph_key(self, f, state, lrs, beta1, beta2, eps)
     g = getattr(self, "_graph", None)
-    if g is None or g.key != key or state.t > g.t_max:
+    # every queued step may still advance t on the device: the replay being
+    # launched runs at t <= state.t + len(pending) + 1, which the bias table
+    # must cover (t_max is the largest pre-step t it covers)
+    if g is None or g.key != key or state.t + len(pending) > g.t_max:
         while pending:                           # captures start from committed state
             pending[0].loss()
         self._graph = None
@@ -740,7 +753,7 @@ class Renderer:
             f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
             b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
             float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
-            b["W"].data_ptr(), b["I"].data_ptr(), None, 0, float(self.grid.num_voxels), None,
+            b["W"].data_ptr(), b["I"].data_ptr(), None, 0, 0, float(self.grid.num_voxels), None,
             None, None, _forward_vpl_arg(self.brick_dims, b["pairs"], b["active"], masks=False), s),
             "forward")
 

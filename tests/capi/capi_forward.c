@@ -115,7 +115,7 @@ int main(int argc, char** argv) {
   float* W = (float*)dev_copy(NULL, (size_t)nv * 4);
   float* I = (float*)dev_copy(NULL, (size_t)nv * 4);
   CK(gsv_forward(pos, ls, rot, rec32, NULL, starts, gids, &g, &k, cutoff, 1e-8, 0, S, W, I, NULL,
-                 0, (double)nv, NULL, NULL, NULL, 0, NULL));
+                 0, 0, (double)nv, NULL, NULL, NULL, 0, NULL));
   CU(cudaDeviceSynchronize());
 
   int64_t* h_starts = (int64_t*)malloc((size_t)(nb + 1) * 8);

@@ -280,9 +280,77 @@ def full_configs():
     return res
 
 
+# ----------------------------------------------------------- full-size parity
+# Size-independent fingerprints of full-size reference outputs, small enough to
+# commit (tests/golden/fingerprint.py, shared with the GPU tests).
+sys.path.insert(0, HERE)
+from fingerprint import (SKETCH_K, grad_sample_idx, hr_sample_idx,  # noqa: E402
+                         sketch)
+
+
+def full_renders():
+    """Reference f32 renders at the benchmarked HR grids: config 3 (256^3),
+    config 4 (256x256x160) and config 5 (512^3, jittered field)."""
+    opts = RenderOptions()
+    out, arrays = {}, {}
+    for cid in (3, 4, 5):
+        t0 = time.perf_counter()
+        cfg, hr, lr, f, mine = problem(cid)
+        grid = mine["render_grid"]
+        idx = build_brick_index(f, grid, opts)
+        c = forward(f, grid, idx, opts)
+        I = np.asarray(c.I)
+        cov = np.asarray(c.W) >= opts.epsilon_w
+        sel = hr_sample_idx(grid.num_voxels, cid)
+        arrays[f"c{cid}_sample_I"] = I[sel].astype(np.float32)
+        out[str(cid)] = {"dims": list(grid.dims), "pairs": idx.pair_count,
+                         "field": field_sha(f), "I_sha": sha(I),
+                         "coverage_sha": sha(np.packbits(cov)),
+                         "covered": int(cov.sum()),
+                         "I_sum": float(np.sum(I, dtype=np.float64)),
+                         "I_sketch": sketch(I), "seconds": time.perf_counter() - t0}
+        del idx, c, I, cov
+        print(f"render config {cid}: {time.perf_counter() - t0:.1f}s", flush=True)
+    return out, arrays
+
+
+def full_grads():
+    """Reference f32 train-step gradients at the LR grids of configs 2, 3 and
+    4: forward -> loss_and_grad(l1) -> backward (optimize.py:171-183).  The
+    GPU reproduces dL/dI = sign(I - T)/V from its own render; voxels where
+    |I_ref - T| <= 1e-5 could flip sign within the intensity bar, so their
+    reference signs are stored and injected."""
+    opts = RenderOptions()
+    out, arrays = {}, {}
+    for cid in (2, 3, 4):
+        t0 = time.perf_counter()
+        cfg, hr, lr, f, mine = problem(cid)
+        idx = build_brick_index(f, lr.grid, opts)
+        c = forward(f, lr.grid, idx, opts)
+        loss, dl = loss_and_grad(c.volume(), lr, "l1")
+        d = np.asarray(c.I, dtype=np.float64) - lr.linear().astype(np.float64)
+        amb = np.flatnonzero(np.abs(d) <= 1e-5)
+        gr = backward(f, lr.grid, idx, c, dl, opts)
+        sel = grad_sample_idx(f.count, cid)
+        e = {"N": f.count, "field": field_sha(f), "loss": loss, "pairs": idx.pair_count,
+             "ambiguous": int(amb.shape[0]), "groups": {}}
+        arrays[f"c{cid}_amb_idx"] = amb.astype(np.int64)
+        arrays[f"c{cid}_amb_sign"] = np.sign(d[amb]).astype(np.int8)
+        for k in G:
+            g = np.asarray(getattr(gr, k), dtype=np.float64)
+            arrays[f"c{cid}_grad_{k}"] = g[sel]
+            e["groups"][k] = {"norm": float(np.linalg.norm(g)), "sketch": sketch(g)}
+        e["seconds"] = time.perf_counter() - t0
+        out[str(cid)] = e
+        del idx, c, gr
+        print(f"grads config {cid}: {time.perf_counter() - t0:.1f}s", flush=True)
+    return out, arrays
+
+
 def main():
     meta = {"versions": versions(), "generated_by": "tests/golden/make_golden.py"}
-    which = set(sys.argv[1:]) or {"sweep", "config1", "full", "fit", "metrics", "io"}
+    which = set(sys.argv[1:]) or {"sweep", "config1", "full", "fit", "metrics", "io",
+                                  "renders", "grads"}
     if "sweep" in which:
         with open(os.path.join(HERE, "sweep.json"), "w") as fh:
             json.dump({"meta": meta, "cases": sweep()}, fh)
@@ -296,6 +364,16 @@ def main():
     if "full" in which:
         with open(os.path.join(HERE, "full_configs.json"), "w") as fh:
             json.dump({"meta": meta, "configs": full_configs()}, fh)
+    if "renders" in which:
+        out, arrays = full_renders()
+        np.savez_compressed(os.path.join(HERE, "full_renders.npz"), **arrays)
+        with open(os.path.join(HERE, "full_renders.json"), "w") as fh:
+            json.dump({"meta": meta, "sketch_k": SKETCH_K, "configs": out}, fh, indent=1)
+    if "grads" in which:
+        out, arrays = full_grads()
+        np.savez_compressed(os.path.join(HERE, "full_grads.npz"), **arrays)
+        with open(os.path.join(HERE, "full_grads.json"), "w") as fh:
+            json.dump({"meta": meta, "sketch_k": SKETCH_K, "configs": out}, fh, indent=1)
     if "io" in which:
         with open(os.path.join(HERE, "volume_io.json"), "w") as fh:
             json.dump({"meta": meta, **volume_io()}, fh, indent=1)

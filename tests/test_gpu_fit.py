@@ -412,3 +412,74 @@ def test_fused_update_tma_generic_and_split_paths_agree(n):
     for x, y, z in zip(a, b, c):
         np.testing.assert_array_equal(x, y)
         np.testing.assert_array_equal(x, z)
+
+
+def test_bias_table_recaptures_with_steps_in_flight(monkeypatch):
+    """The device bias-correction table covers t <= t_max.  With steps queued
+    (fit()'s pipeline, plus a deeper queue), the replay being launched runs at
+    state.t + len(pending) + 1: the graph must be re-captured before that
+    passes t_max, so every Adam step uses the right 1 - beta^t.  A tiny table
+    (3 steps) forces several re-captures inside 9 steps; the field must equal
+    the eager path's bit for bit."""
+    import paper_2603_09621_b200.train as train_mod
+    monkeypatch.setattr(train_mod, "_BC_CHUNK", 3)
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    ea = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    eb = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    steps = 9
+    la = []
+    for _ in range(steps):
+        out = ea.forward(fa)
+        la.append(out.loss())
+        ea.update(fa, out, sa, lrs)
+    # queue up to three steps ahead: the ring (4 slots) must also hold
+    handles = [eb.step_async(fb, sb, lrs) for _ in range(3)]
+    lb = []
+    for i in range(steps):
+        lb.append(handles.pop(0).loss())
+        if i + 3 < steps:
+            handles.append(eb.step_async(fb, sb, lrs))
+    assert la == lb and sa.t == sb.t == steps
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    for k in sa.m:
+        assert torch.equal(sa.m[k], sb.m[k]) and torch.equal(sa.v[k], sb.v[k])
+
+
+def test_result_ring_never_overwritten_by_a_deep_queue():
+    """More step_async calls in flight than pinned result slots: each handle
+    still reports its own step's loss (launch blocks on the oldest)."""
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    ea = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    eb = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    la = [ea.step(fa, sa, lrs) for _ in range(10)]
+    hs = [eb.step_async(fb, sb, lrs) for _ in range(10)]
+    lb = [h.loss() for h in hs]
+    assert la == lb and sb.t == 10
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+
+
+def test_f64_target_keeps_f64_in_the_fused_loss():
+    """An f64 target volume is not rounded to f32 by the train step: the
+    fused loss equals loss_and_grad (f64 subtraction, optimize.py:97) for
+    both engines."""
+    p = make_problem(CONFIGS[1])
+    rng = np.random.default_rng(3)
+    t64 = p["lr"].astype(np.float64) + rng.normal(scale=1e-9, size=p["lr"].shape)
+    lr = gs.Volume(p["lr_grid"], t64)
+    for prec in ("f32", "f64"):
+        f = gs.GaussianField(*p["field"])
+        opts = gs.RenderOptions(precision=prec)
+        step = gs.TrainStep(lr, opts, (8, 8, 4), "l1")
+        assert step.target.dtype == torch.float64
+        out = step.forward(f)
+        ref, _ = gs.loss_and_grad(out.cache.volume(), lr, "l1")
+        tol = 1e-12 if prec == "f64" else 1e-9
+        assert abs(out.loss() - ref) <= tol * max(ref, 1.0), (prec, out.loss(), ref)

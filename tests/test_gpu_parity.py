@@ -647,3 +647,45 @@ def test_renderer_slabs_reassemble_the_full_render():
         pairs += r.pair_count()
     np.testing.assert_allclose(got, I_full, rtol=4e-6, atol=1e-9)
     assert pairs == P_full == int(w.sum())
+
+
+def test_backward_with_cache_of_other_precision():
+    """forward(f32) then backward(f64 opts): the converted W and I must stay
+    distinct buffers (a freed temporary can be reused for the next
+    conversion).  Equals backward on explicitly converted copies."""
+    grid, arrs = _sweep_field(100, 2)
+    f = gs.GaussianField(*arrs)
+    o32, o64 = gs.RenderOptions(), gs.RenderOptions(precision="f64")
+    idx = gs.build_brick_index(f, grid, o32)
+    c32 = gs.forward(f, grid, idx, o32)
+    dl = np.random.default_rng(5).normal(size=grid.num_voxels)
+    got = gs.backward(f, grid, idx, c32, dl, o64)
+    conv = RenderCache(grid, c32.S.to(torch.float64).clone(), c32.W.to(torch.float64).clone(),
+                       c32.I.to(torch.float64).clone(), c32.field_version)
+    want = gs.backward(f, grid, idx, conv, dl, o64)
+    for k in GRAD_KEYS:
+        assert torch.equal(getattr(got, k), getattr(want, k)), k
+
+
+def test_binning_workspace_is_per_stream():
+    """Two build_brick_index calls in flight on two streams use separate CUB
+    scratch (the workspace is keyed by stream), and both equal the
+    sequential results."""
+    from paper_2603_09621_b200 import _lib
+    grid = gs.GridSpec((32, 32, 32), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    fa = gs.GaussianField(*random_field_arrays(3000, grid, 7, 0.4, 2.0))
+    fb = gs.GaussianField(*random_field_arrays(2000, grid, 8, 0.4, 2.0))
+    ia, ib = gs.build_brick_index(fa, grid), gs.build_brick_index(fb, grid)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s1):
+        ja = gs.build_brick_index(fa, grid)
+    with torch.cuda.stream(s2):
+        jb = gs.build_brick_index(fb, grid)
+    torch.cuda.synchronize()
+    assert torch.equal(ia.gids, ja.gids) and torch.equal(ia.starts, ja.starts)
+    assert torch.equal(ib.gids, jb.gids) and torch.equal(ib.starts, jb.starts)
+    keys = {k[1] for k in _lib._ws_cache if k[2] == "bin"}
+    assert {s1.cuda_stream, s2.cuda_stream} <= keys
