@@ -14,8 +14,11 @@ CUDA events, inputs resident in HBM.  The same line carries the 256^3 render
 N > 1: launched by torch.distributed.run, one rank per GPU; each rank owns a
 contiguous brick-id range (cuts balanced by pairs per brick, mid-layer cuts
 allowed); one NCCL all_reduce per train step.
---impl reference: the reference's CPU algorithm (oracle/ port, OpenMP, all
-host cores) on the same config, rank 0 only.
+--impl reference: the unmodified reference (gsvol, installed into baseline/_ref)
+through its public fit-loop API on all host cores, each step a fit() iteration
+on a bounded 1/8 sample of the config (its central LR z-slab), scaled to the
+workload; the oracle port only if the reference is not installed.  Rank 0
+only.
 """
 
 from __future__ import annotations
@@ -175,31 +178,149 @@ def cpu_train_step_seconds(p, steps: int, warmup: int):
     return (time.perf_counter() - t0) / steps
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+REF_SLAB_Z = 16          # LR z-voxels of the reference arm's sample (of 128 at config 3)
+
+
+def _import_gsvol(cores: int):
+    """The unmodified reference (gsvol, pip-installed into baseline/_ref) with
+    numba's pool sized to every host core: NUMBA_NUM_THREADS must be set
+    before numba is first imported (gsvol/_numba_env.py caps it at 8
+    otherwise), then set_worker_count(cores) (raster.py:55-59)."""
+    os.environ["NUMBA_NUM_THREADS"] = str(cores)
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "gsv_bench_numba_cache"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import gsvol
+    gsvol.set_worker_count(cores)
+    return gsvol
+
+
+def reference_sample(p, cfg_id: int):
+    """A bounded sample of the workload for the reference's CPU path: the
+    central z-slab of REF_SLAB_Z LR voxels of the config's LR volume (same
+    phantom, same spacing), initialised like fit() (threshold 0: one
+    Gaussian per voxel).  Returns (grid dims, spacing, origin, data, fraction)
+    where fraction = sample Gaussians / workload Gaussians."""
+    g = p["lr_grid"]
+    nz = g.dims[2]
+    dz = min(REF_SLAB_Z, nz)
+    z0 = (nz - dz) // 2
+    data = np.ascontiguousarray(p["lr"][:, :, z0:z0 + dz])
+    origin = (g.origin[0], g.origin[1], g.origin[2] + z0 * g.spacing[2])
+    return (g.dims[0], g.dims[1], dz), tuple(g.spacing), origin, data, dz / nz
+
+
+def gsvol_train_step_seconds(p, cfg_id: int, steps: int, warmup: int, cores: int):
+    """Seconds per config-size fit() iteration of the real reference, from
+    `steps` timed iterations on the bounded sample (reference_sample), scaled
+    by the sample's Gaussian fraction.  The loop body is fit()'s
+    (optimize.py:177-197) through gsvol's public API; JIT compilation is
+    warmed on a 4^3 grid first, as gsvol/bench.py:28-31 does."""
+    gsvol = _import_gsvol(cores)
+    from gsvol import (AdamState, FitConfig, GridSpec, InitConfig, RenderOptions, Volume,
+                       backward, build_brick_index, forward, init_from_volume, loss_and_grad,
+                       step_optimizer)
+    dims, sp, org, data, frac = reference_sample(p, cfg_id)
+    grid = GridSpec(dims, sp, org)
+    lr = Volume(grid, data)
+    opts = RenderOptions()
+
+    def one(f, st, lrs, vol):
+        idx = build_brick_index(f, vol.grid, opts)
+        cache = forward(f, vol.grid, idx, opts)
+        loss, dl = loss_and_grad(cache.volume(), vol, "l1")
+        grads = backward(f, vol.grid, idx, cache, dl, opts)
+        step_optimizer(f, grads, st, lrs)
+        f.normalize_rotations()
+        return loss
+
+    # JIT warm-up on a tiny problem (every kernel of the loop body)
+    wg = GridSpec((4, 4, 4), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    wv = Volume(wg, np.random.default_rng(0).uniform(size=(4, 4, 4)).astype(np.float32))
+    wf = init_from_volume(wv, InitConfig(background_threshold=0.0))
+    one(wf, AdamState.create(wf), FitConfig().resolved_lrs(wg.spacing), wv)
+    f = init_from_volume(lr, InitConfig(background_threshold=0.0))
+    st = AdamState.create(f)
+    lrs = FitConfig().resolved_lrs(grid.spacing)
+    for _ in range(warmup):
+        one(f, st, lrs, lr)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one(f, st, lrs, lr)
+    sec = (time.perf_counter() - t0) / steps
+    return sec / frac, {"sample_dims": list(dims), "sample_N": int(f.count),
+                        "fraction": frac, "sample_s_per_step": sec,
+                        "numba_threads": int(gsvol.worker_count()),
+                        "cpu": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_available() -> str | None:
+    """None if the real reference imports from baseline/_ref, else why not."""
+    if not os.path.isdir(os.path.join(REF_DIR, "gsvol")):
+        return "baseline/_ref/gsvol not installed"
+    try:
+        import numba  # noqa: F401
+        import scipy  # noqa: F401
+    except ImportError as e:
+        return f"reference dependency missing: {e}"
+    return None
+
+
+def cpu_baseline_entry(p, cfg_id: int, steps: int, warmup: int) -> dict:
+    """The reference's CPU path on this host: the real gsvol when it is
+    installed (kind "reference"), else the oracle port (kind "port")."""
+    cores = host_threads()
+    why = reference_available()
+    if why is None:
+        sec, info = gsvol_train_step_seconds(p, cfg_id, steps, warmup, cores)
+        d, n = info["sample_dims"], info["sample_N"]
+        return {"value": 1.0 / sec, "unit": "it/s", "cores": cores, "kind": "reference",
+                "sample": f"{steps} fit() iterations of the unmodified reference (gsvol from "
+                          f"baseline/_ref, numba {info['numba_threads']} threads) on the "
+                          f"central {d[0]}x{d[1]}x{d[2]} LR z-slab of config {cfg_id} "
+                          f"(N={n}, {info['fraction']:.4g} of the workload), scaled by "
+                          "1/fraction",
+                "detail": info}
+    sec = cpu_train_step_seconds(p, steps, warmup)
+    return {"value": 1.0 / sec, "unit": "it/s", "cores": cores, "kind": "port",
+            "sample": f"{steps} full config-{cfg_id} train iterations (oracle/: numpy binning "
+                      f"+ OpenMP C loops, all cores); real reference unavailable: {why}"}
+
+
 def run_reference(args, dist, rank):
     if rank != 0:
         return
     p = problem_for(args.config)
-    cores = host_threads()
-    sec = cpu_train_step_seconds(p, args.steps, args.warmup)
-    v = 1.0 / sec
-    cfg = _config_dict(args, p, None, int(os.environ.get("WORLD_SIZE", "1")))
+    cpu = cpu_baseline_entry(p, args.config, args.steps, args.warmup)
+    v = cpu["value"]
+    cfg = _config_dict(args, p, int(os.environ.get("WORLD_SIZE", "1")))
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "it/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-            "cpu_baseline": {"value": v, "unit": "it/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full config-{args.config} train "
-                                       "iterations (oracle/: numpy binning + OpenMP C loops)"},
+            "cpu_baseline": cpu,
             "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(args, p, pairs, ws):
+def _config_dict(args, p, ws):
     return {"workload": f"config {args.config}: fit step on {p['lr_grid'].dims} LR "
                         f"(x2 -> {p['hr_grid'].dims} HR), N={p['field'][0].shape[0]} Gaussians",
             "lr_dims": list(p["lr_grid"].dims), "hr_dims": list(p["hr_grid"].dims),
-            "N": int(p["field"][0].shape[0]), "pairs_lr": pairs, "brick_dims": [8, 8, 4],
+            "N": int(p["field"][0].shape[0]), "brick_dims": [8, 8, 4],
             "loss": "l1", "optimizer": "Adam (f64 master)",
             "parallelism": f"brick-range slabs x{ws} (pair-balanced)",
             "l2": "inputs larger than L2 (f64 field + Adam moments = 0.7 GB, pairs 0.1 GB)"}
@@ -457,17 +578,14 @@ def run_ours(args, dist, ws, rank, local):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cores = host_threads()
-        sec = cpu_train_step_seconds(p, 1, 0)
-        cpu = {"value": 1.0 / sec, "unit": "it/s", "cores": cores, "kind": "port",
-               "sample": f"1 full config-{args.config} train iteration on the host "
-                         "(oracle/: numpy binning + OpenMP C loops, all cores)"}
+        cpu = cpu_baseline_entry(p, args.config, 2, 1)
 
     if rank == 0:
         line = {"metric": METRIC, "value": 1000.0 / ms, "unit": "it/s", "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic", "config": _config_dict(args, p, pairs, ws),
+                "dtype": "f32", "data": "synthetic", "config": _config_dict(args, p, ws),
+                "pairs_lr": pairs,
                 "render": render, "render512": render512,
                 "phases_ms": {k: v[1] for k, v in phases.items()},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,

@@ -2,8 +2,12 @@
 hashes of the reference's own lists, LR intensities at 4096 sampled voxels and
 the LR loss vs the reference (tests/golden/full_configs.json)."""
 
+import json
+import os
+
 import numpy as np
 import pytest
+import torch
 
 import paper_2603_09621_b200 as gs
 from paper_2603_09621_b200.synth import CONFIGS, make_problem, sha256
@@ -43,6 +47,14 @@ def test_full_size_lists_and_render(cid):
 # config 3 (256^3), config 4 (256x256x160) and config 5 (512^3, jittered field)
 # -- 65536 seeded sample voxels, the coverage mask's sha256, I_sum and a sign
 # sketch of the whole volume (tests/golden/fingerprint.py).
+def _log(**kw):
+    """Measured parity margins, appended as JSON lines to $GSV_PARITY_LOG."""
+    path = os.environ.get("GSV_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps(kw) + "\n")
+
+
 def _fp():
     import sys
     from conftest import GOLDEN
@@ -84,6 +96,8 @@ def test_full_size_hr_render_vs_reference(cid):
     assert sha256(np.packbits(cov)) == ref["coverage_sha"], cid
     assert abs(float(np.sum(I, dtype=np.float64)) - ref["I_sum"]) <= 1e-5 * ref["covered"]
     rms = fp.sketch_rms_error(fp.sketch_torch(c.I), ref["I_sketch"]) / np.sqrt(grid.num_voxels)
+    _log(test="hr_render", cid=cid, max_abs_err_sampled=float(err.max()),
+         rms_err_estimate=rms, covered=int(cov.sum()))
     assert rms <= 1e-6, (cid, rms)
     # the pooled, graph-replayed render path (bench.py's render) is the same kernel
     r = gs.Renderer(grid, opts)
@@ -121,6 +135,7 @@ def _check_grads(fp, grads, ref, arrays, cid, what):
         # norm-wise per group (north_star: 1e-5 relative), full vector via the
         # sketch, plus the exact relative error on the sampled Gaussians
         est = fp.sketch_rms_error(fp.sketch_torch(g), r["sketch"]) / r["norm"]
+        _log(test="grads", path=what, cid=cid, group=k, rel_err_estimate=est)
         assert est <= 1e-5, (what, cid, k, est)
         gs_ = g[sel.to(g.device)].cpu().numpy().astype(np.float64)
         rs_ = arrays[f"c{cid}_grad_{k}"]
