@@ -12,7 +12,7 @@ import torch
 import paper_2603_09621_b200 as gs
 from paper_2603_09621_b200.synth import CONFIGS, make_problem, sha256
 
-from conftest import load_json
+from conftest import GRAD_KEYS, load_json
 
 pytestmark = pytest.mark.gpu
 
