@@ -185,18 +185,25 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
  * target volume's own dtype.
  * loss_kind: 0 = l1, 1 = l2.  vox_count = global voxel count V, so
  * dL/dI = sign(I-T)/V (l1) or 2(I-T)/V (l2) exactly as optimize.py:99-102.
- * vpl: voxels per lane of the f32 kernel: 2 (4x4x4 warp tiles when the
- * brick dims are multiples of 4, 4 warps per 8x8x4 brick), 4 (columns of 4
- * in z: 8x4x4 tiles, 2 warps), 8 (8x8x4 bricks only: one warp per brick,
- * two columns per lane, one hit list per y-half), or 0 = auto (8 for 8x8x4
- * bricks, else 4 when bdz % 4 == 0 and the brick has <= 64 columns, else 2).
+ * vpl: the f32 kernel: 2 (4x4x4 warp tiles when the brick dims are
+ * multiples of 4, 4 warps per 8x8x4 brick), 4 (columns of 4 in z: 8x4x4
+ * tiles, 2 warps), 8 (8x8x4 bricks only: one warp per brick, two columns
+ * per lane, one hit list per y-half), 16 (8x8x4 bricks only: grouped
+ * columns -- consecutive pairs with the same footprint rectangle form a
+ * group, whose columns are dealt to the lanes; fastest at LR densities; the
+ * Python API uses it when pairs <= 8 x the Gaussians reaching the index), or
+ * 0 = auto (8 for 8x8x4 bricks, else 4 when bdz % 4 == 0 and the brick has
+ * <= 64 columns, else 2).  S, W, I are bit-identical for a given vpl; across
+ * vpl 8 and 16 they agree to f32 rounding (different association).
  * live_masks (optional, f32): P x 4 uint2 (pair-major: a pair's 8 words are
  * 32 contiguous bytes), the forward's exact truncation decisions, consumed by
  * gsv_backward so it walks only live voxels.  Word w of a pair (uint2 w/2,
- * .x/.y = w%2) holds the live bits of
- * warp tile w/vpl at depth w%vpl, bit = lane.  Requires a brick that fills
- * the CTA's warp tiles exactly (vpl 2: 128 columns of 2; vpl 4: 64 of 4 --
- * e.g. 8x8x4).
+ * .x/.y = w%2) holds, for vpl 2/4/8, the live bits of warp tile w/v at
+ * depth w%v, bit = lane (v = 4 for vpl 8, whose masks use the VPL-4
+ * layout); for vpl 16, brick row y = w, bit 4x + z.  Pass gsv_backward the
+ * matching mask_vpl (4 for vpl 8, 16 for vpl 16).  Requires a brick that
+ * fills the CTA's warp tiles exactly (vpl 2: 128 columns of 2; vpl 4: 64 of
+ * 4 -- e.g. 8x8x4).
  * ------------------------------------------------------------------------ */
 int gsv_forward(const double* positions, const double* log_scales,
                 const double* rotations, const gsv_record32* rec32,
@@ -225,8 +232,10 @@ int gsv_backward_prep(const void* W, const void* I, const double* dldi,
  * the reference merges in (raster.py:512-516: stable argsort by gid keeps
  * ascending brick order).  partials: float (f32) or double (f64), (P,12).
  * live_masks: the masks gsv_forward wrote for the same index (f32 only), or
- * NULL to find live voxels from exact per-row spans; mask_vpl: the vpl that
- * forward ran with (0 = the same auto rule). */
+ * NULL to find live voxels from exact per-row spans; mask_vpl: the masks'
+ * layout -- 2 or 4 (warp tiles; 4 also for gsv_forward vpl 8), 16 (the
+ * grouped forward's row/column-nibble layout), or 0 = mask_units' auto rule
+ * for the warp-tile kernels. */
 int gsv_backward(const double* positions, const double* log_scales,
                  const double* rotations, const gsv_record32* rec32,
                  const gsv_record64* rec64, const int64_t* starts,

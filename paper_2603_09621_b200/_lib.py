@@ -14,7 +14,10 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsv_b200.so")
+# GSV_LIB: an alternative build of the same ABI (measurement variants built by
+# `python -m paper_2603_09621_b200.build --variant ...`); the default is the
+# in-tree library __graft_entry__.build() produces
+LIB_PATH = os.environ.get("GSV_LIB") or os.path.join(_HERE, "libgsv_b200.so")
 
 c_int = ctypes.c_int
 c_i32 = ctypes.c_int32

@@ -44,7 +44,16 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, variant: str | None = None,
+          defines=()) -> str:
+    """Compile and link.  ``variant`` + ``defines`` (measurement builds): the
+    objects go to csrc/build_<variant>/ and the library to
+    libgsv_b200_<variant>.so, loaded with GSV_LIB=<that path>."""
+    global BUILD, LIB, COMMON
+    if variant:
+        BUILD = os.path.join(CSRC, f"build_{variant}")
+        LIB = os.path.join(HERE, f"libgsv_b200_{variant}.so")
+        COMMON = COMMON + [f"-D{d}" for d in defines]
     os.makedirs(BUILD, exist_ok=True)
     headers = _headers()
     objs = []
@@ -75,4 +84,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("-f", action="store_true")
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("-D", action="append", default=[], help="extra -D (variant builds)")
+    a = ap.parse_args()
+    print(build(verbose=a.v, force=a.f, variant=a.variant, defines=a.D))

@@ -941,6 +941,391 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
   }
 }
 
+// ------------------------------------ forward f32, grouped columns (LR grids)
+// One warp per 8x8x4 brick, like forward32w_kernel, but the voxel tile a warp
+// evaluates adapts to the pairs.  Per 32-entry round every staged pair's
+// footprint inside the brick -- its 3-sigma AABB clipped to the brick's owned
+// voxels: a rectangle of columns (x, y) and a z range -- is computed.
+// Consecutive hits (list order) with the same rectangle form a group: at LR a
+// brick's list runs through each (ix, iy) of its neighbourhood in z, so a
+// group is typically the ~8 Gaussians of one z-run, whose rectangles
+// coincide.  The groups' rectangles are laid end to end and dealt to the
+// lanes 32 columns at a time (a "chunk"); each lane walks its group's pairs
+// in list order and accumulates its column's 4 voxels in registers, exactly
+// the fixed-ownership kernels' per-hit evaluation (nested quadratic at the
+// column top, second differences in z, f64 guard band) -- but only over
+// columns some pair of the group reaches.  At config 3 this evaluates ~2.5x
+// fewer (pair, column) slots than the two-list whole-brick kernel.
+// The group's sum then goes into the brick's shared S and W, one group after
+// another in list order (a group's columns are distinct, so its lanes never
+// conflict).  Per voxel: S = ((S_prev + (c1 + c2 + ...)) + ...) -- a fixed,
+// list-determined association: bit-reproducible across runs and list
+// shuffles (canonical lists), equal to the sequential sum up to f32 rounding.
+// MASKS: the live-voxel masks of the train step's backward, per pair 8
+// words, word y (brick row), bit 4x + z -- one shared atomic OR per lane and
+// evaluated (pair, column).
+#ifndef GSV_COLS_MINB
+#define GSV_COLS_MINB 20        // CTAs (warps) per SM the grouped kernel is built for
+#endif
+// Shared-memory accesses by 32-bit shared address: the base is formed once,
+// outside the loops (plain array indexing let ptxas rematerialise the
+// generic->shared window base, an S2UR with its latency, in every iteration).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("" : "+r"(a));   // opaque: keep it in a register
+  return a;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void red_or_shared(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t rect_word(int x0, int y0, int x1, int y1) {
+  return (uint32_t)x0 | (uint32_t)y0 << 3 | (uint32_t)x1 << 6 | (uint32_t)y1 << 9;
+}
+
+template <bool MASKS>
+__global__ void __launch_bounds__(32, GSV_COLS_MINB)
+forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSrc xsrc,
+                  const gsv_record32* __restrict__ rec,
+                  const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
+                  const __grid_constant__ gsv_grid g, gsv_bricks k, float cut2, double cut2d,
+                  double eps_w,
+                  float* __restrict__ S, float* __restrict__ W, float* __restrict__ I,
+                  const void* __restrict__ target, int target_f64, int loss_kind,
+                  double vox_count, float2* __restrict__ ab, double* __restrict__ loss_part,
+                  uint4* __restrict__ live_masks) {
+  constexpr int Z = 4;
+  __shared__ Pair32 sp[32];                   // the round's hits, compacted (list order)
+  __shared__ uint32_t srect[32];              // hit -> rect_word
+  __shared__ int sgs[33];                     // group -> first hit
+  __shared__ float4 sS4[64], sW4[64];         // S, W of column x + 8 y, z = .x .. .w
+  __shared__ uint32_t smk[MASKS ? 32 * 8 : 1];
+  const int lb = blockIdx.x;
+  const int b = (int)slab_first(k) + lb;
+  const BrickGeom bg = brick_geom(b, g, k);
+  const int64_t lbeg = starts[lb], lend = starts[lb + 1];
+  const int lane = threadIdx.x;
+  const unsigned lt = (1u << lane) - 1u;
+  const float fsx = (float)g.sx, fsy = (float)g.sy, fsz = (float)g.sz;
+  const float isx = (float)(1.0 / g.sx), isy = (float)(1.0 / g.sy), isz = (float)(1.0 / g.sz);
+  // the brick's owned voxel box and centre (brick-local voxel coordinates):
+  // the same quadratic origin as forward32w_kernel
+  const float ftxh = (float)(bg.ex - 1), ftyh = (float)(bg.ey - 1), ftzh = (float)(bg.ez - 1);
+  const float ctx = 0.5f * ftxh, cty = 0.5f * ftyh, ctz = 0.5f * ftzh;
+  const float ext_x = ctx, ext_y = cty, ext_z = ctz;
+  const float mZ = -ctz, mZ1 = mZ + 1.f;
+  sS4[lane] = sS4[lane + 32] = sW4[lane] = sW4[lane + 32] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if constexpr (MASKS) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) smk[lane + 32 * i] = 0u;
+  }
+  __syncwarp();
+  const uint32_t sp_a = smem_addr(sp);
+  const uint32_t smk_a = smem_addr(smk);
+
+  int gid_next = (lbeg + lane < lend) ? __ldg(gids + lbeg + lane) : -1;
+  int gid_next2 = (lbeg + 32 + lane < lend) ? __ldg(gids + lbeg + 32 + lane) : -1;
+  for (int64_t base = lbeg; base < lend; base += 32) {
+    const int gid = gid_next;
+    gid_next = gid_next2;
+    gid_next2 = (base + 64 + lane < lend) ? __ldg(gids + base + 64 + lane) : -1;
+    if (gid_next >= 0) {   // next round's record and position lines, in flight now
+      prefetch_line(rec + gid_next);
+      prefetch_line(pos + 3 * (int64_t)gid_next);
+    }
+    bool hit = false;
+    Pair32 p;
+    uint32_t rw = 0u;
+    if (gid >= 0) {
+      const float4* r4 = reinterpret_cast<const float4*>(rec + gid);
+      const float4 q0 = __ldg(r4), q1 = __ldg(r4 + 1), q2 = __ldg(r4 + 2), q3 = __ldg(r4 + 3);
+      const double* m = pos + 3 * (int64_t)gid;
+      const float mx = (float)(__ldg(m) - bg.px), my = (float)(__ldg(m + 1) - bg.py),
+                  mz = (float)(__ldg(m + 2) - bg.pz);
+      const float cxv = mx * isx, cyv = my * isy, czv = mz * isz;
+      const float hxv = fmaf(q2.w, isx, 1e-3f), hyv = fmaf(q3.x, isy, 1e-3f),
+                  hzv = fmaf(q3.y, isz, 1e-3f);
+      // footprint: the integer voxels of the (widened) 3-sigma box, clipped
+      // to the owned voxels -- every live voxel lies in it
+      const float ax0 = fmaxf(ceilf(cxv - hxv), 0.f), ax1 = fminf(floorf(cxv + hxv), ftxh);
+      const float ay0 = fmaxf(ceilf(cyv - hyv), 0.f), ay1 = fminf(floorf(cyv + hyv), ftyh);
+      const float az0 = fmaxf(ceilf(czv - hzv), 0.f), az1 = fminf(floorf(czv + hzv), ftzh);
+      hit = ax0 <= ax1 && ay0 <= ay1 && az0 <= az1;
+      if (hit && !isinf(cut2)) {
+        // sphere bound |p - mu|^2 / sigma_max^2 <= cut^2 against the footprint box
+        const float ddx = fmaxf(fmaxf(ax0 - cxv, cxv - ax1), 0.f) * fsx;
+        const float ddy = fmaxf(fmaxf(ay0 - cyv, cyv - ay1), 0.f) * fsy;
+        const float ddz = fmaxf(fmaxf(az0 - czv, czv - az1), 0.f) * fsz;
+        const float dist2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
+        hit = dist2 * q3.z <= cut2 * 1.0001f + 1e-6f;
+      }
+      if (hit) {
+        rw = rect_word((int)ax0, (int)ay0, (int)ax1, (int)ay1);
+        const float L[9] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x};
+        float u3[3], e[3][3], umax = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          u3[a] = -fmaf(L[3 * a + 0], mx, fmaf(L[3 * a + 1], my, L[3 * a + 2] * mz));
+          e[0][a] = L[3 * a + 0] * fsx;
+          e[1][a] = L[3 * a + 1] * fsy;
+          e[2][a] = L[3 * a + 2] * fsz;
+          umax = fmaxf(umax, fabsf(u3[a]) + fabsf(e[0][a]) * k.bdx +
+                                 fabsf(e[1][a]) * k.bdy + fabsf(e[2][a]) * k.bdz);
+        }
+        float uc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          uc[a] = fmaf(ctz, e[2][a], fmaf(cty, e[1][a], fmaf(ctx, e[0][a], u3[a])));
+        const float sc = -0.72134752044448170f;   // -(1/2) log2(e)
+        const float lr2 = __log2f(q2.z);
+        const float d00 = fmaf(uc[0], uc[0], fmaf(uc[1], uc[1], uc[2] * uc[2]));
+        p.a.x = fmaf(sc, d00, lr2);
+        p.a.y = 2.f * sc * fmaf(uc[0], e[0][0], fmaf(uc[1], e[0][1], uc[2] * e[0][2]));
+        p.a.z = 2.f * sc * fmaf(uc[0], e[1][0], fmaf(uc[1], e[1][1], uc[2] * e[1][2]));
+        p.a.w = 2.f * sc * fmaf(uc[0], e[2][0], fmaf(uc[1], e[2][1], uc[2] * e[2][2]));
+        p.b.x = sc * fmaf(e[0][0], e[0][0], fmaf(e[0][1], e[0][1], e[0][2] * e[0][2]));
+        p.b.y = sc * fmaf(e[1][0], e[1][0], fmaf(e[1][1], e[1][1], e[1][2] * e[1][2]));
+        p.b.z = sc * fmaf(e[2][0], e[2][0], fmaf(e[2][1], e[2][1], e[2][2] * e[2][2]));
+        p.b.w = 2.f * sc * fmaf(e[0][0], e[1][0], fmaf(e[0][1], e[1][1], e[0][2] * e[1][2]));
+        p.c.x = 2.f * sc * fmaf(e[0][0], e[2][0], fmaf(e[0][1], e[2][1], e[0][2] * e[2][2]));
+        p.c.y = 2.f * sc * fmaf(e[1][0], e[2][0], fmaf(e[1][1], e[2][1], e[1][2] * e[2][2]));
+        p.c.z = q2.y;
+        const float qmag = fabsf(p.a.x) + ext_x * fabsf(p.a.y) + ext_y * fabsf(p.a.z) +
+                           ext_z * fabsf(p.a.w) + ext_x * ext_x * fabsf(p.b.x) +
+                           ext_y * ext_y * fabsf(p.b.y) + ext_z * ext_z * fabsf(p.b.z) +
+                           ext_x * ext_y * fabsf(p.b.w) + ext_x * ext_z * fabsf(p.c.x) +
+                           ext_y * ext_z * fabsf(p.c.y);
+        const float guard = isinf(cut2) ? 0.f
+                            : 0.72134752f * (kGuardRel * cut2 + kGuardMag * umax * sqrtf(cut2)) +
+                                  2.5e-6f * qmag;
+        const float qcut = isinf(cut2) ? -INFINITY : fmaf(sc, cut2, lr2);
+        p.c.w = qcut + guard;
+        p.d = make_float4(qcut - guard, __int_as_float(gid), 0.f, 0.f);
+      }
+    }
+    // ---- the round's hits, compacted in list order, and their groups
+    const unsigned hitmask = __ballot_sync(kFull, hit);
+    const int nh = __popc(hitmask);
+    const int r = __popc(hitmask & lt);
+    if (hit) {
+      sp[r] = p;
+      srect[r] = rw;
+    }
+    __syncwarp();
+    // hit r (lane r) starts a group unless its rectangle equals hit r-1's
+    const uint32_t myrect = lane < nh ? srect[lane] : 0u;
+    const bool gstart_ = lane < nh && (lane == 0 || srect[lane - 1] != myrect);
+    const unsigned gmask = __ballot_sync(kFull, gstart_);
+    const int ng = __popc(gmask);
+    if (gstart_) sgs[__popc(gmask & lt)] = lane;
+    if (lane == 0) sgs[ng] = nh;
+    __syncwarp();
+    // lane gg describes group gg: first hit, size, column area, column prefix
+    const int gfirst = lane < ng ? sgs[lane] : nh;
+    const int gsize = lane < ng ? sgs[lane + 1] - gfirst : 0;
+    const uint32_t grect = lane < ng ? srect[gfirst] : 0u;
+    const int gwx = (int)((grect >> 6) & 7u) - (int)(grect & 7u) + 1;
+    const int gwy = (int)((grect >> 9) & 7u) - (int)((grect >> 3) & 7u) + 1;
+    const int garea = lane < ng ? gwx * gwy : 0;
+    int incl = garea;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += n;
+    }
+    const int gpre = incl - garea;
+    const int T = __shfl_sync(kFull, incl, 31);
+    for (int c0 = 0; c0 < T; c0 += 32) {
+      const int s = c0 + lane;
+      const bool valid = s < T;
+      // the group owning column slot s
+      const int cnt0 = __popc(__ballot_sync(kFull, lane < ng && gpre <= c0));
+      const unsigned sb = __reduce_or_sync(kFull, (lane < ng && gpre > c0 && gpre < c0 + 32)
+                                                      ? 1u << (gpre - c0) : 0u);
+      const int myg = valid ? cnt0 - 1 + __popc(sb & ((2u << lane) - 1u)) : cnt0 - 1;
+      const int glast = __shfl_sync(kFull, myg, min(31, T - 1 - c0));
+      const int gf = cnt0 - 1;
+      const int h0 = __shfl_sync(kFull, gfirst, myg);
+      const int hk_all = __shfl_sync(kFull, gsize, myg);   // every lane shuffles
+      const int hk = valid ? hk_all : 0;
+      const int kk = s - __shfl_sync(kFull, gpre, myg);
+      const uint32_t rc = __shfl_sync(kFull, grect, myg);
+      const int wx = (int)((rc >> 6) & 7u) - (int)(rc & 7u) + 1;
+      const int dy = kk / wx;
+      const int x = (int)(rc & 7u) + kk - dy * wx;
+      const int y = (int)((rc >> 3) & 7u) + dy;
+      const float mX = (float)x - ctx, mY = (float)y - cty;
+      const int kmax = __reduce_max_sync(kFull, hk);
+      float aS[Z], aW[Z];
+#pragma unroll
+      for (int h = 0; h < Z; ++h) aS[h] = aW[h] = 0.f;
+      bool any = false;
+      // Evaluate pair j at this lane's column: live nibble (f32 test), the
+      // guard-band nibble, and w = 2^q per voxel.
+      auto eval = [&](uint32_t ja, bool act, float4& pc, float2& pd, float* w, uint32_t& lm,
+                      uint32_t& bm) {
+        const float4 pa = lds_f4(ja), pb = lds_f4(ja + 16);
+        pc = lds_f4(ja + 32);
+        const float4 p4 = lds_f4(ja + 48);   // qlo, gid
+        pd = make_float2(p4.x, p4.y);
+        float q[Z];
+        const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
+        const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
+        const float t3 = fmaf(pb.z, mZ, pa.w);
+        q[0] = fmaf(mX, t1, fmaf(mY, t2, fmaf(mZ, t3, pa.x)));
+        float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, mZ1, t3)));
+        const float d2q = 2.f * pb.z;
+#pragma unroll
+        for (int h = 1; h < Z; ++h) {
+          q[h] = q[h - 1] + dq;
+          dq += d2q;
+        }
+        lm = 0u;
+        bm = 0u;
+#pragma unroll
+        for (int h = 0; h < Z; ++h) {
+          const bool own = act && h < bg.ez;
+          const bool lv = own && q[h] >= pc.w;
+          w[h] = ex2_approx(q[h]);
+          lm |= (uint32_t)lv << h;
+          bm |= (uint32_t)(own && !lv && q[h] >= pd.x) << h;
+        }
+      };
+      auto band_fix = [&](const float2& pd, uint32_t bm, uint32_t& lm) {
+        const int gidj = __float_as_int(pd.y);
+#pragma unroll
+        for (int h = 0; h < Z; ++h)
+          if (((bm >> h) & 1u) &&
+              exact_live(gidj, bg.x0 + x, bg.y0 + y, bg.z0 + h, xsrc, g, cut2d))
+            lm |= 1u << h;
+      };
+      auto accumulate = [&](float A, const float* w, uint32_t lm) {
+#pragma unroll
+        for (int h = 0; h < Z; ++h)
+          if ((lm >> h) & 1u) {
+            aS[h] = fmaf(A, w[h], aS[h]);
+            aW[h] += w[h];
+          }
+      };
+#ifndef GSV_COLS_UNROLL
+#define GSV_COLS_UNROLL 1       // 2: two pairs per iteration (measured slower)
+#endif
+#if GSV_COLS_UNROLL == 1
+      for (int t = 0; t < kmax; ++t) {
+        const bool act0 = t < hk;
+        const uint32_t ja0 = sp_a + (uint32_t)(act0 ? h0 + t : h0) * (uint32_t)sizeof(Pair32);
+        float4 pc0;
+        float2 pd0;
+        float w0[Z];
+        uint32_t lm0, bm0;
+        eval(ja0, act0, pc0, pd0, w0, lm0, bm0);
+        if (__any_sync(kFull, bm0 != 0u)) band_fix(pd0, bm0, lm0);
+        accumulate(pc0.z, w0, lm0);
+        any |= lm0 != 0u;
+        if constexpr (MASKS) {
+          if (lm0) red_or_shared(smk_a + 4u * (uint32_t)(8 * (h0 + t) + y), lm0 << (4 * x));
+        }
+      }
+#else
+      // two pairs per iteration (independent chains), accumulated in list order
+      for (int t = 0; t < kmax; t += 2) {
+        const bool act0 = t < hk, act1 = t + 1 < hk;
+        const uint32_t ja0 = sp_a + (uint32_t)(act0 ? h0 + t : h0) * (uint32_t)sizeof(Pair32);
+        const uint32_t ja1 = sp_a + (uint32_t)(act1 ? h0 + t + 1 : h0) * (uint32_t)sizeof(Pair32);
+        float4 pc0, pc1;
+        float2 pd0, pd1;
+        float w0[Z], w1[Z];
+        uint32_t lm0, lm1, bm0, bm1;
+        eval(ja0, act0, pc0, pd0, w0, lm0, bm0);
+        eval(ja1, act1, pc1, pd1, w1, lm1, bm1);
+        if (__any_sync(kFull, (bm0 | bm1) != 0u)) {
+          band_fix(pd0, bm0, lm0);
+          band_fix(pd1, bm1, lm1);
+        }
+        accumulate(pc0.z, w0, lm0);
+        accumulate(pc1.z, w1, lm1);
+        any |= (lm0 | lm1) != 0u;
+        if constexpr (MASKS) {
+          if (lm0) red_or_shared(smk_a + 4u * (uint32_t)(8 * (h0 + t) + y), lm0 << (4 * x));
+          if (lm1) red_or_shared(smk_a + 4u * (uint32_t)(8 * (h0 + t + 1) + y), lm1 << (4 * x));
+        }
+      }
+#endif
+      // the groups' sums into the brick's S and W, one group after another
+      const int col = x + 8 * y;
+      for (int gg = gf; gg <= glast; ++gg) {
+        if (valid && myg == gg && any) {
+          float4 sv = sS4[col], wv = sW4[col];
+          sv.x += aS[0]; sv.y += aS[1]; sv.z += aS[2]; sv.w += aS[3];
+          wv.x += aW[0]; wv.y += aW[1]; wv.z += aW[2]; wv.w += aW[3];
+          sS4[col] = sv;
+          sW4[col] = wv;
+        }
+        __syncwarp();
+      }
+    }
+    if constexpr (MASKS) {
+      // each entry's 32-byte mask record (zero for pairs without a footprint)
+      __syncwarp();
+      if (gid >= 0) {
+        uint4 m0 = make_uint4(0u, 0u, 0u, 0u), m1 = m0;
+        if (hit) {
+          const uint4* src = reinterpret_cast<const uint4*>(smk + 8 * r);
+          m0 = src[0];
+          m1 = src[1];
+        }
+        uint4* dst = live_masks + 2 * (base + lane);
+        dst[0] = m0;
+        dst[1] = m1;
+      }
+      __syncwarp();
+      reinterpret_cast<uint4*>(smk)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
+      reinterpret_cast<uint4*>(smk)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncwarp();
+  }
+  // Epilogue: normalise, store, fused loss (optimize.py:91-103).
+  double lsum = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int v = lane + 32 * i;
+    const int x = v & 7, y = (v >> 3) & 7, z = v >> 6;
+    if (!(x < bg.ex && y < bg.ey && z < bg.ez)) continue;
+    const float2 sw = make_float2(reinterpret_cast<const float*>(sS4)[4 * (v & 63) + z],
+                                  reinterpret_cast<const float*>(sW4)[4 * (v & 63) + z]);
+    const int64_t lin = (int64_t)(bg.x0 + x) +
+                        (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
+    const bool cov = (double)sw.y >= eps_w;
+    const float iv = cov ? __fdiv_rn(sw.x, sw.y) : 0.f;
+    S[lin] = sw.x;
+    W[lin] = sw.y;
+    I[lin] = iv;
+    if (target) {
+      const double d = (double)iv - target_value(target, target_f64, lin);
+      double dl;
+      if (loss_kind == 0) {
+        lsum += fabs(d);
+        dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / vox_count;
+      } else {
+        lsum += d * d;
+        dl = 2.0 * d / vox_count;
+      }
+      const float alpha = (cov && dl != 0.0) ? (float)(dl / (double)sw.y) : 0.f;
+      ab[lin] = make_float2(alpha, iv);
+    }
+  }
+  if (target) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(kFull, lsum, o);
+    if (lane == 0) loss_part[lb] = lsum;
+  }
+}
+
 // --------------------------------------------------------------- forward f64
 struct __align__(16) Pair64 {
   double l[9];
@@ -1402,11 +1787,12 @@ backward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 // set bits of its pair -- exactly the live voxels, nothing else.
 constexpr int kBwdMChunk = 2048;
 
-// ARITH: the default 8x8x4 brick with vpl-4 masks, where word wi = 4 w + z
-// and bit b map to brick voxel index b + 32 w + 64 z -- decoded with integer
-// ops instead of the (word, bit) LUT, keeping the shared-memory pipe for the
-// {alpha, I} gathers (the kernel's bound).
-template <bool ARITH>
+// ARITH (8x8x4 bricks): the voxel of (word, bit) is decoded with integer ops
+// instead of the (word, bit) LUT, keeping the shared-memory pipe for the
+// {alpha, I} gathers (the kernel's bound).  ARITH 1: vpl-4 masks, word
+// wi = 4 w + z, bit b -> brick voxel index b + 32 w + 64 z.  ARITH 2: the
+// column-packed forward's masks, word y, bit 4 x + z -> x + 8 y + 64 z.
+template <int ARITH>
 __global__ void __launch_bounds__(kBwdThreads, 3)
 backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
                    const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
@@ -1444,7 +1830,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
     a2 = make_uint2(m23.x, m23.y);
     a3 = make_uint2(m23.z, m23.w);
   };
-  for (int e = tid; e < 256; e += kBwdThreads) {
+  for (int e = tid; e < (ARITH ? 0 : 256); e += kBwdThreads) {   // (word, bit) LUT
     const int wi = e >> 5, u = ((wi >> wsh) << 5) + (e & 31);
     float4 v = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
     if (u < units) {
@@ -1551,7 +1937,9 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
             myw[nw << 5] = words[w];
             // ARITH: the word's brick-voxel base 32 (w / 4) + 64 (w % 4); else
             // its LUT row
-            myb[nw << 5] = (unsigned short)(ARITH ? ((w >> 2) << 5) + ((w & 3) << 6) : w << 5);
+            myb[nw << 5] = (unsigned short)(ARITH == 2 ? w << 3
+                                            : ARITH == 1 ? ((w >> 2) << 5) + ((w & 3) << 6)
+                                                         : w << 5);
             ++nw;
           }
         myw[nw << 5] = 0u;
@@ -1579,7 +1967,8 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
         float fx, fy, fz;
         float2 v_ab;
         if (ARITH) {
-          const int vi = wb + bit;              // x + 8 y + 64 z
+          // x + 8 y + 64 z
+          const int vi = ARITH == 2 ? wb + (bit >> 2) + ((bit & 3) << 6) : wb + bit;
           v_ab = sab[vi];
           fx = (float)(vi & 7);
           fy = (float)((vi >> 3) & 7);
@@ -1780,7 +2169,27 @@ int gsv_forward(const double* positions, const double* log_scales, const double*
     // vpl | 0x200: keep the two tiles of a VPL-4 brick in one CTA (measurement)
     const bool no_split = (vpl & 0x200) != 0;
     vpl &= 0xff;
-    GSV_REQUIRE(vpl == 0 || vpl == 2 || vpl == 4 || vpl == 8, "vpl must be 0, 2, 4 or 8");
+    GSV_REQUIRE(vpl == 0 || vpl == 2 || vpl == 4 || vpl == 8 || vpl == 16,
+                "vpl must be 0, 2, 4, 8 or 16");
+    if (vpl == 16) {
+      // column-packed: one warp per 8x8x4 brick, (pair, column) slots dealt
+      // to the lanes; live masks in the column-nibble layout
+      GSV_REQUIRE(bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4,
+                  "vpl 16 needs 8x8x4 bricks");
+      const ExactSrc xc{positions, log_scales, rotations, rec64};
+      if (live_masks != nullptr)
+        forward32c_kernel<true><<<(unsigned)nb, 32, 0, s>>>(
+            positions, xc, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
+            (float*)S, (float*)W, (float*)I, target, target_f64, loss_kind, vox_count,
+            (float2*)ab, loss_part, (uint4*)live_masks);
+      else
+        forward32c_kernel<false><<<(unsigned)nb, 32, 0, s>>>(
+            positions, xc, rec32, starts, gids, *grid, *bricks, (float)cut2d, cut2d, eps_w,
+            (float*)S, (float*)W, (float*)I, target, target_f64, loss_kind, vox_count,
+            (float2*)ab, loss_part, nullptr);
+      GSV_CHECK_LAUNCH("forward32c_kernel");
+      return GSV_OK;
+    }
     // auto: the whole-brick two-list kernel for 8x8x4 bricks (fastest at every
     // pair density measured), else the warp-tile kernels
     if (vpl == 0 && bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4) vpl = 8;
@@ -1898,19 +2307,24 @@ int gsv_backward(const double* positions, const double* log_scales, const double
   cudaStream_t s = as_stream(stream);
   if (precision == 0 && live_masks != nullptr) {
     if (mask_vpl == 0) mask_vpl = mask_vpl_auto(*bricks);
-    GSV_REQUIRE(mask_vpl == 2 || mask_vpl == 4, "mask_vpl must be 0, 2 or 4");
-    GSV_REQUIRE(mask_units(*bricks, mask_vpl) == (mask_vpl == 4 ? 64 : 128),
+    const bool b884 = bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4;
+    GSV_REQUIRE(mask_vpl == 2 || mask_vpl == 4 || mask_vpl == 16,
+                "mask_vpl must be 0, 2, 4 or 16");
+    GSV_REQUIRE(mask_vpl != 16 || b884, "mask_vpl 16 (column-packed masks) needs 8x8x4 bricks");
+    GSV_REQUIRE(mask_vpl == 16 || mask_units(*bricks, mask_vpl) == (mask_vpl == 4 ? 64 : 128),
                 "live masks need a brick that fills one CTA's warp tiles exactly "
                 "(e.g. 8x8x4)");
-    const bool arith = mask_vpl == 4 && bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4;
-    if (arith)
-      backward32m_kernel<true><<<(unsigned)nb, kBwdThreads, 0, s>>>(
-          positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,
-          (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials);
+#define GSV_BWDM(A)                                                                            \
+  backward32m_kernel<A><<<(unsigned)nb, kBwdThreads, 0, s>>>(                                  \
+      positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,               \
+      (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials)
+    if (mask_vpl == 16)
+      GSV_BWDM(2);
+    else if (mask_vpl == 4 && b884)
+      GSV_BWDM(1);
     else
-      backward32m_kernel<false><<<(unsigned)nb, kBwdThreads, 0, s>>>(
-          positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,
-          (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials);
+      GSV_BWDM(0);
+#undef GSV_BWDM
     GSV_CHECK_LAUNCH("backward32m_kernel");
   } else if (precision == 0) {
     const int64_t bvox = (int64_t)bricks->bdx * bricks->bdy * bricks->bdz;

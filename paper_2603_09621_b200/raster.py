@@ -321,18 +321,50 @@ def _resolve_vpl(brick_dims) -> int:
     return 4 if bz % 4 == 0 and bx * by * (bz // 4) <= 64 else 2
 
 
+# Pairs per reaching Gaussian up to which the grouped-column forward is used
+# (LR grids: ~4.3 at configs 1-4; the 256^3 render has 11.5, 512^3 46).
+_GROUPED_MAX_DENSITY = 8.0
+
+
+def _use_grouped(brick_dims, pairs: int, n: int) -> bool:
+    """The grouped-column forward (gsv_forward vpl 16) for 8x8x4 bricks when
+    Gaussians are small against a brick (pairs <= 8 per reaching Gaussian:
+    LR training grids).  There its z-runs of identical footprints make
+    ~2.4x fewer (pair, column) evaluations than the two-list whole-brick
+    kernel and the forward runs ~7% faster; at HR densities groups shrink to
+    ~1.3 pairs and the whole-brick kernel wins (2.0 vs 3.0 ms at 256^3).
+    The choice depends only on the index, so the train step, forward() and
+    Renderer render bit-identically at a given grid.  GSV_FWD_COLS=0 / =1
+    forces the whole-brick / grouped kernel (measurement, A-B runs)."""
+    if tuple(brick_dims) != (8, 8, 4) or os.environ.get("GSV_NO_WHOLE") \
+            or os.environ.get("GSV_VPL"):
+        return False
+    forced = os.environ.get("GSV_FWD_COLS", "")
+    if forced in ("0", "1"):
+        return forced == "1"
+    return pairs <= _GROUPED_MAX_DENSITY * max(n, 1)
+
+
+def _train_mask_vpl(brick_dims, pairs: int, n: int) -> int:
+    """Mask layout of the train step's forward -> masked backward: 16 (the
+    grouped forward's column-nibble masks) or, for the whole-brick and
+    warp-tile forwards, their warp-tile layout (_resolve_vpl)."""
+    return 16 if _use_grouped(brick_dims, pairs, n) else _resolve_vpl(brick_dims)
+
+
 def _forward_vpl_arg(brick_dims, pairs: int = 0, n: int = 0, masks: bool = True) -> int:
-    """gsv_forward's vpl argument.  8x8x4 bricks (the default) use 8: one warp
-    per brick, two columns per lane, the pairs of each 32-pair round compacted
-    into one hit list per y-half (with live masks for the train step).  It is
-    the fastest form at every pair density measured (LR train forward 0.99 ->
-    0.91 ms, 256^3 render 2.26 -> 2.01 ms), and using it for every path keeps
-    the train step, forward() and Renderer bit-identical.  Other bricks use the
-    warp-tile kernels (_resolve_vpl); GSV_NO_WHOLE=1 or GSV_VPL=2|4 force those
+    """gsv_forward's vpl argument.  8x8x4 bricks (the default): 16, the
+    grouped-column kernel, at LR densities (_use_grouped), else 8, one warp
+    per brick with two columns per lane and the pairs of each 32-pair round
+    compacted into one hit list per y-half (LR train forward 0.99 -> 0.91 ms,
+    256^3 render 2.26 -> 2.01 ms against the warp-tile kernels).  Either
+    writes live masks for the train step.  Other bricks use the warp-tile
+    kernels (_resolve_vpl); GSV_NO_WHOLE=1 or GSV_VPL=2|4 force those
     (measurement), GSV_NO_SPLIT keeps a brick's two tiles in one CTA.
-    pairs / n (the Gaussians reaching the index) are kept for callers and
-    tools that report the density."""
-    del pairs, n, masks
+    pairs / n: the index's pairs and the Gaussians reaching it."""
+    del masks
+    if _use_grouped(brick_dims, pairs, n):
+        return 16
     if (tuple(brick_dims) == (8, 8, 4) and not os.environ.get("GSV_NO_WHOLE")
             and not os.environ.get("GSV_VPL")):
         return 8
@@ -342,6 +374,8 @@ def _forward_vpl_arg(brick_dims, pairs: int = 0, n: int = 0, masks: bool = True)
 def _masks_fit(brick_dims, vpl: int) -> bool:
     """Live masks need a brick that fills one CTA's warp tiles exactly (4
     planes of mask words), e.g. the default 8x8x4."""
+    if vpl == 16:
+        return tuple(brick_dims) == (8, 8, 4)
     bx, by, bz = brick_dims
     return bx * by * (-(-bz // vpl)) == (64 if vpl == 4 else 128)
 

@@ -27,8 +27,8 @@ import torch
 from . import _lib
 from .field import GaussianField
 from .raster import (BrickIndex, GradientBuffer, RenderCache, _alloc, _chain_rule,
-                     _forward_vpl_arg, _masks_fit,
-                     _preprocess, _resolve_vpl, _scan,
+                     _forward_vpl_arg, _masks_fit, _reaching,
+                     _preprocess, _resolve_vpl, _scan, _train_mask_vpl,
                      _forward_into, _pair_partials, build_brick_index)
 from .render import RenderOptions
 from .volume import Volume
@@ -172,7 +172,7 @@ class TrainStep:
         # exactly the forward's live voxels
         bd = self.brick_dims
         masks = None
-        self._mask_vpl = _resolve_vpl(bd)
+        self._mask_vpl = _train_mask_vpl(bd, idx.pair_count, _reaching(f, idx))
         if (opts.precision == "f32" and _masks_fit(bd, self._mask_vpl)
                 and not os.environ.get("GSV_NO_LIVE_MASKS")):
             masks = pool.get("live_masks", (max(idx.pair_count, 1), 4, 2), torch.int32)
@@ -353,7 +353,7 @@ def _graph_supported(self) -> bool:
             return False
     bd = self.brick_dims
     return (self.opts.precision == "f32"
-            and _masks_fit(bd, _resolve_vpl(bd))
+            and (tuple(bd) == (8, 8, 4) or _masks_fit(bd, _resolve_vpl(bd)))
             and not os.environ.get("GSV_NO_GRAPH") and not os.environ.get("GSV_NO_LIVE_MASKS")
             and not os.environ.get("GSV_TAIL_SPLIT"))
 
@@ -387,7 +387,7 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(),
         int(self.target.dtype == torch.float64), self.loss_kind,
         float(nvox), b["ab"].data_ptr(), b["loss_part"].data_ptr(), b["masks"].data_ptr(),
-        _forward_vpl_arg(self.brick_dims), s), "forward")
+        b["fwd_vpl"], s), "forward")
     _lib.check(lib.gsv_sum(b["loss_part"].data_ptr(), b["nb"], b["loss_sum"].data_ptr(), s),
                "sum")
     if not self.sharded:
@@ -508,7 +508,11 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
         b["govf"] = gp.get("govf", (1,), torch.int32)
     b["t"] = gp.get("t", (1,), torch.int64)
     b["bc"] = _bias_corrections(beta1, beta2, state.t, _BC_CHUNK).to(dev)
-    b["vpl"] = _resolve_vpl(self.brick_dims)
+    # the forward kernel (and so the mask layout) for this capture, from the
+    # pair density seen at capture (raster._use_grouped)
+    reach = n if self.slab is None else int(torch.count_nonzero(b["counts"]).item())
+    b["vpl"] = _train_mask_vpl(self.brick_dims, pairs, reach)
+    b["fwd_vpl"] = _forward_vpl_arg(self.brick_dims, pairs, reach)
     hp = _lib.GsvAdamHparams()
     for i, name in enumerate(("positions", "log_scales", "rotations", "raw_amplitude",
                               "raw_relax")):

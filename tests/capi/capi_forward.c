@@ -114,8 +114,12 @@ int main(int argc, char** argv) {
   float* S = (float*)dev_copy(NULL, (size_t)nv * 4);
   float* W = (float*)dev_copy(NULL, (size_t)nv * 4);
   float* I = (float*)dev_copy(NULL, (size_t)nv * 4);
+  /* the Python API's kernel choice (raster._forward_vpl_arg): the grouped
+   * forward (vpl 16) for 8x8x4 bricks at <= 8 pairs per Gaussian, else auto */
+  const int b884 = bd[0] == 8 && bd[1] == 8 && bd[2] == 4;
+  const int vpl = (b884 && pairs <= 8 * n) ? 16 : 0;
   CK(gsv_forward(pos, ls, rot, rec32, NULL, starts, gids, &g, &k, cutoff, 1e-8, 0, S, W, I, NULL,
-                 0, 0, (double)nv, NULL, NULL, NULL, 0, NULL));
+                 0, 0, (double)nv, NULL, NULL, NULL, vpl, NULL));
   CU(cudaDeviceSynchronize());
 
   int64_t* h_starts = (int64_t*)malloc((size_t)(nb + 1) * 8);

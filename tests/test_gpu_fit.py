@@ -241,18 +241,23 @@ def test_graph_step_recaptures_on_new_hyperparameters():
     np.testing.assert_array_equal(_pack(fa), _pack(fb))
 
 
-@pytest.mark.parametrize("vpl", ["2", "4"])
+@pytest.mark.parametrize("vpl", ["2", "4", "16", "whole"])
 def test_masked_backward_matches_span_backward(vpl, monkeypatch):
-    """The train step's backward walks the forward's live masks (either warp
-    tile layout); its merged gradients equal the public span backward's --
-    both evaluate exactly the live pair-voxels -- up to f32 rounding."""
-    monkeypatch.setenv("GSV_VPL", vpl)
+    """The train step's backward walks the forward's live masks (the warp-tile
+    layouts, the whole-brick kernel's VPL-4 layout, or the column-packed
+    kernel's column-nibble layout, the default); its merged gradients equal
+    the public span backward's -- both evaluate exactly the live pair-voxels
+    -- up to f32 rounding."""
+    if vpl in ("2", "4"):
+        monkeypatch.setenv("GSV_VPL", vpl)
+    elif vpl == "whole":
+        monkeypatch.setenv("GSV_FWD_COLS", "0")
     p = make_problem(CONFIGS[2])
     lr = gs.Volume(p["lr_grid"], p["lr"])
     f = gs.GaussianField(*p["field"])
     step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
     out = step.forward(f)
-    assert step._masks is not None and step._mask_vpl == int(vpl)
+    assert step._masks is not None and step._mask_vpl == (4 if vpl == "whole" else int(vpl))
     gm = step.backward(f, out)
     idx = gs.build_brick_index(f, lr.grid)
     c = gs.forward(f, lr.grid, idx)
@@ -483,3 +488,57 @@ def test_f64_target_keeps_f64_in_the_fused_loss():
         ref, _ = gs.loss_and_grad(out.cache.volume(), lr, "l1")
         tol = 1e-12 if prec == "f64" else 1e-9
         assert abs(out.loss() - ref) <= tol * max(ref, 1.0), (prec, out.loss(), ref)
+
+
+def _mask_voxels(masks, vpl):
+    """(P, 256) bool: brick voxel x + 8 y + 64 z of each pair, decoded from
+    the VPL-4 layout (word 4 (y >> 2) + z, bit x + 8 (y & 3)) or the
+    column-nibble layout (word y, bit 4 x + z)."""
+    words = masks.reshape(-1, 8).cpu().numpy().view(np.uint32)
+    bits = ((words[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool)  # P,8,32
+    out = np.zeros((words.shape[0], 256), dtype=bool)
+    w, b = np.meshgrid(np.arange(8), np.arange(32), indexing="ij")
+    if vpl == 4:
+        x, y, z = b & 7, 4 * (w >> 2) + (b >> 3), w & 3
+    else:
+        x, y, z = b >> 2, w, b & 3
+    out[:, (x + 8 * y + 64 * z).ravel()] = bits.reshape(words.shape[0], 256)
+    return out
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "ragged"])
+def test_grouped_forward_matches_whole_brick_kernel(case, monkeypatch):
+    """The grouped-column forward (gsv_forward vpl 16, the default at LR) against
+    the two-list whole-brick kernel (vpl 8): the same live voxels per pair
+    (same quadratic, same guard band), the same coverage, and S, W, I equal
+    up to the f32 rounding of the grouped association; bit-reproducible run
+    to run.  The ragged grid has partial bricks on every axis."""
+    from paper_2603_09621_b200.field import random_field_arrays
+    if case == "ragged":
+        grid = gs.GridSpec((30, 21, 13), (1.0, 1.2, 0.9), (0.5, -1.0, 2.0))
+        arrs = random_field_arrays(4000, grid, 11, 0.4, 2.0)
+        tgt = gs.Volume(grid, np.random.default_rng(2).uniform(size=grid.dims).astype(np.float32))
+    else:
+        p = make_problem(CONFIGS[1 if case == "c1" else 2])
+        grid, arrs, tgt = p["lr_grid"], p["field"], gs.Volume(p["lr_grid"], p["lr"])
+    res = {}
+    for mode in ("0", "", "again"):
+        monkeypatch.setenv("GSV_FWD_COLS", "0" if mode == "0" else "1")
+        f = gs.GaussianField(*arrs)
+        step = gs.TrainStep(tgt, gs.RenderOptions(), (8, 8, 4), "l1")
+        out = step.forward(f)
+        res[mode] = (out.cache.S.clone(), out.cache.W.clone(), out.cache.I.clone(),
+                     out.loss(), step._mask_vpl,
+                     _mask_voxels(step._masks[:out.idx.pair_count], step._mask_vpl))
+    a, b, c = res["0"], res[""], res["again"]
+    assert a[4] == 4 and b[4] == 16
+    for i in range(3):
+        assert torch.equal(b[i], c[i]), i                     # reproducible
+    np.testing.assert_array_equal(a[5], b[5])                 # identical live decisions
+    assert b[5].any()
+    assert torch.equal(a[1] >= 1e-8, b[1] >= 1e-8)            # identical coverage
+    for i in range(2):                                        # S, W: f32 association only
+        d = (a[i] - b[i]).abs().max().item()
+        assert d <= 2e-6 * max(1.0, a[i].abs().max().item()), (i, d)
+    assert (a[2] - b[2]).abs().max().item() <= 1e-6
+    assert abs(a[3] - b[3]) <= 1e-6 * max(1e-3, abs(a[3]))     # sign(I - T) at I ~ T
