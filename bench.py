@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--no-render512", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the config-2 fit and config-4 step/render extra keys")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-count", action="store_true", help="skip the CUPTI launch count "
@@ -507,17 +509,28 @@ def run_ours(args, dist, ws, rank, local):
                      "pairs": r5_renderer.pair_count() if ws == 1 else None,
                      "field": "config-5 jittered"}
         del f5, r5_renderer
+    # ---------------- the other BASELINE configs (N = 1): config 2 as a
+    # fixed-iteration fit() through the public API, config 4 as train steps
+    # plus its HR render (BASELINE.json configs[1] and [3])
+    other = None
+    if ws == 1 and not args.no_configs:
+        other = {"2": config2_fit(gs, dev, 200), "4": config4_step_render(gs, dev, args)}
     clocks = sampler.stop()
 
     # ---------------- roofline of the dominant pair kernel (live pair-voxels)
-    cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
     out_idx = out.idx
     _lib.check(lib.gsv_diag_count_live(
         f.positions.data_ptr(), out_idx._aux.rec32.data_ptr(), f.log_scales.data_ptr(),
         f.rotations.data_ptr(), out_idx.starts.data_ptr(), out_idx.gids.data_ptr(),
         _lib.make_grid(lr_grid), _lib.make_bricks(lr_grid, bd, my_slab), 3.0, cnt.data_ptr(),
         _lib.stream_ptr()), "count_live")
-    e_live, e_brick, e_tile = (int(x) for x in cnt.tolist())
+    e_live, e_brick, e_tile, e_group = (int(x) for x in cnt.tolist())
+    # the slots the train step's forward kernel evaluates: the grouped-column
+    # kernel at LR densities (raster._use_grouped), else the whole-brick tiles
+    from paper_2603_09621_b200.raster import _use_grouped
+    grouped = _use_grouped(bd, pairs, f.count)
+    e_eval = e_group if grouped else e_tile
     peak = fp32_peak(lib, dev)
     t_fwd = phases.get("forward", (0, float("nan")))[1]
     t_bwd = phases.get("backward", (0, float("nan")))[1]
@@ -552,21 +565,25 @@ def run_ours(args, dist, ws, rank, local):
                 "unit": "TFLOP/s", "frac": achieved / peak["tflops"], "traffic": traffic,
                 "peak_source": peak["source"],
                 "evaluated": {
-                    "E_tile": e_tile if dom == "forward" else None,
-                    "live_fraction": (e_live / e_tile) if (dom == "forward" and e_tile) else None,
+                    "kernel": "forward32c_kernel (grouped columns)" if grouped
+                    else "forward32w_kernel (two-list whole brick)",
+                    "E_evaluated": e_eval if dom == "forward" else None,
+                    "E_tile_whole_brick": e_tile, "E_group": e_group if grouped else None,
+                    "live_fraction": (e_live / e_eval) if (dom == "forward" and e_eval) else None,
                     "issue_active_pct": issue,
                     # the same 28 FLOP counted per evaluated slot: what the kernel
                     # sustains; frac above is that times the live fraction
-                    "achieved_evaluated": (e_tile * fl / (t_dom * 1e-3) / 1e12)
-                    if (dom == "forward" and e_tile) else None,
-                    "frac_evaluated": (e_tile * fl / (t_dom * 1e-3) / 1e12 / peak["tflops"])
-                    if (dom == "forward" and e_tile) else None,
-                    "note": "the forward evaluates every (pair, voxel) slot of each warp tile "
-                            "a pair's 3-sigma box and sphere bound reach (E_tile; every such "
-                            "hit has a live voxel, tools/deadhits.py); frac counts live "
-                            "pair-voxels only (SURVEY 8d's unit), frac_evaluated every "
-                            "evaluated slot; issue_active_pct is the kernel's issue-slot use "
-                            "from the ncu capture in profiles/"},
+                    "achieved_evaluated": (e_eval * fl / (t_dom * 1e-3) / 1e12)
+                    if (dom == "forward" and e_eval) else None,
+                    "frac_evaluated": (e_eval * fl / (t_dom * 1e-3) / 1e12 / peak["tflops"])
+                    if (dom == "forward" and e_eval) else None,
+                    "note": "E_evaluated counts the (pair, voxel) slots the forward kernel "
+                            "issues, idle lanes included: 128 per chunk iteration of the "
+                            "grouped kernel (E_group), or 128 per warp-tile hit of the "
+                            "whole-brick kernel (E_tile_whole_brick, for comparison); frac "
+                            "counts live pair-voxels only (SURVEY 8d's unit), frac_evaluated "
+                            "every evaluated slot; issue_active_pct is the kernel's "
+                            "issue-slot use from the ncu capture in profiles/"},
                 "work": {"E_live": e_live, "E_brick": e_brick,
                 "flop_per_live_pair_voxel": fl, "ms_per_launch": t_dom},
                 "hbm": {"algorithmic_bytes": bytes_alg,
@@ -586,12 +603,78 @@ def run_ours(args, dist, ws, rank, local):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic", "config": _config_dict(args, p, ws),
                 "pairs_lr": pairs,
-                "render": render, "render512": render512,
+                "render": render, "render512": render512, "configs": other,
                 "phases_ms": {k: v[1] for k, v in phases.items()},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
                 "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
                 "loss_last": losses[-1]}
         print(json.dumps(line), flush=True)
+
+
+def config2_fit(gs, dev, iterations: int) -> dict:
+    """Config 2 (128x128x64 LR -> x2, N = 1,048,576): one whole fit() of
+    `iterations` iterations through the public API (init, graph capture,
+    every iteration's loss read), wall clock."""
+    import torch
+    p = problem_for(2)
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    gs.fit(lr, gs.InitConfig(background_threshold=0.0), gs.FitConfig(iterations=3))  # warm-up
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    f, rep = gs.fit(lr, gs.InitConfig(background_threshold=0.0),
+                    gs.FitConfig(iterations=iterations))
+    torch.cuda.synchronize(dev)
+    sec = time.perf_counter() - t0
+    return {"workload": "config 2: fit() on 128x128x64 LR (x2 -> 256x256x128), "
+                        f"N={f.count}, {iterations} iterations, init and final render included",
+            "value": iterations / sec, "unit": "it/s", "seconds": sec,
+            "final_loss": rep.final["loss"], "timing": "wall clock around fit()"}
+
+
+def config4_step_render(gs, dev, args) -> dict:
+    """Config 4 (256x256x40 LR, spacing (1,1,4), x4 through-plane -> 256x256x160,
+    N = 2,621,440): graph-replayed train steps (CUDA events) and the HR render
+    (Renderer graph replays)."""
+    import torch
+    p = problem_for(4)
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"], device=dev)
+    st = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    for _ in range(args.warmup):
+        step.step(f, st, lrs)
+    torch.cuda.synchronize(dev)
+    s = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    h = step.step_async(f, st, lrs)
+    for i in range(args.steps):
+        nxt = step.step_async(f, st, lrs) if i + 1 < args.steps else None
+        h.loss()
+        h = nxt
+    e1.record(s)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / args.steps
+    r = gs.Renderer(p["hr_grid"], gs.RenderOptions(), (8, 8, 4), device=dev)
+    for _ in range(3):
+        r(f)
+    kr = max(1, min(args.steps, 10))
+    torch.cuda.synchronize(dev)
+    e0.record(s)
+    for _ in range(kr):
+        r(f)
+    e1.record(s)
+    torch.cuda.synchronize(dev)
+    ms_r = e0.elapsed_time(e1) / kr
+    nv = p["hr_grid"].num_voxels
+    return {"workload": "config 4: fit step on 256x256x40 LR (spacing 1,1,4), "
+                        f"N={f.count}; render at 256x256x160",
+            "train": {"value": 1000.0 / ms, "unit": "it/s", "ms_per_step": ms,
+                      "steps": args.steps},
+            "render": {"value": nv / (ms_r * 1e-3) / 1e9, "unit": "Gvoxel/s",
+                       "ms_per_render": ms_r, "renders": kr,
+                       "pairs": r.pair_count()}}
 
 
 def fp32_peak(lib, dev) -> dict:

@@ -17,8 +17,11 @@ extern "C" {
  * f32 forward decides them) of an index: the roofline work unit of
  * SURVEY.md §8d.  Also counts every (pair, voxel) of the brick (E_brick) and,
  * for 8x8x4 bricks, the (pair, voxel) slots the f32 forward evaluates: 128 per
- * pair x warp-tile hit under its staging tests (E_tile).  counters: device
- * uint64[3] = {E_live, E_brick, E_tile}, accumulated. */
+ * pair x warp-tile hit under its staging tests (E_tile), and the slots the
+ * grouped-column forward (gsv_forward vpl 16) evaluates: 128 per chunk
+ * iteration, a chunk running max(group size) iterations (E_group).
+ * counters: device uint64[4] = {E_live, E_brick, E_tile, E_group},
+ * accumulated. */
 int gsv_diag_count_live(const double* positions, const gsv_record32* rec32,
                         const double* log_scales, const double* rotations,
                         const int64_t* starts, const int32_t* gids,

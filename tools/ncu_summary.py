@@ -29,9 +29,22 @@ METRICS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
     ("launch__registers_per_thread", "registers"),
     ("smsp__inst_executed.sum", "warp instructions"),
+    # pipe utilisation (the north_star's FP32 / SFU evidence): FMA pipe cycles,
+    # FMA / XU (MUFU: ex2, rcp, sqrt) / FP64 / ALU / LSU instruction issue
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe cycles %"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe inst %"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe inst %"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe inst %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe cycles %"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe inst %"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe inst %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared bank conflicts"),
+    ("dram__bytes_read.sum.per_second", "DRAM read rate"),
 ]
 
-ROLE = {"forward32_kernel": "forward", "backward32m_kernel": "backward",
+ROLE = {"forward32c_kernel": "forward", "forward32_kernel": "forward_tiles",
+        "backward32m_kernel": "backward",
         "backward32_kernel": "backward_span", "tail_kernel": "update",
         "tail_tma_kernel": "update_eager", "forward32w_kernel": "render_forward",
         "preprocess_kernel": "preprocess", "emit_kernel": "emit", "emit_warp_kernel": "emit"}
