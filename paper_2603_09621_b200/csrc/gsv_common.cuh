@@ -34,6 +34,21 @@ int cuda_status(cudaError_t e, const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Device-side bounds checks for the debug variant (compute-sanitizer is not
+// available on the GPU pool): `python -m paper_2603_09621_b200.build
+// --variant dcheck -D GSV_DEBUG_CHECKS=1`, loaded with GSV_LIB; a failed check
+// traps the kernel (the launch returns an error).  Compiled out otherwise.
+#if defined(GSV_DEBUG_CHECKS) && GSV_DEBUG_CHECKS
+#define GSV_DCHECK(cond)  \
+  do {                    \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define GSV_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // ------------------------------------------------------- unfused f64 math
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }

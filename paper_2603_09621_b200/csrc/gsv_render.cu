@@ -1218,6 +1218,8 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 #if GSV_COLS_UNROLL == 1
       for (int t = 0; t < kmax; ++t) {
         const bool act0 = t < hk;
+        GSV_DCHECK(!act0 || (h0 + t >= 0 && h0 + t < nh && x >= 0 && x < bg.ex && y >= 0 &&
+                             y < bg.ey));
         const uint32_t ja0 = sp_a + (uint32_t)(act0 ? h0 + t : h0) * (uint32_t)sizeof(Pair32);
         float4 pc0;
         float2 pd0;
@@ -1258,6 +1260,7 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 #endif
       // the groups' sums into the brick's S and W, one group after another
       const int col = x + 8 * y;
+      GSV_DCHECK(!valid || (col >= 0 && col < 64 && myg >= 0 && myg < ng && kk >= 0));
       for (int gg = gf; gg <= glast; ++gg) {
         if (valid && myg == gg && any) {
           float4 sv = sS4[col], wv = sW4[col];
@@ -1279,6 +1282,7 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
           m0 = src[0];
           m1 = src[1];
         }
+        GSV_DCHECK(base + lane < lend && (!hit || r < nh));
         uint4* dst = live_masks + 2 * (base + lane);
         dst[0] = m0;
         dst[1] = m1;
@@ -1300,6 +1304,7 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
                                   reinterpret_cast<const float*>(sW4)[4 * (v & 63) + z]);
     const int64_t lin = (int64_t)(bg.x0 + x) +
                         (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
+    GSV_DCHECK(lin >= 0 && lin < (int64_t)g.nx * g.ny * g.nz);
     const bool cov = (double)sw.y >= eps_w;
     const float iv = cov ? __fdiv_rn(sw.x, sw.y) : 0.f;
     S[lin] = sw.x;
@@ -1969,6 +1974,8 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
         if (ARITH) {
           // x + 8 y + 64 z
           const int vi = ARITH == 2 ? wb + (bit >> 2) + ((bit & 3) << 6) : wb + bit;
+          GSV_DCHECK(vi >= 0 && vi < 256 && (vi & 7) < bg.ex && ((vi >> 3) & 7) < bg.ey &&
+                     (vi >> 6) < bg.ez);
           v_ab = sab[vi];
           fx = (float)(vi & 7);
           fy = (float)((vi >> 3) & 7);

@@ -693,6 +693,7 @@ tail_tma_kernel(const float* __restrict__ partials, const int64_t* __restrict__ 
         __syncthreads();
       }
       const int64_t a0 = max(my0, c0), a1 = min(my1, c0 + np);
+      GSV_DCHECK(np >= 0 && np <= kTmaChunk && (a0 >= a1 || (a0 >= c0 && a1 <= c0 + np)));
       for (int64_t e = a0; e < a1; ++e) {
         const float4* pp = buf + 3 * (e - c0);
         const float4 x = pp[0], y = pp[1], z = pp[2];
