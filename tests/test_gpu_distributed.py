@@ -123,3 +123,72 @@ def test_sharded_graph_step_with_captured_nccl_all_reduce(cfg_id):
         for k in F:
             np.testing.assert_allclose(r[k], getattr(f1, k).cpu().numpy(), rtol=0, atol=2e-6,
                                        err_msg=k)
+
+
+# --------------------------------------------- owner-computes + halo exchange
+def _run_halo(rank, world, port, cfg_id, out_dir, margin, check_margin):
+    from paper_2603_09621_b200.distributed import pair_weights, slab_ranges, brick_count
+    from paper_2603_09621_b200.halo import HaloTrainStep
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    torch.cuda.set_device(0)
+    p = make_problem(CONFIGS[cfg_id])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    st = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    w = pair_weights(f, lr.grid)
+    slabs = slab_ranges(brick_count(lr.grid, (8, 8, 4)), world, weights=w)
+    step = HaloTrainStep(lr, slabs, rank, dist.group.WORLD, margin=margin,
+                         check_margin=check_margin)
+    step.attach(f, st)
+    n_local = step.plan.n_local
+    losses = [step.step(lrs) for _ in range(STEPS)]
+    fg, sg = step.gather()
+    if rank == 0:
+        np.savez(os.path.join(out_dir, "r0.npz"), losses=np.array(losses), t=sg.t,
+                 n_local=n_local, n=f.count, replans=step.replans,
+                 **{k: getattr(fg, k).detach().cpu().numpy() for k in F},
+                 **{"m_" + k: sg.m[k].cpu().numpy() for k in F})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _single_eager(cfg_id):
+    p = make_problem(CONFIGS[cfg_id])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    st = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    losses = []
+    for _ in range(STEPS):
+        out = step.forward(f)
+        losses.append(out.loss())
+        step.update(f, out, st, lrs)
+    return f, st, losses
+
+
+@pytest.mark.parametrize("cfg_id,world,margin,check", [(1, 2, 1.0, 1e-3), (2, 3, 1.0, 1e-3),
+                                                       (1, 2, 0.0, 0.5)])
+def test_halo_step_matches_single_gpu(cfg_id, world, margin, check):
+    """Owner-computes + halo exchange (halo.py): each rank holds ~1/world of
+    the Gaussians plus a halo, exchanges only halo rows, runs Adam on the
+    Gaussians it owns.  Same losses and parameters as the single-GPU step up
+    to the f64 association of the halo partial sums; a check margin above
+    the plan's forces the re-plan path after every step."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_run_halo, args=(world, _free_port(), cfg_id, d, margin, check),
+                 nprocs=world, join=True)
+        r = np.load(os.path.join(d, "r0.npz"))
+        f1, s1, l1 = _single_eager(cfg_id)
+        assert int(r["t"]) == STEPS
+        assert int(r["n_local"]) < int(r["n"])              # a rank holds a part only
+        np.testing.assert_allclose(r["losses"], l1, rtol=1e-12)
+        for k in F:
+            np.testing.assert_allclose(r[k], getattr(f1, k).cpu().numpy(), rtol=0, atol=1e-9,
+                                       err_msg=k)
+            np.testing.assert_allclose(r["m_" + k], s1.m[k].cpu().numpy(), rtol=0,
+                                       atol=1e-9, err_msg=k)
+        if check > margin:
+            assert int(r["replans"]) >= 2                    # re-planned after a step
