@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-count", action="store_true", help="skip the CUPTI launch count "
                     "(needed under ncu)")
+    ap.add_argument("--shard", default="halo", choices=["halo", "allreduce"],
+                    help="N > 1: owner-computes + halo exchange (halo.py) or the "
+                         "replicated step with one all_reduce (TrainStep + group)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path with ranks sharing a GPU")
     return ap.parse_args()
@@ -324,7 +327,8 @@ def _config_dict(args, p, ws):
             "lr_dims": list(p["lr_grid"].dims), "hr_dims": list(p["hr_grid"].dims),
             "N": int(p["field"][0].shape[0]), "brick_dims": [8, 8, 4],
             "loss": "l1", "optimizer": "Adam (f64 master)",
-            "parallelism": f"brick-range slabs x{ws} (pair-balanced)",
+            "parallelism": f"brick-range slabs x{ws} (pair-balanced)" + (
+                "" if ws == 1 else f", {args.shard} exchange"),
             "l2": "inputs larger than L2 (f64 field + Adam moments = 0.7 GB, pairs 0.1 GB)"}
 
 
@@ -377,6 +381,35 @@ def run_ours(args, dist, ws, rank, local):
     def train_launch():
         return step.step_async(f, state, lrs)
 
+    set_target = step.set_target
+    halo = None
+    if ws > 1 and args.shard == "halo":
+        # owner-computes + halo exchange: each rank steps its compact local
+        # field; the replicated `f` stays at its initial values (it serves the
+        # renders and the roofline census below)
+        from paper_2603_09621_b200.distributed import brick_count, slab_ranges
+        from paper_2603_09621_b200.halo import HaloTrainStep
+        slabs = slab_ranges(brick_count(lr_grid, bd), ws,
+                            weights=pair_weights(f, lr_grid, opts, bd))
+        halo = HaloTrainStep(lr, slabs, rank, group, opts, bd, "l1")
+        halo.attach(f, gs.AdamState.create(f))
+
+        class _Done:
+            def __init__(self, v):
+                self.v = v
+
+            def loss(self):
+                return self.v
+
+        def train_launch():                      # noqa: F811 -- the halo step
+            return _Done(halo.step(lrs))
+
+        def eager_iter():                        # noqa: F811
+            halo.step(lrs)
+            return None
+
+        set_target = halo.inner.set_target
+
     def barrier():
         if dist:
             dist.barrier()
@@ -400,6 +433,9 @@ def run_ours(args, dist, ws, rank, local):
         out = eager_iter()
     barrier()
     phases = timer.summary()
+    if halo is not None:
+        out = step.forward(f)                    # the slab index for the census below
+        phases = {"halo_step": (0, float("nan"))}
     pairs = out.idx.pair_count
     step.timer = None
     # ---------------- train: warmup, then exactly K timed steps
@@ -435,7 +471,7 @@ def run_ours(args, dist, ws, rank, local):
 
         def e2e_launch():
             cur.wait_event(ready)
-            step.set_target(staging)
+            set_target(staging)
             freed.record(cur)
             prefetch()                         # next step's input, overlapped
             return step.step_async(f, state, lrs)

@@ -65,7 +65,27 @@ def time_rank(lr, f_local, slab, reps=5):
         if i >= 2:
             res["slab"].append(a.elapsed_time(b))
             res["tail"].append(c.elapsed_time(d))
-    return {k: sum(v) / len(v) for k, v in res.items()}
+    out = {k: sum(v) / len(v) for k, v in res.items()}
+    # the same rank work as one CUDA-graph replay (bin + forward + masked
+    # backward + merge/chain/Adam tail over the local rows): the per-rank
+    # compute floor without host launch overhead
+    g = gs.TrainStep(lr, opts, (8, 8, 4), "l1", slab=slab)
+    fg = f_local.copy()
+    sg = gs.AdamState.create(fg)
+    for _ in range(3):
+        g.step(fg, sg, lrs)
+    a, b = _events()
+    torch.cuda.synchronize()
+    a.record()
+    h = g.step_async(fg, sg, lrs)
+    for i in range(10):
+        nxt = g.step_async(fg, sg, lrs) if i + 1 < 10 else None
+        h.loss()
+        h = nxt
+    b.record()
+    torch.cuda.synchronize()
+    out["graph_step"] = a.elapsed_time(b) / 10
+    return out
 
 
 def main():
@@ -103,12 +123,12 @@ def main():
         out["ranks"][k] = {
             "slabs": len(slabs), "rank": r, "n_local": plan.n_local,
             "owned": int(plan.owned.sum()), "halo_rows_out": rows_out,
-            "halo": {"compute_ms": halo_t["slab"] + halo_t["tail"], **halo_t,
+            "halo": {"eager_compute_ms": halo_t["slab"] + halo_t["tail"], **halo_t,
                      "a2a_ms_model": a2a_ms,
-                     "step_ms_model": halo_t["slab"] + halo_t["tail"] + a2a_ms},
-            "allreduce": {"compute_ms": full_t["slab"] + full_t["tail"], **full_t,
+                     "step_ms_model": halo_t["graph_step"] + a2a_ms},
+            "allreduce": {"eager_compute_ms": full_t["slab"] + full_t["tail"], **full_t,
                           "allreduce_ms_model": ar_ms,
-                          "step_ms_model": full_t["slab"] + full_t["tail"] + ar_ms}}
+                          "step_ms_model": full_t["graph_step"] + ar_ms}}
         print(k, json.dumps(out["ranks"][k]), flush=True)
     print(json.dumps(out))
 
