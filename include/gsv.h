@@ -40,7 +40,9 @@ extern "C" {
  * carries a brick-id range [b0, b1) instead of whole z-layers [bz0, bz1),
  * and the box record's 4th word holds k0 (see gsv_preprocess); 4 -- live
  * masks are pair-major (P x 4 uint2, see gsv_forward); 5 -- gsv_forward takes
- * the fused loss's target as float32 or float64 (target_dtype). */
+ * the fused loss's target as float32 or float64 (target_dtype), vpl 16 (the
+ * grouped-column forward, its column-nibble masks = gsv_backward mask_vpl
+ * 16), and the device setup entry points (resample, init). */
 #define GSV_ABI_VERSION 5
 
 typedef enum {
@@ -386,6 +388,40 @@ int gsv_render_naive(const double* positions, const double* log_scales,
                      const double* raw_relax, int64_t n, int relax_enabled,
                      const gsv_grid* grid, double cutoff_sigma, double eps_w,
                      int precision, void* I, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Setup of a fit on the device.
+ *
+ * gsv_resample_trilinear: resample_trilinear (volume.py:126-154): samples
+ * src (float32 or float64, x-fastest) at the voxel centres of dst_grid with
+ * clamp-to-edge, f64 accumulation in the reference's operation order, the
+ * result in the source dtype -- bit-identical to the reference.
+ *
+ * init_from_volume (field.py:212-234) in three calls:
+ *   gsv_init_workspace(grid, &bytes)          CUB scratch size;
+ *   gsv_init_count(data, f64, grid, thr, slot, ws, bytes, stream)
+ *       slot (V+1, int64, device): exclusive scan of the mask data >= thr in
+ *       numpy argwhere order (C order over [ix, iy, iz]); slot[V] = N (read
+ *       it to size the field);
+ *   gsv_init_fill(data, f64, grid, thr, slot, log_scales3 (host, 3 doubles:
+ *       log(scale_factor * spacing) as numpy computes it), raw_relax
+ *       (logit(relax_init)), positions (N,3), log_scales (N,3),
+ *       rotations (N,4), raw_amplitude (N), raw_relax_out (N), stream).
+ * positions, log_scales, rotations and raw_relax are bit-identical to the
+ * reference; raw_amplitude = logit(clip(I, 1e-4, 1 - 1e-4)) is within a few
+ * ulp (device log/log1p in xsf's formula; scipy uses glibc's).
+ * ------------------------------------------------------------------------ */
+int gsv_resample_trilinear(const void* src, int src_f64, const gsv_grid* src_grid,
+                           void* out, const gsv_grid* dst_grid, void* stream);
+int gsv_init_workspace(const gsv_grid* grid, size_t* bytes);
+int gsv_init_count(const void* data, int data_f64, const gsv_grid* grid,
+                   double threshold, int64_t* slot, void* workspace,
+                   size_t workspace_bytes, void* stream);
+int gsv_init_fill(const void* data, int data_f64, const gsv_grid* grid,
+                  double threshold, const int64_t* slot, const double* log_scales3,
+                  double raw_relax, double* positions, double* log_scales,
+                  double* rotations, double* raw_amplitude, double* raw_relax_out,
+                  void* stream);
 
 #ifdef __cplusplus
 }

@@ -98,6 +98,11 @@ _SIGS = {
                    c_vp, c_vp],
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
+    "gsv_resample_trilinear": [c_vp, c_int, GP, c_vp, GP, c_vp],
+    "gsv_init_workspace": [GP, c_szp],
+    "gsv_init_count": [c_vp, c_int, GP, c_dbl, c_vp, c_vp, ctypes.c_size_t, c_vp],
+    "gsv_init_fill": [c_vp, c_int, GP, c_dbl, c_vp, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
+                      c_vp],
     # include/gsv_diag.h (measurement only)
     "gsv_diag_count_live": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl, c_vp, c_vp],
     "gsv_diag_fma_probe": [c_int, c_int, c_vp, c_vp],

@@ -28,7 +28,7 @@ COMMON += os.environ.get("GSV_NVCC_EXTRA", "").split()
 # FMA (bit-exact bounds vs numpy, SURVEY.md §0 finding 1).
 EXTRA = {"gsv_bin.cu": ["-fmad=false"]}
 SOURCES = ["gsv_capi.cu", "gsv_bin.cu", "gsv_render.cu", "gsv_train.cu", "gsv_metrics.cu",
-           "gsv_util.cu", "gsv_diag.cu"]
+           "gsv_util.cu", "gsv_diag.cu", "gsv_setup.cu"]
 
 
 def _headers():

@@ -183,7 +183,21 @@ def resample_trilinear_np(src_data: np.ndarray, src: GridSpec, target: GridSpec)
 
 
 def resample_trilinear(v: Volume, target: GridSpec) -> Volume:
-    return Volume(target, resample_trilinear_np(v.numpy(), v.grid, target))
+    """resample_trilinear (volume.py:126-154).  On a CUDA volume this runs
+    gsv_resample_trilinear (bit-identical to the reference: same f64
+    operation order, result in the source dtype); a host volume takes the
+    numpy restatement."""
+    if v.device.type != "cuda":
+        return Volume(target, resample_trilinear_np(v.numpy(), v.grid, target))
+    from . import _lib
+    lib = _lib.lib()
+    src = v.linear().contiguous()
+    out = torch.empty(target.num_voxels, dtype=src.dtype, device=src.device)
+    _lib.check(lib.gsv_resample_trilinear(src.data_ptr(), int(src.dtype == torch.float64),
+                                          _lib.make_grid(v.grid), out.data_ptr(),
+                                          _lib.make_grid(target), _lib.stream_ptr()),
+               "resample_trilinear")
+    return Volume.from_linear(target, out)
 
 
 def normalize_intensity(v: Volume) -> Volume:
