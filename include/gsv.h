@@ -411,6 +411,18 @@ int gsv_render_naive(const double* positions, const double* log_scales,
  * reference; raw_amplitude = logit(clip(I, 1e-4, 1 - 1e-4)) is within a few
  * ulp (device log/log1p in xsf's formula; scipy uses glibc's).
  * ------------------------------------------------------------------------ */
+/* LR-consistency loss (the north_star's HR-render-then-downsample training
+ * mode; no reference counterpart, not part of the parity claims): the LR
+ * prediction is the mean of each LR voxel's fx*fy*fz HR voxels of an HR
+ * render I (HR dims = LR dims x factors, HR voxels nested in LR voxels);
+ * per LR voxel the L1/L2 loss of optimize.py:91-103 against target (float32
+ * or float64); dL/dI_HR = dL/dI_LR / (fx fy fz), written as the backward's
+ * ab (HR, float2 {dL/dI / W, I}); loss_part: gsv_pool_loss_blocks(lr_grid)
+ * doubles (sum them with gsv_sum). */
+int gsv_pool_loss_blocks(const gsv_grid* lr_grid);
+int gsv_pool_loss(const float* I, const float* W, const void* target, int target_dtype,
+                  const gsv_grid* hr_grid, const gsv_grid* lr_grid, int fx, int fy, int fz,
+                  int loss_kind, double eps_w, float* ab, double* loss_part, void* stream);
 int gsv_resample_trilinear(const void* src, int src_f64, const gsv_grid* src_grid,
                            void* out, const gsv_grid* dst_grid, void* stream);
 int gsv_init_workspace(const gsv_grid* grid, size_t* bytes);

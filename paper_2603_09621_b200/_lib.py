@@ -99,6 +99,9 @@ _SIGS = {
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
     "gsv_resample_trilinear": [c_vp, c_int, GP, c_vp, GP, c_vp],
+    "gsv_pool_loss_blocks": [GP],
+    "gsv_pool_loss": [c_vp, c_vp, c_vp, c_int, GP, GP, c_int, c_int, c_int, c_int, c_dbl, c_vp,
+                      c_vp, c_vp],
     "gsv_init_workspace": [GP, c_szp],
     "gsv_init_count": [c_vp, c_int, GP, c_dbl, c_vp, c_vp, ctypes.c_size_t, c_vp],
     "gsv_init_fill": [c_vp, c_int, GP, c_dbl, c_vp, c_vp, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,

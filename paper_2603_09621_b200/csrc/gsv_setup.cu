@@ -125,6 +125,66 @@ init_fill_kernel(InitMask m, const int64_t* __restrict__ slot, gsv_grid g, doubl
   rr[i] = raw_relax;
 }
 
+// LR-consistency loss (north_star (c); no reference counterpart): the LR
+// prediction is the mean of each LR voxel's fx*fy*fz HR voxels of the HR
+// render; loss and dL/dI per LR voxel as loss_and_grad (optimize.py:91-103);
+// dL/dI_HR = dL/dI_LR / (fx fy fz) for each HR voxel of the block, written
+// as the backward's {alpha = dL/dI / W, I}.  One thread per LR voxel; the
+// mean is summed in x-fastest order in f64; per-CTA loss partials (fixed
+// tree) for a deterministic total.
+constexpr int kPoolThreads = 256;
+__global__ void __launch_bounds__(kPoolThreads)
+pool_loss_kernel(const float* __restrict__ I, const float* __restrict__ W,
+                 const void* __restrict__ target, int target_f64, gsv_grid hr, gsv_grid lr,
+                 int fx, int fy, int fz, int kind, double eps_w, float2* __restrict__ ab,
+                 double* __restrict__ part) {
+  __shared__ double sh[kPoolThreads / 32];
+  const int64_t nl = (int64_t)lr.nx * lr.ny * lr.nz;
+  const int64_t v = blockIdx.x * (int64_t)kPoolThreads + threadIdx.x;
+  double acc = 0.0;
+  if (v < nl) {
+    const int x = (int)(v % lr.nx), y = (int)((v / lr.nx) % lr.ny),
+              z = (int)(v / ((int64_t)lr.nx * lr.ny));
+    const double inv_n = 1.0 / (double)(fx * fy * fz);
+    double sum = 0.0;
+    for (int c = 0; c < fz; ++c)
+      for (int b = 0; b < fy; ++b)
+        for (int a = 0; a < fx; ++a) {
+          const int64_t h = (int64_t)(x * fx + a) +
+                            (int64_t)hr.nx * ((y * fy + b) + (int64_t)hr.ny * (z * fz + c));
+          sum += (double)I[h];
+        }
+    const double d = sum * inv_n - load_vox(target, target_f64, v);
+    double dl;
+    if (kind == 0) {
+      acc = fabs(d);
+      dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / (double)nl;
+    } else {
+      acc = d * d;
+      dl = 2.0 * d / (double)nl;
+    }
+    const double dh = dl * inv_n;
+    for (int c = 0; c < fz; ++c)
+      for (int b = 0; b < fy; ++b)
+        for (int a = 0; a < fx; ++a) {
+          const int64_t h = (int64_t)(x * fx + a) +
+                            (int64_t)hr.nx * ((y * fy + b) + (int64_t)hr.ny * (z * fz + c));
+          const double w = (double)W[h];
+          const float alpha = (w >= eps_w && dh != 0.0) ? (float)(dh / w) : 0.f;
+          ab[h] = make_float2(alpha, I[h]);
+        }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kPoolThreads / 32; ++w) t += sh[w];
+    part[blockIdx.x] = t;
+  }
+}
+
 }  // namespace
 }  // namespace gsv
 
@@ -143,6 +203,28 @@ int gsv_resample_trilinear(const void* src, int src_f64, const gsv_grid* src_gri
   resample_kernel<<<(unsigned)((nv + 255) / 256), 256, 0, as_stream(stream)>>>(
       src, src_f64, *src_grid, out, *dst_grid);
   GSV_CHECK_LAUNCH("resample_kernel");
+  return GSV_OK;
+}
+
+int gsv_pool_loss_blocks(const gsv_grid* lr_grid) {
+  const int64_t nl = (int64_t)lr_grid->nx * lr_grid->ny * lr_grid->nz;
+  return (int)((nl + kPoolThreads - 1) / kPoolThreads);
+}
+
+int gsv_pool_loss(const float* I, const float* W, const void* target, int target_dtype,
+                  const gsv_grid* hr_grid, const gsv_grid* lr_grid, int fx, int fy, int fz,
+                  int loss_kind, double eps_w, float* ab, double* loss_part, void* stream) {
+  GSV_REQUIRE(hr_grid && lr_grid, "grids required");
+  GSV_REQUIRE(fx >= 1 && fy >= 1 && fz >= 1, "factors must be >= 1");
+  GSV_REQUIRE(hr_grid->nx == lr_grid->nx * fx && hr_grid->ny == lr_grid->ny * fy &&
+                  hr_grid->nz == lr_grid->nz * fz,
+              "HR dims must be the LR dims times the factors");
+  GSV_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (l1) or 1 (l2)");
+  GSV_REQUIRE(target_dtype == 0 || target_dtype == 1, "target_dtype must be 0 or 1");
+  pool_loss_kernel<<<(unsigned)gsv_pool_loss_blocks(lr_grid), kPoolThreads, 0,
+                     as_stream(stream)>>>(I, W, target, target_dtype, *hr_grid, *lr_grid, fx, fy,
+                                          fz, loss_kind, eps_w, (float2*)ab, loss_part);
+  GSV_CHECK_LAUNCH("pool_loss_kernel");
   return GSV_OK;
 }
 
