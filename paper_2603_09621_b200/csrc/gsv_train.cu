@@ -56,7 +56,15 @@ __device__ __forceinline__ void rotation_jacobians(const double* q, double J[4][
 // (raster.py:524-549): G = sym(G6); d ls_k = -2 e^{-2 ls_k} (R^T G R)_kk;
 // d q_j = 2 tr(G dR_j D R^T); sigmoid chains.  out[12] in field order:
 // positions(3), log_scales(3), rotations(4), raw_amplitude, raw_relax.
-__device__ __forceinline__ void chain_one(const double* s, const double* ls, const double* q,
+#ifndef GSV_CHAIN_NOINLINE
+#define GSV_CHAIN_NOINLINE 0
+#endif
+#if GSV_CHAIN_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void chain_one(const double* s, const double* ls, const double* q,
                                           double ra, double rr, int relax_enabled,
                                           double out[12]) {
   double G[9];
@@ -134,7 +142,15 @@ chain_kernel(const double* __restrict__ gsum, const double* __restrict__ ls,
 // Adam on one element, numpy operand order of step_optimizer
 // (optimize.py:141-147): m*b1 + (1-b1) g; v*b2 + ((1-b2) g) g;
 // p -= (lr (m/bc1)) / (sqrt(v/bc2) + eps).
-__device__ __forceinline__ double adam_one(double p, double& m, double& v, double g, double lr,
+#ifndef GSV_ADAM_NOINLINE
+#define GSV_ADAM_NOINLINE 1     // one out-of-line Adam body: less code, update 0.376 -> 0.363 ms
+#endif
+#if GSV_ADAM_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+double adam_one(double p, double& m, double& v, double g, double lr,
                                            double b1, double b2, double eps, double bc1,
                                            double bc2) {
   m = add(mul(m, b1), mul(sub(1.0, b1), g));
