@@ -27,6 +27,13 @@ namespace gsv {
 namespace {
 
 constexpr int kBwdThreads = 256;
+#ifndef GSV_BWDM_THREADS
+#define GSV_BWDM_THREADS 256     // masked backward CTA size (measurement builds may change it)
+#endif
+#ifndef GSV_BWDM_WARPS
+#define GSV_BWDM_WARPS 24        // warps per SM it is built for
+#endif
+constexpr int kBwdMThreads = GSV_BWDM_THREADS;
 constexpr int kBwdSmemVoxels = 2048; // brick voxels staged in smem by the backward
 // f32 truncation guard band.  Each v component is u + x e_x + y e_y + z e_z
 // with |terms| <= umax, so |dv| <= ~8 ulp(umax) ~ 4.8e-7 umax (f32 rounding of
@@ -1798,7 +1805,7 @@ constexpr int kBwdMChunk = 2048;
 // wi = 4 w + z, bit b -> brick voxel index b + 32 w + 64 z.  ARITH 2: the
 // column-packed forward's masks, word y, bit 4 x + z -> x + 8 y + 64 z.
 template <int ARITH>
-__global__ void __launch_bounds__(kBwdThreads, 3)
+__global__ void __launch_bounds__(kBwdMThreads, GSV_BWDM_WARPS * 32 / kBwdMThreads)
 backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restrict__ rec,
                    const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                    const int64_t* __restrict__ gstart, const int32_t* __restrict__ box,
@@ -1806,8 +1813,8 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
                    int mvpl, const float2* __restrict__ ab, float4* __restrict__ partials) {
   __shared__ float2 sab[256];                 // brick voxels (units <= 128)
   __shared__ float4 slut[256];                // (word << 5) | bit -> (x, y, z, sab index)
-  __shared__ unsigned swords[kBwdThreads / 32][9][32];   // per lane: its pair's non-empty
-  __shared__ unsigned short swbase[kBwdThreads / 32][9][32];  // mask words, LUT bases
+  __shared__ unsigned swords[kBwdMThreads / 32][9][32];   // per lane: its pair's non-empty
+  __shared__ unsigned short swbase[kBwdMThreads / 32][9][32];  // mask words, LUT bases
   __shared__ int sgid[kBwdMChunk];
   __shared__ unsigned short sorder[kBwdMChunk];
   __shared__ unsigned short scost[kBwdMChunk];
@@ -1835,7 +1842,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
     a2 = make_uint2(m23.x, m23.y);
     a3 = make_uint2(m23.z, m23.w);
   };
-  for (int e = tid; e < (ARITH ? 0 : 256); e += kBwdThreads) {   // (word, bit) LUT
+  for (int e = tid; e < (ARITH ? 0 : 256); e += kBwdMThreads) {   // (word, bit) LUT
     const int wi = e >> 5, u = ((wi >> wsh) << 5) + (e & 31);
     float4 v = make_float4(0.f, 0.f, 0.f, __int_as_float(0));
     if (u < units) {
@@ -1852,7 +1859,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
   }
   {
     const int nv = bg.ex * bg.ey * bg.ez;
-    for (int v = tid; v < nv; v += kBwdThreads) {
+    for (int v = tid; v < nv; v += kBwdMThreads) {
       const int x = v % bg.ex, y = (v / bg.ex) % bg.ey, z = v / (bg.ex * bg.ey);
       const int64_t lin =
           (int64_t)(bg.x0 + x) + (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
@@ -1865,7 +1872,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
     __syncthreads();
     // (1) cost = live voxels of the pair; 4 pairs' loads in flight per thread
 #pragma unroll 4
-    for (int t = tid; t < cnt; t += kBwdThreads) {
+    for (int t = tid; t < cnt; t += kBwdMThreads) {
       const int64_t jt = cbase + t;
       uint2 a0, a1, a2, a3;
       load_masks(jt, a0, a1, a2, a3);
@@ -1893,7 +1900,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       for (int i = 0; i < 4; ++i) { shist[4 * tid + i] = run; run += v[i]; }
     }
     __syncthreads();
-    for (int t = tid; t < cnt; t += kBwdThreads) {
+    for (int t = tid; t < cnt; t += kBwdMThreads) {
       const int slot = atomicAdd(&shist[kBwdBuckets - 1 - min((int)scost[t], kBwdBuckets - 1)], 1);
       sorder[slot] = (unsigned short)t;
     }
@@ -1902,7 +1909,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
     // groups of 32 pairs of similar cost (heaviest first), dealt round-robin
     // to the warps: balanced without a work queue
     const int ngroups = (cnt + 31) >> 5;
-    for (int grp = tid >> 5; grp < ngroups; grp += kBwdThreads / 32) {
+    for (int grp = tid >> 5; grp < ngroups; grp += kBwdMThreads / 32) {
       const int s = (grp << 5) + lane;
       if (s >= cnt) continue;
       const int t = sorder[s];
@@ -2322,7 +2329,7 @@ int gsv_backward(const double* positions, const double* log_scales, const double
                 "live masks need a brick that fills one CTA's warp tiles exactly "
                 "(e.g. 8x8x4)");
 #define GSV_BWDM(A)                                                                            \
-  backward32m_kernel<A><<<(unsigned)nb, kBwdThreads, 0, s>>>(                                  \
+  backward32m_kernel<A><<<(unsigned)nb, kBwdMThreads, 0, s>>>(                                  \
       positions, rec32, starts, gids, gstart, box, *grid, *bricks, (float)cut2d,               \
       (const uint2*)live_masks, mask_vpl, (const float2*)ab, (float4*)partials)
     if (mask_vpl == 16)
