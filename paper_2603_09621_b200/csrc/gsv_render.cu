@@ -20,6 +20,7 @@
 // f64 engine: the reference arithmetic in double (precision="f64").
 #include <cfloat>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gsv_common.cuh"
 
@@ -972,7 +973,7 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 // words, word y (brick row), bit 4x + z -- one shared atomic OR per lane and
 // evaluated (pair, column).
 #ifndef GSV_COLS_MINB
-#define GSV_COLS_MINB 20        // CTAs (warps) per SM the grouped kernel is built for
+#define GSV_COLS_MINB 16        // CTAs (warps) per SM the grouped kernel is built for
 #endif
 // Shared-memory accesses by 32-bit shared address: the base is formed once,
 // outside the loops (plain array indexing let ptxas rematerialise the
@@ -1135,8 +1136,11 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
     // lane gg describes group gg: first hit, size, column area, column prefix
     const int gfirst = lane < ng ? sgs[lane] : nh;
     const int gsize = lane < ng ? sgs[lane + 1] - gfirst : 0;
-    const uint32_t grect = lane < ng ? srect[gfirst] : 0u;
+    uint32_t grect = lane < ng ? srect[gfirst] : 0u;
     const int gwx = (int)((grect >> 6) & 7u) - (int)(grect & 7u) + 1;
+    // ceil(512 / wx) in bits 12-21: column k of the rectangle is row
+    // (k * magic) >> 9 exactly for k < 64, wx <= 8 (no division per chunk)
+    grect |= ((512u + (uint32_t)gwx - 1u) / (uint32_t)gwx) << 12;
     const int gwy = (int)((grect >> 9) & 7u) - (int)((grect >> 3) & 7u) + 1;
     const int garea = lane < ng ? gwx * gwy : 0;
     int incl = garea;
@@ -1163,7 +1167,7 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
       const int kk = s - __shfl_sync(kFull, gpre, myg);
       const uint32_t rc = __shfl_sync(kFull, grect, myg);
       const int wx = (int)((rc >> 6) & 7u) - (int)(rc & 7u) + 1;
-      const int dy = kk / wx;
+      const int dy = (int)(((uint32_t)kk * ((rc >> 12) & 1023u)) >> 9);
       const int x = (int)(rc & 7u) + kk - dy * wx;
       const int y = (int)((rc >> 3) & 7u) + dy;
       const float mX = (float)x - ctx, mY = (float)y - cty;
@@ -1223,23 +1227,68 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 #define GSV_COLS_UNROLL 1       // 2: two pairs per iteration (measured slower)
 #endif
 #if GSV_COLS_UNROLL == 1
-      for (int t = 0; t < kmax; ++t) {
-        const bool act0 = t < hk;
-        GSV_DCHECK(!act0 || (h0 + t >= 0 && h0 + t < nh && x >= 0 && x < bg.ex && y >= 0 &&
-                             y < bg.ey));
-        const uint32_t ja0 = sp_a + (uint32_t)(act0 ? h0 + t : h0) * (uint32_t)sizeof(Pair32);
-        float4 pc0;
-        float2 pd0;
-        float w0[Z];
-        uint32_t lm0, bm0;
-        eval(ja0, act0, pc0, pd0, w0, lm0, bm0);
-        if (__any_sync(kFull, bm0 != 0u)) band_fix(pd0, bm0, lm0);
-        accumulate(pc0.z, w0, lm0);
-        any |= lm0 != 0u;
-        if constexpr (MASKS) {
-          if (lm0) red_or_shared(smk_a + 4u * (uint32_t)(8 * (h0 + t) + y), lm0 << (4 * x));
+      // Lean form (the default): inactive lanes get infinite thresholds, the
+      // live tests drive predicated accumulation directly, the rare guard
+      // band adds its voxels in the same iteration (so per voxel the pairs
+      // stay in list order); full-depth bricks skip the owned-z tests.
+      auto walk = [&](auto fullz) {
+        for (int t = 0; t < kmax; ++t) {
+          const bool act0 = t < hk;
+          GSV_DCHECK(!act0 || (h0 + t >= 0 && h0 + t < nh && x >= 0 && x < bg.ex && y >= 0 &&
+                               y < bg.ey));
+          const uint32_t ja = sp_a + (uint32_t)(act0 ? h0 + t : h0) * (uint32_t)sizeof(Pair32);
+          const float4 pa = lds_f4(ja), pb = lds_f4(ja + 16), pc = lds_f4(ja + 32);
+          const float4 p4 = lds_f4(ja + 48);   // qlo, gid
+          float q[Z];
+          const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
+          const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
+          const float t3 = fmaf(pb.z, mZ, pa.w);
+          q[0] = fmaf(mX, t1, fmaf(mY, t2, fmaf(mZ, t3, pa.x)));
+          float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, mZ1, t3)));
+          const float d2q = 2.f * pb.z;
+#pragma unroll
+          for (int h = 1; h < Z; ++h) {
+            q[h] = q[h - 1] + dq;
+            dq += d2q;
+          }
+          const float tl = act0 ? pc.w : INFINITY, tb = act0 ? p4.x : INFINITY;
+          bool lv[Z], band = false;
+          uint32_t lm = 0u;
+#pragma unroll
+          for (int h = 0; h < Z; ++h) {
+            bool ownz = true;
+            if constexpr (!decltype(fullz)::value) ownz = h < bg.ez;
+            lv[h] = ownz && q[h] >= tl;
+            const float w = ex2_approx(q[h]);
+            if (lv[h]) {
+              aS[h] = fmaf(pc.z, w, aS[h]);
+              aW[h] += w;
+            }
+            lm |= (uint32_t)lv[h] << h;
+            band |= ownz && !lv[h] && q[h] >= tb;
+          }
+          if (__any_sync(kFull, band)) {
+            const int gidj = __float_as_int(p4.y);
+#pragma unroll
+            for (int h = 0; h < Z; ++h)
+              if (!lv[h] && q[h] >= tb && h < bg.ez &&
+                  exact_live(gidj, bg.x0 + x, bg.y0 + y, bg.z0 + h, xsrc, g, cut2d)) {
+                const float w = ex2_approx(q[h]);
+                aS[h] = fmaf(pc.z, w, aS[h]);
+                aW[h] += w;
+                lm |= 1u << h;
+              }
+          }
+          any |= lm != 0u;
+          if constexpr (MASKS) {
+            if (lm) red_or_shared(smk_a + 4u * (uint32_t)(8 * (h0 + t) + y), lm << (4 * x));
+          }
         }
-      }
+      };
+      if (bg.ez == Z)
+        walk(std::integral_constant<bool, true>());
+      else
+        walk(std::integral_constant<bool, false>());
 #else
       // two pairs per iteration (independent chains), accumulated in list order
       for (int t = 0; t < kmax; t += 2) {
