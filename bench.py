@@ -480,8 +480,8 @@ def run_ours(args, dist, ws, rank, local):
         prefetch()
         run_fit_steps(min(args.warmup, 3), e2e_launch)
         barrier()
-        # wall clock: at least 100 steps (~0.2 s) so host jitter averages out
-        k_e2e = max(args.steps, 100)
+        # wall clock: at least 300 steps (~0.6 s) so host jitter averages out
+        k_e2e = max(args.steps, 300)
         caps0 = getattr(step, "graph_captures", 0)
         t0 = time.perf_counter()
         loss = run_fit_steps(k_e2e, e2e_launch)[-1]   # loss device -> host each step
