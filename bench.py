@@ -455,29 +455,25 @@ def run_ours(args, dist, ws, rank, local):
     e2e = None
     if not args.no_e2e:
         host_t = torch.from_numpy(np.ascontiguousarray(p["lr"].ravel(order="F"))).pin_memory()
-        # input pipeline: step k+1's target is copied H2D (pinned) on a copy
-        # stream while step k runs; each step then loads it into the step's
-        # target buffer with an 8 MB device copy (stream-ordered)
-        staging = torch.empty_like(host_t, device=dev)
-        copy_s = torch.cuda.Stream(device=dev)
-        ready, freed = torch.cuda.Event(), torch.cuda.Event()
-        cur = torch.cuda.current_stream(dev)
+        if halo is None:
+            # the step's input is the pinned host target: every step copies it
+            # H2D itself, inside the replayed graph on a branch that overlaps
+            # binning (TrainStep.set_target_source)
+            step.set_target_source(host_t)
 
-        def prefetch():
-            copy_s.wait_event(freed)
-            with torch.cuda.stream(copy_s):
-                staging.copy_(host_t, non_blocking=True)
-                ready.record(copy_s)
-
-        def e2e_launch():
-            cur.wait_event(ready)
-            set_target(staging)
-            freed.record(cur)
-            prefetch()                         # next step's input, overlapped
-            return step.step_async(f, state, lrs)
-
-        freed.record(cur)
-        prefetch()
+            def e2e_launch():
+                return step.step_async(f, state, lrs)
+            h2d_note = ("pinned host target copied H2D by every step inside the replayed graph, "
+                        "on a branch overlapping binning (TrainStep.set_target_source)")
+            api = ("TrainStep.set_target_source + TrainStep.step_async/StepHandle.loss "
+                   "(fit()'s loop body: CUDA-graph replay + 16-byte loss read, one step "
+                   "queued ahead)")
+        else:
+            def e2e_launch():
+                set_target(host_t)                 # pinned H2D, stream-ordered
+                return train_launch()
+            h2d_note = "pinned host target copied H2D (stream-ordered) before each halo step"
+            api = "HaloTrainStep.step (eager, per rank) with TrainStep.set_target"
         run_fit_steps(min(args.warmup, 3), e2e_launch)
         barrier()
         # wall clock: at least 300 steps (~0.6 s) so host jitter averages out
@@ -487,14 +483,12 @@ def run_ours(args, dist, ws, rank, local):
         loss = run_fit_steps(k_e2e, e2e_launch)[-1]   # loss device -> host each step
         barrier()
         sec = max_over_ranks((time.perf_counter() - t0) / k_e2e)
+        if halo is None:
+            step.set_target_source(None)
         e2e = {"value": 1.0 / sec, "unit": "it/s", "steps": k_e2e,
                "graph_captures": getattr(step, "graph_captures", 0) - caps0,
-               "h2d_bytes_per_step": host_t.numel() * 4,
-               "d2h_bytes_per_step": 16, "api": "TrainStep.set_target + TrainStep.step_async/"
-               "StepHandle.loss (fit()'s loop body: CUDA-graph replay + 16-byte loss read, "
-               "one step queued ahead)",
-               "h2d": "pinned H2D of each step's target on a copy stream, overlapped with "
-               "the previous step (prefetch), then an 8 MB device copy into the step's buffer", "last_loss": loss}
+               "h2d_bytes_per_step": host_t.numel() * host_t.element_size(),
+               "d2h_bytes_per_step": 16, "api": api, "h2d": h2d_note, "last_loss": loss}
 
     # ---------------- render at the 256^3 HR grid (bin + forward)
     hr_renderer = gs.Renderer(hr_grid, opts, bd, slab=my_hr_slab, device=dev)

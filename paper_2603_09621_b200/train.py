@@ -132,6 +132,30 @@ class TrainStep:
             src = src.to(self.target.dtype)
         self.target.copy_(src, non_blocking=True)
 
+    def set_target_source(self, host_target) -> None:
+        """Bind a pinned host tensor (linear x-fastest, the target's dtype) as
+        the per-step input: every step then copies it H2D into the target
+        buffer itself -- inside the replayed graph, on a branch that overlaps
+        binning and joins before the forward, or first thing in an eager
+        step.  Rewrite the host tensor between steps to feed a new target; a
+        step that is in flight (step_async) may still be reading it.  None
+        unbinds."""
+        if host_target is None:
+            self._target_src = None
+            return
+        src = host_target.reshape(-1)
+        if src.device.type != "cpu" or not src.is_pinned():
+            raise ValueError("the target source must be a pinned host tensor")
+        if src.numel() != self.target.numel() or src.dtype != self.target.dtype:
+            raise ValueError(f"the target source must hold {self.target.numel()} values of "
+                             f"{self.target.dtype}")
+        self._target_src = src
+
+    def _load_target_source(self) -> None:
+        src = getattr(self, "_target_src", None)
+        if src is not None:
+            self.target.copy_(src, non_blocking=True)
+
     def _mark(self, name):
         if self.timer is not None:
             self.timer(name)
@@ -155,6 +179,7 @@ class TrainStep:
     def forward(self, f: GaussianField) -> StepOutput:
         lib = _lib.lib()
         grid, opts = self.grid, self.opts
+        self._load_target_source()
         self._mark("bin")
         idx = build_brick_index(f, grid, opts, self.brick_dims, slab=self.slab, pool=self.pool)
         aux = idx._aux
@@ -337,6 +362,7 @@ def _graph_key(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps):
             f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), int(f.amplitude_enabled),
             int(f.relax_enabled), tuple(state.m[g].data_ptr() for g in groups),
             tuple(state.v[g].data_ptr() for g in groups), self.target.data_ptr(),
+            (lambda t: None if t is None else t.data_ptr())(getattr(self, "_target_src", None)),
             tuple(float(lrs[g]) for g in groups), float(beta1), float(beta2), float(eps))
 
 
@@ -368,6 +394,17 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
     grid, opts, n = self.grid, self.opts, f.count
     gr, br = _lib.make_grid(grid), b["bricks"]
     cap = g.cap
+    # the bound host target (set_target_source): its H2D copy runs on a
+    # branch of the graph that overlaps binning and joins before the forward
+    src = getattr(self, "_target_src", None)
+    join = None
+    if src is not None:
+        cur = torch.cuda.current_stream()
+        side = b.setdefault("h2d_stream", torch.cuda.Stream(device=self.target.device))
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            self.target.copy_(src, non_blocking=True)
+        join = side
     # rec32 / counts / box for this step were written by the previous replay's
     # tail (or by _graph_preprocess): binning starts at the scan
     ws = b["ws"]
@@ -380,6 +417,8 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         b["starts"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(), ws.data_ptr(),
         ws.numel(), s), "bin_fill_capacity")
     nvox = grid.num_voxels
+    if join is not None:
+        torch.cuda.current_stream().wait_stream(join)
     _lib.check(lib.gsv_forward(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,

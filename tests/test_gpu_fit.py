@@ -542,3 +542,36 @@ def test_grouped_forward_matches_whole_brick_kernel(case, monkeypatch):
         assert d <= 2e-6 * max(1.0, a[i].abs().max().item()), (i, d)
     assert (a[2] - b[2]).abs().max().item() <= 1e-6
     assert abs(a[3] - b[3]) <= 1e-6 * max(1e-3, abs(a[3]))     # sign(I - T) at I ~ T
+
+
+def test_target_source_copies_h2d_inside_each_step():
+    """TrainStep.set_target_source: every step (graph replay or eager) copies
+    the pinned host target H2D itself; rewriting the host tensor between steps
+    feeds the new target.  Same losses and field as set_target before each step."""
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    host = torch.from_numpy(np.ascontiguousarray(p["lr"].ravel(order="F"))).pin_memory()
+    rng = np.random.default_rng(1)
+    targets = [host.clone()] + [host.clone() + torch.from_numpy(
+        rng.normal(scale=0.01, size=host.numel()).astype(np.float32)) for _ in range(3)]
+    res = []
+    for mode in ("source", "set"):
+        f = gs.GaussianField(*p["field"])
+        st = gs.AdamState.create(f)
+        step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+        if mode == "source":
+            step.set_target_source(host)
+        losses = []
+        for t in targets:
+            if mode == "source":
+                torch.cuda.synchronize()          # no step in flight reads the host tensor
+                host.copy_(t)
+            else:
+                step.set_target(t.to("cuda"))
+            losses.append(step.step(f, st, lrs))
+        res.append((losses, _pack(f)))
+    assert res[0][0] == res[1][0]
+    np.testing.assert_array_equal(res[0][1], res[1][1])
+    with pytest.raises(ValueError):
+        gs.TrainStep(lr).set_target_source(torch.zeros(5))
