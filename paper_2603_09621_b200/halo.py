@@ -42,6 +42,7 @@ every Gaussian reaching a slab is in that rank's local set at every step.
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -69,21 +70,28 @@ def _slab_of(ids: torch.Tensor, b0s: torch.Tensor) -> torch.Tensor:
     return torch.searchsorted(b0s, ids, right=True) - 1
 
 
+def reach_consts(grid, brick_dims, slabs, device):
+    """The device constants reach_and_owner needs (built once: a CUDA-graph
+    capture may not create tensors from host data)."""
+    return {"dims": torch.tensor(grid.dims, dtype=torch.float64, device=device),
+            "org": torch.tensor(grid.origin, dtype=torch.float64, device=device),
+            "sp": torch.tensor(grid.spacing, dtype=torch.float64, device=device),
+            "bd": torch.tensor(brick_dims, dtype=torch.int64, device=device),
+            "bg": [-(-d // b) for d, b in zip(grid.dims, brick_dims)],
+            "b0s": torch.tensor([s[0] for s in slabs], dtype=torch.int64, device=device)}
+
+
 def reach_and_owner(positions, log_scales, rotations, grid, brick_dims, slabs,
-                    cutoff_sigma: float = 3.0, margin: float = 0.0):
+                    cutoff_sigma: float = 3.0, margin: float = 0.0, consts=None):
     """(owner, r_lo, r_hi) per Gaussian, int64 tensors on the inputs' device.
 
     The box is binning's conservative 3-sigma box (raster.py:173-198) widened
     by `margin` voxels; r_lo > r_hi when it misses the grid.  The owner's
     slab holds the brick of the centre voxel (clamped into the grid), so a
     Gaussian inside the grid is always in its owner's reach."""
-    dev = positions.device
-    dims = torch.tensor(grid.dims, dtype=torch.float64, device=dev)
-    org = torch.tensor(grid.origin, dtype=torch.float64, device=dev)
-    sp = torch.tensor(grid.spacing, dtype=torch.float64, device=dev)
-    bd = torch.tensor(brick_dims, dtype=torch.int64, device=dev)
-    bg = [-(-d // b) for d, b in zip(grid.dims, brick_dims)]
-    b0s = torch.tensor([s[0] for s in slabs], dtype=torch.int64, device=dev)
+    c = consts if consts is not None else reach_consts(grid, brick_dims, slabs,
+                                                       positions.device)
+    dims, org, sp, bd, bg, b0s = c["dims"], c["org"], c["sp"], c["bd"], c["bg"], c["b0s"]
     R = _rotation(rotations)
     var = torch.exp(2.0 * log_scales)
     sig = torch.einsum("nkm,nm->nk", R * R, var)
@@ -101,9 +109,9 @@ def reach_and_owner(positions, log_scales, rotations, grid, brick_dims, slabs,
     r_hi = _slab_of(idmax, b0s)
     r_lo = torch.where(inside, r_lo, torch.ones_like(r_lo))
     r_hi = torch.where(inside, r_hi, torch.zeros_like(r_hi))
-    c = torch.minimum(torch.clamp(torch.round((positions - org) / sp), min=0).to(torch.int64),
-                      hi_lim) // bd
-    owner = _slab_of(c[:, 0] + bg[0] * (c[:, 1] + bg[1] * c[:, 2]), b0s)
+    cv = torch.minimum(torch.clamp(torch.round((positions - org) / sp), min=0).to(torch.int64),
+                       hi_lim) // bd
+    owner = _slab_of(cv[:, 0] + bg[0] * (cv[:, 1] + bg[1] * cv[:, 2]), b0s)
     return owner, r_lo, r_hi
 
 
@@ -188,6 +196,87 @@ def _unpack_params(f: GaussianField, idx: torch.Tensor, rows: torch.Tensor) -> N
     f.raw_relax.index_copy_(0, idx, rows[:, 11].contiguous())
 
 
+class _Resolved:
+    """A finished step's handle (eager mode), like train.StepHandle."""
+
+    def __init__(self, v):
+        self.v = v
+
+    def loss(self):
+        return self.v
+
+
+# ------------------------------------------------- graph-capturable hooks
+class _HaloHooks:
+    """The halo step's exchanges as hooks of TrainStep's captured graph
+    (train._graph_body): fixed plan, fixed buffers and splits, NCCL
+    collectives -- nothing reads the host, so one replay holds a whole step."""
+
+    def __init__(self, hs: "HaloTrainStep"):
+        p, dev = hs.plan, hs.f.device
+        self.dist, self.group = hs.dist, hs.group
+        self.world = hs.world
+        self.to_owner, self.from_peer = p.to_owner, p.from_peer
+        self.n_to = [int(t.shape[0]) for t in p.to_owner]
+        self.n_from = [int(t.shape[0]) for t in p.from_peer]
+        self.cat_to = torch.cat(p.to_owner)
+        self.cat_from = torch.cat(p.from_peer)
+        z = lambda k: torch.zeros((max(k, 1), _ROWW), dtype=torch.float64, device=dev)  # noqa
+        self.part_send, self.part_recv = z(sum(self.n_to)), z(sum(self.n_from))
+        self.prm_send, self.prm_recv = z(sum(self.n_from)), z(sum(self.n_to))
+        self.red2 = torch.zeros(2, dtype=torch.float64, device=dev)
+        self.oi = torch.nonzero(p.owned).view(-1)
+        self.plan_lo, self.plan_hi = p.r_lo[self.oi], p.r_hi[self.oi]
+        self.consts = reach_consts(hs.target.grid, hs.bd, hs.slabs, dev)
+        self.grid, self.bd, self.slabs = hs.target.grid, hs.bd, hs.slabs
+        self.cut, self.check_margin = hs.opts.cutoff_sigma, hs.check_margin
+
+    def _a2a(self, recv, send, n_recv, n_send):
+        ns, nr = sum(n_send), sum(n_recv)
+        self.dist.all_to_all_single(recv[:nr].view(-1), send[:ns].view(-1),
+                                    [c * _ROWW for c in n_recv], [c * _ROWW for c in n_send],
+                                    group=self.group)
+
+    def exchange_partials(self, gsum):
+        ns = sum(self.n_to)
+        if ns:
+            torch.index_select(gsum, 0, self.cat_to, out=self.part_send[:ns])
+        self._a2a(self.part_recv, self.part_send, self.n_from, self.n_to)
+        o = 0
+        for q in range(self.world):
+            c = self.n_from[q]
+            if c:
+                gsum.index_add_(0, self.from_peer[q], self.part_recv[o:o + c])
+            o += c
+
+    def reduce_loss(self, loss_sum, overflow, gloss, govf):
+        self.red2[0:1].copy_(loss_sum[0:1])
+        self.red2[1:2].copy_(overflow[0:1].to(torch.float64))
+        self.dist.all_reduce(self.red2, group=self.group)
+        gloss.copy_(self.red2[0:1])
+        govf.copy_((self.red2[1:2] > 0).to(torch.int32))
+
+    def exchange_params(self, f):
+        ns = sum(self.n_from)
+        if ns:
+            self.prm_send[:ns].copy_(_pack_params(f, self.cat_from))
+        self._a2a(self.prm_recv, self.prm_send, self.n_to, self.n_from)
+        o = 0
+        for q in range(self.world):
+            c = self.n_to[q]
+            if c:
+                _unpack_params(f, self.to_owner[q], self.prm_recv[o:o + c])
+            o += c
+
+    def reach_check(self, f, result):
+        oi = self.oi
+        _, lo, hi = reach_and_owner(f.positions[oi], f.log_scales[oi], f.rotations[oi],
+                                    self.grid, self.bd, self.slabs, self.cut, self.check_margin,
+                                    consts=self.consts)
+        bad = (lo <= hi) & ((lo < self.plan_lo) | (hi > self.plan_hi))
+        result[1:2] += 4.0 * bad.any().to(torch.float64).view(1)
+
+
 # ------------------------------------------------------------- the step
 class HaloTrainStep:
     """fit()'s iteration sharded over ranks with owner-computes + halo
@@ -209,8 +298,12 @@ class HaloTrainStep:
         self.opts, self.bd, self.loss_kind, self.margin = opts, tuple(brick_dims), loss, margin
         # the reach check's widening: a hair above the binning's own rounding
         # (the plan's f64 torch box and the binning's numpy-order box agree
-        # to an ulp); larger values re-plan earlier (tests force re-plans)
+        # to an ulp); larger values re-plan earlier (tests force re-plans).
+        # Graph mode queues one step ahead, so it checks against half the
+        # margin: the queued step stays inside the plan.
         self.check_margin = check_margin
+        if self.graph_mode:
+            self.check_margin = max(check_margin, 0.5 * margin)
         self.replans = 0
         self.last_halo = None
 
@@ -228,18 +321,57 @@ class HaloTrainStep:
                                {k: v[g].contiguous() for k, v in state.v.items()})
         self.n_global = f.count
         self.amp_en, self.rel_en = f.amplitude_enabled, f.relax_enabled
-        self.inner = TrainStep(self.target, self.opts, self.bd, self.loss_kind,
-                               slab=self.slabs[self.rank])
+        if self.graph_mode:
+            # the whole iteration as one CUDA-graph replay: TrainStep's
+            # sharded graph with the halo exchanges as its collective hooks
+            self.inner = TrainStep(self.target, self.opts, self.bd, self.loss_kind,
+                                   slab=self.slabs[self.rank], process_group=self.group,
+                                   world_size=self.world)
+            self.inner.halo_hooks = _HaloHooks(self)
+        else:
+            self.inner = TrainStep(self.target, self.opts, self.bd, self.loss_kind,
+                                   slab=self.slabs[self.rank])
         self.replans += 1
         self.last_halo = p.halo_counts()
 
+    @property
+    def graph_mode(self) -> bool:
+        """NCCL (collectives capturable), the f32 engine, graphs not disabled."""
+        return (_backend(self.dist, self.group) == "nccl" and self.opts.precision == "f32"
+                and not os.environ.get("GSV_NO_GRAPH")
+                and not os.environ.get("GSV_NO_SHARD_GRAPH"))
+
     def _replan(self) -> None:
+        if self.graph_mode:
+            while self.inner.__dict__.get("_pending"):
+                self.inner._pending[0].loss()
         f, st = self.gather()
         self.attach(f, st)
+
+    def step_async(self, lrs: dict, beta1: float = 0.9, beta2: float = 0.999,
+                   eps: float = 1e-8):
+        """Graph mode: enqueue one replay (one step may be queued behind another,
+        as fit() runs; a flagged reach violation re-plans before the next
+        launch -- the check's half-margin hysteresis keeps the queued step
+        valid).  Eager mode: the step runs to completion."""
+        if not self.graph_mode:
+            return _Resolved(self.step(lrs, beta1, beta2, eps))
+        if self.inner.__dict__.get("_replan_needed"):
+            self._replan()
+        return self.inner.step_async(self.f, self.state, lrs, beta1, beta2, eps)
 
     # -- one iteration
     def step(self, lrs: dict, beta1: float = 0.9, beta2: float = 0.999,
              eps: float = 1e-8) -> float:
+        if self.graph_mode:
+            loss = self.step_async(lrs, beta1, beta2, eps).loss()
+            if self.inner.__dict__.get("_replan_needed"):
+                self._replan()
+            return loss
+        return self._step_eager(lrs, beta1, beta2, eps)
+
+    def _step_eager(self, lrs: dict, beta1: float = 0.9, beta2: float = 0.999,
+                    eps: float = 1e-8) -> float:
         from .raster import _pair_partials
         from .train import _adam_launch
         dist, group, p, f = self.dist, self.group, self.plan, self.f

@@ -440,7 +440,21 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         b["ab"].data_ptr(), b["masks"].data_ptr(), b["vpl"], b["partials"].data_ptr(), s),
         "backward")
     gsum = None
-    if self.sharded:
+    hooks = getattr(self, "halo_hooks", None)
+    if hooks is not None:
+        # owner-computes + halo exchange (halo.py): merge, the halo rows'
+        # partials to their owners, a 2-value all_reduce of {loss, overflow}
+        # for the gate; the parameter exchange and the reach check follow the
+        # update below
+        _lib.check(lib.gsv_merge(b["partials"].data_ptr(), b["gstart"].data_ptr(), n, 0,
+                                 b["gsum"].data_ptr(), s), "merge")
+        hooks.exchange_partials(b["gsum"])
+        hooks.reduce_loss(b["loss_sum"], b["overflow"], b["gloss"], b["govf"])
+        _lib.check(lib.gsv_step_gate(b["gloss"].data_ptr(), b["govf"].data_ptr(),
+                                     b["gate"].data_ptr(), b["result"].data_ptr(), s),
+                   "step_gate")
+        gsum = b["gsum"]
+    elif self.sharded:
         # merge this slab's pair partials per Gaussian, then the step's one
         # collective: partials + loss + overflow flag in a single all_reduce;
         # the gate then sees the global loss and any rank's overflow
@@ -471,6 +485,11 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         ctypes.byref(b["hp"]), b["bc"].data_ptr(), b["t"].data_ptr(), b["gate"].data_ptr(), gr,
         br, float(opts.cutoff_sigma), None if split_prep else b["rec32"].data_ptr(),
         b["counts"].data_ptr(), b["box"].data_ptr(), s), "fused_update_device")
+    if hooks is not None:
+        # owners' updated rows to the ranks holding them as halo (a gated step
+        # sends unchanged rows), then the reach check into the result flags
+        hooks.exchange_params(f)
+        hooks.reach_check(f, b["result"])
     if split_prep:
         # the next step's records from a separate pass over the updated field
         # (a gated step leaves the field, and so its records, unchanged)
@@ -626,6 +645,8 @@ class StepHandle:
                 p._value = _step_launch(step, p._f, p._state, p._lrs, *p._hyper).loss()
             return self._value
         loss = loss_sum / step.grid.num_voxels
+        if flags & 4:                            # a Gaussian left its planned reach
+            step._replan_needed = True           # (halo.py re-plans before the next step)
         if not flags & 2:                        # applied (finite loss)
             state.t += 1
             g.t_synced = state.t

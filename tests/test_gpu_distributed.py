@@ -192,3 +192,49 @@ def test_halo_step_matches_single_gpu(cfg_id, world, margin, check):
                                        atol=1e-9, err_msg=k)
         if check > margin:
             assert int(r["replans"]) >= 2                    # re-planned after a step
+
+
+def _run_halo_nccl(rank, world, port, cfg_id, out_dir):
+    from paper_2603_09621_b200.distributed import brick_count, pair_weights, slab_ranges
+    from paper_2603_09621_b200.halo import HaloTrainStep
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world, device_id=torch.device("cuda", 0))
+    torch.cuda.set_device(0)
+    p = make_problem(CONFIGS[cfg_id])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    st = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    slabs = slab_ranges(brick_count(lr.grid, (8, 8, 4)), world,
+                        weights=pair_weights(f, lr.grid))
+    step = HaloTrainStep(lr, slabs, rank, dist.group.WORLD)
+    step.attach(f, st)
+    assert step.graph_mode
+    h = step.step_async(lrs)
+    losses = []
+    for i in range(STEPS):                     # fit()'s loop: one step queued ahead
+        nxt = step.step_async(lrs) if i + 1 < STEPS else None
+        losses.append(h.loss())
+        h = nxt
+    captured = getattr(step.inner, "_graph", None) is not None
+    fg, sg = step.gather()
+    np.savez(os.path.join(out_dir, "r0.npz"), losses=np.array(losses), t=sg.t,
+             captured=captured, **{k: getattr(fg, k).detach().cpu().numpy() for k in F})
+    dist.destroy_process_group()
+
+
+def test_halo_step_graph_over_nccl():
+    """The halo step over NCCL is one captured CUDA graph per iteration: the
+    halo exchanges (all_to_all_single with the plan's fixed splits) and the
+    {loss, overflow} all_reduce are its collectives, the reach check writes a
+    result flag.  World size 1 here (one GPU): the exchanges are empty, so it
+    must equal the single-GPU graph step."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_run_halo_nccl, args=(1, _free_port(), 1, d), nprocs=1, join=True)
+        r = np.load(os.path.join(d, "r0.npz"))
+        f1, l1 = _single(1)
+        assert bool(r["captured"]) and int(r["t"]) == STEPS
+        np.testing.assert_allclose(r["losses"], l1, rtol=1e-12)
+        for k in F:
+            np.testing.assert_allclose(r[k], getattr(f1, k).cpu().numpy(), rtol=0, atol=1e-12,
+                                       err_msg=k)
