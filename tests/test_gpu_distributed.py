@@ -238,3 +238,32 @@ def test_halo_step_graph_over_nccl():
         for k in F:
             np.testing.assert_allclose(r[k], getattr(f1, k).cpu().numpy(), rtol=0, atol=1e-12,
                                        err_msg=k)
+
+
+def _run_empty_slab(rank, world, port, out_dir):
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world, device_id=torch.device("cuda", 0))
+    torch.cuda.set_device(0)
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    f = gs.GaussianField(*p["field"])
+    st = gs.AdamState.create(f)
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    # an empty brick range: the forward writes no loss partial at all
+    step = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1", slab=(0, 0),
+                        process_group=dist.group.WORLD, world_size=world)
+    losses = [step.step(f, st, lrs) for _ in range(2)]
+    np.savez(os.path.join(out_dir, "r0.npz"), losses=np.array(losses),
+             captured=getattr(step, "_graph", None) is not None)
+    dist.destroy_process_group()
+
+
+def test_empty_slab_graph_step_reports_zero_loss():
+    """A rank whose slab is empty (slab_ranges allows b0 == b1) contributes an
+    exact 0 to the step's loss sum in the captured graph (its loss partial
+    buffer starts zeroed; the forward writes none)."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_run_empty_slab, args=(1, _free_port(), d), nprocs=1, join=True)
+        r = np.load(os.path.join(d, "r0.npz"))
+        assert bool(r["captured"])
+        assert np.all(r["losses"] == 0.0), r["losses"]
