@@ -1176,58 +1176,7 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 #pragma unroll
       for (int h = 0; h < Z; ++h) aS[h] = aW[h] = 0.f;
       bool any = false;
-      // Evaluate pair j at this lane's column: live nibble (f32 test), the
-      // guard-band nibble, and w = 2^q per voxel.
-      auto eval = [&](uint32_t ja, bool act, float4& pc, float2& pd, float* w, uint32_t& lm,
-                      uint32_t& bm) {
-        const float4 pa = lds_f4(ja), pb = lds_f4(ja + 16);
-        pc = lds_f4(ja + 32);
-        const float4 p4 = lds_f4(ja + 48);   // qlo, gid
-        pd = make_float2(p4.x, p4.y);
-        float q[Z];
-        const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
-        const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
-        const float t3 = fmaf(pb.z, mZ, pa.w);
-        q[0] = fmaf(mX, t1, fmaf(mY, t2, fmaf(mZ, t3, pa.x)));
-        float dq = fmaf(pc.y, mY, fmaf(pc.x, mX, fmaf(pb.z, mZ1, t3)));
-        const float d2q = 2.f * pb.z;
-#pragma unroll
-        for (int h = 1; h < Z; ++h) {
-          q[h] = q[h - 1] + dq;
-          dq += d2q;
-        }
-        lm = 0u;
-        bm = 0u;
-#pragma unroll
-        for (int h = 0; h < Z; ++h) {
-          const bool own = act && h < bg.ez;
-          const bool lv = own && q[h] >= pc.w;
-          w[h] = ex2_approx(q[h]);
-          lm |= (uint32_t)lv << h;
-          bm |= (uint32_t)(own && !lv && q[h] >= pd.x) << h;
-        }
-      };
-      auto band_fix = [&](const float2& pd, uint32_t bm, uint32_t& lm) {
-        const int gidj = __float_as_int(pd.y);
-#pragma unroll
-        for (int h = 0; h < Z; ++h)
-          if (((bm >> h) & 1u) &&
-              exact_live(gidj, bg.x0 + x, bg.y0 + y, bg.z0 + h, xsrc, g, cut2d))
-            lm |= 1u << h;
-      };
-      auto accumulate = [&](float A, const float* w, uint32_t lm) {
-#pragma unroll
-        for (int h = 0; h < Z; ++h)
-          if ((lm >> h) & 1u) {
-            aS[h] = fmaf(A, w[h], aS[h]);
-            aW[h] += w[h];
-          }
-      };
-#ifndef GSV_COLS_UNROLL
-#define GSV_COLS_UNROLL 1       // 2: two pairs per iteration (measured slower)
-#endif
-#if GSV_COLS_UNROLL == 1
-      // Lean form (the default): inactive lanes get infinite thresholds, the
+      // The pair loop: inactive lanes get infinite thresholds, the
       // live tests drive predicated accumulation directly, the rare guard
       // band adds its voxels in the same iteration (so per voxel the pairs
       // stay in list order); full-depth bricks skip the owned-z tests.
@@ -1289,31 +1238,6 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
         walk(std::integral_constant<bool, true>());
       else
         walk(std::integral_constant<bool, false>());
-#else
-      // two pairs per iteration (independent chains), accumulated in list order
-      for (int t = 0; t < kmax; t += 2) {
-        const bool act0 = t < hk, act1 = t + 1 < hk;
-        const uint32_t ja0 = sp_a + (uint32_t)(act0 ? h0 + t : h0) * (uint32_t)sizeof(Pair32);
-        const uint32_t ja1 = sp_a + (uint32_t)(act1 ? h0 + t + 1 : h0) * (uint32_t)sizeof(Pair32);
-        float4 pc0, pc1;
-        float2 pd0, pd1;
-        float w0[Z], w1[Z];
-        uint32_t lm0, lm1, bm0, bm1;
-        eval(ja0, act0, pc0, pd0, w0, lm0, bm0);
-        eval(ja1, act1, pc1, pd1, w1, lm1, bm1);
-        if (__any_sync(kFull, (bm0 | bm1) != 0u)) {
-          band_fix(pd0, bm0, lm0);
-          band_fix(pd1, bm1, lm1);
-        }
-        accumulate(pc0.z, w0, lm0);
-        accumulate(pc1.z, w1, lm1);
-        any |= (lm0 | lm1) != 0u;
-        if constexpr (MASKS) {
-          if (lm0) red_or_shared(smk_a + 4u * (uint32_t)(8 * (h0 + t) + y), lm0 << (4 * x));
-          if (lm1) red_or_shared(smk_a + 4u * (uint32_t)(8 * (h0 + t + 1) + y), lm1 << (4 * x));
-        }
-      }
-#endif
       // the groups' sums into the brick's S and W, one group after another
       const int col = x + 8 * y;
       GSV_DCHECK(!valid || (col >= 0 && col < 64 && myg >= 0 && myg < ng && kk >= 0));
