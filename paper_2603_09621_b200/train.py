@@ -35,6 +35,20 @@ from .volume import Volume
 
 LOSS_KINDS = {"l1": 0, "l2": 1}
 
+# GSV_NVTX=1 brackets every phase, capture and replay with NVTX ranges (for
+# nsys / ncu --nvtx); off by default so the replay path stays host-lean
+NVTX = os.environ.get("GSV_NVTX", "") == "1"
+
+
+def _nvtx_push(name: str) -> None:
+    if NVTX:
+        torch.cuda.nvtx.range_push(name)
+
+
+def _nvtx_pop() -> None:
+    if NVTX:
+        torch.cuda.nvtx.range_pop()
+
 
 class PhaseTimer:
     """CUDA events on the launching stream around each kernel phase.
@@ -53,9 +67,14 @@ class PhaseTimer:
         ev.record(s)
         if self._open is not None:
             self.events.append((self._open[0], self._open[1], ev))
+            _nvtx_pop()
         self._open = (name, ev) if name is not None else None
+        if name is not None:
+            _nvtx_push("gsv." + name)
 
     def reset(self):
+        if self._open is not None:
+            _nvtx_pop()
         self.events.clear()
         self._open = None
 
@@ -688,7 +707,9 @@ def _step_launch(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
         while pending:                           # captures start from committed state
             pending[0].loss()
         self._graph = None
+        _nvtx_push("gsv.step.capture")
         g = self._graph = _graph_capture(self, f, state, lrs, beta1, beta2, eps, key)
+        _nvtx_pop()
     b = g.bufs
     if not pending:
         # the field / step count were changed outside the graph
@@ -698,7 +719,9 @@ def _step_launch(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
         if g.prep_version != f.version:
             _graph_preprocess(self, f, b)
             g.prep_version = f.version
+    _nvtx_push("gsv.step.replay")
     g.graph.replay()
+    _nvtx_pop()
     slot = self.__dict__.get("_launches", 0) % _RESULT_SLOTS
     self._launches = self.__dict__.get("_launches", 0) + 1
     b["result_host"][slot].copy_(b["result"], non_blocking=True)
@@ -771,7 +794,9 @@ class Renderer:
             self._graph = None
             g = self._graph = self._capture(f, key)
         b = g.bufs
+        _nvtx_push("gsv.render.replay")
         g.graph.replay()
+        _nvtx_pop()
         b["ovf_host"].copy_(b["overflow"], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))

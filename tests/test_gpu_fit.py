@@ -575,3 +575,38 @@ def test_target_source_copies_h2d_inside_each_step():
     np.testing.assert_array_equal(res[0][1], res[1][1])
     with pytest.raises(ValueError):
         gs.TrainStep(lr).set_target_source(torch.zeros(5))
+
+
+def test_nvtx_ranges_wrap_phases_and_replays(monkeypatch):
+    """GSV_NVTX=1: phases, captures and replays are bracketed by balanced
+    NVTX ranges; the step's results do not change."""
+    import paper_2603_09621_b200.train as train_mod
+    pushed = []
+    monkeypatch.setattr(train_mod, "NVTX", True)
+    monkeypatch.setattr(torch.cuda.nvtx, "range_push", lambda n: pushed.append(n) or 0)
+    monkeypatch.setattr(torch.cuda.nvtx, "range_pop", lambda: pushed.append(None) or 0)
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
+    timer = train_mod.PhaseTimer()
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    ta = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1", timer=timer)
+    tb = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    out = ta.forward(fa)
+    ta.update(fa, out, sa, lrs)
+    la = [ta.step(fa, sa, lrs) for _ in range(2)]
+    monkeypatch.setattr(train_mod, "NVTX", False)
+    out = tb.forward(fb)
+    tb.update(fb, out, sb, lrs)
+    lb = [tb.step(fb, sb, lrs) for _ in range(2)]
+    assert la == lb
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    names = [n for n in pushed if n is not None]
+    assert {"gsv.bin", "gsv.forward", "gsv.step.capture", "gsv.step.replay"} <= set(names)
+    depth = 0
+    for n in pushed:
+        depth += 1 if n is not None else -1
+        assert depth >= 0
+    assert depth == 0
+    assert timer.summary()["forward"][0] >= 1
