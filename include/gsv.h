@@ -42,8 +42,9 @@ extern "C" {
  * masks are pair-major (P x 4 uint2, see gsv_forward); 5 -- gsv_forward takes
  * the fused loss's target as float32 or float64 (target_dtype), vpl 16 (the
  * grouped-column forward, its column-nibble masks = gsv_backward mask_vpl
- * 16), and the device setup entry points (resample, init). */
-#define GSV_ABI_VERSION 5
+ * 16), and the device setup entry points (resample, init); 6 -- adds
+ * gsv_step_advance_publish (the graph step's result into a pinned ring). */
+#define GSV_ABI_VERSION 6
 
 typedef enum {
   GSV_OK = 0,
@@ -333,6 +334,13 @@ int gsv_fused_update_device(const float* partials, const int64_t* gstart, const 
                             const gsv_bricks* bricks, double cutoff_sigma,
                             gsv_record32* rec32, int32_t* counts, int32_t* box, void* stream);
 int gsv_step_advance(int64_t* step, const int32_t* gate, void* stream);
+/* gsv_step_advance, then the step's 16-byte result straight into slot
+ * (*counter % slots) of a ring in pinned host memory (ring: 2 * slots
+ * doubles, host-allocated page-locked, device-accessible under UVA) and
+ * *counter += 1 -- the replayed graph's last node, so no separate D2H copy
+ * sits between consecutive replays. */
+int gsv_step_advance_publish(int64_t* step, const int32_t* gate, const double* result,
+                             double* ring, int64_t* counter, int slots, void* stream);
 
 /* Sharded graph step: the one all_reduce buffer red (N x 12
  * float) = the merged per-Gaussian partials gsum (gsv_merge, N x 12 double)

@@ -88,6 +88,7 @@ _SIGS = {
                                 ctypes.POINTER(GsvAdamHparams), c_vp, c_vp, c_vp, GP, BP,
                                 c_dbl, c_vp, c_vp, c_vp, c_vp],
     "gsv_step_advance": [c_vp, c_vp, c_vp],
+    "gsv_step_advance_publish": [c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp],
     "gsv_metric_blocks": [c_i64],
     "gsv_sq_diff_sum": [c_vp, c_int, c_vp, c_int, c_i64, c_vp, c_vp, c_vp],
     "gsv_ssim3d_workspace": [GP, c_szp],
@@ -113,7 +114,7 @@ _SIGS = {
 _RESTYPES = {"gsv_last_error": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)
-ABI_VERSION = 5        # GSV_ABI_VERSION of include/gsv.h these signatures follow
+ABI_VERSION = 6        # GSV_ABI_VERSION of include/gsv.h these signatures follow
 
 _lib = None
 

@@ -350,6 +350,17 @@ __global__ void advance_kernel(int64_t* __restrict__ t, const int32_t* __restric
   if (*gate == 0) *t += 1;
 }
 
+__global__ void advance_publish_kernel(int64_t* __restrict__ t, const int32_t* __restrict__ gate,
+                                       const double* __restrict__ result, double* ring,
+                                       int64_t* __restrict__ counter, int slots) {
+  if (*gate == 0) *t += 1;
+  const int64_t k = *counter;
+  double* dst = ring + 2 * (k % slots);
+  dst[0] = result[0];
+  dst[1] = result[1];
+  *counter = k + 1;
+}
+
 // Sharded graph step: the one all_reduce carries the merged partials (f32,
 // N x 12; column 11 is free), this rank's loss in [0][11] and its capacity
 // overflow flag in [1][11].
@@ -1034,6 +1045,16 @@ int gsv_step_advance(int64_t* step, const int32_t* gate, void* stream) {
   GSV_REQUIRE(step && gate, "null pointer argument");
   advance_kernel<<<1, 1, 0, as_stream(stream)>>>(step, gate);
   GSV_CHECK_LAUNCH("advance_kernel");
+  return GSV_OK;
+}
+
+int gsv_step_advance_publish(int64_t* step, const int32_t* gate, const double* result,
+                             double* ring, int64_t* counter, int slots, void* stream) {
+  GSV_REQUIRE(step && gate && result && ring && counter, "null pointer argument");
+  GSV_REQUIRE(slots >= 1, "slots must be >= 1");
+  advance_publish_kernel<<<1, 1, 0, as_stream(stream)>>>(step, gate, result, ring, counter,
+                                                         slots);
+  GSV_CHECK_LAUNCH("advance_publish_kernel");
   return GSV_OK;
 }
 

@@ -360,9 +360,10 @@ class _StepGraph:
     The graph holds the whole iteration -- preprocess, scan, capacity-mode
     binning (pair count never read by the host), forward with the fused loss
     and live masks, loss sum, gate, masked backward, the one-pass tail with
-    the step counter and bias corrections read on the device, step advance,
-    and one 16-byte D2H of {loss sum, flags} -- so a replay costs one launch
-    and one stream sync, with no per-kernel host work.
+    the step counter and bias corrections read on the device, and the step
+    advance, whose kernel also writes the 16-byte {loss sum, flags} result
+    into a pinned host ring -- so a replay costs one launch and one event
+    wait, with no per-kernel host work and no copy node between replays.
     """
 
     def __init__(self, key, cap: int, t_max: int):
@@ -373,6 +374,7 @@ class _StepGraph:
         self.prep_version = -1
         self.graph = None
         self.bufs: dict = {}
+        self.launches = 0            # replays so far (ring slot = launches % _RESULT_SLOTS)
 
 
 def _graph_key(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps):
@@ -513,7 +515,12 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         # the next step's records from a separate pass over the updated field
         # (a gated step leaves the field, and so its records, unchanged)
         _graph_preprocess(self, f, b)
-    _lib.check(lib.gsv_step_advance(b["t"].data_ptr(), b["gate"].data_ptr(), s), "step_advance")
+    # the step's result goes straight into the pinned ring (no D2H copy node
+    # between consecutive replays)
+    _lib.check(lib.gsv_step_advance_publish(
+        b["t"].data_ptr(), b["gate"].data_ptr(), b["result"].data_ptr(),
+        b["result_host"].data_ptr(), b["rcount"].data_ptr(), _RESULT_SLOTS, s),
+        "step_advance_publish")
 
 
 def _graph_preprocess(self, f: GaussianField, b: dict) -> None:
@@ -575,9 +582,10 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     b["overflow"] = gp.get("overflow", (1,), torch.int32)
     b["gate"] = gp.get("gate", (1,), torch.int32)
     b["result"] = gp.get("result", (2,), torch.float64)
-    # results leave the device outside the graph, into a ring of pinned slots,
-    # so a step in flight never overwrites the one being read
+    # results go into a ring of pinned slots (written by the graph's last
+    # kernel), so a step in flight never overwrites the one being read
     b["result_host"] = torch.zeros((_RESULT_SLOTS, 2), dtype=torch.float64).pin_memory()
+    b["rcount"] = gp.get("rcount", (1,), torch.int64)
     if self.sharded:
         b["gsum"] = gp.get("gsum", (n, 12), torch.float64)
         b["red"] = gp.get("red", (n, 12), torch.float32)
@@ -615,6 +623,8 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     g.prep_version = f.version
     b["t"].fill_(int(state.t))
     g.t_synced = state.t
+    b["rcount"].zero_()            # ring slot of replay k = k % _RESULT_SLOTS
+    g.launches = 0
     return g
 
 
@@ -722,9 +732,8 @@ def _step_launch(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
     _nvtx_push("gsv.step.replay")
     g.graph.replay()
     _nvtx_pop()
-    slot = self.__dict__.get("_launches", 0) % _RESULT_SLOTS
-    self._launches = self.__dict__.get("_launches", 0) + 1
-    b["result_host"][slot].copy_(b["result"], non_blocking=True)
+    slot = g.launches % _RESULT_SLOTS
+    g.launches += 1
     ev = torch.cuda.Event()
     ev.record(torch.cuda.current_stream(f.device))
     h = StepHandle(self, f, state, lrs, hyper, g=g, slot=slot, event=ev)
