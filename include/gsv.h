@@ -43,7 +43,8 @@ extern "C" {
  * the fused loss's target as float32 or float64 (target_dtype), vpl 16 (the
  * grouped-column forward, its column-nibble masks = gsv_backward mask_vpl
  * 16), and the device setup entry points (resample, init); 6 -- adds
- * gsv_step_advance_publish (the graph step's result into a pinned ring). */
+ * gsv_step_advance_publish (the graph step's result into a pinned ring) and
+ * incremental binning (gsv_preprocess_track, gsv_bin_incremental). */
 #define GSV_ABI_VERSION 6
 
 typedef enum {
@@ -161,6 +162,42 @@ int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box,
                           int32_t* vals_tmp, int32_t* keys_out, int32_t* gids_out,
                           int64_t* starts_out, const int32_t* dry, int32_t* overflow,
                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Incremental binning for consecutive fit() iterations (CUDA-graph
+ * capturable).  gsv_preprocess_track is gsv_preprocess (f32 records only)
+ * that also appends every Gaussian whose pair count or box record differs
+ * from the values counts / box held before the call: chg_gid[e], chg_old[4 e
+ * .. 4 e + 3] (the old box record), chg_oldcnt[e], e = atomicAdd(chg_count);
+ * entries beyond chg_cap are dropped (the count still grows).
+ * gsv_bin_incremental turns the recorded changes into per-brick edits and
+ * rebuilds the lists (starts, gids: the lists of the OLD boxes, capacity
+ * entries) for the current counts / box: starts_out (nbricks_slab + 1) and
+ * gids_out are the new lists, copied back into starts / gids for the next
+ * call; *chg_count is reset.  The result equals gsv_bin_fill for the current
+ * boxes (each list ascending in gid).  *overflow = more than chg_cap changes,
+ * more than 16384 edits, more than capacity pairs, edited lists whose pair
+ * count differs from gstart[n] (gsv_bin_scan of counts), or *dry != 0 -- then
+ * starts_out is all zero (empty lists downstream) and starts / gids are left
+ * as they were (after an excess of changes or edits *chg_count is left above
+ * chg_cap, so later calls overflow too); the caller rebuilds from scratch.
+ * Scratch: ops (16384 x uint64), nops (1 int32), lens (nbricks_slab + 1
+ * int32); workspace from gsv_bin_incremental_workspace(nbricks_slab). */
+int gsv_preprocess_track(const double* positions, const double* log_scales,
+                         const double* rotations, const double* raw_amplitude,
+                         const double* raw_relax, int64_t n, int relax_enabled,
+                         double cutoff_sigma, const gsv_grid* grid, const gsv_bricks* bricks,
+                         gsv_record32* rec32, int32_t* counts, int32_t* box,
+                         int32_t* chg_count, int32_t* chg_gid, int32_t* chg_old,
+                         int32_t* chg_oldcnt, int chg_cap, void* stream);
+int gsv_bin_incremental_workspace(int32_t nbricks, size_t* bytes);
+int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t* gstart,
+                        int64_t n, int64_t capacity,
+                        const gsv_bricks* bricks, int32_t* chg_count, const int32_t* chg_gid,
+                        const int32_t* chg_old, const int32_t* chg_oldcnt, int chg_cap,
+                        int64_t* starts, int32_t* gids, int64_t* starts_out, int32_t* gids_out,
+                        unsigned long long* ops, int32_t* nops, int32_t* lens,
+                        const int32_t* dry, int32_t* overflow, void* workspace,
+                        size_t workspace_bytes, void* stream);
 
 /* Canonical-order check and repair for caller-supplied lists
  * (BrickIndex.lists_sorted / canonicalized, raster.py:91-112).

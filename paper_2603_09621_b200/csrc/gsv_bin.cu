@@ -187,6 +187,249 @@ __global__ void unsorted_kernel(const int64_t* __restrict__ starts,
     }
 }
 
+// ------------------------------------------------- incremental binning
+// Between two fit() iterations only a few Gaussians change their brick box
+// (~100 of 2.1 M per step at config 3), so the graph step keeps last step's
+// lists and edits them: the preprocess pass records every Gaussian whose box
+// or pair count changed (PrepArgs change tracking); incr_ops_kernel turns
+// those into (brick, gid, remove | insert) edits, sorted by (brick, gid);
+// the new list lengths are scanned into new CSR starts; incr_merge_kernel
+// rebuilds each list -- a copy for the untouched bricks, an ordered merge of
+// the surviving and inserted gids for the edited ones -- into the output
+// buffers, which are then copied back as the next step's input.  The result
+// equals a full rebuild (each list is the ascending gids of the Gaussians
+// whose box run contains the brick); any capacity excess (edits, changed
+// Gaussians, pairs) raises the overflow flag and the caller rebuilds.
+constexpr int kOpsCap = 16384;      // edits per step (sorted in one CTA's shared memory)
+
+// Is slab-local brick `key` in the box run (box record, count) of a Gaussian?
+__device__ __forceinline__ bool run_contains(const GBox& gb, int cnt, int key,
+                                             const gsv_bricks& k) {
+  if (cnt <= 0) return false;
+  const int bgl = key + k.b0;
+  const int plane = k.bgx * k.bgy;
+  const int bz = bgl / plane, rem = bgl - bz * plane;
+  const int by = rem / k.bgx, bx = rem - by * k.bgx;
+  const int rx = bx - gb.blo_x, ry = by - gb.blo_y, rz = bz - gb.blo_z;
+  if (rx < 0 || rx >= gb.nb_x || ry < 0 || ry >= gb.nb_y || rz < 0 || rz >= gb.nb_z)
+    return false;
+  const int r = rx + gb.nb_x * (ry + gb.nb_y * rz) - gb.k0;
+  return r >= 0 && r < cnt;
+}
+
+template <class F>
+__device__ __forceinline__ void for_each_box_run(const GBox& b, int c, const gsv_bricks& k,
+                                                 F f) {
+  if (c <= 0) return;
+  int rx = b.k0 % b.nb_x;
+  const int t = b.k0 / b.nb_x;
+  int ry = t % b.nb_y;
+  const int bxy = k.bgx * k.bgy;
+  int key = b.blo_x + k.bgx * (b.blo_y + k.bgy * b.blo_z) - k.b0 + rx + k.bgx * ry +
+            bxy * (t / b.nb_y);
+  for (int r = 0; r < c; ++r) {
+    f(key);
+    ++key;
+    if (++rx == b.nb_x) {
+      rx = 0;
+      key += k.bgx - b.nb_x;
+      if (++ry == b.nb_y) {
+        ry = 0;
+        key += bxy - k.bgx * b.nb_y;
+      }
+    }
+  }
+}
+
+// edit key: brick << 32 | gid << 1 | insert
+__global__ void __launch_bounds__(1024)
+incr_ops_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
+                gsv_bricks k, int32_t* __restrict__ chg_count,
+                const int32_t* __restrict__ chg_gid, const int32_t* __restrict__ chg_old,
+                const int32_t* __restrict__ chg_oldcnt, int chg_cap,
+                const int32_t* __restrict__ dry, unsigned long long* __restrict__ ops,
+                int32_t* __restrict__ nops_out, int32_t* __restrict__ overflow) {
+  extern __shared__ unsigned long long sops[];   // kOpsCap entries
+  __shared__ int snops, sbad;
+  const int tid = threadIdx.x;
+  const int nc = *chg_count;
+  if (tid == 0) {
+    snops = 0;
+    sbad = (dry != nullptr && *dry != 0) ? 2 : (nc > chg_cap ? 1 : 0);
+  }
+  __syncthreads();
+  if (sbad == 0) {
+    for (int e = tid; e < nc; e += blockDim.x) {
+      const int gid = chg_gid[e];
+      const GBox ob = unpack_box(chg_old, e), nbx = unpack_box(box, gid);
+      const int oc = chg_oldcnt[e], ncnt = counts[gid];
+      auto push = [&](int key, unsigned ins) {
+        const int j = atomicAdd(&snops, 1);
+        if (j < kOpsCap)
+          sops[j] = ((unsigned long long)(unsigned)key << 32) | ((unsigned)gid << 1) | ins;
+        else
+          sbad = 1;
+      };
+      for_each_box_run(ob, oc, k, [&](int key) {
+        if (!run_contains(nbx, ncnt, key, k)) push(key, 0u);
+      });
+      for_each_box_run(nbx, ncnt, k, [&](int key) {
+        if (!run_contains(ob, oc, key, k)) push(key, 1u);
+      });
+    }
+  }
+  __syncthreads();
+  const int n = sbad ? 0 : min(snops, kOpsCap);
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int i = n + tid; i < p2; i += blockDim.x) sops[i] = ~0ull;
+  __syncthreads();
+  // bitonic sort of the n edits (padded to a power of two)
+  for (int size = 2; size <= p2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < p2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const unsigned long long a = sops[i], b = sops[j];
+          const bool up = (i & size) == 0;
+          if ((a > b) == up) {
+            sops[i] = b;
+            sops[j] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = tid; i < n; i += blockDim.x) ops[i] = sops[i];
+  if (tid == 0) {
+    *nops_out = n;
+    *overflow = sbad ? 1 : 0;
+    // consumed; after an excess the count stays above the cap, so steps
+    // already queued behind this one overflow too until the caller rebuilds
+    if (sbad == 0) *chg_count = 0;
+  }
+}
+
+// first edit index with key >= v
+__device__ __forceinline__ int ops_lower(const unsigned long long* __restrict__ ops, int n,
+                                         unsigned long long v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ops[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256)
+incr_len_kernel(const int64_t* __restrict__ starts, int32_t nb,
+                const unsigned long long* __restrict__ ops, const int32_t* __restrict__ nops,
+                int32_t* __restrict__ lens) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nb) return;
+  if (b == nb) {
+    lens[b] = 0;
+    return;
+  }
+  const int n = *nops;
+  int d = 0;
+  if (n > 0) {
+    const int p0 = ops_lower(ops, n, (unsigned long long)(unsigned)b << 32);
+    const int p1 = ops_lower(ops, n, (unsigned long long)(unsigned)(b + 1) << 32);
+    for (int p = p0; p < p1; ++p) d += (ops[p] & 1ull) ? 1 : -1;
+  }
+  lens[b] = (int32_t)(starts[b + 1] - starts[b]) + d;
+}
+
+// the edited lists must hold exactly the pairs the counts give (gstart[n])
+// and fit the capacity
+__global__ void incr_check_kernel(const int64_t* __restrict__ starts_out, int32_t nb,
+                                  const int64_t* __restrict__ gstart, int64_t n, int64_t cap,
+                                  int32_t* __restrict__ overflow) {
+  const int64_t p = starts_out[nb];
+  if (p > cap || p != gstart[n]) *overflow = 1;
+}
+
+// one warp per brick: copy, or merge the surviving and inserted gids
+__global__ void __launch_bounds__(256)
+incr_merge_kernel(const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
+                  const int64_t* __restrict__ starts_out, int32_t* __restrict__ gids_out,
+                  int32_t nb, const unsigned long long* __restrict__ ops,
+                  const int32_t* __restrict__ nops, const int32_t* __restrict__ overflow) {
+  const int b = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= nb || *overflow != 0) return;
+  const int64_t os = starts[b], oe = starts[b + 1], ns = starts_out[b];
+  const int len = (int)(oe - os);
+  const int n = *nops;
+  int p0 = 0, p1 = 0;
+  if (n > 0) {
+    p0 = ops_lower(ops, n, (unsigned long long)(unsigned)b << 32);
+    p1 = ops_lower(ops, n, (unsigned long long)(unsigned)(b + 1) << 32);
+  }
+  if (p0 == p1) {
+    for (int i = lane; i < len; i += 32) gids_out[ns + i] = gids[os + i];
+    return;
+  }
+  // surviving entries: shifted by the removals before and insertions before
+  for (int i = lane; i < len; i += 32) {
+    const int g = gids[os + i];
+    int rm_lt = 0, in_lt = 0;
+    bool removed = false;
+    for (int p = p0; p < p1; ++p) {
+      const unsigned long long o = ops[p];
+      const int og = (int)((unsigned)o >> 1);
+      const bool ins = o & 1ull;
+      if (og < g) {
+        if (ins) ++in_lt; else ++rm_lt;
+      } else if (og == g && !ins) {
+        removed = true;
+      }
+    }
+    if (!removed) gids_out[ns + i - rm_lt + in_lt] = g;
+  }
+  // inserted entries
+  for (int p = p0 + lane; p < p1; p += 32) {
+    const unsigned long long o = ops[p];
+    if (!(o & 1ull)) continue;
+    const int h = (int)((unsigned)o >> 1);
+    int lo = 0, hi = len;                      // old entries < h
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (gids[os + mid] < h) lo = mid + 1; else hi = mid;
+    }
+    int rm_lt = 0, in_lt = 0;
+    for (int q = p0; q < p1; ++q) {
+      const unsigned long long u = ops[q];
+      const int ug = (int)((unsigned)u >> 1);
+      if (ug < h) {
+        if (u & 1ull) ++in_lt; else ++rm_lt;
+      }
+    }
+    gids_out[ns + lo - rm_lt + in_lt] = h;
+  }
+}
+
+// overflow: empty lists downstream; otherwise the output becomes next step's input
+__global__ void __launch_bounds__(256)
+incr_commit_kernel(int64_t* __restrict__ starts, int32_t* __restrict__ gids,
+                   int64_t* __restrict__ starts_out, const int32_t* __restrict__ gids_out,
+                   int32_t nb, const int32_t* __restrict__ overflow) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (*overflow != 0) {
+    for (int64_t i = i0; i <= nb; i += stride) starts_out[i] = 0;
+    return;
+  }
+  for (int64_t i = i0; i <= nb; i += stride) starts[i] = starts_out[i];
+  const int64_t p = starts_out[nb];
+  const int64_t p4 = p >> 2;
+  const int4* src = reinterpret_cast<const int4*>(gids_out);
+  int4* dst = reinterpret_cast<int4*>(gids);
+  for (int64_t i = i0; i < p4; i += stride) dst[i] = src[i];
+  for (int64_t i = 4 * p4 + i0; i < p; i += stride) gids[i] = gids_out[i];
+}
+
 // Slabs of at most 65536 bricks sort 16-bit keys: a quarter less traffic
 // per radix pass (the key buffers, allocated for int32, are used at half width).
 inline bool keys16(int64_t nb) { return nb <= 65536; }
@@ -395,6 +638,91 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in, int32_t* gid
                                                      (int)pairs, nbricks, starts, starts + 1,
                                                      as_stream(stream));
   if (e != cudaSuccess) return cuda_status(e, "DeviceSegmentedSort::SortKeys");
+  return GSV_OK;
+}
+
+int gsv_preprocess_track(const double* positions, const double* log_scales,
+                         const double* rotations, const double* raw_amplitude,
+                         const double* raw_relax, int64_t n, int relax_enabled,
+                         double cutoff_sigma, const gsv_grid* grid, const gsv_bricks* bricks,
+                         gsv_record32* rec32, int32_t* counts, int32_t* box,
+                         int32_t* chg_count, int32_t* chg_gid, int32_t* chg_old,
+                         int32_t* chg_oldcnt, int chg_cap, void* stream) {
+  if (int s = validate_grid_bricks(grid, bricks)) return s;
+  GSV_REQUIRE(n >= 0, "n must be >= 0");
+  GSV_REQUIRE(cutoff_sigma > 0, "cutoff_sigma must be positive");
+  GSV_REQUIRE(chg_count && chg_gid && chg_old && chg_oldcnt && chg_cap >= 0,
+              "null change-tracking buffer");
+  GSV_REQUIRE(n == 0 || (positions && log_scales && rotations && raw_amplitude &&
+                         raw_relax && rec32 && counts && box),
+              "null pointer argument");
+  if (n == 0) return GSV_OK;
+  const int dense = isinf(cutoff_sigma) ? 1 : 0;
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  const PrepArgs pa{*grid, *bricks, cutoff_sigma, dense, relax_enabled, rec32, nullptr, counts,
+                    box, chg_count, chg_gid, chg_old, chg_oldcnt, chg_cap};
+  preprocess_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
+      positions, log_scales, rotations, raw_amplitude, raw_relax, n, pa);
+  GSV_CHECK_LAUNCH("preprocess_kernel");
+  return GSV_OK;
+}
+
+int gsv_bin_incremental_workspace(int32_t nbricks, size_t* bytes) {
+  GSV_REQUIRE(bytes != nullptr, "bytes must not be NULL");
+  size_t scan_bytes = 0;
+  thrust::transform_iterator<ToI64, const int32_t*, int64_t> it(nullptr, ToI64());
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, it, (int64_t*)nullptr,
+                                                (int)nbricks + 1);
+  if (e != cudaSuccess) return cuda_status(e, "DeviceScan sizing");
+  *bytes = scan_bytes + 256;
+  return GSV_OK;
+}
+
+int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t* gstart,
+                        int64_t n, int64_t capacity,
+                        const gsv_bricks* bricks, int32_t* chg_count, const int32_t* chg_gid,
+                        const int32_t* chg_old, const int32_t* chg_oldcnt, int chg_cap,
+                        int64_t* starts, int32_t* gids, int64_t* starts_out, int32_t* gids_out,
+                        unsigned long long* ops, int32_t* nops, int32_t* lens,
+                        const int32_t* dry, int32_t* overflow, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  GSV_REQUIRE(bricks && counts && box && gstart && chg_count && chg_gid && chg_old && chg_oldcnt &&
+                  starts && gids && starts_out && gids_out && ops && nops && lens && overflow,
+              "null pointer argument");
+  GSV_REQUIRE(capacity >= 1 && capacity < (int64_t)INT32_MAX, "capacity %lld out of range",
+              (long long)capacity);
+  cudaStream_t s = as_stream(stream);
+  const int64_t nb = slab_bricks(*bricks);
+  constexpr size_t ops_smem = sizeof(unsigned long long) * kOpsCap;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t ea = cudaFuncSetAttribute(incr_ops_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)ops_smem);
+    if (ea != cudaSuccess) return cuda_status(ea, "incr_ops_kernel smem attribute");
+    attr = true;
+  }
+  incr_ops_kernel<<<1, 1024, ops_smem, s>>>(counts, box, *bricks, chg_count, chg_gid, chg_old,
+                                            chg_oldcnt, chg_cap, dry, ops, nops, overflow);
+  GSV_CHECK_LAUNCH("incr_ops_kernel");
+  incr_len_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(starts, (int32_t)nb, ops,
+                                                                    nops, lens);
+  GSV_CHECK_LAUNCH("incr_len_kernel");
+  thrust::transform_iterator<ToI64, const int32_t*, int64_t> it(lens, ToI64());
+  size_t bytes = workspace_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(workspace, bytes, it, starts_out, (int)nb + 1, s);
+  if (e != cudaSuccess) return cuda_status(e, "DeviceScan::ExclusiveSum");
+  incr_check_kernel<<<1, 1, 0, s>>>(starts_out, (int32_t)nb, gstart, n, capacity, overflow);
+  GSV_CHECK_LAUNCH("incr_check_kernel");
+  if (nb > 0) {
+    incr_merge_kernel<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, s>>>(
+        starts, gids, starts_out, gids_out, (int32_t)nb, ops, nops, overflow);
+    GSV_CHECK_LAUNCH("incr_merge_kernel");
+  }
+  incr_commit_kernel<<<1184, 256, 0, s>>>(starts, gids, starts_out, gids_out, (int32_t)nb,
+                                          overflow);
+  GSV_CHECK_LAUNCH("incr_commit_kernel");
   return GSV_OK;
 }
 

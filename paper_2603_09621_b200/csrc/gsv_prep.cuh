@@ -35,6 +35,14 @@ struct PrepArgs {
   gsv_record64* rec64;  // optional (f64 engine)
   int32_t* counts;
   int32_t* box;
+  // optional change tracking (incremental binning, gsv_bin_incremental): a
+  // Gaussian whose pair count or box differs from what counts / box held
+  // before this pass is appended as (gid, old box, old count)
+  int32_t* chg_count;
+  int32_t* chg_gid;
+  int32_t* chg_old;      // 4 ints per entry (the old box record)
+  int32_t* chg_oldcnt;
+  int chg_cap;
 };
 
 // Number of bricks of the box (origin blo, extent nb) whose brick id is < b;
@@ -167,12 +175,25 @@ __device__ __forceinline__ void preprocess_one(int64_t i, const double p[3], con
     }
   }
   if (cnt == 0) nb[0] = nb[1] = nb[2] = 0;
-  pa.counts[i] = cnt;
   int4 bx;
   bx.x = (int)(blo[0] & 0xFFFF) | ((int)(blo[1] & 0xFFFF) << 16);
   bx.y = (int)(blo[2] & 0xFFFF) | ((nb[0] & 0xFFFF) << 16);
   bx.z = (nb[1] & 0xFFFF) | ((nb[2] & 0xFFFF) << 16);
   bx.w = k0;
+  if (pa.chg_count != nullptr) {
+    const int oc = pa.counts[i];
+    const int4 ob = reinterpret_cast<const int4*>(pa.box)[i];
+    if (oc != cnt ||
+        (cnt > 0 && (ob.x != bx.x || ob.y != bx.y || ob.z != bx.z || ob.w != bx.w))) {
+      const int e = atomicAdd(pa.chg_count, 1);
+      if (e < pa.chg_cap) {
+        pa.chg_gid[e] = (int32_t)i;
+        reinterpret_cast<int4*>(pa.chg_old)[e] = ob;
+        pa.chg_oldcnt[e] = oc;
+      }
+    }
+  }
+  pa.counts[i] = cnt;
   reinterpret_cast<int4*>(pa.box)[i] = bx;
 }
 

@@ -342,6 +342,8 @@ _GRAPH_HEADROOM = 1.15       # pair capacity over the pair count seen at capture
 _RENDER_HEADROOM = 1.05
 _RESULT_SLOTS = 4            # pinned result slots (at most 2 steps are in flight)
 _BC_CHUNK = 16384            # bias-correction table length per capture
+_CHG_CAP = 8192              # changed Gaussians tracked per step (incremental binning)
+_OPS_CAP = 16384             # list edits per step (kOpsCap of gsv_bin.cu)
 
 
 def _bias_corrections(beta1: float, beta2: float, t0: int, count: int) -> torch.Tensor:
@@ -431,18 +433,32 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
     ws = b["ws"]
     _lib.check(lib.gsv_bin_scan(b["counts"].data_ptr(), n, b["gstart"].data_ptr(),
                                 ws.data_ptr(), ws.numel(), s), "bin_scan")
-    k = b["keys"]
-    _lib.check(lib.gsv_bin_fill_capacity(
-        b["counts"].data_ptr(), b["box"].data_ptr(), b["gstart"].data_ptr(), n, cap, br,
-        k[0].data_ptr(), k[1].data_ptr(), k[2].data_ptr(), b["gids"].data_ptr(),
-        b["starts"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(), ws.data_ptr(),
-        ws.numel(), s), "bin_fill_capacity")
+    if b["incr"]:
+        # last step's lists edited for the Gaussians whose boxes changed
+        # (recorded by the previous step's preprocess pass)
+        _lib.check(lib.gsv_bin_incremental(
+            b["counts"].data_ptr(), b["box"].data_ptr(), b["gstart"].data_ptr(), n, cap, br,
+            b["chg_count"].data_ptr(),
+            b["chg_gid"].data_ptr(), b["chg_old"].data_ptr(), b["chg_oldcnt"].data_ptr(),
+            _CHG_CAP, b["starts"].data_ptr(), b["gids"].data_ptr(), b["starts_out"].data_ptr(),
+            b["gids_out"].data_ptr(), b["ops"].data_ptr(), b["nops"].data_ptr(),
+            b["lens"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(),
+            ws.data_ptr(), ws.numel(), s), "bin_incremental")
+    else:
+        k = b["keys"]
+        _lib.check(lib.gsv_bin_fill_capacity(
+            b["counts"].data_ptr(), b["box"].data_ptr(), b["gstart"].data_ptr(), n, cap, br,
+            k[0].data_ptr(), k[1].data_ptr(), k[2].data_ptr(), b["gids"].data_ptr(),
+            b["starts"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(),
+            ws.data_ptr(), ws.numel(), s), "bin_fill_capacity")
+    # the lists the kernels read (incremental: starts_out is zeroed on overflow)
+    lst = b["starts_out"] if b["incr"] else b["starts"]
     nvox = grid.num_voxels
     if join is not None:
         torch.cuda.current_stream().wait_stream(join)
     _lib.check(lib.gsv_forward(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
-        b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(), gr, br,
+        b["rec32"].data_ptr(), None, lst.data_ptr(), b["gids"].data_ptr(), gr, br,
         float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
         b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(),
         int(self.target.dtype == torch.float64), self.loss_kind,
@@ -456,7 +472,7 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
                    "step_gate")
     _lib.check(lib.gsv_backward(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
-        b["rec32"].data_ptr(), None, b["starts"].data_ptr(), b["gids"].data_ptr(),
+        b["rec32"].data_ptr(), None, lst.data_ptr(), b["gids"].data_ptr(),
         b["gstart"].data_ptr(), b["box"].data_ptr(), gr, br, float(opts.cutoff_sigma), 0,
         b["ab"].data_ptr(), b["masks"].data_ptr(), b["vpl"], b["partials"].data_ptr(), s),
         "backward")
@@ -527,6 +543,16 @@ def _graph_preprocess(self, f: GaussianField, b: dict) -> None:
     """gsv_preprocess into the graph's buffers: before the first replay, and
     whenever the field was changed outside the graph (version mismatch)."""
     lib = _lib.lib()
+    if b.get("track"):
+        # incremental binning: also record the Gaussians whose boxes change
+        _lib.check(lib.gsv_preprocess_track(
+            f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
+            f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), f.count, int(f.relax_enabled),
+            float(self.opts.cutoff_sigma), _lib.make_grid(self.grid), b["bricks"],
+            b["rec32"].data_ptr(), b["counts"].data_ptr(), b["box"].data_ptr(),
+            b["chg_count"].data_ptr(), b["chg_gid"].data_ptr(), b["chg_old"].data_ptr(),
+            b["chg_oldcnt"].data_ptr(), _CHG_CAP, _lib.stream_ptr()), "preprocess_track")
+        return
     _lib.check(lib.gsv_preprocess(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         f.raw_amplitude.data_ptr(), f.raw_relax.data_ptr(), f.count, int(f.relax_enabled),
@@ -564,7 +590,26 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     g.bufs = b
     nbytes = ctypes.c_size_t(0)
     _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
-    b["ws"] = gp.get("ws", (nbytes.value,), torch.uint8)
+    wsb = nbytes.value
+    # incremental binning: single GPU, whole grid, next-step records from the
+    # separate preprocess pass (GSV_BIN_INCREMENTAL=0 rebuilds every step)
+    b["incr"] = (os.environ.get("GSV_BIN_INCREMENTAL", "1") == "1" and not self.sharded
+                 and self.slab is None and getattr(self, "halo_hooks", None) is None
+                 and os.environ.get("GSV_GRAPH_FUSED_PREP") != "1")
+    if b["incr"]:
+        _lib.check(lib.gsv_bin_incremental_workspace(nb, ctypes.byref(nbytes)),
+                   "bin_incremental_workspace")
+        wsb = max(wsb, nbytes.value)
+        b["chg_count"] = gp.get("chg_count", (1,), torch.int32)
+        b["chg_gid"] = gp.get("chg_gid", (_CHG_CAP,), torch.int32)
+        b["chg_old"] = gp.get("chg_old", (_CHG_CAP, 4), torch.int32)
+        b["chg_oldcnt"] = gp.get("chg_oldcnt", (_CHG_CAP,), torch.int32)
+        b["starts_out"] = gp.get("starts_out", (nb + 1,), torch.int64)
+        b["gids_out"] = gp.get("gids_out", (cap,), torch.int32)
+        b["ops"] = gp.get("ops", (_OPS_CAP,), torch.int64)
+        b["nops"] = gp.get("nops", (1,), torch.int32)
+        b["lens"] = gp.get("lens", (nb + 1,), torch.int32)
+    b["ws"] = gp.get("ws", (wsb,), torch.uint8)
     b["keys"] = gp.get("keys", (3, cap), torch.int32)
     b["gids"] = gp.get("gids", (cap,), torch.int32)
     b["starts"] = gp.get("starts", (nb + 1,), torch.int64)
@@ -607,6 +652,20 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     groups = ("positions", "log_scales", "rotations", "raw_amplitude", "raw_relax")
     b["mv"] = (ctypes.c_void_p * 10)(*([state.m[x].data_ptr() for x in groups] +
                                        [state.v[x].data_ptr() for x in groups]))
+    if b["incr"]:
+        # the first lists in full (from the records of _graph_preprocess above);
+        # from here on the preprocess pass tracks box changes
+        k = b["keys"]
+        b["dry"].zero_()
+        _lib.check(lib.gsv_bin_fill_capacity(
+            b["counts"].data_ptr(), b["box"].data_ptr(), b["gstart"].data_ptr(), n, cap,
+            bricks, k[0].data_ptr(), k[1].data_ptr(), k[2].data_ptr(), b["gids"].data_ptr(),
+            b["starts"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(),
+            b["ws"].data_ptr(), b["ws"].numel(), _lib.stream_ptr()), "bin_fill_capacity")
+        # lists that did not fit make the first replay report an overflow
+        # (more changes than tracked), which re-captures with more room
+        b["chg_count"].fill_(0 if pairs <= cap else _CHG_CAP + 1)
+        b["track"] = True
     # dry run (every kernel once, empty lists, no update), then capture
     side = torch.cuda.Stream(device=dev)
     side.wait_stream(torch.cuda.current_stream(dev))
@@ -665,7 +724,14 @@ class StepHandle:
                 drained.append(p)
             if step._graph is g:
                 b = g.bufs
-                local = bool(int(b["overflow"].item())) if step.sharded else True
+                if step.sharded:
+                    local = bool(int(b["overflow"].item()))
+                elif b.get("incr"):
+                    # incremental binning also overflows on too many edits:
+                    # more room only if the pairs did not fit
+                    local = int(b["gstart"][-1].item()) > g.cap
+                else:
+                    local = True
                 step._graph = None
                 step._graph = _graph_capture(step, f, state, self._lrs, *self._hyper, g.key,
                                              min_cap=int(g.cap * 1.5) if local else g.cap)

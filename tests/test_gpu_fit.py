@@ -610,3 +610,58 @@ def test_nvtx_ranges_wrap_phases_and_replays(monkeypatch):
         assert depth >= 0
     assert depth == 0
     assert timer.summary()["forward"][0] >= 1
+
+
+def _moving_run(steps, lr_scale, monkeypatch=None, chg_cap=None):
+    """Eager vs graph steps with a large position / scale learning rate, so
+    Gaussians cross brick boundaries and the graph's incremental binning
+    edits its lists every step."""
+    import paper_2603_09621_b200.train as train_mod
+    if chg_cap is not None:
+        monkeypatch.setattr(train_mod, "_CHG_CAP", chg_cap)
+    p = make_problem(CONFIGS[1])
+    lr = gs.Volume(p["lr_grid"], p["lr"])
+    fa, fb = gs.GaussianField(*p["field"]), gs.GaussianField(*p["field"])
+    sa, sb = gs.AdamState.create(fa), gs.AdamState.create(fb)
+    lrs = dict(gs.FitConfig().resolved_lrs(lr.grid.spacing))
+    lrs["positions"] *= lr_scale
+    lrs["log_scales"] *= lr_scale
+    ea = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    eb = gs.TrainStep(lr, gs.RenderOptions(), (8, 8, 4), "l1")
+    la, lb, pairs = [], [], []
+    prev = None
+    for i in range(steps):
+        out = ea.forward(fa)
+        la.append(out.loss())
+        pairs.append(out.idx.pair_count)
+        ea.update(fa, out, sa, lrs)
+        if i == steps - 1:
+            prev = fb.copy()
+        lb.append(eb.step(fb, sb, lrs))
+    return (fa, sa, la), (fb, sb, lb), eb, prev, pairs
+
+
+def test_incremental_binning_lists_equal_full_rebuild():
+    """After steps that move Gaussians across bricks, the graph's edited lists
+    are the lists a full binning of the same field gives, and training stays
+    bit-identical to the eager step (which bins from scratch)."""
+    (fa, sa, la), (fb, sb, lb), eb, prev, pairs = _moving_run(12, 60.0)
+    g = eb._graph
+    assert g.bufs["incr"]
+    assert len(set(pairs)) > 1                      # boxes did change
+    idx = gs.build_brick_index(prev, eb.grid)       # the field the last step binned
+    P = idx.pair_count
+    assert torch.equal(g.bufs["starts"], idx.starts)
+    assert torch.equal(g.bufs["gids"][:P], idx.gids.to(torch.int32))
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    assert la == lb
+
+
+def test_incremental_binning_overflow_rebuilds(monkeypatch):
+    """More changed Gaussians than tracked: the step reports an overflow, the
+    graph is re-captured with full binning, and the result equals eager."""
+    (fa, sa, la), (fb, sb, lb), eb, _, pairs = _moving_run(6, 60.0, monkeypatch, chg_cap=2)
+    assert len(set(pairs)) > 1
+    assert eb.graph_captures >= 2
+    np.testing.assert_array_equal(_pack(fa), _pack(fb))
+    assert la == lb and sa.t == sb.t
