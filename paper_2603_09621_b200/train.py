@@ -591,10 +591,10 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
     nbytes = ctypes.c_size_t(0)
     _lib.check(lib.gsv_bin_workspace(n, cap, nb, ctypes.byref(nbytes)), "bin_workspace")
     wsb = nbytes.value
-    # incremental binning: single GPU, whole grid, next-step records from the
-    # separate preprocess pass (GSV_BIN_INCREMENTAL=0 rebuilds every step)
-    b["incr"] = (os.environ.get("GSV_BIN_INCREMENTAL", "1") == "1" and not self.sharded
-                 and self.slab is None and getattr(self, "halo_hooks", None) is None
+    # incremental binning (any slab; sharded and halo steps too), with the
+    # next-step records from the separate preprocess pass
+    # (GSV_BIN_INCREMENTAL=0 rebuilds the lists every step)
+    b["incr"] = (os.environ.get("GSV_BIN_INCREMENTAL", "1") == "1"
                  and os.environ.get("GSV_GRAPH_FUSED_PREP") != "1")
     if b["incr"]:
         _lib.check(lib.gsv_bin_incremental_workspace(nb, ctypes.byref(nbytes)),
