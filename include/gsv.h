@@ -173,7 +173,8 @@ int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box,
  * rebuilds the lists (starts, gids: the lists of the OLD boxes, capacity
  * entries) for the current counts / box: starts_out (nbricks_slab + 1) and
  * gids_out are the new lists, copied back into starts / gids for the next
- * call; *chg_count is reset.  The result equals gsv_bin_fill for the current
+ * call when copy_back != 0 (otherwise the caller swaps the two buffer pairs
+ * for the next call); *chg_count is reset.  The result equals gsv_bin_fill for the current
  * boxes (each list ascending in gid).  *overflow = more than chg_cap changes,
  * more than 16384 edits, more than capacity pairs, edited lists whose pair
  * count differs from gstart[n] (gsv_bin_scan of counts), or *dry != 0 -- then
@@ -196,8 +197,8 @@ int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t
                         const int32_t* chg_old, const int32_t* chg_oldcnt, int chg_cap,
                         int64_t* starts, int32_t* gids, int64_t* starts_out, int32_t* gids_out,
                         unsigned long long* ops, int32_t* nops, int32_t* lens,
-                        const int32_t* dry, int32_t* overflow, void* workspace,
-                        size_t workspace_bytes, void* stream);
+                        const int32_t* dry, int32_t* overflow, int copy_back,
+                        void* workspace, size_t workspace_bytes, void* stream);
 
 /* Canonical-order check and repair for caller-supplied lists
  * (BrickIndex.lists_sorted / canonicalized, raster.py:91-112).

@@ -63,9 +63,9 @@ _SIGS = {
     "gsv_preprocess_track": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_dbl, GP, BP,
                              c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp],
     "gsv_bin_incremental_workspace": [c_i32, c_szp],
-    "gsv_bin_incremental": [c_vp, c_vp, c_vp, c_i64, c_i64, BP, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp,
-                            c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t,
-                            c_vp],
+    "gsv_bin_incremental": [c_vp, c_vp, c_vp, c_i64, c_i64, BP, c_vp, c_vp, c_vp, c_vp, c_int,
+                            c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
+                            ctypes.c_size_t, c_vp],
     "gsv_lists_unsorted": [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp],
     "gsv_canonicalize_workspace": [c_i64, c_i32, c_szp],
     "gsv_canonicalize": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp],

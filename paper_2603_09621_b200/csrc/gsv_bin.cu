@@ -410,17 +410,19 @@ incr_merge_kernel(const int64_t* __restrict__ starts, const int32_t* __restrict_
   }
 }
 
-// overflow: empty lists downstream; otherwise the output becomes next step's input
+// overflow: empty lists downstream; otherwise (copy_back) the output becomes
+// next step's input -- a caller that alternates the two buffers skips the copy
 __global__ void __launch_bounds__(256)
 incr_commit_kernel(int64_t* __restrict__ starts, int32_t* __restrict__ gids,
                    int64_t* __restrict__ starts_out, const int32_t* __restrict__ gids_out,
-                   int32_t nb, const int32_t* __restrict__ overflow) {
+                   int32_t nb, const int32_t* __restrict__ overflow, int copy_back) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (*overflow != 0) {
     for (int64_t i = i0; i <= nb; i += stride) starts_out[i] = 0;
     return;
   }
+  if (!copy_back) return;
   for (int64_t i = i0; i <= nb; i += stride) starts[i] = starts_out[i];
   const int64_t p = starts_out[nb];
   const int64_t p4 = p >> 2;
@@ -685,8 +687,8 @@ int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t
                         const int32_t* chg_old, const int32_t* chg_oldcnt, int chg_cap,
                         int64_t* starts, int32_t* gids, int64_t* starts_out, int32_t* gids_out,
                         unsigned long long* ops, int32_t* nops, int32_t* lens,
-                        const int32_t* dry, int32_t* overflow, void* workspace,
-                        size_t workspace_bytes, void* stream) {
+                        const int32_t* dry, int32_t* overflow, int copy_back,
+                        void* workspace, size_t workspace_bytes, void* stream) {
   GSV_REQUIRE(bricks && counts && box && gstart && chg_count && chg_gid && chg_old && chg_oldcnt &&
                   starts && gids && starts_out && gids_out && ops && nops && lens && overflow,
               "null pointer argument");
@@ -720,8 +722,9 @@ int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t
         starts, gids, starts_out, gids_out, (int32_t)nb, ops, nops, overflow);
     GSV_CHECK_LAUNCH("incr_merge_kernel");
   }
-  incr_commit_kernel<<<1184, 256, 0, s>>>(starts, gids, starts_out, gids_out, (int32_t)nb,
-                                          overflow);
+  // without the copy only the overflow case has work: a small grid
+  incr_commit_kernel<<<copy_back ? 1184 : 32, 256, 0, s>>>(starts, gids, starts_out, gids_out,
+                                                          (int32_t)nb, overflow, copy_back);
   GSV_CHECK_LAUNCH("incr_commit_kernel");
   return GSV_OK;
 }

@@ -377,6 +377,14 @@ class _StepGraph:
         self.graph = None
         self.bufs: dict = {}
         self.launches = 0            # replays so far (ring slot = launches % _RESULT_SLOTS)
+        self.graphs: list = []       # incremental binning: [even replays, odd replays]
+
+    def lists(self):
+        """(starts, gids) of the last replay (the capture's lists before any)."""
+        b = self.bufs
+        if not b.get("incr") or self.launches == 0:
+            return b["starts"], b["gids"]
+        return _list_buffers(b, (self.launches - 1) % 2)[1]
 
 
 def _graph_key(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps):
@@ -407,9 +415,11 @@ def _graph_supported(self) -> bool:
             and not os.environ.get("GSV_TAIL_SPLIT"))
 
 
-def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
+def _graph_body(self, f: GaussianField, g: _StepGraph, parity: int = 0) -> None:
     """The launch sequence captured into the graph (also run once, dry, to
-    warm every kernel up before capture)."""
+    warm every kernel up before capture).  With incremental binning two
+    graphs are captured that alternate the list buffers: parity 0 edits
+    (starts, gids) into (starts_out, gids_out), parity 1 the other way."""
     import ctypes
     lib = _lib.lib()
     b = g.bufs
@@ -436,14 +446,17 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
     if b["incr"]:
         # last step's lists edited for the Gaussians whose boxes changed
         # (recorded by the previous step's preprocess pass)
+        src, dst = _list_buffers(b, parity)
         _lib.check(lib.gsv_bin_incremental(
             b["counts"].data_ptr(), b["box"].data_ptr(), b["gstart"].data_ptr(), n, cap, br,
             b["chg_count"].data_ptr(),
             b["chg_gid"].data_ptr(), b["chg_old"].data_ptr(), b["chg_oldcnt"].data_ptr(),
-            _CHG_CAP, b["starts"].data_ptr(), b["gids"].data_ptr(), b["starts_out"].data_ptr(),
-            b["gids_out"].data_ptr(), b["ops"].data_ptr(), b["nops"].data_ptr(),
-            b["lens"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(),
+            _CHG_CAP, src[0].data_ptr(), src[1].data_ptr(), dst[0].data_ptr(),
+            dst[1].data_ptr(), b["ops"].data_ptr(), b["nops"].data_ptr(),
+            b["lens"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(), 0,
             ws.data_ptr(), ws.numel(), s), "bin_incremental")
+        # the kernels read the edited lists (starts zeroed on overflow)
+        lst, lgids = dst
     else:
         k = b["keys"]
         _lib.check(lib.gsv_bin_fill_capacity(
@@ -451,14 +464,13 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
             k[0].data_ptr(), k[1].data_ptr(), k[2].data_ptr(), b["gids"].data_ptr(),
             b["starts"].data_ptr(), b["dry"].data_ptr(), b["overflow"].data_ptr(),
             ws.data_ptr(), ws.numel(), s), "bin_fill_capacity")
-    # the lists the kernels read (incremental: starts_out is zeroed on overflow)
-    lst = b["starts_out"] if b["incr"] else b["starts"]
+        lst, lgids = b["starts"], b["gids"]
     nvox = grid.num_voxels
     if join is not None:
         torch.cuda.current_stream().wait_stream(join)
     _lib.check(lib.gsv_forward(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
-        b["rec32"].data_ptr(), None, lst.data_ptr(), b["gids"].data_ptr(), gr, br,
+        b["rec32"].data_ptr(), None, lst.data_ptr(), lgids.data_ptr(), gr, br,
         float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
         b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(),
         int(self.target.dtype == torch.float64), self.loss_kind,
@@ -472,7 +484,7 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
                    "step_gate")
     _lib.check(lib.gsv_backward(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
-        b["rec32"].data_ptr(), None, lst.data_ptr(), b["gids"].data_ptr(),
+        b["rec32"].data_ptr(), None, lst.data_ptr(), lgids.data_ptr(),
         b["gstart"].data_ptr(), b["box"].data_ptr(), gr, br, float(opts.cutoff_sigma), 0,
         b["ab"].data_ptr(), b["masks"].data_ptr(), b["vpl"], b["partials"].data_ptr(), s),
         "backward")
@@ -537,6 +549,12 @@ def _graph_body(self, f: GaussianField, g: _StepGraph) -> None:
         b["t"].data_ptr(), b["gate"].data_ptr(), b["result"].data_ptr(),
         b["result_host"].data_ptr(), b["rcount"].data_ptr(), _RESULT_SLOTS, s),
         "step_advance_publish")
+
+
+def _list_buffers(b: dict, parity: int):
+    """((starts, gids) read, (starts, gids) written) of an incremental replay."""
+    a, o = (b["starts"], b["gids"]), (b["starts_out"], b["gids_out"])
+    return (a, o) if parity == 0 else (o, a)
 
 
 def _graph_preprocess(self, f: GaussianField, b: dict) -> None:
@@ -675,10 +693,13 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
         b["dry"].zero_()
     torch.cuda.current_stream(dev).wait_stream(side)
     torch.cuda.synchronize(dev)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
-        _graph_body(self, f, g)
-    g.graph = graph
+    g.graphs = []
+    for parity in range(2 if b["incr"] else 1):
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
+            _graph_body(self, f, g, parity)
+        g.graphs.append(graph)
+    g.graph = g.graphs[0]
     g.prep_version = f.version
     b["t"].fill_(int(state.t))
     g.t_synced = state.t
@@ -796,7 +817,7 @@ def _step_launch(self, f: GaussianField, state, lrs: dict, beta1: float = 0.9,
             _graph_preprocess(self, f, b)
             g.prep_version = f.version
     _nvtx_push("gsv.step.replay")
-    g.graph.replay()
+    g.graphs[g.launches % len(g.graphs)].replay()   # incremental: alternate list buffers
     _nvtx_pop()
     slot = g.launches % _RESULT_SLOTS
     g.launches += 1

@@ -651,8 +651,9 @@ def test_incremental_binning_lists_equal_full_rebuild():
     assert len(set(pairs)) > 1                      # boxes did change
     idx = gs.build_brick_index(prev, eb.grid)       # the field the last step binned
     P = idx.pair_count
-    assert torch.equal(g.bufs["starts"], idx.starts)
-    assert torch.equal(g.bufs["gids"][:P], idx.gids.to(torch.int32))
+    starts, gids = g.lists()
+    assert torch.equal(starts, idx.starts)
+    assert torch.equal(gids[:P], idx.gids.to(torch.int32))
     np.testing.assert_array_equal(_pack(fa), _pack(fb))
     assert la == lb
 
@@ -676,7 +677,8 @@ def test_incremental_binning_on_a_slab():
     assert eb._graph.bufs["incr"] and len(set(pairs)) > 1
     idx = build_brick_index(prev, eb.grid, gs.RenderOptions(), (8, 8, 4), slab=slab)
     P = idx.pair_count
-    assert torch.equal(eb._graph.bufs["starts"], idx.starts)
-    assert torch.equal(eb._graph.bufs["gids"][:P], idx.gids.to(torch.int32))
+    starts, gids = eb._graph.lists()
+    assert torch.equal(starts, idx.starts)
+    assert torch.equal(gids[:P], idx.gids.to(torch.int32))
     np.testing.assert_array_equal(_pack(fa), _pack(fb))
     assert la == lb
