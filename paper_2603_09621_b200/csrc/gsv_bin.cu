@@ -321,23 +321,27 @@ __device__ __forceinline__ int ops_lower(const unsigned long long* __restrict__ 
   return lo;
 }
 
+// lens[b] = the new list length, opbeg[b] = the brick's first edit
+// (opbeg[nb] = the edit count)
 __global__ void __launch_bounds__(256)
 incr_len_kernel(const int64_t* __restrict__ starts, int32_t nb,
                 const unsigned long long* __restrict__ ops, const int32_t* __restrict__ nops,
-                int32_t* __restrict__ lens) {
+                int32_t* __restrict__ lens, int32_t* __restrict__ opbeg) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b > nb) return;
+  const int n = *nops;
   if (b == nb) {
     lens[b] = 0;
+    opbeg[b] = n;
     return;
   }
-  const int n = *nops;
-  int d = 0;
+  int d = 0, p0 = 0;
   if (n > 0) {
-    const int p0 = ops_lower(ops, n, (unsigned long long)(unsigned)b << 32);
+    p0 = ops_lower(ops, n, (unsigned long long)(unsigned)b << 32);
     const int p1 = ops_lower(ops, n, (unsigned long long)(unsigned)(b + 1) << 32);
     for (int p = p0; p < p1; ++p) d += (ops[p] & 1ull) ? 1 : -1;
   }
+  opbeg[b] = p0;
   lens[b] = (int32_t)(starts[b + 1] - starts[b]) + d;
 }
 
@@ -350,28 +354,91 @@ __global__ void incr_check_kernel(const int64_t* __restrict__ starts_out, int32_
   if (p > cap || p != gstart[n]) *overflow = 1;
 }
 
-// one warp per brick: copy, or merge the surviving and inserted gids
+// one warp per brick: copy, or merge the surviving and inserted gids.  The
+// brick's edits (sorted by gid) are staged in shared memory with the
+// exclusive prefix count of insertions, so each old entry finds the edits
+// before it by binary search: new index = old index - removals before +
+// insertions before.  Segments over kMergeSeg edits take a linear path.
+constexpr int kMergeSeg = 256;
+
 __global__ void __launch_bounds__(256)
 incr_merge_kernel(const int64_t* __restrict__ starts, const int32_t* __restrict__ gids,
                   const int64_t* __restrict__ starts_out, int32_t* __restrict__ gids_out,
                   int32_t nb, const unsigned long long* __restrict__ ops,
-                  const int32_t* __restrict__ nops, const int32_t* __restrict__ overflow) {
+                  const int32_t* __restrict__ opbeg, const int32_t* __restrict__ overflow) {
+  __shared__ unsigned sg[8][kMergeSeg];   // edit gid << 1 | insert
+  __shared__ int spre[8][kMergeSeg + 1];   // insertions before edit q
+  const int warp = threadIdx.x >> 5;
   const int b = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= nb || *overflow != 0) return;
   const int64_t os = starts[b], oe = starts[b + 1], ns = starts_out[b];
   const int len = (int)(oe - os);
-  const int n = *nops;
-  int p0 = 0, p1 = 0;
-  if (n > 0) {
-    p0 = ops_lower(ops, n, (unsigned long long)(unsigned)b << 32);
-    p1 = ops_lower(ops, n, (unsigned long long)(unsigned)(b + 1) << 32);
-  }
+  const int p0 = opbeg[b], p1 = opbeg[b + 1];
   if (p0 == p1) {
     for (int i = lane; i < len; i += 32) gids_out[ns + i] = gids[os + i];
     return;
   }
-  // surviving entries: shifted by the removals before and insertions before
+  const int seg = p1 - p0;
+  if (seg <= kMergeSeg) {
+    unsigned* eg = sg[warp];
+    int* ep = spre[warp];
+    int run = 0;
+    for (int q0 = 0; q0 < seg; q0 += 32) {
+      const int q = q0 + lane;
+      const unsigned v = q < seg ? (unsigned)ops[p0 + q] : 0u;   // gid << 1 | insert
+      if (q < seg) eg[q] = v;
+      const int ins = (q < seg) ? (int)(v & 1u) : 0;
+      int incl = ins;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (q < seg) ep[q] = run + incl - ins;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) ep[seg] = run;
+    __syncwarp();
+    // surviving entries, four loads in flight per lane
+    for (int i0 = 0; i0 < len; i0 += 128) {
+      int gv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u + lane;
+        gv[u] = i < len ? gids[os + i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u + lane;
+        if (i >= len) break;
+        const int g = gv[u];
+        int lo = 0, hi = seg;                    // first edit with gid >= g
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((int)(eg[mid] >> 1) < g) lo = mid + 1; else hi = mid;
+        }
+        const bool removed = lo < seg && (int)(eg[lo] >> 1) == g && !(eg[lo] & 1u);
+        const int in_lt = ep[lo], rm_lt = lo - in_lt;
+        if (!removed) gids_out[ns + i - rm_lt + in_lt] = g;
+      }
+    }
+    // inserted entries
+    for (int q = lane; q < seg; q += 32) {
+      const unsigned v = eg[q];
+      if (!(v & 1u)) continue;
+      const int h = (int)(v >> 1);
+      int lo = 0, hi = len;                      // old entries < h
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (gids[os + mid] < h) lo = mid + 1; else hi = mid;
+      }
+      const int in_lt = ep[q], rm_lt = q - in_lt;
+      gids_out[ns + lo - rm_lt + in_lt] = h;
+    }
+    return;
+  }
+  // long edit segments: linear counts
   for (int i = lane; i < len; i += 32) {
     const int g = gids[os + i];
     int rm_lt = 0, in_lt = 0;
@@ -388,12 +455,11 @@ incr_merge_kernel(const int64_t* __restrict__ starts, const int32_t* __restrict_
     }
     if (!removed) gids_out[ns + i - rm_lt + in_lt] = g;
   }
-  // inserted entries
   for (int p = p0 + lane; p < p1; p += 32) {
     const unsigned long long o = ops[p];
     if (!(o & 1ull)) continue;
     const int h = (int)((unsigned)o >> 1);
-    int lo = 0, hi = len;                      // old entries < h
+    int lo = 0, hi = len;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (gids[os + mid] < h) lo = mid + 1; else hi = mid;
@@ -708,8 +774,9 @@ int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t
   incr_ops_kernel<<<1, 1024, ops_smem, s>>>(counts, box, *bricks, chg_count, chg_gid, chg_old,
                                             chg_oldcnt, chg_cap, dry, ops, nops, overflow);
   GSV_CHECK_LAUNCH("incr_ops_kernel");
+  int32_t* opbeg = lens + (nb + 1);
   incr_len_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(starts, (int32_t)nb, ops,
-                                                                    nops, lens);
+                                                                    nops, lens, opbeg);
   GSV_CHECK_LAUNCH("incr_len_kernel");
   thrust::transform_iterator<ToI64, const int32_t*, int64_t> it(lens, ToI64());
   size_t bytes = workspace_bytes;
@@ -719,7 +786,7 @@ int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t
   GSV_CHECK_LAUNCH("incr_check_kernel");
   if (nb > 0) {
     incr_merge_kernel<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, s>>>(
-        starts, gids, starts_out, gids_out, (int32_t)nb, ops, nops, overflow);
+        starts, gids, starts_out, gids_out, (int32_t)nb, ops, opbeg, overflow);
     GSV_CHECK_LAUNCH("incr_merge_kernel");
   }
   // without the copy only the overflow case has work: a small grid

@@ -626,7 +626,7 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
         b["gids_out"] = gp.get("gids_out", (cap,), torch.int32)
         b["ops"] = gp.get("ops", (_OPS_CAP,), torch.int64)
         b["nops"] = gp.get("nops", (1,), torch.int32)
-        b["lens"] = gp.get("lens", (nb + 1,), torch.int32)
+        b["lens"] = gp.get("lens", (2 * (nb + 1),), torch.int32)
     b["ws"] = gp.get("ws", (wsb,), torch.uint8)
     b["keys"] = gp.get("keys", (3, cap), torch.int32)
     b["gids"] = gp.get("gids", (cap,), torch.int32)

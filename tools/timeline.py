@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--skip", type=int, default=5, help="fit steps before the profiled ones")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     p = synth.make_problem(synth.CONFIGS[args.config])
@@ -44,7 +45,7 @@ def main():
     step = gs.TrainStep(gs.Volume(p["lr_grid"], p["lr"]), gs.RenderOptions(), (8, 8, 4), "l1")
     state = gs.AdamState.create(f)
     lrs = gs.FitConfig().resolved_lrs(p["lr_grid"].spacing)
-    for _ in range(5):
+    for _ in range(args.skip):
         step.step(f, state, lrs)
     torch.cuda.synchronize()
     marks = []
