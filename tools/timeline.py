@@ -38,10 +38,14 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--skip", type=int, default=5, help="fit steps before the profiled ones")
+    ap.add_argument("--render", action="store_true",
+                    help="profile Renderer replays at the config's render grid instead")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     p = synth.make_problem(synth.CONFIGS[args.config])
     f = gs.GaussianField(*p["field"])
+    if args.render:
+        return render_timeline(f, p["render_grid"], args.steps)
     step = gs.TrainStep(gs.Volume(p["lr_grid"], p["lr"]), gs.RenderOptions(), (8, 8, 4), "l1")
     state = gs.AdamState.create(f)
     lrs = gs.FitConfig().resolved_lrs(p["lr_grid"].spacing)
@@ -94,6 +98,28 @@ def main():
         with open(args.out, "w") as fh:
             json.dump({"steps": report, "raw": [(a, b, short(n)) for a, b, n in rows]}, fh,
                       indent=0)
+
+
+def render_timeline(f, grid, reps):
+    from torch.profiler import ProfilerActivity, profile
+    r = gs.Renderer(grid)
+    for _ in range(3):
+        r(f)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        for _ in range(reps):
+            r(f)
+        torch.cuda.synchronize()
+    rows = sorted((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
+                  if e.device_type == torch.autograd.DeviceType.CUDA)
+    tot = {}
+    for a, b, n in rows:
+        k = short(n)
+        tot[k] = tot.get(k, 0.0) + (b - a)
+    span = (rows[-1][1] - rows[0][0]) / reps
+    print(f"render {grid.dims}: {reps} replays, span per render {span:.1f} us")
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+        print(f"  {v / reps:9.2f} us  {k}")
 
 
 if __name__ == "__main__":
