@@ -212,6 +212,18 @@ int gsv_canonicalize(const int64_t* starts, const int32_t* gids_in,
                      int32_t* gids_out, int32_t nbricks, int64_t pairs,
                      void* workspace, size_t workspace_bytes, void* stream);
 
+/* The fused loss epilogue of the 8x8x4 f32 forward as its own pass, for a
+ * step whose target is still in flight over PCIe while the forward runs
+ * (gsv_forward with target NULL, then this): from the forward's W and I,
+ * writes ab = {dL/dI / W, I} and loss_part (one per brick of the slab) with
+ * the same voxel order per brick as the forward kernel selected by vpl (16:
+ * grouped, 8: whole brick), so both are bit-identical to the fused forward's.
+ * Also added in ABI 6. */
+int gsv_loss_bricks(const gsv_grid* grid, const gsv_bricks* bricks, double eps_w,
+                    const float* W, const float* I, const void* target, int target_dtype,
+                    int loss_kind, double vox_count, int vpl, float* ab, double* loss_part,
+                    void* stream);
+
 /* ------------------------------------------------------------------------
  * Forward render, CTA per brick.  Replaces _forward_kernel
  * (raster.py:240-293).  precision 0 = f32 (S/W/I float32; truncation decided

@@ -69,6 +69,8 @@ _SIGS = {
     "gsv_lists_unsorted": [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp],
     "gsv_canonicalize_workspace": [c_i64, c_i32, c_szp],
     "gsv_canonicalize": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, ctypes.c_size_t, c_vp],
+    "gsv_loss_bricks": [GP, BP, c_dbl, c_vp, c_vp, c_vp, c_int, c_int, c_dbl, c_int, c_vp, c_vp,
+                        c_vp],
     "gsv_forward": [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, GP, BP, c_dbl, c_dbl, c_int,
                     c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_dbl, c_vp, c_vp, c_vp, c_int, c_vp],
     "gsv_backward_prep": [c_vp, c_vp, c_vp, GP, BP, c_dbl, c_int, c_vp, c_vp, c_vp],

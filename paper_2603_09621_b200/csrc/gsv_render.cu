@@ -1311,6 +1311,58 @@ forward32c_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
   }
 }
 
+// ------------------------------------------ the forward's loss epilogue, alone
+// For a graph step whose target arrives over PCIe during binning and the
+// forward (gsv_loss_bricks): exactly the epilogue of forward32c_kernel
+// (order 0: voxel v = lane + 32 i) or of forward32w_kernel (order 1: lane's
+// column A then column B, z inside), one warp per 8x8x4 brick, so the loss
+// partials and {alpha, I} are bit-identical to the fused forward's.
+__global__ void __launch_bounds__(32)
+loss_bricks_kernel(const __grid_constant__ gsv_grid g, gsv_bricks k, double eps_w,
+                   const float* __restrict__ W, const float* __restrict__ I,
+                   const void* __restrict__ target, int target_f64, int loss_kind,
+                   double vox_count, int order, float2* __restrict__ ab,
+                   double* __restrict__ loss_part) {
+  const int lb = blockIdx.x;
+  const int b = (int)slab_first(k) + lb;
+  const BrickGeom bg = brick_geom(b, g, k);
+  const int lane = threadIdx.x;
+  double lsum = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int x, y, z;
+    if (order == 0) {
+      const int v = lane + 32 * i;
+      x = v & 7;
+      y = (v >> 3) & 7;
+      z = v >> 6;
+    } else {
+      x = lane & 7;
+      y = (lane >> 3) + 4 * (i >> 2);
+      z = i & 3;
+    }
+    if (!(x < bg.ex && y < bg.ey && z < bg.ez)) continue;
+    const int64_t lin = (int64_t)(bg.x0 + x) +
+                        (int64_t)g.nx * ((bg.y0 + y) + (int64_t)g.ny * (bg.z0 + z));
+    const float wv = W[lin], iv = I[lin];
+    const bool cov = (double)wv >= eps_w;
+    const double d = (double)iv - target_value(target, target_f64, lin);
+    double dl;
+    if (loss_kind == 0) {
+      lsum += fabs(d);
+      dl = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / vox_count;
+    } else {
+      lsum += d * d;
+      dl = 2.0 * d / vox_count;
+    }
+    const float alpha = (cov && dl != 0.0) ? (float)(dl / (double)wv) : 0.f;
+    ab[lin] = make_float2(alpha, iv);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(kFull, lsum, o);
+  if (lane == 0) loss_part[lb] = lsum;
+}
+
 // --------------------------------------------------------------- forward f64
 struct __align__(16) Pair64 {
   double l[9];
@@ -2130,6 +2182,27 @@ naive_kernel(const double* __restrict__ pos, const double* __restrict__ ls,
 using namespace gsv;
 
 extern "C" {
+
+int gsv_loss_bricks(const gsv_grid* grid, const gsv_bricks* bricks, double eps_w,
+                    const float* W, const float* I, const void* target, int target_dtype,
+                    int loss_kind, double vox_count, int vpl, float* ab, double* loss_part,
+                    void* stream) {
+  if (int s = validate_grid_bricks(grid, bricks)) return s;
+  GSV_REQUIRE(bricks->bdx == 8 && bricks->bdy == 8 && bricks->bdz == 4,
+              "gsv_loss_bricks needs 8x8x4 bricks");
+  GSV_REQUIRE(vpl == 16 || vpl == 8, "vpl must be 16 (grouped) or 8 (whole-brick forward)");
+  GSV_REQUIRE(W && I && target && ab && loss_part, "null pointer argument");
+  GSV_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss_kind must be 0 (l1) or 1 (l2)");
+  GSV_REQUIRE(target_dtype == 0 || target_dtype == 1,
+              "target_dtype must be 0 (float32) or 1 (float64)");
+  const int64_t nb = slab_bricks(*bricks);
+  if (nb == 0) return GSV_OK;
+  loss_bricks_kernel<<<(unsigned)nb, 32, 0, as_stream(stream)>>>(
+      *grid, *bricks, eps_w, W, I, target, target_dtype, loss_kind, vox_count, vpl == 16 ? 0 : 1,
+      (float2*)ab, loss_part);
+  GSV_CHECK_LAUNCH("loss_bricks_kernel");
+  return GSV_OK;
+}
 
 int gsv_forward(const double* positions, const double* log_scales, const double* rotations,
                 const gsv_record32* rec32, const gsv_record64* rec64, const int64_t* starts,

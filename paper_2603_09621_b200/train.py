@@ -466,16 +466,26 @@ def _graph_body(self, f: GaussianField, g: _StepGraph, parity: int = 0) -> None:
             ws.data_ptr(), ws.numel(), s), "bin_fill_capacity")
         lst, lgids = b["starts"], b["gids"]
     nvox = grid.num_voxels
-    if join is not None:
+    # a target arriving over PCIe: the forward runs without the fused loss and
+    # the copy joins before the loss pass (bit-identical partials), so the
+    # H2D overlaps binning and the whole forward
+    split = join is not None and b["fwd_vpl"] in (16, 8) and tuple(self.brick_dims) == (8, 8, 4)
+    if join is not None and not split:
         torch.cuda.current_stream().wait_stream(join)
+    tdt = int(self.target.dtype == torch.float64)
     _lib.check(lib.gsv_forward(
         f.positions.data_ptr(), f.log_scales.data_ptr(), f.rotations.data_ptr(),
         b["rec32"].data_ptr(), None, lst.data_ptr(), lgids.data_ptr(), gr, br,
         float(opts.cutoff_sigma), float(opts.epsilon_w), 0, b["S"].data_ptr(),
-        b["W"].data_ptr(), b["I"].data_ptr(), self.target.data_ptr(),
-        int(self.target.dtype == torch.float64), self.loss_kind,
-        float(nvox), b["ab"].data_ptr(), b["loss_part"].data_ptr(), b["masks"].data_ptr(),
-        b["fwd_vpl"], s), "forward")
+        b["W"].data_ptr(), b["I"].data_ptr(), None if split else self.target.data_ptr(),
+        tdt, self.loss_kind, float(nvox), b["ab"].data_ptr(), b["loss_part"].data_ptr(),
+        b["masks"].data_ptr(), b["fwd_vpl"], s), "forward")
+    if split:
+        torch.cuda.current_stream().wait_stream(join)
+        _lib.check(lib.gsv_loss_bricks(
+            gr, br, float(opts.epsilon_w), b["W"].data_ptr(), b["I"].data_ptr(),
+            self.target.data_ptr(), tdt, self.loss_kind, float(nvox), b["fwd_vpl"],
+            b["ab"].data_ptr(), b["loss_part"].data_ptr(), s), "loss_bricks")
     _lib.check(lib.gsv_sum(b["loss_part"].data_ptr(), b["nb"], b["loss_sum"].data_ptr(), s),
                "sum")
     if not self.sharded:

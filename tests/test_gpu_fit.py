@@ -544,10 +544,15 @@ def test_grouped_forward_matches_whole_brick_kernel(case, monkeypatch):
     assert abs(a[3] - b[3]) <= 1e-6 * max(1e-3, abs(a[3]))     # sign(I - T) at I ~ T
 
 
-def test_target_source_copies_h2d_inside_each_step():
+@pytest.mark.parametrize("fwd", ["grouped", "whole"])
+def test_target_source_copies_h2d_inside_each_step(fwd, monkeypatch):
     """TrainStep.set_target_source: every step (graph replay or eager) copies
     the pinned host target H2D itself; rewriting the host tensor between steps
-    feeds the new target.  Same losses and field as set_target before each step."""
+    feeds the new target.  Same losses and field as set_target before each step
+    (the graph then runs the loss as its own pass after the forward,
+    gsv_loss_bricks, bit-identical to the fused epilogue of either forward)."""
+    if fwd == "whole":
+        monkeypatch.setenv("GSV_FWD_COLS", "0")
     p = make_problem(CONFIGS[1])
     lr = gs.Volume(p["lr_grid"], p["lr"])
     lrs = gs.FitConfig().resolved_lrs(lr.grid.spacing)
