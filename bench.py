@@ -140,9 +140,12 @@ def dist_setup(args):
 from paper_2603_09621_b200.distributed import pair_weights, slab_for_rank  # noqa: E402
 
 
-def problem_for(cfg_id):
+def problem_for(cfg_id, device=None):
+    """The benchmark problem (phantom -> degrade -> init).  With a CUDA device
+    the phantom and degrade run there (bit-identical, faster setup); the
+    reference arm builds its inputs on the host."""
     from paper_2603_09621_b200 import synth
-    return synth.make_problem(synth.CONFIGS[cfg_id])
+    return synth.make_problem(synth.CONFIGS[cfg_id], device=device)
 
 
 # ----------------------------------------------------------------- CPU arm
@@ -341,7 +344,7 @@ def run_ours(args, dist, ws, rank, local):
 
     dev = torch.device("cuda", local)
     lib = _lib.lib()
-    p = problem_for(args.config)
+    p = problem_for(args.config, dev)
     lr_grid, hr_grid = p["lr_grid"], p["hr_grid"]
     lr = gs.Volume(lr_grid, p["lr"])
     opts = gs.RenderOptions()
@@ -646,7 +649,7 @@ def config2_fit(gs, dev, iterations: int) -> dict:
     `iterations` iterations through the public API (init, graph capture,
     every iteration's loss read), wall clock."""
     import torch
-    p = problem_for(2)
+    p = problem_for(2, dev)
     lr = gs.Volume(p["lr_grid"], p["lr"])
     gs.fit(lr, gs.InitConfig(background_threshold=0.0), gs.FitConfig(iterations=3))  # warm-up
     torch.cuda.synchronize(dev)
@@ -666,7 +669,7 @@ def config4_step_render(gs, dev, args) -> dict:
     N = 2,621,440): graph-replayed train steps (CUDA events) and the HR render
     (Renderer graph replays)."""
     import torch
-    p = problem_for(4)
+    p = problem_for(4, dev)
     lr = gs.Volume(p["lr_grid"], p["lr"])
     f = gs.GaussianField(*p["field"], device=dev)
     st = gs.AdamState.create(f)

@@ -481,6 +481,18 @@ int gsv_pool_loss_blocks(const gsv_grid* lr_grid);
 int gsv_pool_loss(const float* I, const float* W, const void* target, int target_dtype,
                   const gsv_grid* hr_grid, const gsv_grid* lr_grid, int fx, int fy, int fz,
                   int loss_kind, double eps_w, float* ab, double* loss_part, void* stream);
+/* gsv_phantom: generate_phantom (phantom.py:52-75) on the device.  prims:
+ * nprims x 7 doubles {cx, cy, cz, a_x, a_y, a_z, intensity} (semi-axes for
+ * kind 0 = ellipsoids, sigmas for kind 1 = gaussian mixture), rasterized at
+ * the voxel centres origin + index * spacing with the max at overlaps; then,
+ * if radius > 0, ndimage.gaussian_filter with the 2 radius + 1 weights
+ * (scipy's _gaussian_kernel1d, computed by the caller) along x, y, z with
+ * scipy's symmetric-correlation order and "reflect" edges; clipped to [0, 1]
+ * and written as float32, x-fastest linear.  Ellipsoids are bit-identical
+ * to the reference; the mixture's exp is the device's (within an ulp).
+ * scratch: 2 V doubles.  Added in ABI 6. */
+int gsv_phantom(const gsv_grid* grid, int kind, int nprims, const double* prims, int radius,
+                const double* weights, double* scratch, float* out, void* stream);
 int gsv_resample_trilinear(const void* src, int src_f64, const gsv_grid* src_grid,
                            void* out, const gsv_grid* dst_grid, void* stream);
 int gsv_init_workspace(const gsv_grid* grid, size_t* bytes);

@@ -107,6 +107,7 @@ _SIGS = {
                    c_vp, c_vp],
     "gsv_render_naive": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_int, GP, c_dbl, c_dbl, c_int,
                          c_vp, c_vp],
+    "gsv_phantom": [GP, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp],
     "gsv_resample_trilinear": [c_vp, c_int, GP, c_vp, GP, c_vp],
     "gsv_pool_loss_blocks": [GP],
     "gsv_pool_loss": [c_vp, c_vp, c_vp, c_int, GP, GP, c_int, c_int, c_int, c_int, c_dbl, c_vp,

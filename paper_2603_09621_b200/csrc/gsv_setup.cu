@@ -1,6 +1,6 @@
 // gsv_setup.cu -- one-time setup of a fit on the device:
-// trilinear resampling (volume.py:126-154) and init_from_volume
-// (field.py:212-234).
+// phantom rasterization and blur (phantom.py:52-75), trilinear resampling
+// (volume.py:126-154) and init_from_volume (field.py:212-234).
 //
 // resample: the reference's numpy operation order, every product and sum an
 // explicit round-to-nearest f64 op, so the result is bit-identical to
@@ -185,6 +185,71 @@ pool_loss_kernel(const float* __restrict__ I, const float* __restrict__ W,
   }
 }
 
+// ---- phantom (phantom.py:52-75).  Voxel (i, j, k) at axis_coords (origin +
+// index * spacing); d2 = ((x - c) / a)^2 summed x, y, z left to right, each
+// op rounded as numpy does; max over the primitives in order.  The volume is
+// x-fastest linear (Volume.linear()).  Ellipsoids: intensity where d2 <= 1.
+// Gaussian mixture: intensity * exp(-0.5 d2) (the device exp, within an ulp
+// of numpy's).
+__global__ void __launch_bounds__(256)
+phantom_kernel(gsv_grid g, int kind, int np_, const double* __restrict__ prims,
+               double* __restrict__ out) {
+  const int64_t nv = (int64_t)g.nx * g.ny * g.nz;
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int x = (int)(v % g.nx), y = (int)((v / g.nx) % g.ny),
+            z = (int)(v / ((int64_t)g.nx * g.ny));
+  const double px = add(g.ox, mul((double)x, g.sx)), py = add(g.oy, mul((double)y, g.sy)),
+               pz = add(g.oz, mul((double)z, g.sz));
+  double acc = 0.0;
+  for (int q = 0; q < np_; ++q) {
+    const double* pr = prims + 7 * q;   // cx cy cz ax ay az intensity
+    const double tx = __ddiv_rn(sub(px, pr[0]), pr[3]);
+    const double ty = __ddiv_rn(sub(py, pr[1]), pr[4]);
+    const double tz = __ddiv_rn(sub(pz, pr[2]), pr[5]);
+    const double d2 = add(add(mul(tx, tx), mul(ty, ty)), mul(tz, tz));
+    const double val = kind == 0 ? (d2 <= 1.0 ? pr[6] : 0.0) : mul(pr[6], exp(mul(-0.5, d2)));
+    acc = fmax(acc, val);
+  }
+  out[v] = acc;
+}
+
+// One axis of ndimage.gaussian_filter (scipy's symmetric correlate1d, mode
+// "reflect"): o = x[c] w[r] + sum_{j = -r .. -1} (x[c + j] + x[c - j]) w[r + j]
+// in that order, indices reflected about the half-sample edges.
+__device__ __forceinline__ int reflect_index(int i, int n) {
+  const int p = 2 * n;
+  int m = i % p;
+  if (m < 0) m += p;
+  return m < n ? m : p - 1 - m;
+}
+
+__global__ void __launch_bounds__(256)
+blur_axis_kernel(const double* __restrict__ in, double* __restrict__ out, int nx, int ny, int nz,
+                 int axis, int radius, const double* __restrict__ w) {
+  const int64_t nv = (int64_t)nx * ny * nz;
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((int64_t)nx * ny));
+  const int n = axis == 0 ? nx : (axis == 1 ? ny : nz);
+  const int c = axis == 0 ? x : (axis == 1 ? y : z);
+  const int64_t stride = axis == 0 ? 1 : (axis == 1 ? (int64_t)nx : (int64_t)nx * ny);
+  const int64_t base = v - (int64_t)c * stride;
+  double o = mul(in[v], w[radius]);
+  for (int j = -radius; j < 0; ++j) {
+    const double a = in[base + (int64_t)reflect_index(c + j, n) * stride];
+    const double b = in[base + (int64_t)reflect_index(c - j, n) * stride];
+    o = add(o, mul(add(a, b), w[radius + j]));
+  }
+  out[v] = o;
+}
+
+__global__ void __launch_bounds__(256)
+clip_f32_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t nv) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v < nv) out[v] = (float)fmin(fmax(in[v], 0.0), 1.0);
+}
+
 }  // namespace
 }  // namespace gsv
 
@@ -266,6 +331,35 @@ int gsv_init_fill(const void* data, int data_f64, const gsv_grid* grid, double t
       m, slot, *grid, log_scales3[0], log_scales3[1], log_scales3[2], raw_relax, positions,
       log_scales, rotations, raw_amplitude, raw_relax_out);
   GSV_CHECK_LAUNCH("init_fill_kernel");
+  return GSV_OK;
+}
+
+int gsv_phantom(const gsv_grid* grid, int kind, int nprims, const double* prims, int radius,
+                const double* weights, double* scratch, float* out, void* stream) {
+  GSV_REQUIRE(grid && out && scratch, "null pointer argument");
+  GSV_REQUIRE(grid->nx >= 1 && grid->ny >= 1 && grid->nz >= 1, "grid dims must be >= 1");
+  GSV_REQUIRE(kind == 0 || kind == 1, "kind must be 0 (ellipsoids) or 1 (gaussian mixture)");
+  GSV_REQUIRE(nprims >= 0 && (nprims == 0 || prims != nullptr), "bad primitive list");
+  GSV_REQUIRE(radius >= 0 && (radius == 0 || weights != nullptr), "bad blur weights");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nv = (int64_t)grid->nx * grid->ny * grid->nz;
+  const unsigned blocks = (unsigned)((nv + 255) / 256);
+  double* a = scratch;
+  double* b = scratch + nv;
+  phantom_kernel<<<blocks, 256, 0, s>>>(*grid, kind, nprims, prims, a);
+  GSV_CHECK_LAUNCH("phantom_kernel");
+  if (radius > 0) {
+    for (int axis = 0; axis < 3; ++axis) {
+      blur_axis_kernel<<<blocks, 256, 0, s>>>(a, b, grid->nx, grid->ny, grid->nz, axis, radius,
+                                              weights);
+      GSV_CHECK_LAUNCH("blur_axis_kernel");
+      double* t = a;
+      a = b;
+      b = t;
+    }
+  }
+  clip_f32_kernel<<<blocks, 256, 0, s>>>(a, out, nv);
+  GSV_CHECK_LAUNCH("clip_f32_kernel");
   return GSV_OK;
 }
 

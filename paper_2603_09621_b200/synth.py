@@ -1,10 +1,12 @@
-"""Synthetic benchmark inputs -- host setup.
+"""Synthetic benchmark inputs -- setup.
 
 Restates the reference's phantom generator (phantom.py:52-108) and the
 degrade/init recipe with the same numpy/scipy calls, so the LR volumes and
 initial fields are bit-identical to the reference's (pinned by sha256 in
-tests/golden/).  This runs once per problem on the host, like the
-reference's setup; it is not part of the rendering path.
+tests/golden/).  generate_phantom_device / make_problem(device=...) run the
+phantom and the degrade on the GPU (gsv_phantom: scipy's gaussian_filter
+order restated), bit-identical for the ellipsoid phantoms.  Setup, not the
+rendering path.
 """
 
 from __future__ import annotations
@@ -60,6 +62,47 @@ def generate_ellipsoids(prims, grid: GridSpec, smooth_sigma: float = 0.0) -> np.
     return out.astype(np.float32)
 
 
+def gaussian_kernel1d(sigma: float, truncate: float = 4.0):
+    """(weights, radius) of ndimage.gaussian_filter's order-0 kernel
+    (scipy _gaussian_kernel1d with radius int(truncate * sigma + 0.5))."""
+    sd = float(sigma)
+    radius = int(truncate * sd + 0.5)
+    x = np.arange(-radius, radius + 1)
+    phi = np.exp(-0.5 / (sd * sd) * x ** 2)
+    return phi / phi.sum(), radius
+
+
+def generate_phantom_device(prims, grid: GridSpec, smooth_sigma: float = 0.0,
+                            kind: str = "ellipsoids", device=None):
+    """generate_phantom (phantom.py:52-75) on the GPU (gsv_phantom): the
+    float32 volume as an x-fastest linear CUDA tensor.  prims: objects with
+    center, semi_axes (ellipsoids) or sigmas (gaussian mixture), intensity.
+    Ellipsoids are bit-identical to generate_ellipsoids (the host path)."""
+    import torch
+    from . import _lib
+    if kind not in ("ellipsoids", "gaussian-mixture"):
+        raise ValueError(f"unknown phantom kind {kind!r}")
+    if smooth_sigma < 0:
+        raise ValueError("smooth_sigma must be >= 0")
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    rows = [list(q.center) + list(q.semi_axes if kind == "ellipsoids" else q.sigmas) +
+            [float(q.intensity)] for q in prims]
+    pr = torch.tensor(np.asarray(rows, dtype=np.float64).reshape(-1, 7), device=dev)
+    radius, w = 0, None
+    if smooth_sigma > 0:
+        wn, radius = gaussian_kernel1d(smooth_sigma)
+        w = torch.from_numpy(wn).to(dev)
+    nv = grid.num_voxels
+    scratch = torch.empty(2 * nv, dtype=torch.float64, device=dev)
+    out = torch.empty(nv, dtype=torch.float32, device=dev)
+    lib = _lib.lib()
+    _lib.check(lib.gsv_phantom(_lib.make_grid(grid), 0 if kind == "ellipsoids" else 1,
+                               len(rows), pr.data_ptr() if rows else None, radius,
+                               None if w is None else w.data_ptr(), scratch.data_ptr(),
+                               out.data_ptr(), _lib.stream_ptr()), "phantom")
+    return out
+
+
 @dataclass(frozen=True)
 class BenchConfig:
     name: str
@@ -80,16 +123,26 @@ CONFIGS = {
 }
 
 
-def make_problem(cfg: BenchConfig, seed: int = 11):
+def make_problem(cfg: BenchConfig, seed: int = 11, device=None):
     """HR phantom -> trilinear LR -> init field (threshold 0 => N = #LR voxels).
 
     Returns dict(hr_grid, hr (np f32), lr_grid, lr (np f32), field arrays,
     render_grid).  Same recipe as the reference conftest (conftest.py:26-32).
+    device (a CUDA device): the phantom and the resampling run there
+    (gsv_phantom, gsv_resample_trilinear; bit-identical), the rest as on the host.
     """
     hr_grid = GridSpec(cfg.hr_dims, (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
-    hr = generate_ellipsoids(random_ellipsoids(hr_grid, seed), hr_grid, smooth_sigma=0.7)
     lr_grid = grid_covering_extent(hr_grid, cfg.lr_dims)
-    lr = resample_trilinear_np(hr, hr_grid, lr_grid)
+    prims = random_ellipsoids(hr_grid, seed)
+    if device is not None:
+        from .volume import Volume, resample_trilinear
+        hr_t = generate_phantom_device(prims, hr_grid, 0.7, device=device)
+        hr_v = Volume.from_linear(hr_grid, hr_t)
+        hr = hr_v.numpy()
+        lr = resample_trilinear(hr_v, lr_grid).numpy()
+    else:
+        hr = generate_ellipsoids(prims, hr_grid, smooth_sigma=0.7)
+        lr = resample_trilinear_np(hr, hr_grid, lr_grid)
     arrays = list(init_arrays_from_volume(lr, lr_grid, InitConfig(background_threshold=0.0)))
     if cfg.jitter:
         arrays = jitter_field(arrays, lr_grid)

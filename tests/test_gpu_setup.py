@@ -59,3 +59,57 @@ def test_init_from_volume_on_device(case):
         np.testing.assert_array_equal(got[k], want[k])
     ulp = np.abs(got[3] - want[3]) / np.spacing(np.abs(want[3]))
     assert ulp.max() <= 4, ulp.max()
+
+
+# ------------------------------------------------ phantom (phantom.py:52-75)
+@pytest.mark.parametrize("dims,sigma,seed", [((64, 64, 64), 0.7, 11), ((37, 20, 9), 1.3, 3),
+                                             ((256, 256, 128), 0.7, 11), ((5, 3, 2), 2.5, 7),
+                                             ((24, 24, 24), 0.0, 5)])
+def test_phantom_ellipsoids_bit_identical(dims, sigma, seed):
+    """The device phantom (rasterization, scipy's gaussian_filter order with
+    reflect edges, clip, float32) equals the host restatement bit for bit,
+    which in turn equals the reference (tests/test_oracle_golden.py)."""
+    from paper_2603_09621_b200.synth import (generate_ellipsoids, generate_phantom_device,
+                                             random_ellipsoids)
+    g = GridSpec(dims, (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    prims = random_ellipsoids(g, seed)
+    want = generate_ellipsoids(prims, g, smooth_sigma=sigma)
+    got = gs.Volume.from_linear(g, generate_phantom_device(prims, g, sigma)).numpy()
+    np.testing.assert_array_equal(got, want)
+
+
+def test_phantom_gaussian_mixture_matches_reference_formula():
+    from scipy import ndimage
+    from paper_2603_09621_b200.synth import generate_phantom_device
+
+    class Blob:
+        def __init__(self, c, s, i):
+            self.center, self.sigmas, self.intensity = c, s, i
+
+    g = GridSpec((33, 21, 17), (0.8, 1.1, 1.5), (-2.0, 1.0, 0.5))
+    rng = np.random.default_rng(2)
+    lo, hi = (np.asarray(a) for a in g.extent())
+    blobs = [Blob(tuple(lo + (hi - lo) * rng.uniform(0.2, 0.8, 3)),
+                  tuple((hi - lo) * rng.uniform(0.05, 0.15, 3)), float(rng.uniform(0.3, 1.0)))
+             for _ in range(5)]
+    xs, ys, zs = (g.axis_coords(k) for k in range(3))
+    xs, ys, zs = xs[:, None, None], ys[None, :, None], zs[None, None, :]
+    want = np.zeros(g.dims)
+    for b in blobs:
+        (cx, cy, cz), (sx, sy, sz) = b.center, b.sigmas
+        d2 = ((xs - cx) / sx) ** 2 + ((ys - cy) / sy) ** 2 + ((zs - cz) / sz) ** 2
+        np.maximum(want, b.intensity * np.exp(-0.5 * d2), out=want)
+    want = np.clip(ndimage.gaussian_filter(want, sigma=0.9), 0.0, 1.0).astype(np.float32)
+    got = gs.Volume.from_linear(g, generate_phantom_device(blobs, g, 0.9,
+                                                           kind="gaussian-mixture")).numpy()
+    # exp on the device vs numpy: within an ulp before the blur
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-7)
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_make_problem_on_device_identical(cid):
+    from paper_2603_09621_b200.synth import sha256
+    a = make_problem(CONFIGS[cid])
+    b = make_problem(CONFIGS[cid], device=torch.device("cuda", 0))
+    assert sha256(a["hr"]) == sha256(b["hr"]) and sha256(a["lr"]) == sha256(b["lr"])
+    assert sha256(*a["field"]) == sha256(*b["field"])
