@@ -138,8 +138,19 @@ __device__ __forceinline__ void preprocess_one(int64_t i, const double p[3], con
     const double spc[3] = {g.sx, g.sy, g.sz};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const double glo = __ddiv_rn(sub(sub(p[a], half[a]), org[a]), spc[a]);
-      const double ghi = __ddiv_rn(sub(add(p[a], half[a]), org[a]), spc[a]);
+      // a power-of-two spacing divides exactly as a product with its
+      // (exact) reciprocal: two f64 multiplies instead of two divisions
+      const bool pow2 = (__double_as_longlong(spc[a]) & 0x000FFFFFFFFFFFFFLL) == 0 &&
+                        spc[a] >= 0x1p-1000 && spc[a] <= 0x1p1000;
+      double glo, ghi;
+      if (pow2) {
+        const double inv = __drcp_rn(spc[a]);
+        glo = mul(sub(sub(p[a], half[a]), org[a]), inv);
+        ghi = mul(sub(add(p[a], half[a]), org[a]), inv);
+      } else {
+        glo = __ddiv_rn(sub(sub(p[a], half[a]), org[a]), spc[a]);
+        ghi = __ddiv_rn(sub(add(p[a], half[a]), org[a]), spc[a]);
+      }
       int64_t vlo = np_to_int64(ceil(sub(glo, 0.5)));
       int64_t vhi = np_to_int64(floor(add(ghi, 0.5)));
       vlo = clip64(vlo, 0, dims[a] - 1);
