@@ -4,7 +4,8 @@
 python tools/e2e_probe.py [--config 3] [--steps 100]
 Wall-clocks fit()'s pipelined loop (step_async, one step queued ahead, loss
 read per step) with: nothing else; set_target from a device tensor each
-step; the bench's pinned-H2D prefetch on a copy stream + set_target.
+step; a pinned-H2D prefetch on a copy stream + set_target; the bench's
+set_target_source (the H2D inside each replayed graph).
 """
 
 from __future__ import annotations
@@ -73,8 +74,12 @@ def main():
 
     freed.record(cur)
     prefetch()
+    def source():
+        return step.step_async(f, state, lrs)
+
     for name, fn in (("plain", plain), ("set_target", with_target), ("h2d", with_h2d),
-                     ("plain", plain)):
+                     ("source", source), ("plain", plain)):
+        step.set_target_source(host_t if name == "source" else None)
         loop(5, fn)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
