@@ -181,8 +181,10 @@ int gsv_bin_fill_capacity(const int32_t* counts, const int32_t* box,
  * starts_out is all zero (empty lists downstream) and starts / gids are left
  * as they were (after an excess of changes or edits *chg_count is left above
  * chg_cap, so later calls overflow too); the caller rebuilds from scratch.
- * Scratch: ops (16384 x uint64), nops (1 int32), lens (2 (nbricks_slab + 1)
- * int32); workspace from gsv_bin_incremental_workspace(nbricks_slab). */
+ * Scratch: ops (2 x 16384 uint64), nops (1 int32, zero before the first
+ * call), lens (8 (nbricks_slab + 1) int32, 8-byte aligned, zero before the
+ * first call; after an overflow the scratch is poisoned and every later call
+ * overflows until it is zeroed again); workspace from gsv_bin_incremental_workspace(nbricks_slab). */
 int gsv_preprocess_track(const double* positions, const double* log_scales,
                          const double* rotations, const double* raw_amplitude,
                          const double* raw_relax, int64_t n, int relax_enabled,

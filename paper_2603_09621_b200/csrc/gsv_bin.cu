@@ -189,18 +189,23 @@ __global__ void unsorted_kernel(const int64_t* __restrict__ starts,
 
 // ------------------------------------------------- incremental binning
 // Between two fit() iterations only a few Gaussians change their brick box
-// (~100 of 2.1 M per step at config 3), so the graph step keeps last step's
-// lists and edits them: the preprocess pass records every Gaussian whose box
-// or pair count changed (PrepArgs change tracking); incr_ops_kernel turns
-// those into (brick, gid, remove | insert) edits, sorted by (brick, gid);
-// the new list lengths are scanned into new CSR starts; incr_merge_kernel
-// rebuilds each list -- a copy for the untouched bricks, an ordered merge of
-// the surviving and inserted gids for the edited ones -- into the output
-// buffers, which are then copied back as the next step's input.  The result
+// (~100 of 2.1 M per step at config 3; up to ~2000 in iterations 20-60), so
+// the graph step keeps last step's lists and edits them.  The preprocess pass
+// records every Gaussian whose box or pair count changed (PrepArgs change
+// tracking).  incr_ops_kernel turns those into (brick, gid, remove | insert)
+// edits -- the bricks of the old box run not in the new one and vice versa --
+// appended to a flat array while per-brick counters count each brick's
+// edits and its length change; the new lengths and the edit counts are
+// scanned together (one packed int64 scan) into the new CSR starts and the
+// per-brick edit offsets; the edits are scattered into per-brick segments
+// (the counters return to zero on the way); one warp per brick then copies
+// its list (no edits) or sorts its few edits by gid and merges the survivors
+// and the insertions in gid order into the output buffers.  The result
 // equals a full rebuild (each list is the ascending gids of the Gaussians
-// whose box run contains the brick); any capacity excess (edits, changed
-// Gaussians, pairs) raises the overflow flag and the caller rebuilds.
-constexpr int kOpsCap = 16384;      // edits per step (sorted in one CTA's shared memory)
+// whose box run contains the brick); any capacity excess (changed Gaussians,
+// edits, pairs) or a pair count that differs from the counts' scan raises
+// the overflow flag and the caller rebuilds.
+constexpr int kOpsCap = 16384;      // edits per step
 
 // Is slab-local brick `key` in the box run (box record, count) of a Gaussian?
 __device__ __forceinline__ bool run_contains(const GBox& gb, int cnt, int key,
@@ -217,148 +222,155 @@ __device__ __forceinline__ bool run_contains(const GBox& gb, int cnt, int key,
   return r >= 0 && r < cnt;
 }
 
-template <class F>
-__device__ __forceinline__ void for_each_box_run(const GBox& b, int c, const gsv_bricks& k,
-                                                 F f) {
-  if (c <= 0) return;
-  int rx = b.k0 % b.nb_x;
-  const int t = b.k0 / b.nb_x;
-  int ry = t % b.nb_y;
-  const int bxy = k.bgx * k.bgy;
-  int key = b.blo_x + k.bgx * (b.blo_y + k.bgy * b.blo_z) - k.b0 + rx + k.bgx * ry +
-            bxy * (t / b.nb_y);
-  for (int r = 0; r < c; ++r) {
-    f(key);
-    ++key;
-    if (++rx == b.nb_x) {
-      rx = 0;
-      key += k.bgx - b.nb_x;
-      if (++ry == b.nb_y) {
-        ry = 0;
-        key += bxy - k.bgx * b.nb_y;
-      }
-    }
-  }
+// Per-brick scratch of the incremental pass (int32 words, B = slab bricks;
+// 8 (B + 1) words, zero when first used): [0, B+1) edit counters, [B+1,
+// 2B+2) length changes (both back to zero after every clean call), then
+// int64 [B+1] packed (length << 24 | edits), int64 [B+1] its exclusive
+// scan, int32 [B+1] the edit offsets, and one poison word: set by any
+// overflow (not a dry run), it makes every later call overflow -- the
+// counters may be dirty -- until the caller rebuilds with fresh scratch.
+struct IncrScratch {
+  int32_t* bcnt;
+  int32_t* bdelta;
+  int64_t* packed;
+  int64_t* scanned;
+  int32_t* opbeg;
+  int32_t* poison;
+  __host__ __device__ IncrScratch(int32_t* w, int64_t nb)
+      : bcnt(w), bdelta(w + (nb + 1)), packed(reinterpret_cast<int64_t*>(w + 2 * (nb + 1))),
+        scanned(reinterpret_cast<int64_t*>(w + 4 * (nb + 1))), opbeg(w + 6 * (nb + 1)),
+        poison(w + 7 * (nb + 1)) {}
+};
+
+// slab-local brick of entry r (box order from k0) of a box run
+__device__ __forceinline__ int run_brick(const GBox& b, int r, const gsv_bricks& k) {
+  const int t = b.k0 + r;
+  const int rx = t % b.nb_x, u = t / b.nb_x;
+  const int ry = u % b.nb_y, rz = u / b.nb_y;
+  return (b.blo_x + rx) + k.bgx * ((b.blo_y + ry) + k.bgy * (b.blo_z + rz)) - k.b0;
 }
 
-// edit key: brick << 32 | gid << 1 | insert
-__global__ void __launch_bounds__(1024)
+// edit key: brick << 32 | gid << 1 | insert.  One warp per changed Gaussian:
+// the lanes take the bricks of its old and new box runs, keep those not in
+// the other run, and the warp reserves its edits with one atomic.
+__global__ void __launch_bounds__(128)
 incr_ops_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ box,
-                gsv_bricks k, int32_t* __restrict__ chg_count,
+                gsv_bricks k, const int32_t* __restrict__ chg_count,
                 const int32_t* __restrict__ chg_gid, const int32_t* __restrict__ chg_old,
                 const int32_t* __restrict__ chg_oldcnt, int chg_cap,
-                const int32_t* __restrict__ dry, unsigned long long* __restrict__ ops,
-                int32_t* __restrict__ nops_out, int32_t* __restrict__ overflow) {
-  extern __shared__ unsigned long long sops[];   // kOpsCap entries
-  __shared__ int snops, sbad;
-  const int tid = threadIdx.x;
+                const int32_t* __restrict__ dry, unsigned long long* __restrict__ raw,
+                int32_t* __restrict__ nraw, int32_t* __restrict__ bcnt,
+                int32_t* __restrict__ bdelta) {
   const int nc = *chg_count;
-  if (tid == 0) {
-    snops = 0;
-    sbad = (dry != nullptr && *dry != 0) ? 2 : (nc > chg_cap ? 1 : 0);
-  }
-  __syncthreads();
-  if (sbad == 0) {
-    for (int e = tid; e < nc; e += blockDim.x) {
-      const int gid = chg_gid[e];
-      const GBox ob = unpack_box(chg_old, e), nbx = unpack_box(box, gid);
-      const int oc = chg_oldcnt[e], ncnt = counts[gid];
-      auto push = [&](int key, unsigned ins) {
-        const int j = atomicAdd(&snops, 1);
-        if (j < kOpsCap)
-          sops[j] = ((unsigned long long)(unsigned)key << 32) | ((unsigned)gid << 1) | ins;
-        else
-          sbad = 1;
-      };
-      for_each_box_run(ob, oc, k, [&](int key) {
-        if (!run_contains(nbx, ncnt, key, k)) push(key, 0u);
-      });
-      for_each_box_run(nbx, ncnt, k, [&](int key) {
-        if (!run_contains(ob, oc, key, k)) push(key, 1u);
-      });
-    }
-  }
-  __syncthreads();
-  const int n = sbad ? 0 : min(snops, kOpsCap);
-  int p2 = 1;
-  while (p2 < n) p2 <<= 1;
-  for (int i = n + tid; i < p2; i += blockDim.x) sops[i] = ~0ull;
-  __syncthreads();
-  // bitonic sort of the n edits (padded to a power of two)
-  for (int size = 2; size <= p2; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < p2; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const unsigned long long a = sops[i], b = sops[j];
-          const bool up = (i & size) == 0;
-          if ((a > b) == up) {
-            sops[i] = b;
-            sops[j] = a;
-          }
-        }
+  if (nc > chg_cap || (dry != nullptr && *dry != 0)) return;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < nc; e += nwarps) {
+    const int gid = chg_gid[e];
+    const GBox ob = unpack_box(chg_old, e), nbx = unpack_box(box, gid);
+    const int oc = chg_oldcnt[e], ncnt = counts[gid];
+    const int rounds = (max(oc, ncnt) + 31) >> 5;
+    for (int q = 0; q < rounds; ++q) {
+      const int r = 32 * q + lane;
+      int krm = -1, kin = -1;
+      if (r < oc) {
+        const int key = run_brick(ob, r, k);
+        if (!run_contains(nbx, ncnt, key, k)) krm = key;
       }
-      __syncthreads();
+      if (r < ncnt) {
+        const int key = run_brick(nbx, r, k);
+        if (!run_contains(ob, oc, key, k)) kin = key;
+      }
+      const int m = (krm >= 0) + (kin >= 0);
+      int incl = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (tot == 0) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(nraw, tot);   // past kOpsCap: overflow, seen in *nraw
+      int j = __shfl_sync(0xffffffffu, base, 0) + incl - m;
+      if (krm >= 0) {
+        if (j < kOpsCap) {
+          raw[j] = ((unsigned long long)(unsigned)krm << 32) | ((unsigned)gid << 1);
+          atomicAdd(bcnt + krm, 1);
+          atomicAdd(bdelta + krm, -1);
+        }
+        ++j;
+      }
+      if (kin >= 0 && j < kOpsCap) {
+        raw[j] = ((unsigned long long)(unsigned)kin << 32) | ((unsigned)gid << 1) | 1u;
+        atomicAdd(bcnt + kin, 1);
+        atomicAdd(bdelta + kin, 1);
+      }
     }
-  for (int i = tid; i < n; i += blockDim.x) ops[i] = sops[i];
-  if (tid == 0) {
-    *nops_out = n;
-    *overflow = sbad ? 1 : 0;
-    // consumed; after an excess the count stays above the cap, so steps
-    // already queued behind this one overflow too until the caller rebuilds
-    if (sbad == 0) *chg_count = 0;
   }
 }
 
-// first edit index with key >= v
-__device__ __forceinline__ int ops_lower(const unsigned long long* __restrict__ ops, int n,
-                                         unsigned long long v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (ops[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// lens[b] = the new list length, opbeg[b] = the brick's first edit
-// (opbeg[nb] = the edit count)
+// packed[b] = new length << 24 | edits of brick b; thread nb also decides the
+// step's first overflow conditions
 __global__ void __launch_bounds__(256)
-incr_len_kernel(const int64_t* __restrict__ starts, int32_t nb,
-                const unsigned long long* __restrict__ ops, const int32_t* __restrict__ nops,
-                int32_t* __restrict__ lens, int32_t* __restrict__ opbeg) {
+incr_len_kernel(const int64_t* __restrict__ starts, int32_t nb, const int32_t* __restrict__ bcnt,
+                const int32_t* __restrict__ bdelta, int64_t* __restrict__ packed,
+                const int32_t* __restrict__ chg_count, int chg_cap,
+                const int32_t* __restrict__ nraw, const int32_t* __restrict__ dry,
+                const int32_t* __restrict__ poison, int32_t* __restrict__ overflow) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b > nb) return;
-  const int n = *nops;
   if (b == nb) {
-    lens[b] = 0;
-    opbeg[b] = n;
+    packed[b] = 0;
+    *overflow = (*chg_count > chg_cap || *nraw > kOpsCap || (dry != nullptr && *dry != 0) ||
+                 *poison != 0) ? 1 : 0;
     return;
   }
-  int d = 0, p0 = 0;
-  if (n > 0) {
-    p0 = ops_lower(ops, n, (unsigned long long)(unsigned)b << 32);
-    const int p1 = ops_lower(ops, n, (unsigned long long)(unsigned)(b + 1) << 32);
-    for (int p = p0; p < p1; ++p) d += (ops[p] & 1ull) ? 1 : -1;
+  const int64_t len = (starts[b + 1] - starts[b]) + bdelta[b];
+  packed[b] = (len << 24) | (int64_t)bcnt[b];
+}
+
+// split the scan: new starts and edit offsets; the edited lists must hold
+// exactly the pairs the counts give (gstart[n]) and fit the capacity
+__global__ void __launch_bounds__(256)
+incr_split_kernel(const int64_t* __restrict__ scanned, int32_t nb,
+                  int64_t* __restrict__ starts_out, int32_t* __restrict__ opbeg,
+                  const int64_t* __restrict__ gstart, int64_t n, int64_t cap,
+                  int32_t* __restrict__ overflow) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nb) return;
+  const int64_t v = scanned[b];
+  starts_out[b] = v >> 24;
+  opbeg[b] = (int32_t)(v & 0xFFFFFF);
+  if (b == nb) {
+    const int64_t p = v >> 24;
+    if (p > cap || p != gstart[n]) *overflow = 1;
   }
-  opbeg[b] = p0;
-  lens[b] = (int32_t)(starts[b + 1] - starts[b]) + d;
 }
 
-// the edited lists must hold exactly the pairs the counts give (gstart[n])
-// and fit the capacity
-__global__ void incr_check_kernel(const int64_t* __restrict__ starts_out, int32_t nb,
-                                  const int64_t* __restrict__ gstart, int64_t n, int64_t cap,
-                                  int32_t* __restrict__ overflow) {
-  const int64_t p = starts_out[nb];
-  if (p > cap || p != gstart[n]) *overflow = 1;
+// the edits into their bricks' segments; the counters return to zero
+__global__ void __launch_bounds__(256)
+incr_scatter_kernel(const unsigned long long* __restrict__ raw, const int32_t* __restrict__ nraw,
+                    const int32_t* __restrict__ opbeg, int32_t* __restrict__ bcnt,
+                    int32_t* __restrict__ bdelta, unsigned long long* __restrict__ ops,
+                    const int32_t* __restrict__ overflow) {
+  if (*overflow != 0) return;
+  const int n = *nraw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long o = raw[i];
+    const int key = (int)(o >> 32);
+    const int slot = atomicSub(bcnt + key, 1) - 1;
+    ops[opbeg[key] + slot] = o;
+    bdelta[key] = 0;                          // read by incr_len_kernel already
+  }
 }
 
-// one warp per brick: copy, or merge the surviving and inserted gids.  The
-// brick's edits (sorted by gid) are staged in shared memory with the
-// exclusive prefix count of insertions, so each old entry finds the edits
-// before it by binary search: new index = old index - removals before +
-// insertions before.  Segments over kMergeSeg edits take a linear path.
+// one warp per brick: copy, or merge the surviving and inserted gids.  A
+// brick's edits (at most kMergeSeg; gids are distinct within a brick) are
+// ranked by gid into shared memory with the exclusive prefix count of
+// insertions, so each old entry finds the edits before it by binary search:
+// new index = old index - removals before + insertions before.  Longer edit
+// segments take a linear path (order-independent counts).
 constexpr int kMergeSeg = 256;
 
 __global__ void __launch_bounds__(256)
@@ -366,8 +378,8 @@ incr_merge_kernel(const int64_t* __restrict__ starts, const int32_t* __restrict_
                   const int64_t* __restrict__ starts_out, int32_t* __restrict__ gids_out,
                   int32_t nb, const unsigned long long* __restrict__ ops,
                   const int32_t* __restrict__ opbeg, const int32_t* __restrict__ overflow) {
-  __shared__ unsigned sg[8][kMergeSeg];   // edit gid << 1 | insert
-  __shared__ int spre[8][kMergeSeg + 1];   // insertions before edit q
+  __shared__ unsigned sg[8][kMergeSeg];      // edit gid << 1 | insert, sorted
+  __shared__ int spre[8][kMergeSeg + 1];     // insertions before edit q
   const int warp = threadIdx.x >> 5;
   const int b = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -383,12 +395,18 @@ incr_merge_kernel(const int64_t* __restrict__ starts, const int32_t* __restrict_
   if (seg <= kMergeSeg) {
     unsigned* eg = sg[warp];
     int* ep = spre[warp];
+    // rank each edit by gid (distinct within the brick) into its sorted slot
+    for (int q = lane; q < seg; q += 32) {
+      const unsigned v = (unsigned)ops[p0 + q];
+      int r = 0;
+      for (int u = 0; u < seg; ++u) r += (unsigned)ops[p0 + u] < v;
+      eg[r] = v;
+    }
+    __syncwarp();
     int run = 0;
     for (int q0 = 0; q0 < seg; q0 += 32) {
       const int q = q0 + lane;
-      const unsigned v = q < seg ? (unsigned)ops[p0 + q] : 0u;   // gid << 1 | insert
-      if (q < seg) eg[q] = v;
-      const int ins = (q < seg) ? (int)(v & 1u) : 0;
+      const int ins = (q < seg) ? (int)(eg[q] & 1u) : 0;
       int incl = ins;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -477,16 +495,26 @@ incr_merge_kernel(const int64_t* __restrict__ starts, const int32_t* __restrict_
 }
 
 // overflow: empty lists downstream; otherwise (copy_back) the output becomes
-// next step's input -- a caller that alternates the two buffers skips the copy
+// next step's input -- a caller that alternates the two buffers skips the
+// copy.  Resets the edit and change counters for the next call (kept after
+// an overflow, so steps already queued behind this one overflow too until
+// the caller rebuilds).
 __global__ void __launch_bounds__(256)
 incr_commit_kernel(int64_t* __restrict__ starts, int32_t* __restrict__ gids,
                    int64_t* __restrict__ starts_out, const int32_t* __restrict__ gids_out,
-                   int32_t nb, const int32_t* __restrict__ overflow, int copy_back) {
+                   int32_t nb, const int32_t* __restrict__ overflow, int copy_back,
+                   int32_t* __restrict__ nraw, int32_t* __restrict__ chg_count,
+                   const int32_t* __restrict__ dry, int32_t* __restrict__ poison) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (*overflow != 0) {
     for (int64_t i = i0; i <= nb; i += stride) starts_out[i] = 0;
+    if (i0 == 0 && !(dry != nullptr && *dry != 0)) *poison = 1;
     return;
+  }
+  if (i0 == 0) {
+    *nraw = 0;
+    *chg_count = 0;
   }
   if (!copy_back) return;
   for (int64_t i = i0; i <= nb; i += stride) starts[i] = starts_out[i];
@@ -739,9 +767,8 @@ int gsv_preprocess_track(const double* positions, const double* log_scales,
 int gsv_bin_incremental_workspace(int32_t nbricks, size_t* bytes) {
   GSV_REQUIRE(bytes != nullptr, "bytes must not be NULL");
   size_t scan_bytes = 0;
-  thrust::transform_iterator<ToI64, const int32_t*, int64_t> it(nullptr, ToI64());
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, it, (int64_t*)nullptr,
-                                                (int)nbricks + 1);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const int64_t*)nullptr,
+                                                (int64_t*)nullptr, (int)nbricks + 1);
   if (e != cudaSuccess) return cuda_status(e, "DeviceScan sizing");
   *bytes = scan_bytes + 256;
   return GSV_OK;
@@ -760,38 +787,39 @@ int gsv_bin_incremental(const int32_t* counts, const int32_t* box, const int64_t
               "null pointer argument");
   GSV_REQUIRE(capacity >= 1 && capacity < (int64_t)INT32_MAX, "capacity %lld out of range",
               (long long)capacity);
+  GSV_REQUIRE((reinterpret_cast<uintptr_t>(lens) & 7) == 0, "lens must be 8-byte aligned");
   cudaStream_t s = as_stream(stream);
   const int64_t nb = slab_bricks(*bricks);
-  constexpr size_t ops_smem = sizeof(unsigned long long) * kOpsCap;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t ea = cudaFuncSetAttribute(incr_ops_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)ops_smem);
-    if (ea != cudaSuccess) return cuda_status(ea, "incr_ops_kernel smem attribute");
-    attr = true;
-  }
-  incr_ops_kernel<<<1, 1024, ops_smem, s>>>(counts, box, *bricks, chg_count, chg_gid, chg_old,
-                                            chg_oldcnt, chg_cap, dry, ops, nops, overflow);
+  const IncrScratch w(lens, nb);
+  unsigned long long* raw = ops;
+  unsigned long long* sorted = ops + kOpsCap;
+  const unsigned gb = (unsigned)((nb + 1 + 255) / 256);
+  // one warp per changed Gaussian (chg_cap warps: idle ones exit at once)
+  incr_ops_kernel<<<(unsigned)((chg_cap + 3) / 4), 128, 0, s>>>(counts, box, *bricks, chg_count,
+                                                                chg_gid, chg_old,
+                                     chg_oldcnt, chg_cap, dry, raw, nops, w.bcnt, w.bdelta);
   GSV_CHECK_LAUNCH("incr_ops_kernel");
-  int32_t* opbeg = lens + (nb + 1);
-  incr_len_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(starts, (int32_t)nb, ops,
-                                                                    nops, lens, opbeg);
+  incr_len_kernel<<<gb, 256, 0, s>>>(starts, (int32_t)nb, w.bcnt, w.bdelta, w.packed, chg_count,
+                                     chg_cap, nops, dry, w.poison, overflow);
   GSV_CHECK_LAUNCH("incr_len_kernel");
-  thrust::transform_iterator<ToI64, const int32_t*, int64_t> it(lens, ToI64());
   size_t bytes = workspace_bytes;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(workspace, bytes, it, starts_out, (int)nb + 1, s);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(workspace, bytes, w.packed, w.scanned,
+                                                (int)nb + 1, s);
   if (e != cudaSuccess) return cuda_status(e, "DeviceScan::ExclusiveSum");
-  incr_check_kernel<<<1, 1, 0, s>>>(starts_out, (int32_t)nb, gstart, n, capacity, overflow);
-  GSV_CHECK_LAUNCH("incr_check_kernel");
+  incr_split_kernel<<<gb, 256, 0, s>>>(w.scanned, (int32_t)nb, starts_out, w.opbeg, gstart, n,
+                                       capacity, overflow);
+  GSV_CHECK_LAUNCH("incr_split_kernel");
+  incr_scatter_kernel<<<16, 256, 0, s>>>(raw, nops, w.opbeg, w.bcnt, w.bdelta, sorted, overflow);
+  GSV_CHECK_LAUNCH("incr_scatter_kernel");
   if (nb > 0) {
     incr_merge_kernel<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, s>>>(
-        starts, gids, starts_out, gids_out, (int32_t)nb, ops, opbeg, overflow);
+        starts, gids, starts_out, gids_out, (int32_t)nb, sorted, w.opbeg, overflow);
     GSV_CHECK_LAUNCH("incr_merge_kernel");
   }
-  // without the copy only the overflow case has work: a small grid
-  incr_commit_kernel<<<copy_back ? 1184 : 32, 256, 0, s>>>(starts, gids, starts_out, gids_out,
-                                                          (int32_t)nb, overflow, copy_back);
+  // without the copy only the overflow case and the counter reset have work
+  incr_commit_kernel<<<copy_back ? 1184 : 32, 256, 0, s>>>(
+      starts, gids, starts_out, gids_out, (int32_t)nb, overflow, copy_back, nops, chg_count, dry,
+      w.poison);
   GSV_CHECK_LAUNCH("incr_commit_kernel");
   return GSV_OK;
 }

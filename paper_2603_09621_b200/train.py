@@ -634,9 +634,11 @@ def _graph_capture(self, f: GaussianField, state, lrs: dict, beta1, beta2, eps, 
         b["chg_oldcnt"] = gp.get("chg_oldcnt", (_CHG_CAP,), torch.int32)
         b["starts_out"] = gp.get("starts_out", (nb + 1,), torch.int64)
         b["gids_out"] = gp.get("gids_out", (cap,), torch.int32)
-        b["ops"] = gp.get("ops", (_OPS_CAP,), torch.int64)
-        b["nops"] = gp.get("nops", (1,), torch.int32)
-        b["lens"] = gp.get("lens", (2 * (nb + 1),), torch.int32)
+        b["ops"] = gp.get("ops", (2 * _OPS_CAP,), torch.int64)
+        b["nops"] = gp.get("nops", (1,), torch.int32, zeroed=True)
+        b["lens"] = gp.get("lens", (8 * (nb + 1),), torch.int32, zeroed=True)
+        b["nops"].zero_()
+        b["lens"].zero_()
     b["ws"] = gp.get("ws", (wsb,), torch.uint8)
     b["keys"] = gp.get("keys", (3, cap), torch.int32)
     b["gids"] = gp.get("gids", (cap,), torch.int32)
