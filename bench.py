@@ -446,10 +446,12 @@ def run_ours(args, dist, ws, rank, local):
     barrier()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    timed_caps0 = getattr(step, "graph_captures", 0)
     e0.record(s)
     losses = run_fit_steps(args.steps, train_launch)
     e1.record(s)
     barrier()
+    timed_captures = getattr(step, "graph_captures", 0) - timed_caps0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     assert all(math.isfinite(x) for x in losses), "non-finite loss in timed steps"
 
@@ -640,7 +642,7 @@ def run_ours(args, dist, ws, rank, local):
                 "phases_ms": {k: v[1] for k, v in phases.items()},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
                 "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
-                "loss_last": losses[-1]}
+                "graph_captures_timed": timed_captures, "loss_last": losses[-1]}
         print(json.dumps(line), flush=True)
 
 
