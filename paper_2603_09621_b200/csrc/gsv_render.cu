@@ -563,6 +563,36 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
   }
 }
 
+// Shared-memory accesses by 32-bit shared address: the base is formed once,
+// outside the loops (plain array indexing let ptxas rematerialise the
+// generic->shared window base, an S2UR with its latency, in every iteration).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("" : "+r"(a));   // opaque: keep it in a register
+  return a;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 // ------------------------------------------- forward f32, one warp per brick
 // Renders with large Gaussians (pairs >= 8 N: nearly every pair hits both
 // 8x4x4 tiles of a brick): one 32-thread CTA per 8x8x4 brick, lane l owns
@@ -571,15 +601,19 @@ forward32_kernel(const double* __restrict__ pos, const __grid_constant__ ExactSr
 // z-step follow from column A's in 5 FMAs.  No live masks (renders only).
 // Render form (no live masks): kept as its own function -- sharing the
 // masked template measurably changed the render kernel's scheduling (+1.5%).
-__device__ __forceinline__ void eval_column_hits_plain(const Pair32* __restrict__ hits, int nh,
+// hits_a: the 32-bit shared address of the compacted hits (an opaque base,
+// formed once: list B's `wsp + 32` otherwise made ptxas re-derive the shared
+// window base with an S2UR in every iteration)
+__device__ __forceinline__ void eval_column_hits_plain(uint32_t hits_a, int nh,
                                                        float mX, float mY, float mZ, float mZ1,
                                                        int gx, int gy, int gz,
                                                        const ExactSrc& xsrc, const gsv_grid& g,
                                                        double cut2d, float* aS, float* aW) {
   constexpr int Z = 4;
   for (int jj = 0; jj < nh; ++jj) {
-    const float4 pa = hits[jj].a, pb = hits[jj].b, pc = hits[jj].c;
-    const float2 pd = *reinterpret_cast<const float2*>(&hits[jj].d);   // qlo, gid
+    const uint32_t ja = hits_a + (uint32_t)jj * (uint32_t)sizeof(Pair32);
+    const float4 pa = lds_f4(ja), pb = lds_f4(ja + 16), pc = lds_f4(ja + 32);
+    const float2 pd = lds_f2(ja + 48);   // qlo, gid
     float q[Z];
     const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
     const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
@@ -621,15 +655,16 @@ __device__ __forceinline__ void eval_column_hits_plain(const Pair32* __restrict_
 // (the two-list whole-brick forward): q in nested form at the column's first
 // voxel, then second differences; live accumulation, then the guard band.
 template <bool MASKS>
-__device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits, int nh,
+__device__ __forceinline__ void eval_column_hits(uint32_t hits_a, int nh,
                                                  float mX, float mY, float mZ, float mZ1,
                                                  int gx, int gy, int gz, const ExactSrc& xsrc,
                                                  const gsv_grid& g, double cut2d,
-                                                 float* aS, float* aW, uint4* smw) {
+                                                 float* aS, float* aW, uint32_t smw_a) {
   constexpr int Z = 4;
   for (int jj = 0; jj < nh; ++jj) {
-    const float4 pa = hits[jj].a, pb = hits[jj].b, pc = hits[jj].c;
-    const float2 pd = *reinterpret_cast<const float2*>(&hits[jj].d);   // qlo, gid
+    const uint32_t ja = hits_a + (uint32_t)jj * (uint32_t)sizeof(Pair32);
+    const float4 pa = lds_f4(ja), pb = lds_f4(ja + 16), pc = lds_f4(ja + 32);
+    const float2 pd = lds_f2(ja + 48);   // qlo, gid
     float q[Z];
     const float t1 = fmaf(pb.x, mX, fmaf(pb.w, mY, fmaf(pc.x, mZ, pa.y)));
     const float t2 = fmaf(pb.y, mY, fmaf(pc.y, mZ, pa.z));
@@ -653,8 +688,9 @@ __device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits
       }
     }
     if constexpr (MASKS)   // the column's live words of this hit (warp-uniform stores)
-      smw[jj] = make_uint4(__ballot_sync(kFull, live[0]), __ballot_sync(kFull, live[1]),
-                           __ballot_sync(kFull, live[2]), __ballot_sync(kFull, live[3]));
+      sts_u4(smw_a + 16u * (uint32_t)jj,
+             make_uint4(__ballot_sync(kFull, live[0]), __ballot_sync(kFull, live[1]),
+                        __ballot_sync(kFull, live[2]), __ballot_sync(kFull, live[3])));
 #pragma unroll
     for (int h = 0; h < Z; ++h) band |= !live[h] && q[h] >= pd.x;
     if (__any_sync(kFull, band)) {
@@ -672,9 +708,10 @@ __device__ __forceinline__ void eval_column_hits(const Pair32* __restrict__ hits
         }
         const uint4 x = make_uint4(__ballot_sync(kFull, xl[0]), __ballot_sync(kFull, xl[1]),
                                    __ballot_sync(kFull, xl[2]), __ballot_sync(kFull, xl[3]));
-        const uint4 a = smw[jj];
+        const uint4 a = lds_u4(smw_a + 16u * (uint32_t)jj);
         __syncwarp();
-        smw[jj] = make_uint4(a.x | x.x, a.y | x.y, a.z | x.z, a.w | x.w);
+        sts_u4(smw_a + 16u * (uint32_t)jj,
+               make_uint4(a.x | x.x, a.y | x.y, a.z | x.z, a.w | x.w));
       } else {
 #pragma unroll
         for (int h = 0; h < Z; ++h)
@@ -727,6 +764,8 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
   const float ext_x = ctx, ext_y = cty, ext_z = ctz;
   const float mX = (float)lx - ctx, mY = (float)lyA - cty, mZ = -ctz, mZ1 = mZ + 1.f;
   const float twoY4 = fmaf(2.f, mY, 4.f);      // column B = column A + 4 in y
+  const float mYB = mY + 4.f;
+  const uint32_t wsp_a = smem_addr(wsp);
   const int gx = bg.x0 + lx, gyA = bg.y0 + lyA, gyB = bg.y0 + lyB, gz = bg.z0;
   unsigned ownA[Z], ownB[Z];                   // voxels inside the grid (mask words)
   if constexpr (MASKS) {
@@ -834,14 +873,16 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
       if (hitB) wsp[32 + __popc(ballB & lt)] = p;
       __syncwarp();
       if constexpr (MASKS) {
-        eval_column_hits<true>(wsp, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g, cut2d,
-                               aS[0], aW[0], smw);
-        eval_column_hits<true>(wsp + 32, __popc(ballB), mX, mY + 4.f, mZ, mZ1, gx, gyB, gz,
-                               xsrc, g, cut2d, aS[1], aW[1], smw + 32);
+        eval_column_hits<true>(wsp_a, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g,
+                               cut2d, aS[0], aW[0], smem_addr(smw));
+        eval_column_hits<true>(wsp_a + 32u * (uint32_t)sizeof(Pair32), __popc(ballB), mX, mYB,
+                               mZ, mZ1, gx, gyB, gz, xsrc, g, cut2d, aS[1], aW[1],
+                               smem_addr(smw) + 32u * 16u);
       } else {
-        eval_column_hits_plain(wsp, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g, cut2d,
+        eval_column_hits_plain(wsp_a, __popc(ballA), mX, mY, mZ, mZ1, gx, gyA, gz, xsrc, g, cut2d,
                                aS[0], aW[0]);
-        eval_column_hits_plain(wsp + 32, __popc(ballB), mX, mY + 4.f, mZ, mZ1, gx, gyB, gz, xsrc,
+        eval_column_hits_plain(wsp_a + 32u * (uint32_t)sizeof(Pair32), __popc(ballB), mX, mYB,
+                               mZ, mZ1, gx, gyB, gz, xsrc,
                                g, cut2d, aS[1], aW[1]);
       }
       __syncwarp();
@@ -975,20 +1016,6 @@ forward32w_kernel(const double* __restrict__ pos, const __grid_constant__ ExactS
 #ifndef GSV_COLS_MINB
 #define GSV_COLS_MINB 16        // CTAs (warps) per SM the grouped kernel is built for
 #endif
-// Shared-memory accesses by 32-bit shared address: the base is formed once,
-// outside the loops (plain array indexing let ptxas rematerialise the
-// generic->shared window base, an S2UR with its latency, in every iteration).
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("" : "+r"(a));   // opaque: keep it in a register
-  return a;
-}
-__device__ __forceinline__ float4 lds_f4(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-  return v;
-}
 __device__ __forceinline__ void red_or_shared(uint32_t a, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
