@@ -571,6 +571,16 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   asm volatile("" : "+r"(a));   // opaque: keep it in a register
   return a;
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ float2 lds_f2(uint32_t a) {
   float2 v;
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
@@ -2026,13 +2036,17 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
       unsigned nxt = myw[32];                   // next word, prefetched
       int nxb = myb[32];
       int slot = 1;
+      // shared addresses by opaque 32-bit bases (plain indexing re-derived the
+      // shared window base with an S2UR in every walk iteration)
+      const uint32_t myw_a = smem_addr(myw), myb_a = smem_addr(myb), sab_a = smem_addr(sab);
       for (int it = 0; it < cost; ++it) {
         if (cur == 0u) {
           cur = nxt;
           wb = nxb;
           ++slot;
-          nxt = myw[min(slot, 8) << 5];
-          nxb = myb[min(slot, 8) << 5];
+          const uint32_t so = (uint32_t)(min(slot, 8) << 5);
+          nxt = lds_u32(myw_a + 4u * so);
+          nxb = (int)lds_u16(myb_a + 2u * so);
         }
         const int bit = __ffs(cur) - 1;
         cur &= cur - 1u;
@@ -2043,7 +2057,7 @@ backward32m_kernel(const double* __restrict__ pos, const gsv_record32* __restric
           const int vi = ARITH == 2 ? wb + (bit >> 2) + ((bit & 3) << 6) : wb + bit;
           GSV_DCHECK(vi >= 0 && vi < 256 && (vi & 7) < bg.ex && ((vi >> 3) & 7) < bg.ey &&
                      (vi >> 6) < bg.ez);
-          v_ab = sab[vi];
+          v_ab = lds_f2(sab_a + 8u * (uint32_t)vi);
           fx = (float)(vi & 7);
           fy = (float)((vi >> 3) & 7);
           fz = (float)(vi >> 6);
