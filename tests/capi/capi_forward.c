@@ -9,7 +9,12 @@
  *        cutoff; int32 bdx, bdy, bdz; int64 n; then float64 positions[3n],
  *        log_scales[3n], rotations[4n], raw_amplitude[n], raw_relax[n]; int32 relax.
  * Output: int64 pairs, nbricks; int64 starts[nbricks + 1]; int32 gids[pairs];
- *        float32 I[nx ny nz].
+ *        float32 I[nx ny nz]; int32 incremental_ok.
+ *
+ * Then the incremental entry points: every Gaussian moves by +0.37 spacing in
+ * x; gsv_preprocess_track records the ones whose boxes changed, gsv_bin_scan
+ * recounts, gsv_bin_incremental edits the lists, and the result is compared
+ * with a full gsv_bin_fill of the moved field (incremental_ok = 1 if equal).
  */
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -129,6 +134,74 @@ int main(int argc, char** argv) {
   if (pairs > 0) CU(cudaMemcpy(h_gids, gids, (size_t)pairs * 4, cudaMemcpyDeviceToHost));
   CU(cudaMemcpy(h_I, I, (size_t)nv * 4, cudaMemcpyDeviceToHost));
 
+  /* ---- incremental binning after a move */
+  int32_t incremental_ok = 0;
+  {
+    for (int64_t i = 0; i < n; ++i) h[3 * i] += 0.37 * spc[0];
+    CU(cudaMemcpy(pos, h, (size_t)(3 * n) * 8, cudaMemcpyHostToDevice));
+    const int chg_cap = (int)(n > 0 ? n : 1);
+    int32_t* chg_count = (int32_t*)dev_copy(NULL, 4);
+    CU(cudaMemset(chg_count, 0, 4));
+    int32_t* chg_gid = (int32_t*)dev_copy(NULL, (size_t)chg_cap * 4);
+    int32_t* chg_old = (int32_t*)dev_copy(NULL, (size_t)chg_cap * 16);
+    int32_t* chg_oldcnt = (int32_t*)dev_copy(NULL, (size_t)chg_cap * 4);
+    CK(gsv_preprocess_track(pos, ls, rot, ra, rr, n, relax, cutoff, &g, &k, rec32, counts, box,
+                            chg_count, chg_gid, chg_old, chg_oldcnt, chg_cap, NULL));
+    CU(cudaFree(ws));
+    CK(gsv_bin_workspace(n, 1, nb, &ws_bytes));
+    ws = dev_copy(NULL, ws_bytes);
+    CK(gsv_bin_scan(counts, n, gstart, ws, ws_bytes, NULL));
+    int64_t pairs2 = 0;
+    CU(cudaMemcpy(&pairs2, gstart + n, 8, cudaMemcpyDeviceToHost));
+    const int64_t cap = (pairs2 > pairs ? pairs2 : pairs) + 64;
+    int32_t* gids_a = (int32_t*)dev_copy(NULL, (size_t)cap * 4);
+    if (pairs > 0) CU(cudaMemcpy(gids_a, gids, (size_t)pairs * 4, cudaMemcpyDeviceToDevice));
+    int64_t* starts_out = (int64_t*)dev_copy(NULL, (size_t)(nb + 1) * 8);
+    int32_t* gids_out = (int32_t*)dev_copy(NULL, (size_t)cap * 4);
+    unsigned long long* ops = (unsigned long long*)dev_copy(NULL, (size_t)2 * 16384 * 8);
+    int32_t* nops = (int32_t*)dev_copy(NULL, 4);
+    int32_t* lens = (int32_t*)dev_copy(NULL, (size_t)8 * (nb + 1) * 4);
+    int32_t* flags = (int32_t*)dev_copy(NULL, 8);          /* dry, overflow */
+    CU(cudaMemset(nops, 0, 4));
+    CU(cudaMemset(lens, 0, (size_t)8 * (nb + 1) * 4));
+    CU(cudaMemset(flags, 0, 8));
+    size_t iws = 0;
+    CK(gsv_bin_incremental_workspace(nb, &iws));
+    void* ws2 = dev_copy(NULL, iws);
+    CK(gsv_bin_incremental(counts, box, gstart, n, cap, &k, chg_count, chg_gid, chg_old,
+                           chg_oldcnt, chg_cap, starts, gids_a, starts_out, gids_out, ops, nops,
+                           lens, flags, flags + 1, 1, ws2, iws, NULL));
+    /* the full build of the moved field */
+    CU(cudaFree(ws));
+    CK(gsv_bin_workspace(n, pairs2 > 0 ? pairs2 : 1, nb, &ws_bytes));
+    ws = dev_copy(NULL, ws_bytes);
+    const size_t pb2 = (size_t)(pairs2 > 0 ? pairs2 : 1) * 4;
+    int32_t* kt = (int32_t*)dev_copy(NULL, pb2);
+    int32_t* vt = (int32_t*)dev_copy(NULL, pb2);
+    int32_t* ko = (int32_t*)dev_copy(NULL, pb2);
+    int32_t* gf = (int32_t*)dev_copy(NULL, pb2);
+    int64_t* sf = (int64_t*)dev_copy(NULL, (size_t)(nb + 1) * 8);
+    CK(gsv_bin_fill(counts, box, gstart, n, pairs2, &k, kt, vt, ko, gf, sf, ws, ws_bytes, NULL));
+    CU(cudaDeviceSynchronize());
+    int32_t h_flags[2];
+    CU(cudaMemcpy(h_flags, flags, 8, cudaMemcpyDeviceToHost));
+    int64_t* h_si = (int64_t*)malloc((size_t)(nb + 1) * 8);
+    int64_t* h_sf = (int64_t*)malloc((size_t)(nb + 1) * 8);
+    int32_t* h_gi = (int32_t*)malloc(pb2);
+    int32_t* h_gf = (int32_t*)malloc(pb2);
+    CU(cudaMemcpy(h_si, starts, (size_t)(nb + 1) * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(h_sf, sf, (size_t)(nb + 1) * 8, cudaMemcpyDeviceToHost));
+    if (pairs2 > 0) {
+      CU(cudaMemcpy(h_gi, gids_a, (size_t)pairs2 * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(h_gf, gf, (size_t)pairs2 * 4, cudaMemcpyDeviceToHost));
+    }
+    incremental_ok = h_flags[1] == 0;
+    for (int64_t b = 0; b <= nb && incremental_ok; ++b) incremental_ok = h_si[b] == h_sf[b];
+    for (int64_t j = 0; j < pairs2 && incremental_ok; ++j) incremental_ok = h_gi[j] == h_gf[j];
+    printf("capi_forward: incremental pairs %lld -> %lld, equal to a full build: %d\n",
+           (long long)pairs, (long long)pairs2, incremental_ok);
+  }
+
   FILE* out = fopen(argv[2], "wb");
   if (!out) return 1;
   const int64_t nb64 = nb;
@@ -137,6 +210,7 @@ int main(int argc, char** argv) {
   fwrite(h_starts, 8, (size_t)(nb + 1), out);
   if (pairs > 0) fwrite(h_gids, 4, (size_t)pairs, out);
   fwrite(h_I, 4, (size_t)nv, out);
+  fwrite(&incremental_ok, 4, 1, out);
   fclose(out);
   printf("capi_forward: pairs=%lld bricks=%d voxels=%lld\n", (long long)pairs, nb,
          (long long)nv);

@@ -1,7 +1,9 @@
 """The C ABI (include/gsv.h) from plain C: tests/capi/capi_forward.c, built
 with gcc against libgsv_b200.so and cudart only (no Python, no torch), bins
 and renders a field; its lists and intensities are bit-identical to the
-Python API's (same kernels behind both)."""
+Python API's (same kernels behind both).  It also drives the incremental
+binning entry points after moving the field and checks them against a full
+build."""
 
 import os
 import struct
@@ -59,6 +61,8 @@ def test_c_program_matches_python_api(dims, bd):
     gids = np.frombuffer(raw, "<i4", pairs, o)
     o += 4 * pairs
     I = np.frombuffer(raw, "<f4", grid.num_voxels, o)
+    o += 4 * grid.num_voxels
+    incremental_ok = struct.unpack_from("<i", raw, o)[0]
 
     f = gs.GaussianField(*arrs)
     idx = gs.build_brick_index(f, grid, gs.RenderOptions(), bd)
@@ -67,3 +71,6 @@ def test_c_program_matches_python_api(dims, bd):
     np.testing.assert_array_equal(starts, idx.starts.cpu().numpy())
     np.testing.assert_array_equal(gids, idx.gids.cpu().numpy())
     np.testing.assert_array_equal(I, c.I.cpu().numpy())
+    # the incremental entry points (gsv_preprocess_track, gsv_bin_incremental)
+    # from C: after a move, the edited lists equal a full gsv_bin_fill
+    assert incremental_ok == 1
