@@ -613,7 +613,7 @@ constexpr size_t tma_smem() {
 }
 
 #ifndef GSV_TMA_WARPS_PER_SM
-#define GSV_TMA_WARPS_PER_SM 20
+#define GSV_TMA_WARPS_PER_SM 24
 #endif
 template <int NT>
 __global__ void __launch_bounds__(NT, GSV_TMA_WARPS_PER_SM * 32 / NT)
