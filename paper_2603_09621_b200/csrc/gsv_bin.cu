@@ -27,7 +27,10 @@
 namespace gsv {
 namespace {
 
-__global__ void __launch_bounds__(256, 4)
+#ifndef GSV_PREP_MINB
+#define GSV_PREP_MINB 4          // 256-thread CTAs per SM the preprocess is built for
+#endif
+__global__ void __launch_bounds__(256, GSV_PREP_MINB)
 preprocess_kernel(const double* __restrict__ pos, const double* __restrict__ ls,
                   const double* __restrict__ rot, const double* __restrict__ ra,
                   const double* __restrict__ rr, int64_t n, PrepArgs pa) {
