@@ -9,6 +9,10 @@
                N x 12 partial sums, the only collective, when sharded] ->
                gsv_chain_rule.
 
+The graph-replayed step (TrainStep.step / step_async, what fit() calls) is
+the same iteration captured once and replayed; it bins incrementally from the
+second replay on (see _StepGraph).
+
 Sharding: with ``slab=(b0, b1)`` a rank bins, renders and
 back-propagates only its contiguous brick-id range; the per-Gaussian
 merged partials (and the loss, carried in the spare 12th column) are summed
@@ -357,15 +361,19 @@ def _bias_corrections(beta1: float, beta2: float, t0: int, count: int) -> torch.
 
 
 class _StepGraph:
-    """Buffers and the captured CUDA graph of one fused fit() iteration.
+    """Buffers and the captured CUDA graph(s) of one fused fit() iteration.
 
-    The graph holds the whole iteration -- preprocess, scan, capacity-mode
-    binning (pair count never read by the host), forward with the fused loss
-    and live masks, loss sum, gate, masked backward, the one-pass tail with
-    the step counter and bias corrections read on the device, and the step
-    advance, whose kernel also writes the 16-byte {loss sum, flags} result
-    into a pinned host ring -- so a replay costs one launch and one event
-    wait, with no per-kernel host work and no copy node between replays.
+    The graph holds the whole iteration -- the scan of the pair counts, the
+    lists (incremental binning: last step's lists edited for the Gaussians
+    whose boxes changed, gsv_bin_incremental; or a capacity-mode full build),
+    the pair count never read by the host, forward with the fused loss and
+    live masks, loss sum, gate, masked backward, the one-pass tail with the
+    step counter and bias corrections read on the device, the next step's
+    preprocess (with change tracking), and the step advance, whose kernel also
+    writes the 16-byte {loss sum, flags} result into a pinned host ring -- so a
+    replay costs one launch and one event wait, with no per-kernel host work
+    and no copy node between replays.  Incremental binning captures two graphs
+    that alternate the two list buffers (``graphs``, replayed by parity).
     """
 
     def __init__(self, key, cap: int, t_max: int):
